@@ -1,0 +1,163 @@
+/*
+ * oz2g.h — C ABI of the B200-native Ozaki-II (accurate mode) GEMM emulation.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   template<class T> EmulationResult<T> oz2::os_ii(const Matrix<T>& a,
+ *        const Matrix<T>& b, int n, bool keep_intermediates = false)
+ *   (/root/reference/proj/include/oz2/emulate.hpp:54-88)
+ * and for the constant registry it reads
+ *   const ModuliTable& table_for(int n, Prec mode)   (moduli.hpp:145-153).
+ * The reference has no FFI of its own; include/oz2g/emulate.hpp re-presents
+ * `oz2::os_ii<T>` / `EmulationResult<T>` unchanged on top of this ABI, and
+ * INTEGRATION.md shows the ctypes / C++ bindings.
+ *
+ * Plain pointers and sizes only.  Matrices are row-major (matrix.hpp:25-26)
+ * with explicit leading dimensions.  Results are bit-identical to the
+ * reference for any launch configuration (integer GEMMs are exact and the
+ * fp64 accumulation order over moduli is fixed, crt.hpp:99-104).
+ *
+ * Status codes map 1:1 onto the reference's exception classes.
+ */
+#ifndef OZ2G_H
+#define OZ2G_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OZ2G_API_VERSION 1
+
+/* Status codes (return value of every entry point). */
+#define OZ2G_OK 0
+#define OZ2G_INVALID_ARGUMENT 1 /* std::invalid_argument (matrix.hpp:47-49) */
+#define OZ2G_DOMAIN_ERROR 2     /* std::domain_error (emulate.hpp:59, scaling.hpp:90/102, moduli.hpp:94) */
+#define OZ2G_RANGE_ERROR 3      /* std::range_error (scaling.hpp:145/206/220, crt.hpp:144, emulate.hpp:39) */
+#define OZ2G_LOGIC_ERROR 4      /* std::logic_error (scaling.hpp:67/77/179/189) */
+#define OZ2G_CUDA_ERROR 5       /* device / driver failure (no reference counterpart) */
+
+/* Precision of A, B, C (moduli.hpp:23 enum class Prec). */
+#define OZ2G_FP32 0
+#define OZ2G_FP64 1
+
+/* Flags for oz2g_gemm. */
+#define OZ2G_HOST_PTRS 0u    /* A, B, C are host pointers (copies are done inside) */
+#define OZ2G_DEVICE_PTRS 1u  /* A, B, C are device pointers on the current device */
+#define OZ2G_TIMING 2u       /* fill oz2g_diag::stage_ms with per-stage CUDA-event times */
+
+/* Limits (int8gemm.hpp:12, moduli.hpp:38). */
+#define OZ2G_MAX_INNER_DIM (1LL << 17)
+#define OZ2G_MAX_MODULI 49
+
+/*
+ * Optional intermediates (EmulationResult::scaling / ::crt, emulate.hpp:17-24,
+ * scaling.hpp:20-28, crt.hpp:81-87).  Every non-NULL pointer is a HOST buffer
+ * that is filled; NULL members are skipped.  Shapes (row-major, dense):
+ *   mu, mu_prime, e : m        nu, nu_prime, f : n
+ *   Aprime : m*k (fp64)        Bprime : k*n (fp64)
+ *   Cbar : m*n (int32)         Dbar : m*n (fp32)
+ *   W : N*m*n (int8)           C1, C2, Q, Cpp64 : m*n (fp64)   Cpp32 : m*n
+ * Extra evidence beyond the reference's struct (for bit-parity checks of the
+ * device stages):
+ *   Ares : N*m*k int8 residues of A' (crt.hpp:160)
+ *   Bres : N*k*n int8 residues of B' (crt.hpp:161), row-major k x n
+ *   Cprod: N*m*n int32 wrapped INT8 products (crt.hpp:70)
+ *   cmax_row : m, cmax_col : n int32 clearance-product maxima (scaling.hpp:175-192)
+ */
+typedef struct oz2g_intermediates {
+    int16_t *mu, *nu, *mu_prime, *nu_prime;
+    float *e, *f;
+    double *Aprime, *Bprime;
+    int32_t *Cbar;
+    float *Dbar;
+    int8_t *W;
+    double *C1, *C2, *Q, *Cpp64;
+    float *Cpp32;
+    int8_t *Ares, *Bres;
+    int32_t *Cprod;
+    int32_t *cmax_row, *cmax_col;
+} oz2g_intermediates;
+
+/* Per-call diagnostics. */
+typedef struct oz2g_diag {
+    int subnormal;          /* EmulationResult::subnormal (emulate.hpp:23) */
+    int kernels_launched;   /* device kernels launched by this call */
+    double stage_ms[8];     /* with OZ2G_TIMING: 0 H2D, 1 scale (K1), 2 clearance GEMM, 3 exponents,
+                               4 residues, 5 residue GEMMs, 6 CRT + unscale, 7 D2H (ms) */
+} oz2g_diag;
+
+/*
+ * Multi-GPU hook.  After the clearance product, the per-row and per-column
+ * maxima of C̄ (int32, device memory, lengths m and n) must be max-reduced
+ * across every rank that shares the same rows (resp. columns) of C before the
+ * scaling exponents are formed.  When non-NULL, the callback is
+ * invoked on the calling thread with device pointers, to be reduced IN PLACE
+ * (e.g. ncclAllReduce(..., ncclInt32, ncclMax, row_comm/col_comm, stream)).
+ * Return 0 on success.
+ */
+typedef int (*oz2g_reduce_maxima_fn)(int32_t *cmax_row, int64_t m, int32_t *cmax_col, int64_t n,
+                                     void *stream, void *user);
+
+/*
+ * C = os_ii(A, B, nmod) for A (m x k) and B (k x n), row-major with leading
+ * dimensions lda >= k, ldb >= n, ldc >= n; `prec` is OZ2G_FP32 (float*) or
+ * OZ2G_FP64 (double*).  `stream` is a cudaStream_t (NULL = legacy default).
+ * `inter`, `diag`, `reduce_fn` may be NULL.
+ */
+int oz2g_gemm(int prec, int64_t m, int64_t n, int64_t k, const void *A, int64_t lda, const void *B,
+              int64_t ldb, void *C, int64_t ldc, int nmod, unsigned flags, void *stream,
+              oz2g_intermediates *inter, oz2g_diag *diag, oz2g_reduce_maxima_fn reduce_fn, void *reduce_user);
+
+/* Convenience wrappers mirroring os_ii<double>/os_ii<float>. */
+int oz2g_dgemm(int64_t m, int64_t n, int64_t k, const double *A, int64_t lda, const double *B, int64_t ldb,
+               double *C, int64_t ldc, int nmod, unsigned flags, void *stream, oz2g_diag *diag);
+int oz2g_sgemm(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda, const float *B, int64_t ldb,
+               float *C, int64_t ldc, int nmod, unsigned flags, void *stream, oz2g_diag *diag);
+
+/* Message of the last failing call on this thread (exception::what()). */
+const char *oz2g_last_error(void);
+
+/*
+ * table_for(n, mode) (moduli.hpp:78-91, :145-153) without the mpz members;
+ * P is returned as a decimal string.  Callable without a GPU.
+ */
+typedef struct oz2g_table {
+    int n, mode;
+    int p[OZ2G_MAX_MODULI], q[OZ2G_MAX_MODULI], beta[OZ2G_MAX_MODULI];
+    double s1[OZ2G_MAX_MODULI], s2[OZ2G_MAX_MODULI];
+    long rho;
+    double P1, P2, P_inv;
+    float P_prime;
+    char P_dec[160];
+    /* Scaling-exponent step table (scaling.hpp:159-194 as a step function of
+     * the integer clearance maximum c):  shift(c) = shift0 - #{t : c >= thr[t]}. */
+    int shift0, nthr;
+    int32_t thr[64];
+} oz2g_table;
+
+int oz2g_table_for(int n, int mode, oz2g_table *out);
+
+/* fp32_safe_moduli_max() (moduli.hpp:157-170).  Callable without a GPU. */
+int oz2g_fp32_safe_moduli_max(void);
+
+/* The scaling-exponent shift for one clearance maximum c, evaluated directly
+ * (fp32_round_up, log2f, fma_fp32(.., Down), floor — scaling.hpp:171-180).
+ * Callable without a GPU; used to validate the step table. */
+int oz2g_shift_of_cmax(int n, int64_t c);
+
+/* Device-side log2f evaluation used for the e/f diagnostics, exposed so tests
+ * can compare it exhaustively with the host libm (log2_fp32, softfp.hpp:147). */
+int oz2g_device_log2f(const float *x_dev, float *out_dev, int64_t count, void *stream);
+
+/* Library information (compiled arch, number of SMs used, version). */
+int oz2g_version(void);
+
+/* Release cached device workspaces of this thread's current device. */
+void oz2g_release_workspace(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OZ2G_H */

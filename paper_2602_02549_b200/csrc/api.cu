@@ -1,0 +1,546 @@
+// api.cu — the oz2g C ABI (include/oz2g.h): host orchestration of the
+// B200 pipeline that replaces oz2::os_ii<T> (emulate.hpp:54-88).
+//
+//   validation (emulate.hpp:58-61, moduli.hpp:94)
+//   K1  row_scan_A / col_max_B / col_exp_B / bbar_T  (scale_matrices part 1)
+//   K2  tcgen05 clearance GEMM, fused row/col max    (scaling.hpp:140-148)
+//   [optional multi-GPU max-reduction of the maxima]
+//   K3  scaling exponents via the step table          (scaling.hpp:159-194)
+//   K4  fused trunc + N-plane residues of A and B     (scaling.hpp:199-225, crt.hpp:20-65)
+//   K5  N tcgen05 residue GEMMs, fused signed mod p   (crt.hpp:69-79)
+//   K6  CRT accumulate / Q / final reduce / unscale   (crt.hpp:91-150, emulate.hpp:30-46)
+// Errors are raised through a device status word and mapped, in the
+// reference's pipeline order, onto its exception classes.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/oz2g.h"
+#include "device_common.cuh"
+#include "kernels.h"
+#include "tables.h"
+
+namespace oz2g {
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Fail {
+    int code;
+    std::string what;
+};
+
+#define CUDA_TRY(expr)                                                                         \
+    do {                                                                                       \
+        cudaError_t e_ = (expr);                                                               \
+        if (e_ != cudaSuccess)                                                                 \
+            throw Fail{OZ2G_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(e_)};    \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+        if (bytes == 0) bytes = 16;
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            CUDA_TRY(cudaMalloc(&p, bytes));
+            cap = bytes;
+        }
+        return p;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct Workspace {
+    DevBuf A, B, C, abar, bbar, ares, bres, W, mup, nup, mu, nu, bmax, cmax_row, cmax_col, e, f, status;
+    DevBuf x_cbar, x_cprod, x_c1, x_c2, x_q, x_cpp64, x_cpp32, x_ap, x_bp;
+    std::map<std::pair<int, int>, ResidConsts*> rc;  // device copies of residue constants
+    int num_sms = 0;
+    void release() {
+        for (DevBuf* b : {&A, &B, &C, &abar, &bbar, &ares, &bres, &W, &mup, &nup, &mu, &nu, &bmax, &cmax_row,
+                          &cmax_col, &e, &f, &status, &x_cbar, &x_cprod, &x_c1, &x_c2, &x_q, &x_cpp64, &x_cpp32,
+                          &x_ap, &x_bp})
+            b->release();
+        for (auto& kv : rc) cudaFree(kv.second);
+        rc.clear();
+    }
+};
+
+std::mutex g_ws_mtx;
+std::map<int, Workspace*> g_ws;  // per device; calls on one device are serialised
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) throw Fail{OZ2G_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable"};
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 3-D uint8 tensor [planes][rows][kp] (kp contiguous), box {128, box_rows, 1}, 128-B swizzle.
+CUtensorMap make_plane_map(const void* base, int64_t kp, int64_t rows, int64_t planes, int box_rows) {
+    CUtensorMap tm;
+    cuuint64_t dims[3] = {(cuuint64_t)kp, (cuuint64_t)rows, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {(cuuint64_t)kp, (cuuint64_t)(kp * rows)};
+    cuuint32_t box[3] = {128u, (cuuint32_t)box_rows, 1u};
+    cuuint32_t estr[3] = {1u, 1u, 1u};
+    CUresult r = get_encode()(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Fail{OZ2G_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
+    return tm;
+}
+
+ResidConsts build_resid_consts(const Table& t) {
+    ResidConsts rc;
+    std::memset(&rc, 0, sizeof rc);
+    rc.n = t.n;
+    for (int l = 0; l < t.n; ++l) {
+        const uint32_t p = (uint32_t)t.p[l];
+        rc.p[l] = p;
+        rc.magic[l] = (uint32_t)(0x100000000ull / p);
+        rc.c32[l] = (uint32_t)(0x100000000ull % p);
+        uint32_t v = 1 % p;
+        for (int e = 0; e < 256; ++e) {
+            rc.pow2[l][e] = (uint8_t)v;
+            v = (v * 2u) % p;
+        }
+    }
+    return rc;
+}
+
+void fill_gemm_moduli(GemmParams& P, const Table& t) {
+    for (int l = 0; l < t.n; ++l) {
+        const uint32_t p = (uint32_t)t.p[l];
+        P.p[l] = p;
+        P.magic[l] = (uint32_t)(0x100000000ull / p);
+        P.off[l] = (uint32_t)(p * ((0x80000000ull + p - 1) / p));  // multiple of p >= 2^31
+    }
+}
+
+Workspace& workspace(int dev) {
+    std::lock_guard<std::mutex> lk(g_ws_mtx);
+    auto it = g_ws.find(dev);
+    if (it == g_ws.end()) {
+        Workspace* w = new Workspace();
+        CUDA_TRY(cudaDeviceGetAttribute(&w->num_sms, cudaDevAttrMultiProcessorCount, dev));
+        it = g_ws.emplace(dev, w).first;
+    }
+    return *it->second;
+}
+
+std::mutex& device_mutex(int dev) {
+    static std::mutex mtx[64];
+    return mtx[dev & 63];
+}
+
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct Timer {
+    bool on = false;
+    cudaStream_t s = nullptr;
+    std::vector<cudaEvent_t> ev;
+    void mark() {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        ev.push_back(e);
+    }
+    ~Timer() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
+int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
+             void* C, int64_t ldc, int nmod, unsigned flags, cudaStream_t stream, oz2g_intermediates* inter,
+             oz2g_diag* diag, oz2g_reduce_maxima_fn reduce_fn, void* reduce_user) {
+    if (prec != OZ2G_FP32 && prec != OZ2G_FP64) throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_gemm: prec must be OZ2G_FP32 or OZ2G_FP64"};
+    if (m < 0 || n < 0 || k < 0) throw Fail{OZ2G_INVALID_ARGUMENT, "Matrix: negative dimension"};
+    if (lda < k || ldb < n || ldc < n) throw Fail{OZ2G_INVALID_ARGUMENT, "dimension mismatch: leading dimension"};
+    if (k > OZ2G_MAX_INNER_DIM) throw Fail{OZ2G_DOMAIN_ERROR, "os_ii: k exceeds 2^17"};
+    const Table& tab = table_for(nmod, prec);  // std::domain_error for N outside [2, 49]
+    if (diag) std::memset(diag, 0, sizeof *diag);
+    // k == 0: every row of A (and column of B) is zero (scaling.hpp:180/192)
+    if (k == 0) {
+        if (m > 0) throw Fail{OZ2G_DOMAIN_ERROR, "row_pre_exponents: zero row 0"};
+        if (n > 0) throw Fail{OZ2G_DOMAIN_ERROR, "col_pre_exponents: zero column 0"};
+        return OZ2G_OK;
+    }
+    const bool host = (flags & OZ2G_DEVICE_PTRS) == 0;
+    const size_t esz = prec ? 8 : 4;
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> dev_lock(device_mutex(dev));
+    Workspace& ws = workspace(dev);
+    int launches = 0;
+
+    Timer tm;
+    tm.on = diag && (flags & OZ2G_TIMING);
+    tm.s = stream;
+    tm.mark();
+
+    const int64_t kp = round_up(k, 128);
+    const int64_t ldw = round_up(n > 0 ? n : 1, 16);
+    const void* dA = A;
+    const void* dB = B;
+    void* dC = C;
+    int64_t lda_d = lda, ldb_d = ldb, ldc_d = ldc;
+    if (host) {
+        dA = ws.A.get(esz * (size_t)(m * k));
+        dB = ws.B.get(esz * (size_t)(k * n));
+        dC = ws.C.get(esz * (size_t)(m * n));
+        lda_d = k; ldb_d = n; ldc_d = n;
+        if (m * k) CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dA), esz * k, A, esz * lda, esz * k, m, cudaMemcpyHostToDevice, stream));
+        if (k * n) CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dB), esz * n, B, esz * ldb, esz * n, k, cudaMemcpyHostToDevice, stream));
+    }
+    tm.mark();
+
+    DevStatus* st = (DevStatus*)ws.status.get(sizeof(DevStatus));
+    CUDA_TRY(cudaMemsetAsync(st, 0, 8, stream));
+    CUDA_TRY(cudaMemsetAsync(&st->first_row, 0x7f, 16, stream));
+    int32_t* mup = (int32_t*)ws.mup.get(4 * (size_t)m);
+    int32_t* nup = (int32_t*)ws.nup.get(4 * (size_t)n);
+    int32_t* mu = (int32_t*)ws.mu.get(4 * (size_t)m);
+    int32_t* nu = (int32_t*)ws.nu.get(4 * (size_t)n);
+    unsigned long long* bmax = (unsigned long long*)ws.bmax.get(8 * (size_t)n);
+    int32_t* cmax_row = (int32_t*)ws.cmax_row.get(4 * (size_t)m);
+    int32_t* cmax_col = (int32_t*)ws.cmax_col.get(4 * (size_t)n);
+    float* ev = (float*)ws.e.get(4 * (size_t)m);
+    float* fv = (float*)ws.f.get(4 * (size_t)n);
+    int8_t* abar = (int8_t*)ws.abar.get((size_t)(m * kp));
+    int8_t* bbar = (int8_t*)ws.bbar.get((size_t)(n * kp));
+    if (n) CUDA_TRY(cudaMemsetAsync(bmax, 0, 8 * (size_t)n, stream));
+    if (m) CUDA_TRY(cudaMemsetAsync(cmax_row, 0, 4 * (size_t)m, stream));
+    if (n) CUDA_TRY(cudaMemsetAsync(cmax_col, 0, 4 * (size_t)n, stream));
+
+    // ---- K1: pre-exponents and Abar / Bbar^T ----
+    CUDA_TRY(launch_row_scan_A(prec, dA, lda_d, m, k, kp, mup, abar, st, stream)); launches += m > 0;
+    CUDA_TRY(launch_col_max_B(prec, dB, ldb_d, k, n, bmax, st, stream)); launches += n > 0;
+    CUDA_TRY(launch_col_exp_B(bmax, n, nup, st, stream)); launches += n > 0;
+    CUDA_TRY(launch_bbar_T(prec, dB, ldb_d, k, n, kp, nup, bbar, st, stream)); launches += n > 0;
+    tm.mark();
+
+    // ---- K2: clearance product, fused row/col maxima ----
+    const int BM = gemm_tile_m(), BN = gemm_tile_n();
+    GemmParams gp;
+    std::memset(&gp, 0, sizeof gp);
+    gp.m = (int)m;
+    gp.n = (int)n;
+    gp.kblocks = (int)(kp / 128);
+    gp.tiles_m = (int)((m + BM - 1) / BM);
+    gp.tiles_n = (int)((n + BN - 1) / BN);
+    if (m > 0 && n > 0) {
+        const CUtensorMap tA = make_plane_map(abar, kp, m, 1, BM);
+        const CUtensorMap tB = make_plane_map(bbar, kp, n, 1, BN);
+        gp.planes = 1;
+        gp.rowmax = cmax_row;
+        gp.colmax = cmax_col;
+        CUDA_TRY(launch_gemm_i8(EPI_MAX, tA, tB, gp, ws.num_sms, stream)); ++launches;
+        if (inter && inter->Cbar) {
+            GemmParams g2 = gp;
+            g2.C32 = (int32_t*)ws.x_cbar.get(4 * (size_t)(m * n));
+            g2.ldc32 = n;
+            g2.cplane = m * n;
+            CUDA_TRY(launch_gemm_i8(EPI_I32, tA, tB, g2, ws.num_sms, stream)); ++launches;
+        }
+    }
+    if (reduce_fn) {
+        if (reduce_fn(cmax_row, m, cmax_col, n, (void*)stream, reduce_user) != 0)
+            throw Fail{OZ2G_CUDA_ERROR, "oz2g_gemm: reduce_maxima callback failed"};
+    }
+    tm.mark();
+
+    // ---- K3: scaling exponents ----
+    CUDA_TRY(launch_exponents(cmax_row, m, cmax_col, n, mup, nup, tab.shift0, tab.nthr, tab.thr, mu, nu, ev, fv, st,
+                              stream)); ++launches;
+    tm.mark();
+
+    // ---- K4: residue planes ----
+    const int N = tab.n;
+    const auto key = std::make_pair(tab.n, tab.mode);
+    if (!ws.rc.count(key)) {
+        const ResidConsts h = build_resid_consts(tab);
+        ResidConsts* d = nullptr;
+        CUDA_TRY(cudaMalloc(&d, sizeof(ResidConsts)));
+        CUDA_TRY(cudaMemcpy(d, &h, sizeof h, cudaMemcpyHostToDevice));
+        ws.rc[key] = d;
+    }
+    const ResidConsts* rc_dev = ws.rc[key];
+    int8_t* ares = (int8_t*)ws.ares.get((size_t)N * (size_t)(m * kp));
+    int8_t* bres = (int8_t*)ws.bres.get((size_t)N * (size_t)(n * kp));
+    CUDA_TRY(launch_resid_A(prec, dA, lda_d, m, k, kp, mu, rc_dev, N, ares, st, stream)); launches += m > 0;
+    CUDA_TRY(launch_resid_BT(prec, dB, ldb_d, k, n, kp, nu, rc_dev, N, bres, st, stream)); launches += n > 0;
+    tm.mark();
+
+    // ---- K5: residue GEMMs with fused signed mod p ----
+    int8_t* W = (int8_t*)ws.W.get((size_t)N * (size_t)(m * ldw));
+    if (m > 0 && n > 0) {
+        const CUtensorMap tA = make_plane_map(ares, kp, m, N, BM);
+        const CUtensorMap tB = make_plane_map(bres, kp, n, N, BN);
+        gp.planes = N;
+        gp.W = W;
+        gp.ldw = ldw;
+        gp.wplane = m * ldw;
+        fill_gemm_moduli(gp, tab);
+        CUDA_TRY(launch_gemm_i8(EPI_RESID, tA, tB, gp, ws.num_sms, stream)); ++launches;
+        if (inter && inter->Cprod) {
+            GemmParams g2 = gp;
+            g2.C32 = (int32_t*)ws.x_cprod.get(4 * (size_t)N * (size_t)(m * n));
+            g2.ldc32 = n;
+            g2.cplane = m * n;
+            CUDA_TRY(launch_gemm_i8(EPI_I32, tA, tB, g2, ws.num_sms, stream)); ++launches;
+        }
+    }
+    tm.mark();
+
+    // ---- K6: CRT + inverse scaling ----
+    CrtConsts cc;
+    std::memset(&cc, 0, sizeof cc);
+    cc.n = N;
+    cc.mode = tab.mode;
+    for (int l = 0; l < N; ++l) { cc.s1[l] = tab.s1[l]; cc.s2[l] = tab.s2[l]; }
+    cc.P1 = tab.P1; cc.P2 = tab.P2; cc.P_inv = tab.P_inv;
+    CrtExtra ex{nullptr, nullptr, nullptr, nullptr, nullptr};
+    const size_t mn8 = 8 * (size_t)(m * n);
+    if (inter) {
+        if (inter->C1) ex.C1 = (double*)ws.x_c1.get(mn8);
+        if (inter->C2) ex.C2 = (double*)ws.x_c2.get(mn8);
+        if (inter->Q) ex.Q = (double*)ws.x_q.get(mn8);
+        if (inter->Cpp64) ex.Cpp64 = (double*)ws.x_cpp64.get(mn8);
+        if (inter->Cpp32 && prec == OZ2G_FP32) ex.Cpp32 = (float*)ws.x_cpp32.get(mn8 / 2);
+    }
+    CUDA_TRY(launch_crt(prec, W, ldw, m * ldw, m, n, cc, mu, nu, dC, ldc_d, ex, st, stream)); launches += (m * n) > 0;
+    tm.mark();
+
+    if (host && m * n) CUDA_TRY(cudaMemcpy2DAsync(C, esz * ldc, dC, esz * n, esz * n, m, cudaMemcpyDeviceToHost, stream));
+    tm.mark();
+
+    // ---- intermediates (host copies) ----
+    std::vector<int32_t> tmp32;
+    if (inter) {
+        auto get_i16 = [&](int16_t* dst, const int32_t* src, int64_t cnt) {
+            if (!dst || cnt == 0) return;
+            tmp32.resize((size_t)cnt);
+            CUDA_TRY(cudaMemcpyAsync(tmp32.data(), src, 4 * (size_t)cnt, cudaMemcpyDeviceToHost, stream));
+            CUDA_TRY(cudaStreamSynchronize(stream));
+            for (int64_t i = 0; i < cnt; ++i) dst[i] = (int16_t)tmp32[(size_t)i];
+        };
+        get_i16(inter->mu, mu, m);
+        get_i16(inter->nu, nu, n);
+        get_i16(inter->mu_prime, mup, m);
+        get_i16(inter->nu_prime, nup, n);
+        if (inter->e && m) CUDA_TRY(cudaMemcpyAsync(inter->e, ev, 4 * (size_t)m, cudaMemcpyDeviceToHost, stream));
+        if (inter->f && n) CUDA_TRY(cudaMemcpyAsync(inter->f, fv, 4 * (size_t)n, cudaMemcpyDeviceToHost, stream));
+        if (inter->cmax_row && m) CUDA_TRY(cudaMemcpyAsync(inter->cmax_row, cmax_row, 4 * (size_t)m, cudaMemcpyDeviceToHost, stream));
+        if (inter->cmax_col && n) CUDA_TRY(cudaMemcpyAsync(inter->cmax_col, cmax_col, 4 * (size_t)n, cudaMemcpyDeviceToHost, stream));
+        if (inter->Aprime && m * k) {
+            double* d = (double*)ws.x_ap.get(8 * (size_t)(m * k));
+            CUDA_TRY(launch_trunc_scaled(prec, dA, lda_d, m, k, mu, 0, d, stream)); ++launches;
+            CUDA_TRY(cudaMemcpyAsync(inter->Aprime, d, 8 * (size_t)(m * k), cudaMemcpyDeviceToHost, stream));
+        }
+        if (inter->Bprime && k * n) {
+            double* d = (double*)ws.x_bp.get(8 * (size_t)(k * n));
+            CUDA_TRY(launch_trunc_scaled(prec, dB, ldb_d, k, n, nu, 1, d, stream)); ++launches;
+            CUDA_TRY(cudaMemcpyAsync(inter->Bprime, d, 8 * (size_t)(k * n), cudaMemcpyDeviceToHost, stream));
+        }
+        if (m * n) {
+            if (inter->Cbar) CUDA_TRY(cudaMemcpyAsync(inter->Cbar, ws.x_cbar.p, 4 * (size_t)(m * n), cudaMemcpyDeviceToHost, stream));
+            if (inter->W)
+                for (int l = 0; l < N; ++l)
+                    CUDA_TRY(cudaMemcpy2DAsync(inter->W + (size_t)l * (size_t)(m * n), (size_t)n, W + (size_t)l * (size_t)(m * ldw),
+                                               (size_t)ldw, (size_t)n, (size_t)m, cudaMemcpyDeviceToHost, stream));
+            if (inter->Cprod) CUDA_TRY(cudaMemcpyAsync(inter->Cprod, ws.x_cprod.p, 4 * (size_t)N * (size_t)(m * n), cudaMemcpyDeviceToHost, stream));
+            if (ex.C1) CUDA_TRY(cudaMemcpyAsync(inter->C1, ex.C1, mn8, cudaMemcpyDeviceToHost, stream));
+            if (ex.C2) CUDA_TRY(cudaMemcpyAsync(inter->C2, ex.C2, mn8, cudaMemcpyDeviceToHost, stream));
+            if (ex.Q) CUDA_TRY(cudaMemcpyAsync(inter->Q, ex.Q, mn8, cudaMemcpyDeviceToHost, stream));
+            if (ex.Cpp64) CUDA_TRY(cudaMemcpyAsync(inter->Cpp64, ex.Cpp64, mn8, cudaMemcpyDeviceToHost, stream));
+            if (ex.Cpp32) CUDA_TRY(cudaMemcpyAsync(inter->Cpp32, ex.Cpp32, mn8 / 2, cudaMemcpyDeviceToHost, stream));
+        }
+        if (inter->Ares && m * k)
+            for (int l = 0; l < N; ++l)
+                CUDA_TRY(cudaMemcpy2DAsync(inter->Ares + (size_t)l * (size_t)(m * k), (size_t)k, ares + (size_t)l * (size_t)(m * kp),
+                                           (size_t)kp, (size_t)k, (size_t)m, cudaMemcpyDeviceToHost, stream));
+        if (inter->Bres && k * n) {
+            // device planes are B'^T [n][kp]; the reference layout is k x n
+            std::vector<int8_t> t((size_t)(n * kp));
+            for (int l = 0; l < N; ++l) {
+                CUDA_TRY(cudaMemcpyAsync(t.data(), bres + (size_t)l * (size_t)(n * kp), (size_t)(n * kp), cudaMemcpyDeviceToHost, stream));
+                CUDA_TRY(cudaStreamSynchronize(stream));
+                int8_t* dst = inter->Bres + (size_t)l * (size_t)(k * n);
+                for (int64_t h = 0; h < k; ++h)
+                    for (int64_t j = 0; j < n; ++j) dst[h * n + j] = t[(size_t)(j * kp + h)];
+            }
+        }
+    }
+
+    DevStatus hs;
+    CUDA_TRY(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    CUDA_TRY(cudaGetLastError());
+
+    if (inter && inter->Dbar && inter->Cbar)
+        for (int64_t i = 0; i < m * n; ++i) inter->Dbar[i] = fp32_round_up(inter->Cbar[i]);
+
+    if (diag) {
+        diag->subnormal = hs.subnormal ? 1 : 0;
+        diag->kernels_launched = launches;
+        if (tm.on && tm.ev.size() >= 2) {
+            // stage order: 0 H2D, 1 K1 scale, 2 clearance GEMM, 3 exponents, 4 residues,
+            //              5 residue GEMMs, 6 CRT, 7 D2H
+            for (size_t s = 0; s + 1 < tm.ev.size() && s < 8; ++s) {
+                float ms = 0;
+                cudaEventElapsedTime(&ms, tm.ev[s], tm.ev[s + 1]);
+                diag->stage_ms[s] = ms;
+            }
+        }
+    }
+
+    const uint32_t e = hs.err;
+    char buf[160];
+    if (e & (ERR_A_NONFINITE | ERR_A_ZERO_ROW)) {
+        if (e & ERR_A_NONFINITE) throw Fail{OZ2G_DOMAIN_ERROR, "matrix entry is not finite"};
+        snprintf(buf, sizeof buf, "row_pre_exponents: zero row %lld", (long long)hs.first_row);
+        throw Fail{OZ2G_DOMAIN_ERROR, buf};
+    }
+    if (e & ERR_B_NONFINITE) throw Fail{OZ2G_DOMAIN_ERROR, "matrix entry is not finite"};
+    if (e & ERR_B_ZERO_COL) {
+        snprintf(buf, sizeof buf, "col_pre_exponents: zero column %lld", (long long)hs.first_col);
+        throw Fail{OZ2G_DOMAIN_ERROR, buf};
+    }
+    if (e & ERR_CEIL_LOGIC) throw Fail{OZ2G_LOGIC_ERROR, "ceil_abs_scaled: entry above row/column max"};
+    if (e & ERR_E_LOGIC) throw Fail{OZ2G_LOGIC_ERROR, "scaling_exponents: e_i >= 31"};
+    if (e & ERR_MU_RANGE) throw Fail{OZ2G_RANGE_ERROR, "mu: exceeds 16-bit range"};
+    if (e & ERR_NU_RANGE) throw Fail{OZ2G_RANGE_ERROR, "nu: exceeds 16-bit range"};
+    if (e & ERR_TRUNC_A_RANGE) throw Fail{OZ2G_RANGE_ERROR, "truncate_scaled: 2^mu*a overflow"};
+    if (e & ERR_TRUNC_B_RANGE) throw Fail{OZ2G_RANGE_ERROR, "truncate_scaled: b*2^nu overflow"};
+    if (e & ERR_FR_RANGE) throw Fail{OZ2G_RANGE_ERROR, "final_reduce: single(C'') overflows fp32 (N too large for fp32 mode)"};
+    if (e & ERR_INV_RANGE) throw Fail{OZ2G_RANGE_ERROR, "os_ii: inverse scaling overflow"};
+    return OZ2G_OK;
+}
+
+template <class F>
+int guarded(F&& f) {
+    g_last_error.clear();
+    try {
+        return f();
+    } catch (const Fail& x) {
+        g_last_error = x.what;
+        return x.code;
+    } catch (const std::invalid_argument& x) {
+        g_last_error = x.what();
+        return OZ2G_INVALID_ARGUMENT;
+    } catch (const std::domain_error& x) {
+        g_last_error = x.what();
+        return OZ2G_DOMAIN_ERROR;
+    } catch (const std::range_error& x) {
+        g_last_error = x.what();
+        return OZ2G_RANGE_ERROR;
+    } catch (const std::logic_error& x) {
+        g_last_error = x.what();
+        return OZ2G_LOGIC_ERROR;
+    } catch (const std::exception& x) {
+        g_last_error = x.what();
+        return OZ2G_CUDA_ERROR;
+    }
+}
+
+}  // namespace
+}  // namespace oz2g
+
+using namespace oz2g;
+
+extern "C" {
+
+int oz2g_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
+              void* C, int64_t ldc, int nmod, unsigned flags, void* stream, oz2g_intermediates* inter,
+              oz2g_diag* diag, oz2g_reduce_maxima_fn reduce_fn, void* reduce_user) {
+    return guarded([&] {
+        return run_gemm(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, (cudaStream_t)stream, inter, diag,
+                        reduce_fn, reduce_user);
+    });
+}
+
+int oz2g_dgemm(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B, int64_t ldb,
+               double* C, int64_t ldc, int nmod, unsigned flags, void* stream, oz2g_diag* diag) {
+    return oz2g_gemm(OZ2G_FP64, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, stream, nullptr, diag, nullptr, nullptr);
+}
+
+int oz2g_sgemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B, int64_t ldb,
+               float* C, int64_t ldc, int nmod, unsigned flags, void* stream, oz2g_diag* diag) {
+    return oz2g_gemm(OZ2G_FP32, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, stream, nullptr, diag, nullptr, nullptr);
+}
+
+const char* oz2g_last_error(void) { return g_last_error.c_str(); }
+
+int oz2g_table_for(int n, int mode, oz2g_table* out) {
+    return guarded([&] {
+        if (mode != OZ2G_FP32 && mode != OZ2G_FP64) throw Fail{OZ2G_INVALID_ARGUMENT, "table_for: bad mode"};
+        const Table& t = table_for(n, mode);
+        std::memset(out, 0, sizeof *out);
+        out->n = t.n;
+        out->mode = t.mode;
+        for (int l = 0; l < t.n; ++l) {
+            out->p[l] = t.p[l];
+            out->q[l] = t.q[l];
+            out->beta[l] = t.beta[l];
+            out->s1[l] = t.s1[l];
+            out->s2[l] = t.s2[l];
+        }
+        out->rho = t.rho;
+        out->P1 = t.P1;
+        out->P2 = t.P2;
+        out->P_inv = t.P_inv;
+        out->P_prime = t.P_prime;
+        std::snprintf(out->P_dec, sizeof out->P_dec, "%s", t.P_dec.c_str());
+        out->shift0 = t.shift0;
+        out->nthr = t.nthr;
+        for (int q = 0; q < t.nthr; ++q) out->thr[q] = t.thr[q];
+        return OZ2G_OK;
+    });
+}
+
+int oz2g_fp32_safe_moduli_max(void) { return fp32_safe_moduli_max(); }
+
+int oz2g_shift_of_cmax(int n, int64_t c) {
+    const Table& t = table_for(n < 2 ? 2 : (n > 49 ? 49 : n), OZ2G_FP64);
+    return shift_of_cmax(t.P_prime, c, nullptr);
+}
+
+int oz2g_device_log2f(const float* x_dev, float* out_dev, int64_t count, void* stream) {
+    return guarded([&] {
+        CUDA_TRY(launch_log2f(x_dev, out_dev, count, (cudaStream_t)stream));
+        return OZ2G_OK;
+    });
+}
+
+int oz2g_version(void) { return OZ2G_API_VERSION; }
+
+void oz2g_release_workspace(void) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    std::lock_guard<std::mutex> lk(g_ws_mtx);
+    auto it = g_ws.find(dev);
+    if (it != g_ws.end()) it->second->release();
+}
+
+}  // extern "C"

@@ -1,0 +1,98 @@
+// crt.cu — Chinese-Remainder reconstruction and inverse scaling, fused into
+// one HBM-bound pass over the N int8 residue products W_l.
+//
+// Restates, element by element and in the reference's exact operation order:
+//   accumulate    crt.hpp:91-110  C1 = fma chain of s1_l * W_l over l = 0..N-1
+//                                 from +0.0; C2 likewise with s2 (fp64 mode)
+//   compute_q     crt.hpp:113-119 Q = round_half_even(RN(P_inv * C1))
+//   final_reduce  crt.hpp:129-150 C'' = fma(-Q, P2, fma(-Q, P1, C1) + C2);
+//                                 fp32 mode: |C''| >= 0x1.ffffffp+127 is a
+//                                 range error, else C''32 = RN32(C'')
+//   inverse_scale emulate.hpp:30-46 x = ldexp(C'', -mu_i), y = ldexp(x, -nu_j)
+//                                 (two RN scalings), subnormal / overflow flags
+// Every operation is an explicit _rn intrinsic so nvcc cannot contract or
+// reorder; the result is bit-identical to the reference.
+#include <cfloat>
+
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace oz2g {
+
+namespace {
+
+template <class T>
+__global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, int64_t ldw, int64_t wplane,
+                                                  int64_t m, int64_t n, const CrtConsts cc,
+                                                  const int32_t* __restrict__ mu, const int32_t* __restrict__ nu,
+                                                  T* __restrict__ C, int64_t ldc, const CrtExtra ex,
+                                                  DevStatus* st) {
+    // 4 consecutive columns per thread: one 32-bit load per modulus plane
+    const int64_t qn = (n + 3) / 4;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m * qn) return;
+    const int64_t i = t / qn;
+    const int64_t j0 = (t - i * qn) * 4;
+    const int jn = (int)(n - j0 < 4 ? n - j0 : 4);
+    double c1[4] = {0.0, 0.0, 0.0, 0.0}, c2[4] = {0.0, 0.0, 0.0, 0.0};
+    const bool dd = cc.mode == 1;
+    const int8_t* wp = W + i * ldw + j0;
+    for (int l = 0; l < cc.n; ++l) {
+        const uint32_t word = __ldg(reinterpret_cast<const uint32_t*>(wp + (int64_t)l * wplane));
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const double wv = (double)(int8_t)((word >> (8 * b)) & 0xffu);
+            c1[b] = __fma_rn(cc.s1[l], wv, c1[b]);
+            if (dd) c2[b] = __fma_rn(cc.s2[l], wv, c2[b]);
+        }
+    }
+    const int mui = mu[i];
+    bool fr_range = false, inv_range = false, sub = false;
+    for (int b = 0; b < jn; ++b) {
+        const int64_t j = j0 + b;
+        const double q = rint(__dmul_rn(cc.P_inv, c1[b]));
+        const double t1 = __fma_rn(-q, cc.P1, c1[b]);
+        const double t2 = __dadd_rn(t1, c2[b]);
+        const double cpp = __fma_rn(-q, cc.P2, t2);
+        const int64_t o = i * n + j;
+        if (ex.C1) ex.C1[o] = c1[b];
+        if (ex.C2) ex.C2[o] = c2[b];
+        if (ex.Q) ex.Q[o] = q;
+        if (ex.Cpp64) ex.Cpp64[o] = cpp;
+        const int nuj = nu[j];
+        if constexpr (sizeof(T) == 4) {
+            if (cc.mode == 0 && fabs(cpp) >= 0x1.ffffffp+127) { fr_range = true; continue; }
+            const float c32 = __double2float_rn(cpp);
+            if (ex.Cpp32) ex.Cpp32[o] = c32;
+            const float x = ldexpf_rn(c32, -mui);
+            const float y = ldexpf_rn(x, -nuj);
+            inv_range |= !isfinite(x) || !isfinite(y);
+            sub |= (x != 0.0f && fabsf(x) < FLT_MIN) || (y != 0.0f && fabsf(y) < FLT_MIN);
+            C[i * ldc + j] = y;
+        } else {
+            const double x = ldexp_rn(cpp, -mui);
+            const double y = ldexp_rn(x, -nuj);
+            inv_range |= !isfinite(x) || !isfinite(y);
+            sub |= (x != 0.0 && fabs(x) < DBL_MIN) || (y != 0.0 && fabs(y) < DBL_MIN);
+            C[i * ldc + j] = y;
+        }
+    }
+    if (fr_range) atomicOr(&st->err, (uint32_t)ERR_FR_RANGE);
+    if (inv_range) atomicOr(&st->err, (uint32_t)ERR_INV_RANGE);
+    if (sub) atomicOr(&st->subnormal, 1u);
+}
+
+}  // namespace
+
+cudaError_t launch_crt(int prec, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
+                       const CrtConsts& cc, const int32_t* mu, const int32_t* nu, void* C, int64_t ldc,
+                       const CrtExtra& extra, DevStatus* st, cudaStream_t s) {
+    const int64_t work = m * ((n + 3) / 4);
+    if (work == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)((work + 255) / 256);
+    if (prec) crt_kernel<double><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, (double*)C, ldc, extra, st);
+    else crt_kernel<float><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, (float*)C, ldc, extra, st);
+    return cudaGetLastError();
+}
+
+}  // namespace oz2g

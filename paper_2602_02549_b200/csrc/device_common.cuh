@@ -1,0 +1,270 @@
+// device_common.cuh — sm_100a device helpers shared by the oz2g kernels:
+// inline-PTX wrappers for mbarrier, TMA (cp.async.bulk.tensor), tcgen05
+// (alloc / mma kind::i8 / commit / ld) and the exact scalar arithmetic the
+// Ozaki-II stages need (fp decomposition, modular reduction, RN scaling).
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace oz2g {
+
+// ----------------------------------------------------------------------------
+// Error word bits (first failure in reference pipeline order wins on the host)
+// ----------------------------------------------------------------------------
+enum ErrBits : uint32_t {
+    ERR_A_NONFINITE = 1u << 0,   // scaling.hpp:127 (row_abs_max)
+    ERR_A_ZERO_ROW = 1u << 1,    // scaling.hpp:180
+    ERR_B_NONFINITE = 1u << 2,   // scaling.hpp:138 (col_abs_max)
+    ERR_B_ZERO_COL = 1u << 3,    // scaling.hpp:192
+    ERR_CEIL_LOGIC = 1u << 4,    // scaling.hpp:67/77 (cannot happen for valid inputs)
+    ERR_E_LOGIC = 1u << 5,       // scaling.hpp:179/189 e_i >= 31
+    ERR_MU_RANGE = 1u << 6,      // scaling.hpp:145 mu int16 overflow
+    ERR_NU_RANGE = 1u << 7,
+    ERR_TRUNC_A_RANGE = 1u << 8, // scaling.hpp:206
+    ERR_TRUNC_B_RANGE = 1u << 9, // scaling.hpp:220
+    ERR_FR_RANGE = 1u << 10,     // crt.hpp:144 fp32 C'' overflow
+    ERR_INV_RANGE = 1u << 11,    // emulate.hpp:39 inverse scaling overflow
+};
+
+// Device status block: error bits, first offending index per bit class and
+// the subnormal flag.
+struct DevStatus {
+    uint32_t err;
+    uint32_t subnormal;
+    int64_t first_row;  // atomicMin target for zero-row / zero-col messages
+    int64_t first_col;
+};
+
+// ----------------------------------------------------------------------------
+// Exact fp helpers
+// ----------------------------------------------------------------------------
+// |x| = mant * 2^e2 with mant in [2^52, 2^53) for finite nonzero x (normal or
+// subnormal) — the reference's frexp/ldexp(f, 53) decomposition (crt.hpp:41-43,
+// scaling.hpp:64-66) with e = e2 + 53.
+__device__ __forceinline__ void decompose(double x, uint64_t& mant, int& e2) {
+    const uint64_t bits = (uint64_t)__double_as_longlong(x);
+    const int ef = (int)((bits >> 52) & 0x7ff);
+    const uint64_t frac = bits & 0x000fffffffffffffull;
+    if (ef) {
+        mant = frac | (1ull << 52);
+        e2 = ef - 1075;
+    } else {
+        const int lz = __clzll(frac) - 11;
+        mant = frac << lz;
+        e2 = -1074 - lz;
+    }
+}
+
+// ilogb for finite nonzero double (scaling.hpp:182 std::ilogb).
+__device__ __forceinline__ int ilogb_exact(double x) {
+    uint64_t mant; int e2;
+    decompose(x, mant, e2);
+    return e2 + 52;
+}
+
+// 2^s as a double for s in [-1022, 1023].
+__device__ __forceinline__ double pow2d(int s) { return __longlong_as_double((long long)(s + 1023) << 52); }
+__device__ __forceinline__ float pow2f(int s) { return __int_as_float((s + 127) << 23); }
+
+// RN(x * 2^s) with a single rounding: glibc ldexp/scalbn semantics used by
+// inverse_scale (emulate.hpp:37-38).
+__device__ __forceinline__ double ldexp_rn(double x, int s) {
+    if (x == 0.0 || !isfinite(x)) return x;
+    const int ex = ilogb_exact(x);
+    const int et = ex + s;
+    if (et > 1023) return copysign(__longlong_as_double(0x7ff0000000000000ll), x);
+    if (et >= -1022) {
+        // exact: intermediates stay between ex and et, both in the normal range
+        while (s > 1000) { x = __dmul_rn(x, pow2d(1000)); s -= 1000; }
+        while (s < -1000) { x = __dmul_rn(x, pow2d(-1000)); s += 1000; }
+        return __dmul_rn(x, pow2d(s));
+    }
+    if (et < -1075) return copysign(0.0, x);  // |x 2^s| < 2^-1075: RN gives 0
+    // subnormal target: m = x * 2^-ex in [1,2) exact; (m * 2^-1022) exact; one rounding
+    double m = x;
+    int t = -ex;
+    while (t > 1000) { m = __dmul_rn(m, pow2d(1000)); t -= 1000; }
+    while (t < -1000) { m = __dmul_rn(m, pow2d(-1000)); t += 1000; }
+    m = __dmul_rn(m, pow2d(t));
+    m = __dmul_rn(m, pow2d(-1022));
+    return __dmul_rn(m, pow2d(et + 1022));
+}
+
+__device__ __forceinline__ int ilogbf_exact(float x) {
+    const uint32_t bits = (uint32_t)__float_as_int(x);
+    const int ef = (int)((bits >> 23) & 0xff);
+    const uint32_t frac = bits & 0x7fffffu;
+    if (ef) return ef - 127;
+    return -149 + (31 - __clz(frac));
+}
+
+// RN(x * 2^s) for float (std::ldexp(float, int) == scalbnf).
+__device__ __forceinline__ float ldexpf_rn(float x, int s) {
+    if (x == 0.0f || !isfinite(x)) return x;
+    const int ex = ilogbf_exact(x);
+    const int et = ex + s;
+    if (et > 127) return copysignf(__int_as_float(0x7f800000), x);
+    if (et >= -126) {
+        while (s > 120) { x = __fmul_rn(x, pow2f(120)); s -= 120; }
+        while (s < -120) { x = __fmul_rn(x, pow2f(-120)); s += 120; }
+        return __fmul_rn(x, pow2f(s));
+    }
+    if (et < -150) return copysignf(0.0f, x);  // |x 2^s| < 2^-150: RN gives 0
+    float m = x;
+    int t = -ex;
+    while (t > 120) { m = __fmul_rn(m, pow2f(120)); t -= 120; }
+    while (t < -120) { m = __fmul_rn(m, pow2f(-120)); t += 120; }
+    m = __fmul_rn(m, pow2f(t));
+    m = __fmul_rn(m, pow2f(-126));
+    return __fmul_rn(m, pow2f(et + 126));
+}
+
+// ----------------------------------------------------------------------------
+// Modular reduction by a small odd modulus p (<= 255) with a precomputed
+// magic M = floor(2^32 / p): q = umulhi(x, M) is floor(x/p) or one less.
+// ----------------------------------------------------------------------------
+struct ModP {
+    uint32_t p, magic;
+};
+
+__device__ __forceinline__ uint32_t mod_u32(uint32_t x, ModP mp) {
+    const uint32_t q = __umulhi(x, mp.magic);
+    uint32_t r = x - q * mp.p;
+    if (r >= mp.p) r -= mp.p;
+    return r;
+}
+
+// ----------------------------------------------------------------------------
+// mbarrier / TMA / tcgen05 PTX wrappers
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n\t"
+        ".reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n\t"
+        "DONE_%=:\n\t"
+        "}" ::"r"(addr),
+        "r"(parity), "r"(0x989680)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* desc) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(desc)) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* desc, uint64_t* bar, int c0,
+                                            int c1, int c2, uint64_t cache_hint) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(cache_hint)
+        : "memory");
+}
+
+// L2 cache-policy constants (CUTLASS TMA::CacheHintSm90 values).
+constexpr uint64_t kEvictNormal = 0x1000000000000000ull;
+constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
+constexpr uint64_t kEvictLast = 0x14F0000000000000ull;
+
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_relinquish() {
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// D[tmem] (+)= A[smem] * B[smem], int8 x int8 -> int32, one CTA.
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+        "}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// Arrive on an mbarrier once all previously issued tcgen05.mma of this thread
+// complete (implicit tcgen05.fence::before_thread_sync).
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+// 32 lanes x 32 columns of 32-bit TMEM -> 32 registers per thread.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row core
+// groups 1024 B apart (SBO), version 1 (sm_100).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);
+    d |= (uint64_t)1 << 16;             // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;   // SBO
+    d |= (uint64_t)1 << 46;             // descriptor version
+    d |= (uint64_t)2 << 61;             // SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor for kind::i8: s8 x s8 -> s32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+    return (2u << 4)                       // D format S32
+           | (1u << 7) | (1u << 10)        // A, B signed int8
+           | ((uint32_t)(N >> 3) << 17)    // N / 8
+           | ((uint32_t)(M >> 4) << 24);   // M / 16
+}
+
+}  // namespace oz2g

@@ -1,0 +1,276 @@
+// gemm_tc.cu — INT8 x INT8 -> INT32 GEMMs of the Ozaki-II scheme on the
+// 5th-generation tensor cores (tcgen05.mma kind::i8, sm_100a).
+//
+// Replaces the reference's software INT8 engine
+//   gemm_i8_wrap       /root/reference/proj/include/oz2/int8gemm.hpp:17-34
+// at its two call sites, each with a fused epilogue so that the INT32 product
+// is never written to HBM:
+//   EPI_MAX   clearance_product (scaling.hpp:140-148) + the row/column maxima
+//             of scaling_exponents (scaling.hpp:175-192): per-tile max, then
+//             one atomicMax per row / column.  (fp32_round_up and log2f are
+//             monotone, so max commutes with them; they run later on m+n
+//             scalars.)
+//   EPI_RESID residue_gemm_and_reduce (crt.hpp:69-79): W = signed_mod(C', p)
+//             with the p/2 tie mapped to -p/2, stored as int8.
+//   EPI_I32   debug/evidence: store the wrapped INT32 product itself.
+//
+// Exactness: |a|,|b| <= 128 and k <= 2^17 give |sum| <= 2^31; the tensor core
+// accumulates in 32-bit two's complement, which is exactly the reference's
+// uint32 wraparound (int8gemm.hpp:24-30) — and for p = 256 the residue
+// survives the wrap because 256 | 2^32.
+//
+// Kernel shape: persistent, one CTA per SM, 256 threads —
+//   warp 0      TMA producer (one elected lane): A tile 128x128 B and
+//               B tile 256x128 B per stage, 128-byte swizzle, 4 stages;
+//   warp 1      MMA issuer (one lane): 4 x tcgen05.mma 128x256x32 per stage
+//               into a TMEM accumulator (2 x 256 columns, double-buffered);
+//   warp 2      TMEM allocator;
+//   warps 4..7  epilogue: tcgen05.ld 32 lanes x 32 columns, fused reduction.
+// Operands are K-major (A planes [l][m][kp], B planes [l][n][kp]).
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace oz2g {
+
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 128, STAGES = 4;
+constexpr int A_BYTES = BM * BK;  // 16 KB
+constexpr int B_BYTES = BN * BK;  // 32 KB
+constexpr int GROUP_M = 8;
+constexpr uint32_t IDESC = idesc_i8(BM, BN);
+constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
+
+struct TileCoord { int l, tm, tn; };
+
+__device__ __forceinline__ TileCoord decode_unit(int u, int tiles_m, int tiles_n) {
+    const int per_plane = tiles_m * tiles_n;
+    TileCoord c;
+    c.l = u / per_plane;
+    const int t = u - c.l * per_plane;
+    const int group = GROUP_M * tiles_n;
+    const int g = t / group;
+    const int first_m = g * GROUP_M;
+    const int gm = min(tiles_m - first_m, GROUP_M);
+    const int r = t - g * group;
+    c.tm = first_m + r % gm;
+    c.tn = r / gm;
+    return c;
+}
+
+template <int MODE>
+__device__ __forceinline__ void epilogue_chunk(const uint32_t (&v)[32], int row, int col0, int l,
+                                               const GemmParams& P) {
+    const int lane = threadIdx.x & 31;
+    if constexpr (MODE == EPI_MAX) {
+        // row max over this chunk (values are exact non-negative integers)
+        int32_t rmax = 0;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) rmax = max(rmax, (int32_t)v[c]);
+        // column max across the 32 rows of this warp: lane c keeps column c
+        int32_t mine = 0;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+            const int32_t cm = (int32_t)__reduce_max_sync(0xffffffffu, v[c]);
+            if (lane == c) mine = cm;
+        }
+        // columns beyond n and rows beyond m hold TMA zero-fill (harmless for max)
+        if (col0 + lane < P.n) atomicMax(&P.colmax[col0 + lane], mine);
+        if (row < P.m) {
+            // accumulate the row max in a register across chunks: done by caller
+            (void)rmax;
+        }
+    } else if constexpr (MODE == EPI_RESID) {
+        if (row >= P.m) return;
+        const uint32_t p = P.p[l];
+        uint32_t packed[8];
+        if (p == 256u) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                packed[c] = (v[4 * c] & 0xffu) | ((v[4 * c + 1] & 0xffu) << 8) | ((v[4 * c + 2] & 0xffu) << 16) |
+                            ((v[4 * c + 3] & 0xffu) << 24);
+        } else {
+            const ModP mp{p, P.magic[l]};
+            const uint32_t off = P.off[l];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                uint32_t word = 0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const uint32_t r = mod_u32(v[4 * c + b] + off, mp);  // (C' mod p) in [0, p)
+                    const int32_t w = (2u * r > p) ? (int32_t)r - (int32_t)p : (int32_t)r;
+                    word |= ((uint32_t)w & 0xffu) << (8 * b);
+                }
+                packed[c] = word;
+            }
+        }
+        int8_t* dst = P.W + (int64_t)l * P.wplane + (int64_t)row * P.ldw + col0;
+        if (col0 + 32 <= P.n) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+            d4[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+            d4[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+        } else {
+            for (int c = 0; c < 32 && col0 + c < P.n; ++c) dst[c] = (int8_t)((packed[c >> 2] >> (8 * (c & 3))) & 0xff);
+        }
+    } else {  // EPI_I32
+        if (row >= P.m) return;
+        int32_t* dst = P.C32 + (int64_t)l * P.cplane + (int64_t)row * P.ldc32 + col0;
+        for (int c = 0; c < 32 && col0 + c < P.n; ++c) dst[c] = (int32_t)v[c];
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 1)
+    gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ GemmParams P) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
+    if (warp == 2) { tmem_alloc(tmem_slot, 512); tmem_relinquish(); }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int total = P.planes * P.tiles_m * P.tiles_n;
+
+    if (warp == 0) {
+        // ===== TMA producer =====
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int u = blockIdx.x; u < total; u += gridDim.x) {
+            const TileCoord tc = decode_unit(u, P.tiles_m, P.tiles_n);
+            for (int kb = 0; kb < P.kblocks; ++kb) {
+                mbar_wait(&empty[stage], phase ^ 1u);
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
+                    tma_load_3d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, tc.tm * BM, tc.l, kEvictNormal);
+                    tma_load_3d(sB + stage * B_BYTES, &tmB, &full[stage], kb * BK, tc.tn * BN, tc.l, kEvictNormal);
+                }
+                __syncwarp();
+                if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer =====
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int u = blockIdx.x; u < total; u += gridDim.x, ++it) {
+            const int acc = it & 1;
+            const uint32_t aph = (uint32_t)((it >> 1) & 1);
+            mbar_wait(&tempty[acc], aph ^ 1u);
+            tc_fence_after();
+            const uint32_t dtmem = tmem_base + (uint32_t)(acc * BN);
+            for (int kb = 0; kb < P.kblocks; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
+                    const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / 32; ++k)
+                        mma_i8(dtmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), IDESC,
+                               (kb | k) != 0 ? 1u : 0u);
+                    mma_commit(&empty[stage]);
+                }
+                __syncwarp();
+                if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+            }
+            if (lane == 0) mma_commit(&tfull[acc]);
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        // ===== Epilogue =====
+        const int wq = warp - 4;
+        int it = 0;
+        for (int u = blockIdx.x; u < total; u += gridDim.x, ++it) {
+            const TileCoord tc = decode_unit(u, P.tiles_m, P.tiles_n);
+            const int acc = it & 1;
+            const uint32_t aph = (uint32_t)((it >> 1) & 1);
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            const int row = tc.tm * BM + wq * 32 + lane;
+            int32_t rowmax = 0;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld32(tmem_base + ((uint32_t)(wq * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
+                tmem_ld_wait();
+                const int col0 = tc.tn * BN + c * 32;
+                if constexpr (MODE == EPI_MAX) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) rowmax = max(rowmax, (int32_t)v[j]);
+                }
+                epilogue_chunk<MODE>(v, row, col0, tc.l, P);
+            }
+            if constexpr (MODE == EPI_MAX) {
+                if (row < P.m) atomicMax(&P.rowmax[row], rowmax);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+    }
+
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 512);
+    }
+}
+
+}  // namespace
+
+int gemm_smem_bytes() { return SMEM_BYTES; }
+int gemm_tile_m() { return BM; }
+int gemm_tile_n() { return BN; }
+int gemm_tile_k() { return BK; }
+
+cudaError_t launch_gemm_i8(int mode, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& P,
+                           int num_sms, cudaStream_t stream) {
+    const int total = P.planes * P.tiles_m * P.tiles_n;
+    if (total == 0) return cudaSuccess;
+    const int grid = total < num_sms ? total : num_sms;
+    cudaError_t err = cudaSuccess;
+    switch (mode) {
+        case EPI_MAX:
+            err = cudaFuncSetAttribute(gemm_i8_tc_kernel<EPI_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       SMEM_BYTES);
+            if (err != cudaSuccess) return err;
+            gemm_i8_tc_kernel<EPI_MAX><<<grid, 256, SMEM_BYTES, stream>>>(tmA, tmB, P);
+            break;
+        case EPI_RESID:
+            err = cudaFuncSetAttribute(gemm_i8_tc_kernel<EPI_RESID>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+            if (err != cudaSuccess) return err;
+            gemm_i8_tc_kernel<EPI_RESID><<<grid, 256, SMEM_BYTES, stream>>>(tmA, tmB, P);
+            break;
+        default:
+            err = cudaFuncSetAttribute(gemm_i8_tc_kernel<EPI_I32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       SMEM_BYTES);
+            if (err != cudaSuccess) return err;
+            gemm_i8_tc_kernel<EPI_I32><<<grid, 256, SMEM_BYTES, stream>>>(tmA, tmB, P);
+            break;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace oz2g

@@ -1,0 +1,82 @@
+// kernels.h — host-visible launchers of the oz2g device stages.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace oz2g {
+
+struct DevStatus;
+
+enum GemmEpilogue { EPI_MAX = 0, EPI_RESID = 1, EPI_I32 = 2 };
+
+struct GemmParams {
+    int m, n;                 // valid output rows / columns
+    int kblocks;              // kp / 128
+    int planes;               // number of (A_l, B_l) pairs
+    int tiles_m, tiles_n;
+    // EPI_MAX
+    int32_t* rowmax;
+    int32_t* colmax;
+    // EPI_RESID: W[l*wplane + i*ldw + j]
+    int8_t* W;
+    int64_t ldw, wplane;
+    // EPI_I32: C32[l*cplane + i*ldc32 + j]
+    int32_t* C32;
+    int64_t ldc32, cplane;
+    uint32_t p[49], magic[49], off[49];
+};
+
+int gemm_smem_bytes();
+int gemm_tile_m();
+int gemm_tile_n();
+int gemm_tile_k();
+cudaError_t launch_gemm_i8(int mode, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& P,
+                           int num_sms, cudaStream_t stream);
+
+// Residue constants for the scaling kernels (uploaded once per table).
+struct ResidConsts {
+    int n;
+    uint32_t p[49], magic[49], c32[49];  // c32 = 2^32 mod p
+    uint8_t pow2[49][256];               // 2^E mod p, E in [0, 255]
+};
+
+// Stage launchers (scale.cu).  T = float or double inputs; prec selects.
+cudaError_t launch_row_scan_A(int prec, const void* A, int64_t lda, int64_t m, int64_t k, int64_t kp,
+                              int32_t* mu_prime, int8_t* abar, DevStatus* st, cudaStream_t s);
+cudaError_t launch_col_max_B(int prec, const void* B, int64_t ldb, int64_t k, int64_t n,
+                             unsigned long long* bmax, DevStatus* st, cudaStream_t s);
+cudaError_t launch_col_exp_B(const unsigned long long* bmax, int64_t n, int32_t* nu_prime, DevStatus* st,
+                             cudaStream_t s);
+cudaError_t launch_bbar_T(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp,
+                          const int32_t* nu_prime, int8_t* bbar_t, DevStatus* st, cudaStream_t s);
+cudaError_t launch_exponents(const int32_t* cmax_row, int64_t m, const int32_t* cmax_col, int64_t n,
+                             const int32_t* mu_prime, const int32_t* nu_prime, int shift0, int nthr,
+                             const int32_t* thr, int32_t* mu, int32_t* nu, float* e, float* f, DevStatus* st,
+                             cudaStream_t s);
+cudaError_t launch_resid_A(int prec, const void* A, int64_t lda, int64_t m, int64_t k, int64_t kp,
+                           const int32_t* mu, const ResidConsts* rc_dev, int nmod, int8_t* planes,
+                           DevStatus* st, cudaStream_t s);
+cudaError_t launch_resid_BT(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp,
+                            const int32_t* nu, const ResidConsts* rc_dev, int nmod, int8_t* planes,
+                            DevStatus* st, cudaStream_t s);
+cudaError_t launch_trunc_scaled(int prec, const void* X, int64_t ldx, int64_t rows, int64_t cols,
+                                const int32_t* shift, int by_col, double* out, cudaStream_t s);
+cudaError_t launch_log2f(const float* x, float* out, int64_t count, cudaStream_t s);
+
+// CRT + inverse scaling (crt.cu).
+struct CrtConsts {
+    int n, mode;
+    double s1[49], s2[49];
+    double P1, P2, P_inv;
+};
+struct CrtExtra {  // optional device outputs (nullptr = skip)
+    double *C1, *C2, *Q, *Cpp64;
+    float* Cpp32;
+};
+cudaError_t launch_crt(int prec, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
+                       const CrtConsts& cc, const int32_t* mu, const int32_t* nu, void* C, int64_t ldc,
+                       const CrtExtra& extra, DevStatus* st, cudaStream_t s);
+
+}  // namespace oz2g

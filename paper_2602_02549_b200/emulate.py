@@ -1,0 +1,249 @@
+"""Python mirror of the reference's public interface for the hot path.
+
+    os_ii(a, b, n, keep_intermediates=False) -> EmulationResult
+        /root/reference/proj/include/oz2/emulate.hpp:54-88
+    table_for(n, mode) -> ModuliTable            moduli.hpp:145-153
+    fp32_safe_moduli_max() -> int                moduli.hpp:157-170
+
+Same names, argument meaning and error behaviour as the reference: the
+exception classes below correspond one-to-one to std::invalid_argument,
+std::domain_error, std::range_error and std::logic_error.  Everything is
+computed by the native library (liboz2g.so, CUDA on sm_100a) through the C ABI;
+inputs may be host numpy arrays (copied in and out inside the call) or CUDA
+torch tensors (device pointers, no copies).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _lib
+
+F32, F64 = _lib.OZ2G_FP32, _lib.OZ2G_FP64
+K_MAX_INNER_DIM = 1 << 17
+K_MAX_MODULI = 49
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument (matrix.hpp:47-49)."""
+
+
+class DomainError(ValueError):
+    """std::domain_error (emulate.hpp:59, scaling.hpp:90/102, moduli.hpp:94)."""
+
+
+class RangeError(ArithmeticError):
+    """std::range_error (scaling.hpp:145/206/220, crt.hpp:144, emulate.hpp:39)."""
+
+
+class LogicError(RuntimeError):
+    """std::logic_error (scaling.hpp:67/77/179/189)."""
+
+
+class CudaError(RuntimeError):
+    """Device or driver failure (no reference counterpart)."""
+
+
+_EXC = {1: InvalidArgument, 2: DomainError, 3: RangeError, 4: LogicError, 5: CudaError}
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = _lib.load().oz2g_last_error().decode()
+        raise _EXC.get(rc, CudaError)(msg)
+
+
+@dataclass
+class ModuliTable:
+    """moduli.hpp:78-91 (P as a Python int)."""
+    n: int
+    mode: int
+    p: list
+    q: list
+    P: int
+    rho: int
+    P1: float
+    P2: float
+    P_inv: float
+    beta: list
+    s1: list
+    s2: list
+    P_prime: float
+    shift0: int = 0
+    thresholds: list = field(default_factory=list)
+
+
+def table_for(n: int, mode: int = F64) -> ModuliTable:
+    t = _lib.TableC()
+    _check(_lib.load().oz2g_table_for(int(n), int(mode), C.byref(t)))
+    k = t.n
+    return ModuliTable(n=k, mode=t.mode, p=list(t.p[:k]), q=list(t.q[:k]), P=int(t.P_dec.decode()), rho=t.rho,
+                       P1=t.P1, P2=t.P2, P_inv=t.P_inv, beta=list(t.beta[:k]), s1=list(t.s1[:k]),
+                       s2=list(t.s2[:k]), P_prime=t.P_prime, shift0=t.shift0, thresholds=list(t.thr[:t.nthr]))
+
+
+def fp32_safe_moduli_max() -> int:
+    return int(_lib.load().oz2g_fp32_safe_moduli_max())
+
+
+@dataclass
+class ScalingOutput:
+    """scaling.hpp:20-28 (+ the clearance maxima the device actually keeps)."""
+    mu: np.ndarray = None
+    nu: np.ndarray = None
+    mu_prime: np.ndarray = None
+    nu_prime: np.ndarray = None
+    e: np.ndarray = None
+    f: np.ndarray = None
+    Aprime: np.ndarray = None
+    Bprime: np.ndarray = None
+    Cbar: np.ndarray = None
+    Dbar: np.ndarray = None
+    cmax_row: np.ndarray = None
+    cmax_col: np.ndarray = None
+
+
+@dataclass
+class CrtIntermediates:
+    """crt.hpp:81-87 (+ residue planes and wrapped INT32 products)."""
+    W: np.ndarray = None
+    C1: np.ndarray = None
+    C2: np.ndarray = None
+    Q: np.ndarray = None
+    Cpp64: np.ndarray = None
+    Cpp32: np.ndarray = None
+    Ares: np.ndarray = None
+    Bres: np.ndarray = None
+    Cprod: np.ndarray = None
+
+
+@dataclass
+class EmulationResult:
+    """emulate.hpp:17-24."""
+    C: object
+    scaling: ScalingOutput
+    crt: CrtIntermediates
+    table: ModuliTable
+    subnormal: bool
+    kernels_launched: int = 0
+    stage_ms: tuple = ()
+
+
+def _is_torch_cuda(x) -> bool:
+    return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
+
+
+def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = False, out=None,
+          stream=None, timing: bool = False,
+          reduce_maxima: Optional[Callable] = None) -> EmulationResult:
+    """C ~ A*B by Ozaki-II accurate mode with `n` moduli (emulate.hpp:54-88).
+
+    `a`, `b`: 2-D float32/float64 numpy arrays (host) or CUDA torch tensors
+    (row-major, unit column stride).  The precision of the call follows the
+    dtype, like os_ii<float> / os_ii<double>.  `keep_intermediates` returns the
+    reference's ScalingOutput/CrtIntermediates fields; `evidence` also returns
+    the residue planes and wrapped INT32 products.  `reduce_maxima(row_ptr,
+    m, col_ptr, n, stream)` is the multi-GPU hook of oz2g.h.
+    """
+    L = _lib.load()
+    dev = _is_torch_cuda(a)
+    if dev != _is_torch_cuda(b):
+        raise InvalidArgument("os_ii: A and B must both be host arrays or both CUDA tensors")
+    if dev:
+        import torch
+        if a.dtype != b.dtype or a.dtype not in (torch.float32, torch.float64):
+            raise TypeError("os_ii: A and B must both be float32 or float64")
+        if a.dim() != 2 or b.dim() != 2:
+            raise InvalidArgument("os_ii: 2-D matrices expected")
+        if a.stride(1) != 1 or b.stride(1) != 1:
+            raise InvalidArgument("os_ii: unit column stride required (row-major)")
+        prec = F64 if a.dtype == torch.float64 else F32
+        m, k = a.shape
+        k2, nn = b.shape
+        if k != k2:
+            raise InvalidArgument("dimension mismatch: os_ii inner dimension")
+        C_out = out if out is not None else torch.empty((m, nn), dtype=a.dtype, device=a.device)
+        pa, pb, pc = a.data_ptr(), b.data_ptr(), C_out.data_ptr()
+        lda, ldb, ldc = max(a.stride(0), k), max(b.stride(0), nn), max(C_out.stride(0), nn)
+        flags = _lib.OZ2G_DEVICE_PTRS
+        if stream is None:
+            stream = torch.cuda.current_stream(a.device).cuda_stream
+    else:
+        a = np.asarray(a)
+        b = np.asarray(b)
+        if a.dtype != b.dtype or a.dtype not in (np.float32, np.float64):
+            raise TypeError("os_ii: A and B must both be float32 or float64")
+        if a.ndim != 2 or b.ndim != 2:
+            raise InvalidArgument("os_ii: 2-D matrices expected")
+        if a.shape[1] != b.shape[0]:
+            raise InvalidArgument("dimension mismatch: os_ii inner dimension")
+        a = np.ascontiguousarray(a)
+        b = np.ascontiguousarray(b)
+        prec = F64 if a.dtype == np.float64 else F32
+        m, k = a.shape
+        nn = b.shape[1]
+        C_out = np.empty((m, nn), dtype=a.dtype) if out is None else out
+        pa, pb, pc = a.ctypes.data, b.ctypes.data, C_out.ctypes.data
+        lda, ldb, ldc = k, nn, nn
+        flags = _lib.OZ2G_HOST_PTRS
+    if timing:
+        flags |= _lib.OZ2G_TIMING
+
+    inter_c = None
+    sc, cr = ScalingOutput(), CrtIntermediates()
+    keep = {}
+    if keep_intermediates or evidence:
+        inter_c = _lib.Intermediates()
+        N = int(n)
+        spec = dict(mu=(sc, (m,), np.int16), nu=(sc, (nn,), np.int16), mu_prime=(sc, (m,), np.int16),
+                    nu_prime=(sc, (nn,), np.int16), e=(sc, (m,), np.float32), f=(sc, (nn,), np.float32),
+                    cmax_row=(sc, (m,), np.int32), cmax_col=(sc, (nn,), np.int32))
+        if keep_intermediates:
+            spec.update(Aprime=(sc, (m, k), np.float64), Bprime=(sc, (k, nn), np.float64),
+                        Cbar=(sc, (m, nn), np.int32), Dbar=(sc, (m, nn), np.float32),
+                        W=(cr, (N, m, nn), np.int8), C1=(cr, (m, nn), np.float64), C2=(cr, (m, nn), np.float64),
+                        Q=(cr, (m, nn), np.float64), Cpp64=(cr, (m, nn), np.float64))
+            if prec == F32:
+                spec["Cpp32"] = (cr, (m, nn), np.float32)
+        if evidence:
+            spec.update(W=(cr, (N, m, nn), np.int8), Ares=(cr, (N, m, k), np.int8),
+                        Bres=(cr, (N, k, nn), np.int8), Cprod=(cr, (N, m, nn), np.int32))
+        if 2 <= N <= K_MAX_MODULI:
+            for name, (holder, shape, dt) in spec.items():
+                arr = np.zeros(shape, dtype=dt)
+                keep[name] = (holder, arr)
+                setattr(inter_c, name, arr.ctypes.data)
+
+    diag = _lib.Diag()
+    if reduce_maxima is not None:
+        def _cb(rp, mm, cp, nn2, st, user):
+            try:
+                reduce_maxima(rp, mm, cp, nn2, st)
+                return 0
+            except Exception:  # pragma: no cover - reported as a status code
+                import traceback
+                traceback.print_exc()
+                return 1
+        cb = _lib.REDUCE_FN(_cb)
+    else:
+        cb = _lib.REDUCE_FN()
+    rc = L.oz2g_gemm(prec, m, nn, k, pa, lda, pb, ldb, pc, ldc, int(n), flags,
+                     C.c_void_p(int(stream) if stream else 0),
+                     C.byref(inter_c) if inter_c is not None else None, C.byref(diag), cb, None)
+    _check(rc)
+    for name, (holder, arr) in keep.items():
+        setattr(holder, name, arr)
+    return EmulationResult(C=C_out, scaling=sc, crt=cr, table=table_for(n, prec), subnormal=bool(diag.subnormal),
+                           kernels_launched=diag.kernels_launched, stage_ms=tuple(diag.stage_ms))
+
+
+def device_log2f(x_dev, out_dev, stream=None) -> None:
+    """Device log2f used for the e/f diagnostics (tests compare it with libm)."""
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(x_dev.device).cuda_stream
+    _check(_lib.load().oz2g_device_log2f(x_dev.data_ptr(), out_dev.data_ptr(), x_dev.numel(),
+                                         C.c_void_p(int(stream))))

@@ -1,0 +1,87 @@
+"""GPU parity: the CUDA product path (through the C ABI) vs the CPU oracle.
+
+Bit-exact on every integer/byte stage (mu', nu', clearance maxima, mu, nu,
+residue planes, wrapped INT32 products, W) and on the final C (0 ulp: the
+fp64 stages are the reference's own RN operation sequence).
+"""
+import numpy as np
+import pytest
+
+import paper_2602_02549_b200 as oz
+
+pytestmark = pytest.mark.gpu
+
+
+def _eq(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    assert a.shape == b.shape
+    if a.dtype.kind == "f":
+        ok = np.array_equal(a.view(np.uint8), b.view(np.uint8)) or np.array_equal(a, b)
+    else:
+        ok = np.array_equal(a, b)
+    if not ok:
+        bad = np.argwhere(a != b)
+        raise AssertionError(f"{bad.shape[0]} mismatches, first at {bad[:5].tolist()}: "
+                             f"{a[tuple(bad[0])]} vs {b[tuple(bad[0])]}")
+
+
+def test_unit_product_trace(cuda, oracle):
+    # test_emulate.cpp:13-20: mu = nu = 7, A' = B' = 128, W = (0, 64), C1 = 16384, Q = 0, C = 1
+    for dt in (np.float64, np.float32):
+        one = np.ones((1, 1), dtype=dt)
+        r = oz.os_ii(one, one, 2, keep_intermediates=True)
+        assert r.C[0, 0] == 1.0
+        assert r.scaling.mu[0] == 7 and r.scaling.nu[0] == 7
+        assert r.crt.W[:, 0, 0].tolist() == [0, 64]
+        assert r.crt.C1[0, 0] == 16384.0 and r.crt.Q[0, 0] == 0.0 and r.crt.Cpp64[0, 0] == 16384.0
+        for n in (10, 30, 49) if dt == np.float64 else (10, 16):
+            c = oz.os_ii(one, one, n).C[0, 0]
+            assert abs(float(c) - 1.0) <= (2.0 ** -40 if dt == np.float64 else 2.0 ** -18)
+
+
+CASES = [
+    # (m, k, n, phi, N, dtype)
+    (7, 20, 6, 0.0, 2, np.float64),
+    (7, 20, 6, 4.0, 16, np.float64),
+    (7, 20, 6, 4.0, 49, np.float64),
+    (33, 100, 65, 0.5, 14, np.float64),
+    (130, 300, 260, 2.0, 14, np.float64),
+    (64, 1024, 64, 0.0, 16, np.float64),
+    (200, 129, 300, 8.0, 20, np.float64),
+    (7, 20, 6, 0.0, 9, np.float32),
+    (33, 100, 65, 0.5, 8, np.float32),
+    (130, 300, 260, 2.0, 16, np.float32),
+]
+
+
+@pytest.mark.parametrize("m,k,n,phi,N,dt", CASES)
+def test_os_ii_bit_parity(cuda, oracle, m, k, n, phi, N, dt):
+    seed = 1000 * m + 10 * k + n
+    A = oracle.gen_matrix(m, k, phi, oracle.derive_seed(seed, 0, 0), dt)
+    B = oracle.gen_matrix(k, n, phi, oracle.derive_seed(seed, 0, 1), dt)
+    ref = oracle.os_ii(A, B, N, keep_intermediates=True, residues=True)
+    got = oz.os_ii(A, B, N, keep_intermediates=True, evidence=True)
+    s, c, ri = got.scaling, got.crt, ref.inter
+    _eq(s.mu_prime, ri["mu_prime"])
+    _eq(s.nu_prime, ri["nu_prime"])
+    _eq(s.Cbar, ri["Cbar"])
+    _eq(s.Dbar, ri["Dbar"])
+    _eq(s.mu, ri["mu"])
+    _eq(s.nu, ri["nu"])
+    _eq(s.e, ri["e"])
+    _eq(s.f, ri["f"])
+    _eq(s.Aprime, ri["Aprime"])
+    _eq(s.Bprime, ri["Bprime"])
+    _eq(c.Ares, ri["Ares"])
+    _eq(c.Bres, ri["Bres"])
+    _eq(c.Cprod, ri["Cprod"])
+    _eq(c.W, ri["W"])
+    _eq(c.C1, ri["C1"])
+    _eq(c.C2, ri["C2"])
+    _eq(c.Q, ri["Q"])
+    _eq(c.Cpp64, ri["Cpp64"])
+    if dt == np.float32:
+        _eq(c.Cpp32, ri["Cpp32"])
+    _eq(got.C, ref.C)
+    assert got.subnormal == ref.subnormal
