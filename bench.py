@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native Ozaki-II emulated DGEMM (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[3], the metric's own config): emulated DGEMM
+m = n = k = 16384 with N = 16 moduli (the smallest N whose tight bound
+certifies 1e-15 relative to |A||B| at phi = 0), uniform-exponent
+synthetic inputs (phi = 0, entries (u - 1/2), the reference generator's
+distribution, gen.hpp:15-31).  Inputs are 2 GiB each, larger than L2, so no
+flush is needed between steps.
+
+One step = one full os_ii call (scaling, clearance GEMM, residues, N residue
+GEMMs, CRT, inverse scaling).  `value` is device-timed with inputs resident in
+HBM; `e2e` is the same call through the public API with pinned HOST buffers
+(host->device copies of A, B and the device->host copy of C inside the timed
+region).  N > 1 GPUs: C is tiled 2-D over the ranks (strong scaling, SURVEY
+§8e); the clearance maxima are max-reduced over the row / column groups with
+NCCL through the library's reduce hook; time is the max over ranks.
+
+`--impl reference` times the reference algorithm on the host cores instead
+(the CPU oracle port, all threads) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "emulated DGEMM TFLOPS (m=n=k=16384) vs moduli N; max rel err vs bound"
+UNIT = "TFLOP/s"
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def _grid(world: int):
+    """2-D rank grid R x Cc for the output tiles (2x4 at 8 GPUs)."""
+    return {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (2, 4)}.get(world, (world, 1))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"oz2g_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 8 and parts[0].replace(".", "").isdigit():
+                    rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in rows)
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for name, val in zip(names, r[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]), "samples": len(rows),
+                "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit()),
+                "reasons": sorted(reasons)}
+
+
+def gen_device(rows, cols, phi, seed, dtype, device):
+    """The reference generator's distribution, (u - 1/2) * exp(g * phi) with
+    u uniform on (0, 1] and g standard normal (gen.hpp:15-31), drawn on the GPU
+    (torch Philox stream, not the reference's xoshiro stream — parity tests use
+    the exact host stream; the benchmark only needs the distribution)."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    u = torch.rand((rows, cols), dtype=torch.float64, device=device, generator=g)
+    u = 1.0 - u  # (0, 1]
+    v = u - 0.5
+    if phi:
+        v = v * torch.exp(torch.randn((rows, cols), dtype=torch.float64, device=device, generator=g) * phi)
+    v = v.to(dtype)
+    v[v == 0] = 0.25  # the reference redraws zeros; any nonzero keeps rows/cols nonzero
+    return v.contiguous()
+
+
+def cpu_baseline(sample_m: int, sample_n: int, k: int, nmod: int, phi: float, threads: int):
+    """The oracle port (oracle/oz2_oracle.c, restating os_ii) on host cores."""
+    from oracle import oracle as O
+    O.set_threads(threads)
+    A = O.gen_matrix(sample_m, k, phi, O.derive_seed(1, 0, 0))
+    B = O.gen_matrix(k, sample_n, phi, O.derive_seed(1, 0, 1))
+    t0 = time.perf_counter()
+    O.os_ii(A, B, nmod)
+    dt = time.perf_counter() - t0
+    return 2.0 * sample_m * sample_n * k / dt / 1e12, dt
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    m_s = args.cpu_sample
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(m_s, m_s, args.k, args.moduli, args.phi, threads)
+    t_all = 0.0
+    for _ in range(args.steps):
+        v, dt = cpu_baseline(m_s, m_s, args.k, args.moduli, args.phi, threads)
+        vals.append(v)
+        t_all += dt
+    value = float(np.median(vals))
+    sample = f"os_ii on A {m_s}x{args.k} * B {args.k}x{m_s} (full k), N={args.moduli}, phi={args.phi}"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / max(args.steps, 1),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator gen.hpp, xoshiro256** stream)",
+        "config": {"workload": f"Ozaki-II emulated DGEMM m=n=k={args.m}, N={args.moduli} moduli, phi={args.phi}",
+                   "m": args.m, "n": args.m, "k": args.k, "moduli": args.moduli, "phi": args.phi},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--m", type=int, default=16384)
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--moduli", type=int, default=16)
+    ap.add_argument("--phi", type=float, default=0.0)
+    ap.add_argument("--cpu-sample", type=int, default=96, help="rows/cols of the bounded CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-native", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.k is None:
+        args.k = args.m
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_02549_b200 as oz
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    R, Cc = _grid(world)
+    r, c = rank // Cc, rank % Cc
+    m = n = args.m
+    k = args.k
+    mb = (m + R - 1) // R
+    nb = (n + Cc - 1) // Cc
+    rows = slice(r * mb, min(m, (r + 1) * mb))
+    cols = slice(c * nb, min(n, (c + 1) * nb))
+
+    # global inputs from one seed, then this rank's blocks (inputs pre-distributed)
+    A_full = gen_device(m, k, args.phi, 1234, torch.float64, dev)
+    B_full = gen_device(k, n, args.phi, 5678, torch.float64, dev)
+    A = A_full[rows].contiguous()
+    B = B_full[:, cols].contiguous()
+    del A_full, B_full
+    Cout = torch.empty((A.shape[0], B.shape[1]), dtype=torch.float64, device=dev)
+
+    reduce_cb = None
+    if world > 1:
+        row_groups = [dist.new_group([rr * Cc + cc for cc in range(Cc)]) for rr in range(R)]
+        col_groups = [dist.new_group([rr * Cc + cc for rr in range(R)]) for cc in range(Cc)]
+
+        class _Dev:
+            def __init__(self, ptr, cnt):
+                self.__cuda_array_interface__ = {"shape": (cnt,), "typestr": "<i4", "data": (ptr, False),
+                                                 "version": 3, "strides": None}
+
+        def reduce_cb(rp, mm, cp, nn, st):
+            if mm:
+                dist.all_reduce(torch.as_tensor(_Dev(rp, mm), device=dev), op=dist.ReduceOp.MAX, group=row_groups[r])
+            if nn:
+                dist.all_reduce(torch.as_tensor(_Dev(cp, nn), device=dev), op=dist.ReduceOp.MAX, group=col_groups[c])
+
+    stream = torch.cuda.current_stream(dev)
+
+    def step(timing=False):
+        return oz.os_ii(A, B, args.moduli, out=Cout, timing=timing, reduce_maxima=reduce_cb)
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+
+    # per-stage CUDA-event times (one instrumented step, outside the timed loop)
+    stage = step(timing=True).stage_ms
+    launches_per_step = res.kernels_launched
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    # ---- device-timed region ----
+    sampler = ClockSampler(local)
+    barrier()
+    with sampler:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    t_ms = ev0.elapsed_time(ev1)
+    # instrumented steps for the dominant kernel (residue GEMMs), same stream
+    gemm_ms = []
+    for _ in range(3):
+        gemm_ms.append(step(timing=True).stage_ms[5])
+    t_tensor = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_tensor, op=dist.ReduceOp.MAX)
+    t_ms = float(t_tensor.item())
+    ms_per_step = t_ms / args.steps
+    flops = 2.0 * m * n * k
+    value = flops / (ms_per_step * 1e-3) / 1e12
+
+    # ---- end-to-end through the public API with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        A_h = torch.empty(A.shape, dtype=torch.float64, pin_memory=True)
+        B_h = torch.empty(B.shape, dtype=torch.float64, pin_memory=True)
+        C_h = torch.empty(Cout.shape, dtype=torch.float64, pin_memory=True)
+        A_h.copy_(A)
+        B_h.copy_(B)
+        a_np, b_np, c_np = A_h.numpy(), B_h.numpy(), C_h.numpy()
+        oz.os_ii(a_np, b_np, args.moduli, out=c_np, reduce_maxima=reduce_cb)  # warm
+        barrier()
+        e_steps = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            oz.os_ii(a_np, b_np, args.moduli, out=c_np, reduce_maxima=reduce_cb)
+        barrier()
+        te = torch.tensor([(time.perf_counter() - t0) / e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": flops / float(te.item()) / 1e12, "unit": UNIT,
+               "h2d_bytes_per_step": int(8 * (A.numel() + B.numel()) * world),
+               "d2h_bytes_per_step": int(8 * Cout.numel() * world),
+               "timing": "wall clock around blocking os_ii calls (host pointers; copies inside)"}
+        if not torch.equal(torch.from_numpy(c_np).to(dev), Cout):
+            e2e["mismatch_vs_device_path"] = True
+
+    # ---- native cuBLAS DGEMM on the same box (the bar to beat) + error ----
+    native = None
+    err = None
+    if not args.no_native and world == 1:
+        Cn = torch.matmul(A, B)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(3):
+            torch.matmul(A, B, out=Cn)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        native = flops / (e0.elapsed_time(e1) / 3 * 1e-3) / 1e12
+        absAB = torch.matmul(A.abs(), B.abs())
+        err = {"max_abs_diff_vs_native_rel_absAB": float(((Cout - Cn).abs() / absAB).max().item()),
+               "note": "vs native fp64 GEMM (itself inexact); double-double reference is future work"}
+        del Cn, absAB
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks, peak_kind = _peaks()
+    # dominant kernel: the N residue GEMMs (one launch); algorithmic int8 ops = 2*N*m_loc*n_loc*k
+    ops = 2.0 * args.moduli * A.shape[0] * B.shape[1] * k
+    gemm_avg = float(np.mean(gemm_ms))
+    achieved = ops / (gemm_avg * 1e-3) / 1e12
+    int8_peak = 2.0 * peaks["bf16_tflops"]
+    roof = {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s", "frac": achieved / int8_peak,
+            "traffic": None, "kernel": "gemm_i8_tc_kernel<EPI_RESID> (N residue GEMMs, one launch)",
+            "peak_note": f"dense INT8 = 2 x {peak_kind} bf16 burst ({peaks['bf16_tflops']} TF/s); int8 ops counted as FLOPs",
+            "algorithmic_ops_per_launch": ops, "launch_ms": gemm_avg}
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        threads = os.cpu_count() or 1
+        v, dt = cpu_baseline(args.cpu_sample, args.cpu_sample, k, args.moduli, args.phi, threads)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"oracle os_ii on A {args.cpu_sample}x{k} * B {k}x{args.cpu_sample}, N={args.moduli} ({dt:.1f} s)"}
+
+    names = ["h2d", "scale", "clearance_gemm", "exponents", "residues", "residue_gemms", "crt_unscale", "d2h"]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator distribution, phi=0 uniform exponent; drawn on device)",
+        "config": {"workload": f"Ozaki-II emulated DGEMM m=n=k={m}" + (f" (k={k})" if k != m else "")
+                   + f", N={args.moduli} moduli, phi={args.phi}", "m": m, "n": n, "k": k,
+                   "moduli": args.moduli, "phi": args.phi, "parallelism": f"2d-tile {R}x{Cc}",
+                   "l2": "inputs 2 GiB each > L2, no flush"},
+        "clocks": sampler.summary(),
+        "e2e": e2e,
+        "gpu_launches": launches_per_step * args.steps,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "stages_ms": {nm: round(v, 4) for nm, v in zip(names, stage)},
+        "native_dgemm_tflops": native,
+        "accuracy": err,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
