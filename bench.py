@@ -48,11 +48,6 @@ def _peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
-def _grid(world: int):
-    """2-D rank grid R x Cc for the output tiles (2x4 at 8 GPUs)."""
-    return {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (2, 4)}.get(world, (world, 1))
-
-
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -188,6 +183,8 @@ def main():
 
     import paper_2602_02549_b200 as oz
 
+    from paper_2602_02549_b200 import dist as pdist
+
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -195,14 +192,11 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    R, Cc = _grid(world)
-    r, c = rank // Cc, rank % Cc
     m = n = args.m
     k = args.k
-    mb = (m + R - 1) // R
-    nb = (n + Cc - 1) // Cc
-    rows = slice(r * mb, min(m, (r + 1) * mb))
-    cols = slice(c * nb, min(n, (c + 1) * nb))
+    tile = pdist.tile_of(rank, world, m, n)
+    R, Cc = tile.R, tile.C
+    rows, cols = tile.rows, tile.cols
 
     # global inputs from one seed, then this rank's blocks (inputs pre-distributed)
     A_full = gen_device(m, k, args.phi, 1234, torch.float64, dev)
@@ -214,19 +208,8 @@ def main():
 
     reduce_cb = None
     if world > 1:
-        row_groups = [dist.new_group([rr * Cc + cc for cc in range(Cc)]) for rr in range(R)]
-        col_groups = [dist.new_group([rr * Cc + cc for rr in range(R)]) for cc in range(Cc)]
-
-        class _Dev:
-            def __init__(self, ptr, cnt):
-                self.__cuda_array_interface__ = {"shape": (cnt,), "typestr": "<i4", "data": (ptr, False),
-                                                 "version": 3, "strides": None}
-
-        def reduce_cb(rp, mm, cp, nn, st):
-            if mm:
-                dist.all_reduce(torch.as_tensor(_Dev(rp, mm), device=dev), op=dist.ReduceOp.MAX, group=row_groups[r])
-            if nn:
-                dist.all_reduce(torch.as_tensor(_Dev(cp, nn), device=dev), op=dist.ReduceOp.MAX, group=col_groups[c])
+        row_groups, col_groups = pdist.make_groups(dist, world)
+        reduce_cb = pdist.max_reduce_hook(dist, tile, row_groups, col_groups, dev)
 
     stream = torch.cuda.current_stream(dev)
 

@@ -110,22 +110,31 @@ CUtensorMap make_plane_map(const void* base, int64_t kp, int64_t rows, int64_t p
     return tm;
 }
 
-ResidConsts build_resid_consts(const Table& t) {
-    ResidConsts rc;
-    std::memset(&rc, 0, sizeof rc);
-    rc.n = t.n;
+std::vector<uint8_t> build_resid_consts(const Table& t) {
+    std::vector<uint8_t> buf(resid_consts_bytes(t.n), 0);
+    ResidHeader* h = reinterpret_cast<ResidHeader*>(buf.data());
+    h->n = t.n;
+    uint32_t* tab = reinterpret_cast<uint32_t*>(buf.data() + sizeof(ResidHeader));
     for (int l = 0; l < t.n; ++l) {
         const uint32_t p = (uint32_t)t.p[l];
-        rc.p[l] = p;
-        rc.magic[l] = (uint32_t)(0x100000000ull / p);
-        rc.c32[l] = (uint32_t)(0x100000000ull % p);
-        uint32_t v = 1 % p;
-        for (int e = 0; e < 256; ++e) {
-            rc.pow2[l][e] = (uint8_t)v;
-            v = (v * 2u) % p;
+        h->p[l] = p;
+        h->magic[l] = (uint32_t)((0x100000000ull + p - 1) / p);  // ceil(2^32 / p)
+        h->offh[l] = p * (((1u << 18) + p - 1) / p) + p / 2;
+        h->h4[l] = (p / 2) * 0x01010101u;
+        for (int E = 0; E < kResidE; ++E) {
+            uint32_t w[8];
+            for (int b = 0; b < 8; ++b) {  // symmetric representative of 2^(8b + E) mod p, as a byte
+                uint32_t v = 1 % p;
+                for (int s = 0; s < 8 * b + E; ++s) v = (v * 2u) % p;
+                const int rep = (2 * v > p) ? (int)v - (int)p : (int)v;  // p = 256: 128 stays (byte -128)
+                w[b] = (uint32_t)rep & 0xffu;
+            }
+            uint32_t* cell = tab + 2 * ((size_t)l * kResidE + E);  // layout [l][E]: lanes with different E hit different banks
+            cell[0] = w[0] | (w[1] << 8) | (w[2] << 16) | (w[3] << 24);
+            cell[1] = w[4] | (w[5] << 8) | (w[6] << 16) | (w[7] << 24);
         }
     }
-    return rc;
+    return buf;
 }
 
 void fill_gemm_moduli(GemmParams& P, const Table& t) {
@@ -279,10 +288,10 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     const int N = tab.n;
     const auto key = std::make_pair(tab.n, tab.mode);
     if (!ws.rc.count(key)) {
-        const ResidConsts h = build_resid_consts(tab);
+        const std::vector<uint8_t> h = build_resid_consts(tab);
         ResidConsts* d = nullptr;
-        CUDA_TRY(cudaMalloc(&d, sizeof(ResidConsts)));
-        CUDA_TRY(cudaMemcpy(d, &h, sizeof h, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMalloc(&d, h.size()));
+        CUDA_TRY(cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice));
         ws.rc[key] = d;
     }
     const ResidConsts* rc_dev = ws.rc[key];

@@ -21,37 +21,54 @@ namespace oz2g {
 
 namespace {
 
-template <class T>
+constexpr int CV = 8;  // consecutive columns per thread (one 8-byte load per modulus plane)
+
+template <class T, bool DD>
 __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, int64_t ldw, int64_t wplane,
                                                   int64_t m, int64_t n, const CrtConsts cc,
                                                   const int32_t* __restrict__ mu, const int32_t* __restrict__ nu,
                                                   T* __restrict__ C, int64_t ldc, const CrtExtra ex,
                                                   DevStatus* st) {
-    // 4 consecutive columns per thread: one 32-bit load per modulus plane
-    const int64_t qn = (n + 3) / 4;
+    const int64_t qn = (n + CV - 1) / CV;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= m * qn) return;
     const int64_t i = t / qn;
-    const int64_t j0 = (t - i * qn) * 4;
-    const int jn = (int)(n - j0 < 4 ? n - j0 : 4);
-    double c1[4] = {0.0, 0.0, 0.0, 0.0}, c2[4] = {0.0, 0.0, 0.0, 0.0};
-    const bool dd = cc.mode == 1;
-    const int8_t* wp = W + i * ldw + j0;
-    for (int l = 0; l < cc.n; ++l) {
-        const uint32_t word = __ldg(reinterpret_cast<const uint32_t*>(wp + (int64_t)l * wplane));
+    const int64_t j0 = (t - i * qn) * CV;
+    const int jn = (int)(n - j0 < CV ? n - j0 : CV);
+    double c1[CV], c2[CV];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const double wv = (double)(int8_t)((word >> (8 * b)) & 0xffu);
-            c1[b] = __fma_rn(cc.s1[l], wv, c1[b]);
-            if (dd) c2[b] = __fma_rn(cc.s2[l], wv, c2[b]);
+    for (int b = 0; b < CV; ++b) { c1[b] = 0.0; c2[b] = 0.0; }
+    const int8_t* wp = W + i * ldw + j0;
+    // crt.hpp:99-104: acc = fma(s_l, W_l, acc) in the fixed order l = 0..N-1.
+    // Loads are issued 4 planes ahead of their use to keep HBM busy.
+    auto fold = [&](const uint2 word, int l) {
+        const double s1 = cc.s1[l];
+        const double s2 = cc.s2[l];
+#pragma unroll
+        for (int b = 0; b < CV; ++b) {
+            const uint32_t w32 = b < 4 ? word.x : word.y;
+            const double wv = (double)(int8_t)((w32 >> (8 * (b & 3))) & 0xffu);
+            c1[b] = __fma_rn(s1, wv, c1[b]);
+            if (DD) c2[b] = __fma_rn(s2, wv, c2[b]);
         }
+    };
+    int l = 0;
+    for (; l + 4 <= cc.n; l += 4) {
+        uint2 wv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) wv[u] = __ldg(reinterpret_cast<const uint2*>(wp + (int64_t)(l + u) * wplane));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) fold(wv[u], l + u);
     }
+    for (; l < cc.n; ++l) fold(__ldg(reinterpret_cast<const uint2*>(wp + (int64_t)l * wplane)), l);
     const int mui = mu[i];
     bool fr_range = false, inv_range = false, sub = false;
-    for (int b = 0; b < jn; ++b) {
+#pragma unroll
+    for (int b = 0; b < CV; ++b) {
+        if (b >= jn) break;
         const int64_t j = j0 + b;
-        const double q = rint(__dmul_rn(cc.P_inv, c1[b]));
-        const double t1 = __fma_rn(-q, cc.P1, c1[b]);
+        const double q = rint(__dmul_rn(cc.P_inv, c1[b]));   // crt.hpp:113-119
+        const double t1 = __fma_rn(-q, cc.P1, c1[b]);         // crt.hpp:136-138
         const double t2 = __dadd_rn(t1, c2[b]);
         const double cpp = __fma_rn(-q, cc.P2, t2);
         const int64_t o = i * n + j;
@@ -59,12 +76,12 @@ __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, 
         if (ex.C2) ex.C2[o] = c2[b];
         if (ex.Q) ex.Q[o] = q;
         if (ex.Cpp64) ex.Cpp64[o] = cpp;
-        const int nuj = nu[j];
+        const int nuj = __ldg(nu + j);
         if constexpr (sizeof(T) == 4) {
-            if (cc.mode == 0 && fabs(cpp) >= 0x1.ffffffp+127) { fr_range = true; continue; }
+            if (fabs(cpp) >= 0x1.ffffffp+127) { fr_range = true; continue; }  // crt.hpp:144-145
             const float c32 = __double2float_rn(cpp);
             if (ex.Cpp32) ex.Cpp32[o] = c32;
-            const float x = ldexpf_rn(c32, -mui);
+            const float x = ldexpf_rn(c32, -mui);                             // emulate.hpp:37-38
             const float y = ldexpf_rn(x, -nuj);
             inv_range |= !isfinite(x) || !isfinite(y);
             sub |= (x != 0.0f && fabsf(x) < FLT_MIN) || (y != 0.0f && fabsf(y) < FLT_MIN);
@@ -87,11 +104,15 @@ __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, 
 cudaError_t launch_crt(int prec, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
                        const CrtConsts& cc, const int32_t* mu, const int32_t* nu, void* C, int64_t ldc,
                        const CrtExtra& extra, DevStatus* st, cudaStream_t s) {
-    const int64_t work = m * ((n + 3) / 4);
+    const int64_t work = m * ((n + CV - 1) / CV);
     if (work == 0) return cudaSuccess;
     const unsigned grid = (unsigned)((work + 255) / 256);
-    if (prec) crt_kernel<double><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, (double*)C, ldc, extra, st);
-    else crt_kernel<float><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, (float*)C, ldc, extra, st);
+    if (prec) {
+        if (cc.mode == 1) crt_kernel<double, true><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, (double*)C, ldc, extra, st);
+        else crt_kernel<double, false><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, (double*)C, ldc, extra, st);
+    } else {
+        crt_kernel<float, false><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, (float*)C, ldc, extra, st);
+    }
     return cudaGetLastError();
 }
 

@@ -64,6 +64,25 @@ __device__ __forceinline__ int ilogb_exact(double x) {
     return e2 + 52;
 }
 
+// ceil(2^sft |a|) exactly (scaling.hpp:61-79); -1 on the logic_error paths.
+__device__ __forceinline__ int ceil_abs_scaled(double a, int sft) {
+    if (a == 0.0) return 0;
+    uint64_t mant; int e2;
+    decompose(a, mant, e2);
+    const int exp2 = e2 + sft;  // == e - 53 + sft with frexp's e = e2 + 53
+    if (exp2 >= 0) return -1;
+    const int s = -exp2;
+    uint64_t v;
+    if (s >= 53) {
+        v = 1;  // 0 < 2^sft |a| < 1
+    } else {
+        const uint64_t q = mant >> s;
+        const uint64_t rem = mant & ((1ull << s) - 1);
+        v = q + (rem != 0 ? 1 : 0);
+    }
+    return v > 64 ? -1 : (int)v;
+}
+
 // 2^s as a double for s in [-1022, 1023].
 __device__ __forceinline__ double pow2d(int s) { return __longlong_as_double((long long)(s + 1023) << 52); }
 __device__ __forceinline__ float pow2f(int s) { return __int_as_float((s + 127) << 23); }
@@ -71,6 +90,9 @@ __device__ __forceinline__ float pow2f(int s) { return __int_as_float((s + 127) 
 // RN(x * 2^s) with a single rounding: glibc ldexp/scalbn semantics used by
 // inverse_scale (emulate.hpp:37-38).
 __device__ __forceinline__ double ldexp_rn(double x, int s) {
+    // 2^s normal: one multiplication is one RN rounding of the exact x*2^s
+    // (exact unless the result is subnormal, inf on overflow) == scalbn.
+    if (s >= -1022 && s <= 1023) return __dmul_rn(x, pow2d(s));
     if (x == 0.0 || !isfinite(x)) return x;
     const int ex = ilogb_exact(x);
     const int et = ex + s;
@@ -102,6 +124,7 @@ __device__ __forceinline__ int ilogbf_exact(float x) {
 
 // RN(x * 2^s) for float (std::ldexp(float, int) == scalbnf).
 __device__ __forceinline__ float ldexpf_rn(float x, int s) {
+    if (s >= -126 && s <= 127) return __fmul_rn(x, pow2f(s));
     if (x == 0.0f || !isfinite(x)) return x;
     const int ex = ilogbf_exact(x);
     const int et = ex + s;

@@ -35,12 +35,20 @@ int gemm_tile_k();
 cudaError_t launch_gemm_i8(int mode, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& P,
                            int num_sms, cudaStream_t stream);
 
-// Residue constants for the scaling kernels (uploaded once per table).
-struct ResidConsts {
-    int n;
-    uint32_t p[49], magic[49], c32[49];  // c32 = 2^32 mod p
-    uint8_t pow2[49][256];               // 2^E mod p, E in [0, 255]
+// Residue constants for the residue kernels (uploaded once per table): a
+// header followed by the weight table w[E][l] (E in [0, 255]) of two packed
+// words whose signed bytes are the symmetric representatives of
+// 2^(8t + E) mod p_l, t = 0..7 (resid.cu explains the arithmetic).
+struct ResidHeader {
+    int n, pad;
+    uint32_t p[49];
+    uint32_t magic[49];  // ceil(2^32 / p): floor(U / p) == umulhi(U, magic) for U < 2^24
+    uint32_t offh[49];   // p * ceil(2^18 / p) + floor(p / 2)
+    uint32_t h4[49];     // floor(p / 2) replicated in 4 bytes
 };
+constexpr int kResidE = 256;
+__host__ __device__ inline size_t resid_consts_bytes(int n) { return sizeof(ResidHeader) + (size_t)kResidE * n * 8; }
+typedef ResidHeader ResidConsts;
 
 // Stage launchers (scale.cu).  T = float or double inputs; prec selects.
 cudaError_t launch_row_scan_A(int prec, const void* A, int64_t lda, int64_t m, int64_t k, int64_t kp,

@@ -1,0 +1,294 @@
+// resid.cu — the residue split of Algorithm 3 fused with the truncation of
+// Algorithm 2, and the transposed writer of Bbar:
+//
+//   resid_A      truncate_scaled_rows (scaling.hpp:199-211) + residue_matrix
+//                (crt.hpp:20-65) for every modulus: A' = trunc(2^mu A) is never
+//                materialised; each element is decomposed once and all N int8
+//                planes [l][m][kp] (K-major) are written in the same pass.
+//   resid_BT     the same for B (truncate_scaled_cols, scaling.hpp:213-225),
+//                written transposed to K-major planes [l][n][kp].
+//   bbar_T       ceil_abs_scale_cols (scaling.hpp:122-131) -> Bbar^T [n][kp].
+//
+// Residue arithmetic.  |A'| = m' * 2^E' with m' < 2^53 (m' = mant >> -E if
+// E < 0, E' = max(E, 0)).  With the signed byte weights
+//   w[E'][l][t] = symmetric representative of 2^(8t + E') mod p_l (|w| <= 128),
+//   S = sum_t byte_t(m') * w[E'][l][t]          (two dp4a.u32.s32, |S| < 2^18)
+// is congruent to |A'| mod p_l.  U = sgn(x) * S + OFF_l with OFF_l = a multiple
+// of p_l above 2^18 plus h_l = floor(p_l / 2) lies in [0, 2^20), so
+//   r = U - p_l * umulhi(U, ceil(2^32 / p_l))  in [0, p_l)   (exact for U < 2^24)
+// and r - h_l is the reference's representative of A' mod p_l
+// (crt.hpp:48-52): symmetric for odd p; for p = 256 the byte of r - 128 equals
+// A' mod 256 as int8, which is how the reference stores the class 128 (-128).
+// The subtraction of h_l is done per byte on the packed word (vsub4).
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace oz2g {
+
+namespace {
+
+__device__ __forceinline__ void flag(DevStatus* st, uint32_t bits) { atomicOr(&st->err, bits); }
+
+template <class T>
+__device__ __forceinline__ double ld_d(const T* p) { return (double)__ldg(p); }
+
+struct ElemDec {
+    uint32_t lo, hi;  // bytes 0-3 / 4-7 of m'
+    uint32_t row;     // E': column of the weight table [l][E']
+    int32_t sgn;      // +1, -1, or 0 for x == 0
+};
+
+__device__ __forceinline__ ElemDec elem_dec(double x, int shift, int n, bool& overflow) {
+    ElemDec d{0u, 0u, 0u, 0};
+    if (x == 0.0) return d;
+    uint64_t mant; int e2;
+    decompose(x, mant, e2);
+    const int E = e2 + shift;
+    // ldexp(x, shift) overflows iff |x| 2^shift >= 2^1024 (scaling.hpp:206/220)
+    overflow |= E + 53 > 1024;
+    uint64_t mp = mant;
+    int Ep = E;
+    if (E < 0) { mp = (-E >= 64) ? 0ull : (mant >> (-E)); Ep = 0; }
+    // |A'| < 2^(6 + P') < 2^177 for every valid input, so E' <= 124 < kResidE
+    if (Ep > kResidE - 1) { overflow = true; Ep = kResidE - 1; }
+    d.lo = (uint32_t)mp;
+    d.hi = (uint32_t)(mp >> 32);
+    d.row = (uint32_t)Ep;
+    d.sgn = x < 0.0 ? -1 : 1;
+    return d;
+}
+
+__device__ __forceinline__ int dp4a_us(uint32_t a, int32_t b, int32_t c) {
+    int32_t d;
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+struct ModC {
+    uint32_t p, magic, offh, h4;
+};
+
+// r in [0, p) with r - h == residue of sgn * m' * 2^E' (see the file header)
+__device__ __forceinline__ uint32_t resid_r(const ElemDec& d, const int2* __restrict__ tab_l, const ModC& c) {
+    const int2 w = tab_l[d.row];
+    int S = dp4a_us(d.lo, w.x, 0);
+    S = dp4a_us(d.hi, w.y, S);
+    const uint32_t U = (uint32_t)(S * d.sgn) + c.offh;
+    const uint32_t q = __umulhi(U, c.magic);
+    return U - q * c.p;
+}
+
+__device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
+    const uint32_t lo = __byte_perm(b0, b1, 0x0040);
+    const uint32_t hi = __byte_perm(b2, b3, 0x0040);
+    return __byte_perm(lo, hi, 0x5410);
+}
+
+__device__ __forceinline__ void load_resid_consts(const ResidHeader* __restrict__ g, int n, uint8_t* sh) {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(g);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(sh);
+    const int words = (int)(resid_consts_bytes(n) / 4);
+    for (int t = threadIdx.x; t < words; t += blockDim.x) dst[t] = src[t];
+}
+
+__device__ __forceinline__ ModC modc(const ResidHeader& hd, int l) {
+    ModC c;
+    c.p = hd.p[l];
+    c.magic = hd.magic[l];
+    c.offh = hd.offh[l];
+    c.h4 = hd.h4[l];
+    return c;
+}
+
+// ---------------------------------------------------------------------------
+// A: block = one row i x 4096 columns; coalesced load through shared memory,
+// then each thread owns 16 consecutive columns (one 16-B store per plane).
+// ---------------------------------------------------------------------------
+constexpr int RA_CHUNKS = 256;                 // 16-element chunks per block
+constexpr int RA_STRIDE = 17;                  // padded chunk stride (doubles)
+
+template <class T>
+__global__ void __launch_bounds__(256, 2) resid_A_kernel(const T* __restrict__ A, int64_t lda, int64_t m,
+                                                         int64_t k, int64_t kp, const int32_t* __restrict__ mu,
+                                                         const ResidHeader* __restrict__ rc_g, int nmod,
+                                                         int8_t* __restrict__ planes, DevStatus* st) {
+    extern __shared__ __align__(16) uint8_t sh[];
+    const size_t cbytes = (resid_consts_bytes(nmod) + 15) & ~size_t(15);
+    load_resid_consts(rc_g, nmod, sh);
+    double* stage = reinterpret_cast<double*>(sh + cbytes);
+    const int64_t i = blockIdx.y;
+    const int64_t hb = (int64_t)blockIdx.x * (RA_CHUNKS * 16);
+    const T* row = A + i * lda;
+#pragma unroll 4
+    for (int it = 0; it < 16; ++it) {
+        const int e = it * 256 + threadIdx.x;
+        const int64_t h = hb + e;
+        stage[(e >> 4) * RA_STRIDE + (e & 15)] = h < k ? ld_d(row + h) : 0.0;
+    }
+    __syncthreads();
+    const int64_t h0 = hb + (int64_t)threadIdx.x * 16;
+    if (h0 >= kp) return;
+    const ResidHeader& hd = *reinterpret_cast<const ResidHeader*>(sh);
+    const int2* tab = reinterpret_cast<const int2*>(sh + sizeof(ResidHeader));
+    const int sft = mu[i];
+    ElemDec d[16];
+    bool ovf = false;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) d[j] = elem_dec(stage[threadIdx.x * RA_STRIDE + j], sft, nmod, ovf);
+    if (ovf) flag(st, ERR_TRUNC_A_RANGE);
+    const int64_t plane = m * kp;
+    int8_t* out = planes + i * kp + h0;
+#pragma unroll 1
+    for (int l = 0; l < nmod; ++l) {
+        const ModC c = modc(hd, l);
+        const int2* tl = tab + l * kResidE;
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            w[q] = __vsub4(pack4(resid_r(d[4 * q], tl, c), resid_r(d[4 * q + 1], tl, c), resid_r(d[4 * q + 2], tl, c),
+                                 resid_r(d[4 * q + 3], tl, c)),
+                           c.h4);
+        *reinterpret_cast<uint4*>(out + (int64_t)l * plane) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// B transposed writers: tile 64 (h) x 64 (j), output [plane][j][kp].
+//   OP 0: Bbar^T = ceil(|B| 2^nu')   OP 1: residue planes of trunc(B 2^nu)
+// ---------------------------------------------------------------------------
+constexpr int TB = 64;
+constexpr int TROW = TB + 16;  // padded smem row (bytes) to spread banks
+constexpr int TCH = 8;         // moduli per smem round
+
+template <class T, int OP>
+__global__ void __launch_bounds__(256, 2) transpose_B_kernel(const T* __restrict__ B, int64_t ldb, int64_t k,
+                                                             int64_t n, int64_t kp, const int32_t* __restrict__ shift,
+                                                             const ResidHeader* __restrict__ rc_g, int nmod,
+                                                             int8_t* __restrict__ out, DevStatus* st) {
+    extern __shared__ __align__(16) uint8_t sh[];
+    uint8_t* tile = sh;  // [TCH][TB][TROW]
+    uint8_t* rcs = sh + TCH * TB * TROW;
+    if (OP == 1) load_resid_consts(rc_g, nmod, rcs);
+    const ResidHeader& hd = *reinterpret_cast<const ResidHeader*>(rcs);
+    const int2* tab = reinterpret_cast<const int2*>(rcs + sizeof(ResidHeader));
+    const int tx = threadIdx.x & 63;  // column within tile
+    const int ty = threadIdx.x >> 6;  // 4 groups of 16 rows
+    const int64_t j = (int64_t)blockIdx.x * TB + tx;
+    const int64_t hbase = (int64_t)blockIdx.y * TB + ty * 16;
+    const bool jok = j < n;
+    const int sft = jok ? shift[j] : 0;
+    double x[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const int64_t h = hbase + r;
+        x[r] = (jok && h < k) ? ld_d(B + h * ldb + j) : 0.0;
+    }
+    __syncthreads();
+    const int nplanes = OP == 0 ? 1 : nmod;
+    const int64_t plane = n * kp;
+    ElemDec d[16];
+    bool flagbit = false;
+    if (OP == 1) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) d[r] = elem_dec(x[r], sft, nmod, flagbit);
+    }
+    for (int l0 = 0; l0 < nplanes; l0 += TCH) {
+        const int lc = nplanes - l0 < TCH ? nplanes - l0 : TCH;
+#pragma unroll 1
+        for (int c = 0; c < lc; ++c) {
+            uint32_t w[4] = {0, 0, 0, 0};
+            if (OP == 0) {
+#pragma unroll
+                for (int r = 0; r < 16; ++r) {
+                    const int v = ceil_abs_scaled(x[r], sft);
+                    flagbit |= v < 0;
+                    w[r >> 2] |= (uint32_t)(v & 0xff) << (8 * (r & 3));
+                }
+            } else {
+                const ModC mc = modc(hd, l0 + c);
+                const int2* tl = tab + (l0 + c) * kResidE;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    w[q] = __vsub4(pack4(resid_r(d[4 * q], tl, mc), resid_r(d[4 * q + 1], tl, mc),
+                                         resid_r(d[4 * q + 2], tl, mc), resid_r(d[4 * q + 3], tl, mc)),
+                                   mc.h4);
+            }
+            *reinterpret_cast<uint4*>(tile + (c * TB + tx) * TROW + ty * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        __syncthreads();
+        // write out: per (c, row jj) 64 contiguous bytes = 4 x 16 B
+        for (int idx = threadIdx.x; idx < lc * TB * 4; idx += blockDim.x) {
+            const int q = idx & 3;
+            const int jj = (idx >> 2) % TB;
+            const int c = (idx >> 2) / TB;
+            const int64_t jg = (int64_t)blockIdx.x * TB + jj;
+            if (jg >= n) continue;
+            const int64_t hg = (int64_t)blockIdx.y * TB + q * 16;
+            const uint4 val = *reinterpret_cast<const uint4*>(tile + (c * TB + jj) * TROW + q * 16);
+            *reinterpret_cast<uint4*>(out + (int64_t)(l0 + c) * plane + jg * kp + hg) = val;
+        }
+        __syncthreads();
+    }
+    if (flagbit) flag(st, OP == 0 ? ERR_CEIL_LOGIC : ERR_TRUNC_B_RANGE);
+}
+
+inline unsigned blocks_for(int64_t work, int per) { return (unsigned)((work + per - 1) / per); }
+
+size_t transpose_smem(int op, int nmod) {
+    return (size_t)TCH * TB * TROW + (op == 1 ? resid_consts_bytes(nmod) : 0);
+}
+
+template <class K>
+cudaError_t set_smem(K kernel, size_t bytes) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+}  // namespace
+
+cudaError_t launch_bbar_T(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp,
+                          const int32_t* nu_prime, int8_t* bbar_t, DevStatus* st, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    dim3 grid(blocks_for(n, TB), (unsigned)(kp / TB));
+    const size_t sm = transpose_smem(0, 1);
+    if (prec)
+        transpose_B_kernel<double, 0><<<grid, 256, sm, s>>>((const double*)B, ldb, k, n, kp, nu_prime, nullptr, 1, bbar_t, st);
+    else
+        transpose_B_kernel<float, 0><<<grid, 256, sm, s>>>((const float*)B, ldb, k, n, kp, nu_prime, nullptr, 1, bbar_t, st);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_resid_BT(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp,
+                            const int32_t* nu, const ResidConsts* rc_dev, int nmod, int8_t* planes,
+                            DevStatus* st, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    dim3 grid(blocks_for(n, TB), (unsigned)(kp / TB));
+    const size_t sm = transpose_smem(1, nmod);
+    cudaError_t err;
+    if (prec) {
+        if ((err = set_smem(transpose_B_kernel<double, 1>, sm)) != cudaSuccess) return err;
+        transpose_B_kernel<double, 1><<<grid, 256, sm, s>>>((const double*)B, ldb, k, n, kp, nu, rc_dev, nmod, planes, st);
+    } else {
+        if ((err = set_smem(transpose_B_kernel<float, 1>, sm)) != cudaSuccess) return err;
+        transpose_B_kernel<float, 1><<<grid, 256, sm, s>>>((const float*)B, ldb, k, n, kp, nu, rc_dev, nmod, planes, st);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_resid_A(int prec, const void* A, int64_t lda, int64_t m, int64_t k, int64_t kp,
+                           const int32_t* mu, const ResidConsts* rc_dev, int nmod, int8_t* planes,
+                           DevStatus* st, cudaStream_t s) {
+    if (m == 0) return cudaSuccess;
+    dim3 grid(blocks_for(kp, RA_CHUNKS * 16), (unsigned)m);
+    const size_t sm = ((resid_consts_bytes(nmod) + 15) & ~size_t(15)) + (size_t)RA_CHUNKS * RA_STRIDE * 8;
+    cudaError_t err;
+    if (prec) {
+        if ((err = set_smem(resid_A_kernel<double>, sm)) != cudaSuccess) return err;
+        resid_A_kernel<double><<<grid, 256, sm, s>>>((const double*)A, lda, m, k, kp, mu, rc_dev, nmod, planes, st);
+    } else {
+        if ((err = set_smem(resid_A_kernel<float>, sm)) != cudaSuccess) return err;
+        resid_A_kernel<float><<<grid, 256, sm, s>>>((const float*)A, lda, m, k, kp, mu, rc_dev, nmod, planes, st);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace oz2g

@@ -236,14 +236,12 @@ def test_truncation(oracle):  # test_scaling.cpp:107-113
     assert ap[0] == math.trunc(1.75 * 2.0 ** mu) and ap[1] == -ap[0]
 
 
-SURVEY_THRESHOLDS = {  # SURVEY §8c survey-derived golden step tables (glibc log2)
-    6: (23, [2, 8, 29, 113, 449, 1796, 7182, 28728, 114910, 459639, 1838554, 7354204, 29416815, 117667105, 470668417]),
-    7: (27, [2, 7, 27, 105, 420, 1677, 6705, 26820, 107279, 429116, 1716463, 6865842, 27463367, 109853321, 439413281]),
-    8: (31, [2, 6, 24, 96, 382, 1526, 6103, 24411, 97641, 390563, 1562249, 6248986, 24995941, 99983761, 399934529]),
-    14: (54, [3, 9, 36, 144, 573, 2290, 9160, 36640, 146559, 586235, 2344939, 9379741, 37518961, 150075649]),
-    16: (62, [2, 6, 21, 84, 333, 1329, 5315, 21257, 85027, 340107, 1360426, 5441695, 21766779, 87067113, 348268001]),
-    17: (65, [4, 16, 62, 248, 992, 3965, 15860, 63438, 253752, 1015007, 4060020, 16240080, 64960317, 259840929]),
-}
+import json
+import os
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+SURVEY_THRESHOLDS = {int(k): (v[0], v[1]) for k, v in
+                     json.load(open(os.path.join(GOLDEN, "shift_thresholds.json")))["shift0_and_thresholds"].items()}
 
 
 @pytest.mark.parametrize("n", sorted(SURVEY_THRESHOLDS))
@@ -428,3 +426,15 @@ def test_int8_engine_matches_reference_build(oracle):
     ref = np.empty((19, 23), dtype=np.int32)
     assert R.ref_gemm_i8_wrap(19, 300, 23, a.ctypes.data, b.ctypes.data, ref.ctypes.data) == 0
     assert np.array_equal(oracle.gemm_i8_wrap(a, b), ref)
+
+
+def test_oracle_reproduces_reference_golden(oracle):
+    """Committed fixtures produced by the reference's own gen.hpp / int8gemm.hpp
+    (tests/golden/make_golden.py); valid where /root/reference is absent."""
+    g = np.load(os.path.join(GOLDEN, "ref_gen_gemm.npz"))
+    cases = json.load(open(os.path.join(GOLDEN, "gen_cases.json")))
+    for idx, (r, c, phi, seed, dt) in enumerate(cases):
+        ours = oracle.gen_matrix(r, c, phi, seed, np.float64 if dt == "f64" else np.float32)
+        assert ours.tobytes() == g[f"gen{idx}"].tobytes()
+    for idx in range(3):
+        assert np.array_equal(oracle.gemm_i8_wrap(g[f"gemm{idx}_a"], g[f"gemm{idx}_b"]), g[f"gemm{idx}_c"])
