@@ -121,6 +121,7 @@ std::vector<uint8_t> build_resid_consts(const Table& t) {
         h->magic[l] = (uint32_t)((0x100000000ull + p - 1) / p);  // ceil(2^32 / p)
         h->offh[l] = p * (((1u << 18) + p - 1) / p) + p / 2;
         h->h4[l] = (p / 2) * 0x01010101u;
+        h->negp[l] = 0u - p;
         for (int E = 0; E < kResidE; ++E) {
             uint32_t w[8];
             for (int b = 0; b < 8; ++b) {  // symmetric representative of 2^(8b + E) mod p, as a byte

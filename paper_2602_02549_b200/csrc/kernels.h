@@ -36,17 +36,18 @@ cudaError_t launch_gemm_i8(int mode, const CUtensorMap& tmA, const CUtensorMap& 
                            int num_sms, cudaStream_t stream);
 
 // Residue constants for the residue kernels (uploaded once per table): a
-// header followed by the weight table w[E][l] (E in [0, 255]) of two packed
+// header followed by the weight table w[l][E] (E in [0, kResidE)) of two packed
 // words whose signed bytes are the symmetric representatives of
 // 2^(8t + E) mod p_l, t = 0..7 (resid.cu explains the arithmetic).
-struct ResidHeader {
+struct alignas(16) ResidHeader {  // size a multiple of 16: the table that follows is read as int2/uint4
     int n, pad;
     uint32_t p[49];
     uint32_t magic[49];  // ceil(2^32 / p): floor(U / p) == umulhi(U, magic) for U < 2^24
     uint32_t offh[49];   // p * ceil(2^18 / p) + floor(p / 2)
     uint32_t h4[49];     // floor(p / 2) replicated in 4 bytes
+    uint32_t negp[49];   // -p (mod 2^32)
 };
-constexpr int kResidE = 256;
+constexpr int kResidE = 128;  // E' <= 124: |A'| < 2^(6 + P') and P' < 171 for N <= 49
 __host__ __device__ inline size_t resid_consts_bytes(int n) { return sizeof(ResidHeader) + (size_t)kResidE * n * 8; }
 typedef ResidHeader ResidConsts;
 

@@ -11,8 +11,8 @@
 //
 // Residue arithmetic.  |A'| = m' * 2^E' with m' < 2^53 (m' = mant >> -E if
 // E < 0, E' = max(E, 0)).  With the signed byte weights
-//   w[E'][l][t] = symmetric representative of 2^(8t + E') mod p_l (|w| <= 128),
-//   S = sum_t byte_t(m') * w[E'][l][t]          (two dp4a.u32.s32, |S| < 2^18)
+//   w[l][E'][t] = symmetric representative of 2^(8t + E') mod p_l (|w| <= 128),
+//   S = sum_t byte_t(m') * w[l][E'][t]          (two dp4a.u32.s32, |S| < 2^18)
 // is congruent to |A'| mod p_l.  U = sgn(x) * S + OFF_l with OFF_l = a multiple
 // of p_l above 2^18 plus h_l = floor(p_l / 2) lies in [0, 2^20), so
 //   r = U - p_l * umulhi(U, ceil(2^32 / p_l))  in [0, p_l)   (exact for U < 2^24)
@@ -34,11 +34,11 @@ __device__ __forceinline__ double ld_d(const T* p) { return (double)__ldg(p); }
 
 struct ElemDec {
     uint32_t lo, hi;  // bytes 0-3 / 4-7 of m'
-    uint32_t row;     // E': column of the weight table [l][E']
+    uint32_t off;     // 8 * E': byte offset into the weight row of a modulus
     int32_t sgn;      // +1, -1, or 0 for x == 0
 };
 
-__device__ __forceinline__ ElemDec elem_dec(double x, int shift, int n, bool& overflow) {
+__device__ __forceinline__ ElemDec elem_dec(double x, int shift, bool& overflow) {
     ElemDec d{0u, 0u, 0u, 0};
     if (x == 0.0) return d;
     uint64_t mant; int e2;
@@ -53,7 +53,7 @@ __device__ __forceinline__ ElemDec elem_dec(double x, int shift, int n, bool& ov
     if (Ep > kResidE - 1) { overflow = true; Ep = kResidE - 1; }
     d.lo = (uint32_t)mp;
     d.hi = (uint32_t)(mp >> 32);
-    d.row = (uint32_t)Ep;
+    d.off = (uint32_t)Ep * 8u;
     d.sgn = x < 0.0 ? -1 : 1;
     return d;
 }
@@ -65,17 +65,17 @@ __device__ __forceinline__ int dp4a_us(uint32_t a, int32_t b, int32_t c) {
 }
 
 struct ModC {
-    uint32_t p, magic, offh, h4;
+    uint32_t magic, offh, h4, negp;
 };
 
 // r in [0, p) with r - h == residue of sgn * m' * 2^E' (see the file header)
-__device__ __forceinline__ uint32_t resid_r(const ElemDec& d, const int2* __restrict__ tab_l, const ModC& c) {
-    const int2 w = tab_l[d.row];
+__device__ __forceinline__ uint32_t resid_r(const ElemDec& d, const uint8_t* __restrict__ row_l, const ModC& c) {
+    const int2 w = *reinterpret_cast<const int2*>(row_l + d.off);
     int S = dp4a_us(d.lo, w.x, 0);
     S = dp4a_us(d.hi, w.y, S);
     const uint32_t U = (uint32_t)(S * d.sgn) + c.offh;
     const uint32_t q = __umulhi(U, c.magic);
-    return U - q * c.p;
+    return U + q * c.negp;
 }
 
 __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
@@ -85,70 +85,67 @@ __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2,
 }
 
 __device__ __forceinline__ void load_resid_consts(const ResidHeader* __restrict__ g, int n, uint8_t* sh) {
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(g);
-    uint32_t* dst = reinterpret_cast<uint32_t*>(sh);
-    const int words = (int)(resid_consts_bytes(n) / 4);
+    const uint4* src = reinterpret_cast<const uint4*>(g);
+    uint4* dst = reinterpret_cast<uint4*>(sh);
+    const int words = (int)(resid_consts_bytes(n) / 16);
     for (int t = threadIdx.x; t < words; t += blockDim.x) dst[t] = src[t];
 }
 
 __device__ __forceinline__ ModC modc(const ResidHeader& hd, int l) {
     ModC c;
-    c.p = hd.p[l];
     c.magic = hd.magic[l];
     c.offh = hd.offh[l];
     c.h4 = hd.h4[l];
+    c.negp = hd.negp[l];
     return c;
 }
 
 // ---------------------------------------------------------------------------
-// A: block = one row i x 4096 columns; coalesced load through shared memory,
-// then each thread owns 16 consecutive columns (one 16-B store per plane).
+// A: each thread owns 8 consecutive columns of one row (one 8-byte store per
+// plane, 16-byte vector loads).
 // ---------------------------------------------------------------------------
-constexpr int RA_CHUNKS = 256;                 // 16-element chunks per block
-constexpr int RA_STRIDE = 17;                  // padded chunk stride (doubles)
+constexpr int RA_E = 8;
 
 template <class T>
-__global__ void __launch_bounds__(256, 2) resid_A_kernel(const T* __restrict__ A, int64_t lda, int64_t m,
-                                                         int64_t k, int64_t kp, const int32_t* __restrict__ mu,
-                                                         const ResidHeader* __restrict__ rc_g, int nmod,
-                                                         int8_t* __restrict__ planes, DevStatus* st) {
+__global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t k,
+                                                      int64_t kp, const int32_t* __restrict__ mu,
+                                                      const ResidHeader* __restrict__ rc_g, int nmod,
+                                                      int8_t* __restrict__ planes, DevStatus* st) {
     extern __shared__ __align__(16) uint8_t sh[];
-    const size_t cbytes = (resid_consts_bytes(nmod) + 15) & ~size_t(15);
     load_resid_consts(rc_g, nmod, sh);
-    double* stage = reinterpret_cast<double*>(sh + cbytes);
-    const int64_t i = blockIdx.y;
-    const int64_t hb = (int64_t)blockIdx.x * (RA_CHUNKS * 16);
-    const T* row = A + i * lda;
-#pragma unroll 4
-    for (int it = 0; it < 16; ++it) {
-        const int e = it * 256 + threadIdx.x;
-        const int64_t h = hb + e;
-        stage[(e >> 4) * RA_STRIDE + (e & 15)] = h < k ? ld_d(row + h) : 0.0;
-    }
     __syncthreads();
-    const int64_t h0 = hb + (int64_t)threadIdx.x * 16;
+    const int64_t i = blockIdx.y;
+    const int64_t h0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * RA_E;
     if (h0 >= kp) return;
     const ResidHeader& hd = *reinterpret_cast<const ResidHeader*>(sh);
-    const int2* tab = reinterpret_cast<const int2*>(sh + sizeof(ResidHeader));
+    const uint8_t* tab = sh + sizeof(ResidHeader);
     const int sft = mu[i];
-    ElemDec d[16];
+    const T* row = A + i * lda + h0;
+    ElemDec d[RA_E];
     bool ovf = false;
+    if (sizeof(T) == 8 && h0 + RA_E <= k && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) d[j] = elem_dec(stage[threadIdx.x * RA_STRIDE + j], sft, nmod, ovf);
+        for (int j = 0; j < RA_E; j += 2) {
+            const double2 v = __ldg(reinterpret_cast<const double2*>(row + j));
+            d[j] = elem_dec(v.x, sft, ovf);
+            d[j + 1] = elem_dec(v.y, sft, ovf);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < RA_E; ++j) d[j] = elem_dec(h0 + j < k ? ld_d(row + j) : 0.0, sft, ovf);
+    }
     if (ovf) flag(st, ERR_TRUNC_A_RANGE);
     const int64_t plane = m * kp;
     int8_t* out = planes + i * kp + h0;
-#pragma unroll 1
+#pragma unroll 2
     for (int l = 0; l < nmod; ++l) {
         const ModC c = modc(hd, l);
-        const int2* tl = tab + l * kResidE;
-        uint32_t w[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            w[q] = __vsub4(pack4(resid_r(d[4 * q], tl, c), resid_r(d[4 * q + 1], tl, c), resid_r(d[4 * q + 2], tl, c),
-                                 resid_r(d[4 * q + 3], tl, c)),
-                           c.h4);
-        *reinterpret_cast<uint4*>(out + (int64_t)l * plane) = make_uint4(w[0], w[1], w[2], w[3]);
+        const uint8_t* rl = tab + (size_t)l * kResidE * 8;
+        const uint32_t w0 = __vsub4(pack4(resid_r(d[0], rl, c), resid_r(d[1], rl, c), resid_r(d[2], rl, c),
+                                          resid_r(d[3], rl, c)), c.h4);
+        const uint32_t w1 = __vsub4(pack4(resid_r(d[4], rl, c), resid_r(d[5], rl, c), resid_r(d[6], rl, c),
+                                          resid_r(d[7], rl, c)), c.h4);
+        *reinterpret_cast<uint2*>(out + (int64_t)l * plane) = make_uint2(w0, w1);
     }
 }
 
@@ -170,7 +167,7 @@ __global__ void __launch_bounds__(256, 2) transpose_B_kernel(const T* __restrict
     uint8_t* rcs = sh + TCH * TB * TROW;
     if (OP == 1) load_resid_consts(rc_g, nmod, rcs);
     const ResidHeader& hd = *reinterpret_cast<const ResidHeader*>(rcs);
-    const int2* tab = reinterpret_cast<const int2*>(rcs + sizeof(ResidHeader));
+    const uint8_t* tab = rcs + sizeof(ResidHeader);
     const int tx = threadIdx.x & 63;  // column within tile
     const int ty = threadIdx.x >> 6;  // 4 groups of 16 rows
     const int64_t j = (int64_t)blockIdx.x * TB + tx;
@@ -190,7 +187,7 @@ __global__ void __launch_bounds__(256, 2) transpose_B_kernel(const T* __restrict
     bool flagbit = false;
     if (OP == 1) {
 #pragma unroll
-        for (int r = 0; r < 16; ++r) d[r] = elem_dec(x[r], sft, nmod, flagbit);
+        for (int r = 0; r < 16; ++r) d[r] = elem_dec(x[r], sft, flagbit);
     }
     for (int l0 = 0; l0 < nplanes; l0 += TCH) {
         const int lc = nplanes - l0 < TCH ? nplanes - l0 : TCH;
@@ -206,11 +203,11 @@ __global__ void __launch_bounds__(256, 2) transpose_B_kernel(const T* __restrict
                 }
             } else {
                 const ModC mc = modc(hd, l0 + c);
-                const int2* tl = tab + (l0 + c) * kResidE;
+                const uint8_t* rl = tab + (size_t)(l0 + c) * kResidE * 8;
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
-                    w[q] = __vsub4(pack4(resid_r(d[4 * q], tl, mc), resid_r(d[4 * q + 1], tl, mc),
-                                         resid_r(d[4 * q + 2], tl, mc), resid_r(d[4 * q + 3], tl, mc)),
+                    w[q] = __vsub4(pack4(resid_r(d[4 * q], rl, mc), resid_r(d[4 * q + 1], rl, mc),
+                                         resid_r(d[4 * q + 2], rl, mc), resid_r(d[4 * q + 3], rl, mc)),
                                    mc.h4);
             }
             *reinterpret_cast<uint4*>(tile + (c * TB + tx) * TROW + ty * 16) = make_uint4(w[0], w[1], w[2], w[3]);
@@ -278,8 +275,8 @@ cudaError_t launch_resid_A(int prec, const void* A, int64_t lda, int64_t m, int6
                            const int32_t* mu, const ResidConsts* rc_dev, int nmod, int8_t* planes,
                            DevStatus* st, cudaStream_t s) {
     if (m == 0) return cudaSuccess;
-    dim3 grid(blocks_for(kp, RA_CHUNKS * 16), (unsigned)m);
-    const size_t sm = ((resid_consts_bytes(nmod) + 15) & ~size_t(15)) + (size_t)RA_CHUNKS * RA_STRIDE * 8;
+    dim3 grid(blocks_for(kp, 256 * RA_E), (unsigned)m);
+    const size_t sm = resid_consts_bytes(nmod);
     cudaError_t err;
     if (prec) {
         if ((err = set_smem(resid_A_kernel<double>, sm)) != cudaSuccess) return err;
