@@ -65,7 +65,24 @@ extern "C" {
  *   Bres : N*k*n int8 residues of B' (crt.hpp:161), row-major k x n
  *   Cprod: N*m*n int32 wrapped INT8 products (crt.hpp:70)
  *   cmax_row : m, cmax_col : n int32 clearance-product maxima (scaling.hpp:175-192)
+ *   bounds : when non-NULL, the deterministic error bounds of the paper
+ *            (bounds.hpp:182-206) are evaluated in the same pass (below).
  */
+/*
+ * Error bounds on |A B - C| per entry (bounds.hpp:143-206), every operation
+ * rounded upward so each value is a certificate:
+ *   cheap: bound_cheap (bounds.hpp:198-206), r_b scalar;
+ *   tight: bound_tight (bounds.hpp:182-195) with the exact |A'B'| replaced by
+ *          the sound device bound (|C''| + r_const) / (1 - u_coef).
+ * `cheap` / `tight` are optional m*n outputs (host buffers, or device buffers
+ * when `device` != 0); the maxima are always returned.
+ */
+typedef struct oz2g_bounds {
+    double *cheap, *tight;
+    int device;
+    double cheap_max, tight_max;
+} oz2g_bounds;
+
 typedef struct oz2g_intermediates {
     int16_t *mu, *nu, *mu_prime, *nu_prime;
     float *e, *f;
@@ -78,6 +95,7 @@ typedef struct oz2g_intermediates {
     int8_t *Ares, *Bres;
     int32_t *Cprod;
     int32_t *cmax_row, *cmax_col;
+    oz2g_bounds *bounds;
 } oz2g_intermediates;
 
 /* Per-call diagnostics. */
@@ -150,6 +168,13 @@ int oz2g_shift_of_cmax(int n, int64_t c);
 /* Device-side log2f evaluation used for the e/f diagnostics, exposed so tests
  * can compare it exhaustively with the host libm (log2_fp32, softfp.hpp:147). */
 int oz2g_device_log2f(const float *x_dev, float *out_dev, int64_t count, void *stream);
+
+/* Double-double reference product C = A B (hi + lo) for DEVICE fp64
+ * matrices: every product exact (TwoProd), the k-term sum in double-double
+ * (error <= ~k 2^-104 sum|a||b|).  Used to measure the emulation error
+ * against the paper's bounds (the role of error_matrix, oracle.hpp:164-172). */
+int oz2g_dd_gemm(int64_t m, int64_t n, int64_t k, const double *A, int64_t lda, const double *B, int64_t ldb,
+                 double *Chi, double *Clo, int64_t ldc, void *stream);
 
 /* Library information (compiled arch, number of SMs used, version). */
 int oz2g_version(void);

@@ -19,7 +19,12 @@ OZ2G_HOST_PTRS, OZ2G_DEVICE_PTRS, OZ2G_TIMING = 0, 1, 2
 class Intermediates(C.Structure):
     _fields_ = [(name, C.c_void_p) for name in (
         "mu", "nu", "mu_prime", "nu_prime", "e", "f", "Aprime", "Bprime", "Cbar", "Dbar", "W",
-        "C1", "C2", "Q", "Cpp64", "Cpp32", "Ares", "Bres", "Cprod", "cmax_row", "cmax_col")]
+        "C1", "C2", "Q", "Cpp64", "Cpp32", "Ares", "Bres", "Cprod", "cmax_row", "cmax_col", "bounds")]
+
+
+class Bounds(C.Structure):
+    _fields_ = [("cheap", C.c_void_p), ("tight", C.c_void_p), ("device", C.c_int),
+                ("cheap_max", C.c_double), ("tight_max", C.c_double)]
 
 
 class Diag(C.Structure):
@@ -37,7 +42,7 @@ REDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C
 
 EXPORTED = ("oz2g_gemm", "oz2g_dgemm", "oz2g_sgemm", "oz2g_last_error", "oz2g_table_for",
             "oz2g_fp32_safe_moduli_max", "oz2g_shift_of_cmax", "oz2g_device_log2f", "oz2g_version",
-            "oz2g_release_workspace")
+            "oz2g_release_workspace", "oz2g_dd_gemm")
 
 _LIB = None
 
@@ -61,5 +66,7 @@ def load() -> C.CDLL:
     L.oz2g_table_for.argtypes = [C.c_int, C.c_int, C.POINTER(TableC)]
     L.oz2g_shift_of_cmax.argtypes = [C.c_int, C.c_int64]
     L.oz2g_device_log2f.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+    L.oz2g_dd_gemm.argtypes = [C.c_int64] * 3 + [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                                                 C.c_void_p, C.c_int64, C.c_void_p]
     _LIB = L
     return L

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -68,13 +69,13 @@ struct DevBuf {
 
 struct Workspace {
     DevBuf A, B, C, abar, bbar, ares, bres, W, mup, nup, mu, nu, bmax, cmax_row, cmax_col, e, f, status;
-    DevBuf x_cbar, x_cprod, x_c1, x_c2, x_q, x_cpp64, x_cpp32, x_ap, x_bp;
+    DevBuf x_cbar, x_cprod, x_c1, x_c2, x_q, x_cpp64, x_cpp32, x_ap, x_bp, x_bvec, x_bscr, x_bmax, x_bcheap, x_btight;
     std::map<std::pair<int, int>, ResidConsts*> rc;  // device copies of residue constants
     int num_sms = 0;
     void release() {
         for (DevBuf* b : {&A, &B, &C, &abar, &bbar, &ares, &bres, &W, &mup, &nup, &mu, &nu, &bmax, &cmax_row,
                           &cmax_col, &e, &f, &status, &x_cbar, &x_cprod, &x_c1, &x_c2, &x_q, &x_cpp64, &x_cpp32,
-                          &x_ap, &x_bp})
+                          &x_ap, &x_bp, &x_bvec, &x_bscr, &x_bmax, &x_bcheap, &x_btight})
             b->release();
         for (auto& kv : rc) cudaFree(kv.second);
         rc.clear();
@@ -165,6 +166,26 @@ std::mutex& device_mutex(int dev) {
 
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
+// GEMM variant: OZ2G_GEMM=pair selects the CTA-pair (cta_group::2) kernel.
+bool use_pair_gemm() {
+    static const bool v = [] {
+        const char* s = std::getenv("OZ2G_GEMM");
+        return s && std::strcmp(s, "pair") == 0;
+    }();
+    return v;
+}
+
+// Raster group height: one wave of persistent CTAs covers group_m tile-rows,
+// so B tiles are streamed from HBM about tiles_m / group_m times per plane.
+int group_m_for(int tiles_m) {
+    static const int env = [] {
+        const char* s = std::getenv("OZ2G_GROUP_M");
+        return s ? std::atoi(s) : 0;
+    }();
+    int g = env > 0 ? env : 32;
+    return g < tiles_m ? g : (tiles_m > 0 ? tiles_m : 1);
+}
+
 struct Timer {
     bool on = false;
     cudaStream_t s = nullptr;
@@ -251,7 +272,15 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     tm.mark();
 
     // ---- K2: clearance product, fused row/col maxima ----
-    const int BM = gemm_tile_m(), BN = gemm_tile_n();
+    // tile shape: single-CTA 128x256 tiles or CTA-pair 256x256 tiles (cta_group::2)
+    const bool pair = use_pair_gemm();
+    const int BM = pair ? gemm_pair_tile_m() : gemm_tile_m();
+    const int BN = pair ? gemm_pair_tile_n() : gemm_tile_n();
+    const int boxA = pair ? gemm_pair_box_rows() : BM, boxB = pair ? gemm_pair_box_rows() : BN;
+    auto launch_gemm = [&](int mode, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& g) {
+        return pair ? launch_gemm_i8_pair(mode, ta, tb, g, ws.num_sms, stream)
+                    : launch_gemm_i8(mode, ta, tb, g, ws.num_sms, stream);
+    };
     GemmParams gp;
     std::memset(&gp, 0, sizeof gp);
     gp.m = (int)m;
@@ -259,19 +288,20 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     gp.kblocks = (int)(kp / 128);
     gp.tiles_m = (int)((m + BM - 1) / BM);
     gp.tiles_n = (int)((n + BN - 1) / BN);
+    gp.group_m = group_m_for(gp.tiles_m);
     if (m > 0 && n > 0) {
-        const CUtensorMap tA = make_plane_map(abar, kp, m, 1, BM);
-        const CUtensorMap tB = make_plane_map(bbar, kp, n, 1, BN);
+        const CUtensorMap tA = make_plane_map(abar, kp, m, 1, boxA);
+        const CUtensorMap tB = make_plane_map(bbar, kp, n, 1, boxB);
         gp.planes = 1;
         gp.rowmax = cmax_row;
         gp.colmax = cmax_col;
-        CUDA_TRY(launch_gemm_i8(EPI_MAX, tA, tB, gp, ws.num_sms, stream)); ++launches;
+        CUDA_TRY(launch_gemm(EPI_MAX, tA, tB, gp)); ++launches;
         if (inter && inter->Cbar) {
             GemmParams g2 = gp;
             g2.C32 = (int32_t*)ws.x_cbar.get(4 * (size_t)(m * n));
             g2.ldc32 = n;
             g2.cplane = m * n;
-            CUDA_TRY(launch_gemm_i8(EPI_I32, tA, tB, g2, ws.num_sms, stream)); ++launches;
+            CUDA_TRY(launch_gemm(EPI_I32, tA, tB, g2)); ++launches;
         }
     }
     if (reduce_fn) {
@@ -305,20 +335,20 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     // ---- K5: residue GEMMs with fused signed mod p ----
     int8_t* W = (int8_t*)ws.W.get((size_t)N * (size_t)(m * ldw));
     if (m > 0 && n > 0) {
-        const CUtensorMap tA = make_plane_map(ares, kp, m, N, BM);
-        const CUtensorMap tB = make_plane_map(bres, kp, n, N, BN);
+        const CUtensorMap tA = make_plane_map(ares, kp, m, N, boxA);
+        const CUtensorMap tB = make_plane_map(bres, kp, n, N, boxB);
         gp.planes = N;
         gp.W = W;
         gp.ldw = ldw;
         gp.wplane = m * ldw;
         fill_gemm_moduli(gp, tab);
-        CUDA_TRY(launch_gemm_i8(EPI_RESID, tA, tB, gp, ws.num_sms, stream)); ++launches;
+        CUDA_TRY(launch_gemm(EPI_RESID, tA, tB, gp)); ++launches;
         if (inter && inter->Cprod) {
             GemmParams g2 = gp;
             g2.C32 = (int32_t*)ws.x_cprod.get(4 * (size_t)N * (size_t)(m * n));
             g2.ldc32 = n;
             g2.cplane = m * n;
-            CUDA_TRY(launch_gemm_i8(EPI_I32, tA, tB, g2, ws.num_sms, stream)); ++launches;
+            CUDA_TRY(launch_gemm(EPI_I32, tA, tB, g2)); ++launches;
         }
     }
     tm.mark();
@@ -330,14 +360,42 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     cc.mode = tab.mode;
     for (int l = 0; l < N; ++l) { cc.s1[l] = tab.s1[l]; cc.s2[l] = tab.s2[l]; }
     cc.P1 = tab.P1; cc.P2 = tab.P2; cc.P_inv = tab.P_inv;
-    CrtExtra ex{nullptr, nullptr, nullptr, nullptr, nullptr};
+    CrtExtra ex;
+    std::memset(&ex, 0, sizeof ex);
     const size_t mn8 = 8 * (size_t)(m * n);
+    oz2g_bounds* bo = inter ? inter->bounds : nullptr;
+    unsigned long long* bmax_dev = nullptr;
     if (inter) {
         if (inter->C1) ex.C1 = (double*)ws.x_c1.get(mn8);
         if (inter->C2) ex.C2 = (double*)ws.x_c2.get(mn8);
         if (inter->Q) ex.Q = (double*)ws.x_q.get(mn8);
         if (inter->Cpp64) ex.Cpp64 = (double*)ws.x_cpp64.get(mn8);
         if (inter->Cpp32 && prec == OZ2G_FP32) ex.Cpp32 = (float*)ws.x_cpp32.get(mn8 / 2);
+    }
+    if (bo && m * n) {
+        // bounds.hpp:143-206 evaluated in the CRT pass
+        const BoundScalars bs = bound_scalars(tab, k);
+        double* vec = (double*)ws.x_bvec.get(8 * (size_t)(2 * (m + n)) + 4 * (size_t)(m + n) + 16);
+        BoundVecs v;
+        v.RA = vec; v.PA = vec + m; v.CB = vec + 2 * m; v.PB = vec + 2 * m + n;
+        v.ea = reinterpret_cast<int32_t*>(vec + 2 * (m + n));
+        v.eb = v.ea + m;
+        double* scratch = (double*)ws.x_bscr.get(8 * bound_scratch_doubles(m, n, k));
+        CUDA_TRY(launch_bound_vectors(prec, dA, lda_d, m, dB, ldb_d, k, n, cmax_row, cmax_col, mup, nup, bs.t_up,
+                                      scratch, v, stream));
+        launches += 5;
+        bmax_dev = (unsigned long long*)ws.x_bmax.get(16);
+        CUDA_TRY(cudaMemsetAsync(bmax_dev, 0, 16, stream));
+        ex.bnd.on = 1;
+        ex.bnd.v = v;
+        ex.bnd.t2_up = bs.t2_up;
+        ex.bnd.rconst_up = bs.rconst_up;
+        ex.bnd.ucoef = bs.ucoef;
+        ex.bnd.kpr_cheap_up = bs.kpr_cheap_up;
+        ex.bnd.k_rconst_up = bs.k_rconst_up;
+        ex.bnd.max_bits = bmax_dev;
+        if (bo->cheap) ex.bnd.cheap = bo->device ? bo->cheap : (double*)ws.x_bcheap.get(mn8);
+        if (bo->tight) ex.bnd.tight = bo->device ? bo->tight : (double*)ws.x_btight.get(mn8);
     }
     CUDA_TRY(launch_crt(prec, W, ldw, m * ldw, m, n, cc, mu, nu, dC, ldc_d, ex, st, stream)); launches += (m * n) > 0;
     tm.mark();
@@ -403,10 +461,23 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         }
     }
 
+    unsigned long long bmax_host[2] = {0, 0};
+    if (bo && bmax_dev) {
+        CUDA_TRY(cudaMemcpyAsync(bmax_host, bmax_dev, 16, cudaMemcpyDeviceToHost, stream));
+        if (!bo->device && bo->cheap) CUDA_TRY(cudaMemcpyAsync(bo->cheap, ex.bnd.cheap, mn8, cudaMemcpyDeviceToHost, stream));
+        if (!bo->device && bo->tight) CUDA_TRY(cudaMemcpyAsync(bo->tight, ex.bnd.tight, mn8, cudaMemcpyDeviceToHost, stream));
+    }
     DevStatus hs;
     CUDA_TRY(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, stream));
     CUDA_TRY(cudaStreamSynchronize(stream));
     CUDA_TRY(cudaGetLastError());
+    if (bo) {
+        double v0, v1;
+        std::memcpy(&v0, &bmax_host[0], 8);
+        std::memcpy(&v1, &bmax_host[1], 8);
+        bo->cheap_max = v0;
+        bo->tight_max = v1;
+    }
 
     if (inter && inter->Dbar && inter->Cbar)
         for (int64_t i = 0; i < m * n; ++i) inter->Dbar[i] = fp32_round_up(inter->Cbar[i]);
@@ -539,6 +610,16 @@ int oz2g_shift_of_cmax(int n, int64_t c) {
 int oz2g_device_log2f(const float* x_dev, float* out_dev, int64_t count, void* stream) {
     return guarded([&] {
         CUDA_TRY(launch_log2f(x_dev, out_dev, count, (cudaStream_t)stream));
+        return OZ2G_OK;
+    });
+}
+
+int oz2g_dd_gemm(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B, int64_t ldb,
+                 double* Chi, double* Clo, int64_t ldc, void* stream) {
+    return guarded([&] {
+        if (m < 0 || n < 0 || k < 0 || lda < k || ldb < n || ldc < n)
+            throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_dd_gemm: bad dimensions"};
+        CUDA_TRY(launch_dd_gemm(A, lda, B, ldb, m, n, k, Chi, Clo, ldc, (cudaStream_t)stream));
         return OZ2G_OK;
     });
 }

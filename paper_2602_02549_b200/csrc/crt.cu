@@ -12,6 +12,9 @@
 //                                 (two RN scalings), subnormal / overflow flags
 // Every operation is an explicit _rn intrinsic so nvcc cannot contract or
 // reorder; the result is bit-identical to the reference.
+//
+// Optionally (BND) the same pass evaluates the cheap and tight error bounds
+// of bounds.hpp:143-206 for every entry (see bounds.cu for the derivation).
 #include <cfloat>
 
 #include "device_common.cuh"
@@ -23,7 +26,16 @@ namespace {
 
 constexpr int CV = 8;  // consecutive columns per thread (one 8-byte load per modulus plane)
 
-template <class T, bool DD>
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, v, o);
+        v = t > v ? t : v;
+    }
+    return v;
+}
+
+template <class T, bool DD, bool BND>
 __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, int64_t ldw, int64_t wplane,
                                                   int64_t m, int64_t n, const CrtConsts cc,
                                                   const int32_t* __restrict__ mu, const int32_t* __restrict__ nu,
@@ -31,72 +43,113 @@ __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, 
                                                   DevStatus* st) {
     const int64_t qn = (n + CV - 1) / CV;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= m * qn) return;
-    const int64_t i = t / qn;
-    const int64_t j0 = (t - i * qn) * CV;
-    const int jn = (int)(n - j0 < CV ? n - j0 : CV);
-    double c1[CV], c2[CV];
+    const bool active = t < m * qn;
+    unsigned long long bmax_cheap = 0, bmax_tight = 0;
+    if (active) {
+        const int64_t i = t / qn;
+        const int64_t j0 = (t - i * qn) * CV;
+        const int jn = (int)(n - j0 < CV ? n - j0 : CV);
+        double c1[CV], c2[CV];
 #pragma unroll
-    for (int b = 0; b < CV; ++b) { c1[b] = 0.0; c2[b] = 0.0; }
-    const int8_t* wp = W + i * ldw + j0;
-    // crt.hpp:99-104: acc = fma(s_l, W_l, acc) in the fixed order l = 0..N-1.
-    // Loads are issued 4 planes ahead of their use to keep HBM busy.
-    auto fold = [&](const uint2 word, int l) {
-        const double s1 = cc.s1[l];
-        const double s2 = cc.s2[l];
+        for (int b = 0; b < CV; ++b) { c1[b] = 0.0; c2[b] = 0.0; }
+        const int8_t* wp = W + i * ldw + j0;
+        // crt.hpp:99-104: acc = fma(s_l, W_l, acc) in the fixed order l = 0..N-1.
+        // Loads are issued 4 planes ahead of their use to keep HBM busy.
+        auto fold = [&](const uint2 word, int l) {
+            const double s1 = cc.s1[l];
+            const double s2 = cc.s2[l];
+#pragma unroll
+            for (int b = 0; b < CV; ++b) {
+                const uint32_t w32 = b < 4 ? word.x : word.y;
+                const double wv = (double)(int8_t)((w32 >> (8 * (b & 3))) & 0xffu);
+                c1[b] = __fma_rn(s1, wv, c1[b]);
+                if (DD) c2[b] = __fma_rn(s2, wv, c2[b]);
+            }
+        };
+        int l = 0;
+        for (; l + 4 <= cc.n; l += 4) {
+            uint2 wv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) wv[u] = __ldg(reinterpret_cast<const uint2*>(wp + (int64_t)(l + u) * wplane));
+#pragma unroll
+            for (int u = 0; u < 4; ++u) fold(wv[u], l + u);
+        }
+        for (; l < cc.n; ++l) fold(__ldg(reinterpret_cast<const uint2*>(wp + (int64_t)l * wplane)), l);
+
+        const int mui = mu[i];
+        double RAi = 0, PAi = 0;
+        int eai = 0;
+        if (BND) { RAi = ex.bnd.v.RA[i]; PAi = ex.bnd.v.PA[i]; eai = ex.bnd.v.ea[i]; }
+        bool fr_range = false, inv_range = false, sub = false;
 #pragma unroll
         for (int b = 0; b < CV; ++b) {
-            const uint32_t w32 = b < 4 ? word.x : word.y;
-            const double wv = (double)(int8_t)((w32 >> (8 * (b & 3))) & 0xffu);
-            c1[b] = __fma_rn(s1, wv, c1[b]);
-            if (DD) c2[b] = __fma_rn(s2, wv, c2[b]);
+            if (b >= jn) break;
+            const int64_t j = j0 + b;
+            const double q = rint(__dmul_rn(cc.P_inv, c1[b]));   // crt.hpp:113-119
+            const double t1 = __fma_rn(-q, cc.P1, c1[b]);         // crt.hpp:136-138
+            const double t2 = __dadd_rn(t1, c2[b]);
+            const double cpp = __fma_rn(-q, cc.P2, t2);
+            const int64_t o = i * n + j;
+            if (ex.C1) ex.C1[o] = c1[b];
+            if (ex.C2) ex.C2[o] = c2[b];
+            if (ex.Q) ex.Q[o] = q;
+            if (ex.Cpp64) ex.Cpp64[o] = cpp;
+            const int nuj = __ldg(nu + j);
+            if (BND) {
+                const BoundCtx& bc = ex.bnd;
+                const double PBj = bc.v.PB[j], CBj = bc.v.CB[j];
+                const int ebj = bc.v.eb[j];
+                const double base = __dadd_ru(ldexp_ru(__dmul_ru(RAi, PBj), ebj), ldexp_ru(__dmul_ru(PAi, CBj), eai));
+                const double pp = __dmul_ru(PAi, PBj);
+                const double cheap =
+                    __dadd_ru(base, ldexp_ru(__dmul_ru(__dmul_ru(bc.kpr_cheap_up, bc.t2_up), pp), eai + ebj));
+                const double ab_up = __ddiv_ru(__dadd_ru(fabs(cpp), bc.rconst_up), 1.0 - bc.ucoef);
+                const double kpr_t = __dadd_ru(bc.k_rconst_up, __dmul_ru(bc.ucoef, ab_up));
+                const double tight = __dadd_ru(base, ldexp_ru(__dmul_ru(__dmul_ru(kpr_t, bc.t2_up), pp), eai + ebj));
+                if (bc.cheap) bc.cheap[o] = cheap;
+                if (bc.tight) bc.tight[o] = tight;
+                const unsigned long long cb = (unsigned long long)__double_as_longlong(cheap);
+                const unsigned long long tb = (unsigned long long)__double_as_longlong(tight);
+                bmax_cheap = cb > bmax_cheap ? cb : bmax_cheap;
+                bmax_tight = tb > bmax_tight ? tb : bmax_tight;
+            }
+            if constexpr (sizeof(T) == 4) {
+                if (fabs(cpp) >= 0x1.ffffffp+127) { fr_range = true; continue; }  // crt.hpp:144-145
+                const float c32 = __double2float_rn(cpp);
+                if (ex.Cpp32) ex.Cpp32[o] = c32;
+                const float x = ldexpf_rn(c32, -mui);                             // emulate.hpp:37-38
+                const float y = ldexpf_rn(x, -nuj);
+                inv_range |= !isfinite(x) || !isfinite(y);
+                sub |= (x != 0.0f && fabsf(x) < FLT_MIN) || (y != 0.0f && fabsf(y) < FLT_MIN);
+                C[i * ldc + j] = y;
+            } else {
+                const double x = ldexp_rn(cpp, -mui);
+                const double y = ldexp_rn(x, -nuj);
+                inv_range |= !isfinite(x) || !isfinite(y);
+                sub |= (x != 0.0 && fabs(x) < DBL_MIN) || (y != 0.0 && fabs(y) < DBL_MIN);
+                C[i * ldc + j] = y;
+            }
         }
-    };
-    int l = 0;
-    for (; l + 4 <= cc.n; l += 4) {
-        uint2 wv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) wv[u] = __ldg(reinterpret_cast<const uint2*>(wp + (int64_t)(l + u) * wplane));
-#pragma unroll
-        for (int u = 0; u < 4; ++u) fold(wv[u], l + u);
+        if (fr_range) atomicOr(&st->err, (uint32_t)ERR_FR_RANGE);
+        if (inv_range) atomicOr(&st->err, (uint32_t)ERR_INV_RANGE);
+        if (sub) atomicOr(&st->subnormal, 1u);
     }
-    for (; l < cc.n; ++l) fold(__ldg(reinterpret_cast<const uint2*>(wp + (int64_t)l * wplane)), l);
-    const int mui = mu[i];
-    bool fr_range = false, inv_range = false, sub = false;
-#pragma unroll
-    for (int b = 0; b < CV; ++b) {
-        if (b >= jn) break;
-        const int64_t j = j0 + b;
-        const double q = rint(__dmul_rn(cc.P_inv, c1[b]));   // crt.hpp:113-119
-        const double t1 = __fma_rn(-q, cc.P1, c1[b]);         // crt.hpp:136-138
-        const double t2 = __dadd_rn(t1, c2[b]);
-        const double cpp = __fma_rn(-q, cc.P2, t2);
-        const int64_t o = i * n + j;
-        if (ex.C1) ex.C1[o] = c1[b];
-        if (ex.C2) ex.C2[o] = c2[b];
-        if (ex.Q) ex.Q[o] = q;
-        if (ex.Cpp64) ex.Cpp64[o] = cpp;
-        const int nuj = __ldg(nu + j);
-        if constexpr (sizeof(T) == 4) {
-            if (fabs(cpp) >= 0x1.ffffffp+127) { fr_range = true; continue; }  // crt.hpp:144-145
-            const float c32 = __double2float_rn(cpp);
-            if (ex.Cpp32) ex.Cpp32[o] = c32;
-            const float x = ldexpf_rn(c32, -mui);                             // emulate.hpp:37-38
-            const float y = ldexpf_rn(x, -nuj);
-            inv_range |= !isfinite(x) || !isfinite(y);
-            sub |= (x != 0.0f && fabsf(x) < FLT_MIN) || (y != 0.0f && fabsf(y) < FLT_MIN);
-            C[i * ldc + j] = y;
-        } else {
-            const double x = ldexp_rn(cpp, -mui);
-            const double y = ldexp_rn(x, -nuj);
-            inv_range |= !isfinite(x) || !isfinite(y);
-            sub |= (x != 0.0 && fabs(x) < DBL_MIN) || (y != 0.0 && fabs(y) < DBL_MIN);
-            C[i * ldc + j] = y;
+    if (BND) {
+        bmax_cheap = warp_max_u64(bmax_cheap);
+        bmax_tight = warp_max_u64(bmax_tight);
+        if ((threadIdx.x & 31) == 0) {
+            atomicMax(&ex.bnd.max_bits[0], bmax_cheap);
+            atomicMax(&ex.bnd.max_bits[1], bmax_tight);
         }
     }
-    if (fr_range) atomicOr(&st->err, (uint32_t)ERR_FR_RANGE);
-    if (inv_range) atomicOr(&st->err, (uint32_t)ERR_INV_RANGE);
-    if (sub) atomicOr(&st->subnormal, 1u);
+}
+
+template <class T, bool DD>
+void launch_t(unsigned grid, cudaStream_t s, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
+              const CrtConsts& cc, const int32_t* mu, const int32_t* nu, T* C, int64_t ldc, const CrtExtra& ex,
+              DevStatus* st) {
+    if (ex.bnd.on) crt_kernel<T, DD, true><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+    else crt_kernel<T, DD, false><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
 }
 
 }  // namespace
@@ -108,10 +161,10 @@ cudaError_t launch_crt(int prec, const int8_t* W, int64_t ldw, int64_t wplane, i
     if (work == 0) return cudaSuccess;
     const unsigned grid = (unsigned)((work + 255) / 256);
     if (prec) {
-        if (cc.mode == 1) crt_kernel<double, true><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, (double*)C, ldc, extra, st);
-        else crt_kernel<double, false><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, (double*)C, ldc, extra, st);
+        if (cc.mode == 1) launch_t<double, true>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, (double*)C, ldc, extra, st);
+        else launch_t<double, false>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, (double*)C, ldc, extra, st);
     } else {
-        crt_kernel<float, false><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, (float*)C, ldc, extra, st);
+        launch_t<float, false>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, (float*)C, ldc, extra, st);
     }
     return cudaGetLastError();
 }

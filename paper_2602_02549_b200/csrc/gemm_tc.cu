@@ -37,21 +37,20 @@ namespace {
 constexpr int BM = 128, BN = 256, BK = 128, STAGES = 4;
 constexpr int A_BYTES = BM * BK;  // 16 KB
 constexpr int B_BYTES = BN * BK;  // 32 KB
-constexpr int GROUP_M = 8;
 constexpr uint32_t IDESC = idesc_i8(BM, BN);
 constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
 
 struct TileCoord { int l, tm, tn; };
 
-__device__ __forceinline__ TileCoord decode_unit(int u, int tiles_m, int tiles_n) {
+__device__ __forceinline__ TileCoord decode_unit(int u, int tiles_m, int tiles_n, int group_m) {
     const int per_plane = tiles_m * tiles_n;
     TileCoord c;
     c.l = u / per_plane;
     const int t = u - c.l * per_plane;
-    const int group = GROUP_M * tiles_n;
+    const int group = group_m * tiles_n;
     const int g = t / group;
-    const int first_m = g * GROUP_M;
-    const int gm = min(tiles_m - first_m, GROUP_M);
+    const int first_m = g * group_m;
+    const int gm = min(tiles_m - first_m, group_m);
     const int r = t - g * group;
     c.tm = first_m + r % gm;
     c.tn = r / gm;
@@ -156,7 +155,7 @@ __global__ void __launch_bounds__(256, 1)
         int stage = 0;
         uint32_t phase = 0;
         for (int u = blockIdx.x; u < total; u += gridDim.x) {
-            const TileCoord tc = decode_unit(u, P.tiles_m, P.tiles_n);
+            const TileCoord tc = decode_unit(u, P.tiles_m, P.tiles_n, P.group_m);
             for (int kb = 0; kb < P.kblocks; ++kb) {
                 mbar_wait(&empty[stage], phase ^ 1u);
                 if (lane == 0) {
@@ -202,7 +201,7 @@ __global__ void __launch_bounds__(256, 1)
         const int wq = warp - 4;
         int it = 0;
         for (int u = blockIdx.x; u < total; u += gridDim.x, ++it) {
-            const TileCoord tc = decode_unit(u, P.tiles_m, P.tiles_n);
+            const TileCoord tc = decode_unit(u, P.tiles_m, P.tiles_n, P.group_m);
             const int acc = it & 1;
             const uint32_t aph = (uint32_t)((it >> 1) & 1);
             mbar_wait(&tfull[acc], aph);
@@ -237,6 +236,151 @@ __global__ void __launch_bounds__(256, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant: a cluster of 2 CTAs computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 (M = 256, N = 256).  Each CTA loads its 128-row half
+// of A and its 128-row half of B^T per stage (32 KB instead of 48 KB for the
+// same MACs per SM) and keeps its 128 x 256 half of the accumulator in its own
+// TMEM.  The even CTA ("leader") issues the MMAs; its full barrier receives the
+// transaction bytes of both CTAs' TMA loads; MMA completion is committed with
+// multicast to the barriers of both CTAs; both CTAs' epilogue warps release an
+// accumulator stage on the leader's tmem-empty barrier.
+// ---------------------------------------------------------------------------
+constexpr int P_BM = 256, P_BN = 256;     // pair tile
+constexpr int P_HALF = 128;               // rows of A and of B^T per CTA
+constexpr int P_STAGES = 6;
+constexpr int P_STAGE_BYTES = 2 * P_HALF * BK;  // 32 KB per CTA per stage
+constexpr uint32_t P_IDESC = idesc_i8(P_BM, P_BN);
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm_i8_tc_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                           const __grid_constant__ GemmParams P) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+    uint8_t* sA = smem;                                   // [stage][128][128]
+    uint8_t* sB = smem + P_STAGES * P_HALF * BK;          // [stage][128][128]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
+    uint64_t* empty = full + P_STAGES;
+    uint64_t* tfull = empty + P_STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < P_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
+    if (warp == 2) { tmem_alloc_pair(tmem_slot, 512); tmem_relinquish_pair(); }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int clusters = gridDim.x >> 1;
+    const int cid = blockIdx.x >> 1;
+    const int total = P.planes * P.tiles_m * P.tiles_n;
+
+    if (warp == 0) {
+        // ===== TMA producer (both CTAs) =====
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int u = cid; u < total; u += clusters) {
+            const TileCoord tc = decode_unit(u, P.tiles_m, P.tiles_n, P.group_m);
+            const int arow = tc.tm * P_BM + (int)rank * P_HALF;
+            const int brow = tc.tn * P_BN + (int)rank * P_HALF;
+            for (int kb = 0; kb < P.kblocks; ++kb) {
+                mbar_wait(&empty[stage], phase ^ 1u);
+                if (lane == 0) {
+                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
+                    tma_load_3d_pair(sA + stage * P_HALF * BK, &tmA, &full[stage], kb * BK, arow, tc.l, kEvictNormal);
+                    tma_load_3d_pair(sB + stage * P_HALF * BK, &tmB, &full[stage], kb * BK, brow, tc.l, kEvictNormal);
+                }
+                __syncwarp();
+                if (++stage == P_STAGES) { stage = 0; phase ^= 1u; }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer (leader CTA only) =====
+        if (leader) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int u = cid; u < total; u += clusters, ++it) {
+                const int acc = it & 1;
+                const uint32_t aph = (uint32_t)((it >> 1) & 1);
+                mbar_wait(&tempty[acc], aph ^ 1u);
+                tc_fence_after();
+                const uint32_t dtmem = tmem_base + (uint32_t)(acc * P_BN);
+                for (int kb = 0; kb < P.kblocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t a0 = smem_u32(sA + stage * P_HALF * BK);
+                        const uint32_t b0 = smem_u32(sB + stage * P_HALF * BK);
+#pragma unroll
+                        for (int k = 0; k < BK / 32; ++k)
+                            mma_i8_pair(dtmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), P_IDESC,
+                                        (kb | k) != 0 ? 1u : 0u);
+                        mma_commit_pair(&empty[stage], (uint16_t)0x3);
+                    }
+                    __syncwarp();
+                    if (++stage == P_STAGES) { stage = 0; phase ^= 1u; }
+                }
+                if (lane == 0) mma_commit_pair(&tfull[acc], (uint16_t)0x3);
+                __syncwarp();
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== Epilogue (both CTAs): rows tm*256 + rank*128 + [0, 128) =====
+        const int wq = warp - 4;
+        const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
+        int it = 0;
+        for (int u = cid; u < total; u += clusters, ++it) {
+            const TileCoord tc = decode_unit(u, P.tiles_m, P.tiles_n, P.group_m);
+            const int acc = it & 1;
+            const uint32_t aph = (uint32_t)((it >> 1) & 1);
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            const int row = tc.tm * P_BM + (int)rank * P_HALF + wq * 32 + lane;
+            int32_t rowmax = 0;
+#pragma unroll 1
+            for (int c = 0; c < P_BN / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld32(tmem_base + ((uint32_t)(wq * 32) << 16) + (uint32_t)(acc * P_BN + c * 32), v);
+                tmem_ld_wait();
+                const int col0 = tc.tn * P_BN + c * 32;
+                if constexpr (MODE == EPI_MAX) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) rowmax = max(rowmax, (int32_t)v[j]);
+                }
+                epilogue_chunk<MODE>(v, row, col0, tc.l, P);
+            }
+            if constexpr (MODE == EPI_MAX) {
+                if (row < P.m) atomicMax(&P.rowmax[row], rowmax);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * sizeof(uint64_t)));
+        }
+    }
+
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc_pair(tmem_base, 512);
+    }
+}
+
 }  // namespace
 
 int gemm_smem_bytes() { return SMEM_BYTES; }
@@ -268,6 +412,40 @@ cudaError_t launch_gemm_i8(int mode, const CUtensorMap& tmA, const CUtensorMap& 
                                        SMEM_BYTES);
             if (err != cudaSuccess) return err;
             gemm_i8_tc_kernel<EPI_I32><<<grid, 256, SMEM_BYTES, stream>>>(tmA, tmB, P);
+            break;
+    }
+    return cudaGetLastError();
+}
+
+int gemm_pair_tile_m() { return P_BM; }
+int gemm_pair_tile_n() { return P_BN; }
+int gemm_pair_box_rows() { return P_HALF; }
+
+cudaError_t launch_gemm_i8_pair(int mode, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& P,
+                                int num_sms, cudaStream_t stream) {
+    const int total = P.planes * P.tiles_m * P.tiles_n;  // pair tiles
+    if (total == 0) return cudaSuccess;
+    const int pairs = num_sms / 2;
+    const int grid = 2 * (total < pairs ? total : pairs);
+    cudaError_t err = cudaSuccess;
+    switch (mode) {
+        case EPI_MAX:
+            err = cudaFuncSetAttribute(gemm_i8_tc_pair_kernel<EPI_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       P_SMEM_BYTES);
+            if (err != cudaSuccess) return err;
+            gemm_i8_tc_pair_kernel<EPI_MAX><<<grid, 256, P_SMEM_BYTES, stream>>>(tmA, tmB, P);
+            break;
+        case EPI_RESID:
+            err = cudaFuncSetAttribute(gemm_i8_tc_pair_kernel<EPI_RESID>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
+            if (err != cudaSuccess) return err;
+            gemm_i8_tc_pair_kernel<EPI_RESID><<<grid, 256, P_SMEM_BYTES, stream>>>(tmA, tmB, P);
+            break;
+        default:
+            err = cudaFuncSetAttribute(gemm_i8_tc_pair_kernel<EPI_I32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       P_SMEM_BYTES);
+            if (err != cudaSuccess) return err;
+            gemm_i8_tc_pair_kernel<EPI_I32><<<grid, 256, P_SMEM_BYTES, stream>>>(tmA, tmB, P);
             break;
     }
     return cudaGetLastError();

@@ -16,6 +16,7 @@ struct GemmParams {
     int kblocks;              // kp / 128
     int planes;               // number of (A_l, B_l) pairs
     int tiles_m, tiles_n;
+    int group_m;              // tile-rows per raster group (L2 reuse of the B operand)
     // EPI_MAX
     int32_t* rowmax;
     int32_t* colmax;
@@ -34,6 +35,11 @@ int gemm_tile_n();
 int gemm_tile_k();
 cudaError_t launch_gemm_i8(int mode, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& P,
                            int num_sms, cudaStream_t stream);
+int gemm_pair_tile_m();
+int gemm_pair_tile_n();
+int gemm_pair_box_rows();
+cudaError_t launch_gemm_i8_pair(int mode, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& P,
+                                int num_sms, cudaStream_t stream);
 
 // Residue constants for the residue kernels (uploaded once per table): a
 // header followed by the weight table w[l][E] (E in [0, kResidE)) of two packed
@@ -74,15 +80,37 @@ cudaError_t launch_trunc_scaled(int prec, const void* X, int64_t ldx, int64_t ro
                                 const int32_t* shift, int by_col, double* out, cudaStream_t s);
 cudaError_t launch_log2f(const float* x, float* out, int64_t count, cudaStream_t s);
 
+// Error-bound factors (bounds.cu): RA_i = t (|A|v)_i, PA_i = sqrt(max(1, rowmax_i)),
+// ea_i = alpha_i; CB_j, PB_j, eb_j likewise for the columns of B (all rounded up).
+struct BoundVecs {
+    double *RA, *PA, *CB, *PB;
+    int32_t *ea, *eb;
+};
+cudaError_t launch_bound_vectors(int prec, const void* A, int64_t lda, int64_t m, const void* B, int64_t ldb,
+                                 int64_t k, int64_t n, const int32_t* cmax_row, const int32_t* cmax_col,
+                                 const int32_t* mu_prime, const int32_t* nu_prime, double t_up, double* scratch,
+                                 const BoundVecs& v, cudaStream_t s);
+size_t bound_scratch_doubles(int64_t m, int64_t n, int64_t k);
+cudaError_t launch_dd_gemm(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t m, int64_t n,
+                           int64_t k, double* Chi, double* Clo, int64_t ldc, cudaStream_t s);
+
 // CRT + inverse scaling (crt.cu).
 struct CrtConsts {
     int n, mode;
     double s1[49], s2[49];
     double P1, P2, P_inv;
 };
+struct BoundCtx {  // evaluated in the CRT pass when `on`
+    int on;
+    BoundVecs v;
+    double t2_up, rconst_up, ucoef, kpr_cheap_up, k_rconst_up;
+    double *cheap, *tight;             // optional m x n outputs (device)
+    unsigned long long* max_bits;      // [0] cheap max, [1] tight max (bits of positive doubles)
+};
 struct CrtExtra {  // optional device outputs (nullptr = skip)
     double *C1, *C2, *Q, *Cpp64;
     float* Cpp32;
+    BoundCtx bnd;
 };
 cudaError_t launch_crt(int prec, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
                        const CrtConsts& cc, const int32_t* mu, const int32_t* nu, void* C, int64_t ldc,

@@ -316,6 +316,40 @@ const Table& table_for(int n, int mode) {
     return it->second;
 }
 
+// Upward-rounded fp64 image of a positive extended-precision value whose
+// relative error is far below 2^-60: round to nearest, then step up twice.
+static double up2(long double v) {
+    double d = (double)v;
+    d = std::nextafter(d, INFINITY);
+    return std::nextafter(d, INFINITY);
+}
+
+BoundScalars bound_scalars(const Table& t, int64_t k) {
+    // P and rho as extended precision (relative error 2^-64)
+    long double P = 0.0L;
+    for (char ch : t.P_dec) P = P * 10.0L + (long double)(ch - '0');
+    const long double rho = (long double)t.rho;
+    const long double u64 = 0x1p-53L, u32 = 0x1p-24L;
+    BoundScalars b;
+    const long double denom = 32.0L * (P - 1.0L);
+    b.t_up = up2(1.0L / sqrtl(denom));   // bounds.hpp:132-141
+    b.t2_up = up2(1.0L / denom);
+    long double rc;                      // bounds.hpp:74-81
+    if (t.mode == kF32) {
+        rc = (1.0L + u32) * (long double)(t.n + 2) * u64 * rho * P;
+        b.ucoef = 0x1p-24;
+    } else {
+        int clr = 0;
+        while ((1l << clr) < t.rho) ++clr;
+        rc = (1.0L + 3.0L * u64) * ldexpl(1.0L, 1 + clr) * (long double)(t.n + 2) * u64 * u64 * rho * P;
+        b.ucoef = 3.0 * 0x1p-53;
+    }
+    b.rconst_up = up2(rc);
+    b.kpr_cheap_up = up2((long double)k + rc + (long double)b.ucoef * P / 2.0L);  // bounds.hpp:89-92, :201
+    b.k_rconst_up = up2((long double)k + rc);
+    return b;
+}
+
 int fp32_safe_moduli_max() {  // moduli.hpp:157-170
     static const int value = [] {
         const Big limit = Big::of((1u << 24) - 1).shl(105);

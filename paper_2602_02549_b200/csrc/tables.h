@@ -23,6 +23,18 @@ struct Table {
 };
 
 const Table& table_for(int n, int mode);  // throws std::domain_error for N outside [2, 49]
+
+// Scalars of the deterministic error bounds (bounds.hpp:71-92, :132-141),
+// every one rounded upward (u_coef and 1 - u_coef are exact).
+struct BoundScalars {
+    double t_up;         // >= 1 / sqrt(2^5 (P - 1))
+    double t2_up;        // >= 1 / (2^5 (P - 1))
+    double rconst_up;    // >= r_const (R_b without the u|A'B'| term)
+    double ucoef;        // u_coef: 2^-24 (fp32) or 3 * 2^-53 (fp64)
+    double kpr_cheap_up; // >= k + r_const + u_coef * P / 2
+    double k_rconst_up;  // >= k + r_const
+};
+BoundScalars bound_scalars(const Table& t, int64_t k);
 int fp32_safe_moduli_max();
 float fp32_round_up(int64_t v);
 int shift_of_cmax(float p_prime, int64_t c, float* e_out);

@@ -130,6 +130,7 @@ class EmulationResult:
     subnormal: bool
     kernels_launched: int = 0
     stage_ms: tuple = ()
+    bounds: Optional[dict] = None
 
 
 def _is_torch_cuda(x) -> bool:
@@ -137,7 +138,7 @@ def _is_torch_cuda(x) -> bool:
 
 
 def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = False, out=None,
-          stream=None, timing: bool = False,
+          stream=None, timing: bool = False, bounds=False,
           reduce_maxima: Optional[Callable] = None) -> EmulationResult:
     """C ~ A*B by Ozaki-II accurate mode with `n` moduli (emulate.hpp:54-88).
 
@@ -145,8 +146,11 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
     (row-major, unit column stride).  The precision of the call follows the
     dtype, like os_ii<float> / os_ii<double>.  `keep_intermediates` returns the
     reference's ScalingOutput/CrtIntermediates fields; `evidence` also returns
-    the residue planes and wrapped INT32 products.  `reduce_maxima(row_ptr,
-    m, col_ptr, n, stream)` is the multi-GPU hook of oz2g.h.
+    the residue planes and wrapped INT32 products.  `bounds=True` evaluates the
+    paper's error bounds (bounds.hpp) and returns their maxima;
+    `bounds="full"` also returns the m x n cheap / tight bound matrices (same
+    memory space as the inputs).  `reduce_maxima(row_ptr, m, col_ptr, n,
+    stream)` is the multi-GPU hook of oz2g.h.
     """
     L = _lib.load()
     dev = _is_torch_cuda(a)
@@ -216,6 +220,23 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
                 arr = np.zeros(shape, dtype=dt)
                 keep[name] = (holder, arr)
                 setattr(inter_c, name, arr.ctypes.data)
+    bnd_c, bnd_arrays = None, {}
+    if bounds and 2 <= int(n) <= K_MAX_MODULI:
+        if inter_c is None:
+            inter_c = _lib.Intermediates()
+        bnd_c = _lib.Bounds()
+        if bounds == "full":
+            for name in ("cheap", "tight"):
+                if dev:
+                    import torch
+                    arr = torch.empty((m, nn), dtype=torch.float64, device=a.device)
+                    setattr(bnd_c, name, arr.data_ptr())
+                else:
+                    arr = np.zeros((m, nn), dtype=np.float64)
+                    setattr(bnd_c, name, arr.ctypes.data)
+                bnd_arrays[name] = arr
+            bnd_c.device = 1 if dev else 0
+        inter_c.bounds = C.cast(C.pointer(bnd_c), C.c_void_p)
 
     diag = _lib.Diag()
     if reduce_maxima is not None:
@@ -236,8 +257,25 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
     _check(rc)
     for name, (holder, arr) in keep.items():
         setattr(holder, name, arr)
+    bres = None
+    if bnd_c is not None:
+        bres = dict(cheap_max=bnd_c.cheap_max, tight_max=bnd_c.tight_max, **bnd_arrays)
     return EmulationResult(C=C_out, scaling=sc, crt=cr, table=table_for(n, prec), subnormal=bool(diag.subnormal),
-                           kernels_launched=diag.kernels_launched, stage_ms=tuple(diag.stage_ms))
+                           kernels_launched=diag.kernels_launched, stage_ms=tuple(diag.stage_ms), bounds=bres)
+
+
+def dd_gemm(a, b):
+    """Double-double reference product (hi, lo) of CUDA fp64 tensors on the
+    device (oz2g_dd_gemm); used to measure the emulation error."""
+    import torch
+    m, k = a.shape
+    nn = b.shape[1]
+    hi = torch.empty((m, nn), dtype=torch.float64, device=a.device)
+    lo = torch.empty_like(hi)
+    st = torch.cuda.current_stream(a.device).cuda_stream
+    _check(_lib.load().oz2g_dd_gemm(m, nn, k, a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0),
+                                    hi.data_ptr(), lo.data_ptr(), nn, C.c_void_p(int(st))))
+    return hi, lo
 
 
 def device_log2f(x_dev, out_dev, stream=None) -> None:

@@ -1,0 +1,77 @@
+"""Error bounds and measured error on the GPU.
+
+* The device-evaluated cheap / tight bounds are certificates: never below the
+  formula of bounds.hpp (evaluated here to ~2^-300 by oracle/bounds.py) and
+  within a few ulps above it.
+* The actual error |C - AB| (exact AB as Fractions) is below both bounds for
+  every entry — the paper's Theorem 2 on our outputs (SPEC: zero tolerance).
+* The double-double reference GEMM used at scale matches exact products.
+"""
+from fractions import Fraction
+
+import mpmath
+import numpy as np
+import pytest
+
+import paper_2602_02549_b200 as oz
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("m,k,n,phi,N,dt", [
+    (9, 40, 7, 0.0, 8, np.float64), (9, 40, 7, 2.0, 14, np.float64), (6, 64, 5, 8.0, 20, np.float64),
+    (12, 33, 10, 0.5, 16, np.float64), (7, 20, 6, 1.0, 9, np.float32), (8, 50, 8, 0.0, 16, np.float32),
+])
+def test_bounds_are_certificates(cuda, oracle, m, k, n, phi, N, dt):
+    from oracle import bounds as OB
+    A = oracle.gen_matrix(m, k, phi, oracle.derive_seed(11, m, 0), dt)
+    B = oracle.gen_matrix(k, n, phi, oracle.derive_seed(11, n, 1), dt)
+    ref = oracle.os_ii(A, B, N, keep_intermediates=True)
+    got = oz.os_ii(A, B, N, bounds="full")
+    assert np.array_equal(got.C, ref.C)
+    cheap_or, tight_or = OB.bounds(A, B, N, ref.inter["cmax_row"], ref.inter["cmax_col"],
+                                   ref.inter["Aprime"], ref.inter["Bprime"])
+    exact = OB.exact_product(A, B)
+    bc, bt = got.bounds["cheap"], got.bounds["tight"]
+    mpmath.mp.prec = 320
+    for i in range(m):
+        for j in range(n):
+            c_or, t_or = cheap_or[i][j], tight_or[i][j]
+            assert mpmath.mpf(bc[i, j]) >= c_or                      # sound
+            assert mpmath.mpf(bc[i, j]) <= c_or * (1 + mpmath.mpf(2) ** -45)   # tight
+            assert mpmath.mpf(bt[i, j]) >= t_or
+            # the device replaces the exact |A'B'| by (|C''| + r_const)/(1 - u): at most ~u r_const looser
+            assert mpmath.mpf(bt[i, j]) <= t_or * (1 + mpmath.mpf(2) ** -20)
+            assert bt[i, j] <= bc[i, j]
+            err = abs(Fraction(float(got.C[i, j])) - exact[i][j])
+            assert mpmath.mpf(err.numerator) / err.denominator <= t_or   # Theorem 2 on our output
+    assert got.bounds["cheap_max"] == bc.max() and got.bounds["tight_max"] == bt.max()
+
+
+def test_dd_gemm_matches_exact(cuda, oracle):
+    import torch
+    from oracle import bounds as OB
+    A = oracle.gen_matrix(37, 130, 3.0, 5)
+    B = oracle.gen_matrix(130, 29, 3.0, 6)
+    hi, lo = oz.dd_gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    hi, lo = hi.cpu().numpy(), lo.cpu().numpy()
+    exact = OB.exact_product(A, B)
+    absab = np.abs(A) @ np.abs(B)
+    for i in range(37):
+        for j in range(29):
+            err = abs(Fraction(hi[i, j]) + Fraction(lo[i, j]) - exact[i][j])
+            assert err <= Fraction(absab[i, j]) * Fraction(1, 1 << 95)
+
+
+def test_bounds_device_tensors(cuda, oracle):
+    import torch
+    A = oracle.gen_matrix(300, 257, 0.0, 1)
+    B = oracle.gen_matrix(257, 200, 0.0, 2)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    r = oz.os_ii(dA, dB, 16, bounds="full")
+    hi, lo = oz.dd_gemm(dA, dB)
+    err = ((r.C - hi) - lo).abs()
+    assert bool((err <= r.bounds["tight"]).all())
+    assert bool((r.bounds["tight"] <= r.bounds["cheap"]).all())
+    host = oz.os_ii(A, B, 16, bounds=True)
+    assert host.bounds["tight_max"] == float(r.bounds["tight"].max())
