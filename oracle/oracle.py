@@ -255,3 +255,76 @@ def os_ii(A: np.ndarray, B: np.ndarray, n: int, keep_intermediates: bool = False
     if rc != 0:
         raise _EXC.get(rc, RuntimeError)(out.msg.decode())
     return OracleResult(C=Cm, subnormal=bool(out.subnormal), table=M.build_table(n, prec), inter=inter)
+
+
+# ---------------------------------------------------------------- sampled full-size checks
+def _setup_sampled():
+    L = lib()
+    if getattr(L, "_sampled_ready", False):
+        return L
+    L.ora_pre_exponents.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+    L.ora_ceil_scale.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int, C.c_void_p]
+    L.ora_cbar_row_max.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]
+    L.ora_cbar_col_max.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
+                                   C.c_void_p]
+    L.ora_entries.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
+                              C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(_Table), C.c_void_p]
+    L._sampled_ready = True
+    return L
+
+
+def pre_exponents(X: np.ndarray, by_col: bool) -> np.ndarray:
+    """scaling.hpp:86-107 (mu' of every row, or nu' of every column)."""
+    L = _setup_sampled()
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    out = np.empty(X.shape[1] if by_col else X.shape[0], dtype=np.int16)
+    if L.ora_pre_exponents(X.ctypes.data, X.shape[0], X.shape[1], int(by_col), out.ctypes.data) != 0:
+        raise OracleDomainError("zero row/column or non-finite entry")
+    return out
+
+
+def ceil_scale(X: np.ndarray, sft: np.ndarray, by_col: bool) -> np.ndarray:
+    """Abar / Bbar, scaling.hpp:111-131."""
+    L = _setup_sampled()
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    sft = np.ascontiguousarray(sft, dtype=np.int16)
+    out = np.empty(X.shape, dtype=np.int8)
+    if L.ora_ceil_scale(X.ctypes.data, X.shape[0], X.shape[1], sft.ctypes.data, int(by_col), out.ctypes.data) != 0:
+        raise OracleLogicError("ceil_abs_scaled")
+    return out
+
+
+def cbar_row_max(abar, bbar, rows) -> np.ndarray:
+    L = _setup_sampled()
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.empty(len(rows), dtype=np.int32)
+    L.ora_cbar_row_max(abar.ctypes.data, bbar.ctypes.data, abar.shape[1], bbar.shape[1], rows.ctypes.data,
+                       len(rows), out.ctypes.data)
+    return out
+
+
+def cbar_col_max(abar, bbar, cols) -> np.ndarray:
+    L = _setup_sampled()
+    cols = np.ascontiguousarray(cols, dtype=np.int64)
+    out = np.empty(len(cols), dtype=np.int32)
+    L.ora_cbar_col_max(abar.ctypes.data, bbar.ctypes.data, abar.shape[0], abar.shape[1], bbar.shape[1],
+                       cols.ctypes.data, len(cols), out.ctypes.data)
+    return out
+
+
+def entries(A, B, n, mu, nu, rows, cols, prec=1) -> np.ndarray:
+    """C_ij of os_ii for the given (i, j) pairs, with the given mu / nu."""
+    L = _setup_sampled()
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    B = np.ascontiguousarray(B, dtype=np.float64)
+    mu = np.ascontiguousarray(mu, dtype=np.int16)
+    nu = np.ascontiguousarray(nu, dtype=np.int16)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    cols = np.ascontiguousarray(cols, dtype=np.int64)
+    out = np.empty(len(rows), dtype=np.float64 if prec else np.float32)
+    tab = table(n, prec)
+    rc = L.ora_entries(prec, A.ctypes.data, B.ctypes.data, A.shape[1], B.shape[1], mu.ctypes.data, nu.ctypes.data,
+                       rows.ctypes.data, cols.ctypes.data, len(rows), C.byref(tab), out.ctypes.data)
+    if rc != 0:
+        raise _EXC.get(rc, RuntimeError)("ora_entries")
+    return out

@@ -676,3 +676,127 @@ int64_t ora_log2f_monotone_violations(void) {
 void ora_log2f_array(const float *x, int64_t count, float *out) {
     for (int64_t i = 0; i < count; ++i) out[i] = ora_log2_fp32(x[i]);
 }
+
+/* ---------------------------------------------------------------------------
+ * Sampled full-size checks (test infrastructure): pieces of os_ii evaluated
+ * exactly as above for selected rows / columns / entries, so that a device
+ * result at BASELINE sizes (16384^3) can be verified without the O(N m n k)
+ * CPU emulation.
+ * ------------------------------------------------------------------------- */
+
+/* scaling.hpp:86-107 for every row of A (m x k) / column of B (k x n);
+ * returns ORA_DOMAIN on a zero row / column or non-finite entry. */
+int ora_pre_exponents(const double *X, int64_t rows, int64_t cols, int by_col, int16_t *out) {
+    const int64_t cnt = by_col ? cols : rows, len = by_col ? rows : cols;
+    for (int64_t t = 0; t < cnt; ++t) {
+        double mx = 0;
+        for (int64_t h = 0; h < len; ++h) {
+            const double v = fabs(by_col ? X[h * cols + t] : X[t * cols + h]);
+            if (!isfinite(v)) return ORA_DOMAIN;
+            mx = v > mx ? v : mx;
+        }
+        if (mx == 0.0) return ORA_DOMAIN;
+        out[t] = (int16_t)(5l - ilogb(mx));
+    }
+    return ORA_OK;
+}
+
+/* Abar / Bbar (scaling.hpp:111-131) as int8 matrices in the reference layout. */
+typedef struct { const double *x; int64_t rows, cols; const int16_t *sft; int by_col; int8_t *out; volatile int err; } cs_ctx;
+static void cs_row(int64_t i, void *v) {
+    cs_ctx *c = (cs_ctx *)v;
+    for (int64_t h = 0; h < c->cols; ++h)
+        if (ceil_abs_scaled(c->x[i * c->cols + h], c->by_col ? c->sft[h] : c->sft[i], &c->out[i * c->cols + h]) != ORA_OK)
+            c->err = 1;
+}
+int ora_ceil_scale(const double *X, int64_t rows, int64_t cols, const int16_t *sft, int by_col, int8_t *out) {
+    cs_ctx c = {X, rows, cols, sft, by_col, out, 0};
+    parallel_for(rows, cs_row, &c);
+    return c.err ? ORA_LOGIC : ORA_OK;
+}
+
+/* Row maxima of Cbar = Abar * Bbar for selected rows (scaling.hpp:175-183). */
+int ora_cbar_row_max(const int8_t *abar, const int8_t *bbar, int64_t k, int64_t n, const int64_t *rows,
+                     int64_t count, int32_t *out) {
+    int32_t *acc = (int32_t *)xmalloc(sizeof(int32_t) * (size_t)n);
+    for (int64_t q = 0; q < count; ++q) {
+        memset(acc, 0, sizeof(int32_t) * (size_t)n);
+        const int8_t *a = abar + rows[q] * k;
+        for (int64_t h = 0; h < k; ++h) {
+            const int32_t av = a[h];
+            if (!av) continue;
+            const int8_t *b = bbar + h * n;
+            for (int64_t j = 0; j < n; ++j) acc[j] += av * (int32_t)b[j];
+        }
+        int32_t mx = 0;
+        for (int64_t j = 0; j < n; ++j) mx = acc[j] > mx ? acc[j] : mx;
+        out[q] = mx;
+    }
+    free(acc);
+    return ORA_OK;
+}
+
+/* Column maxima of Cbar for selected columns (scaling.hpp:184-192). */
+int ora_cbar_col_max(const int8_t *abar, const int8_t *bbar, int64_t m, int64_t k, int64_t n, const int64_t *cols,
+                     int64_t count, int32_t *out) {
+    int8_t *bc = (int8_t *)xmalloc((size_t)k);
+    for (int64_t q = 0; q < count; ++q) {
+        for (int64_t h = 0; h < k; ++h) bc[h] = bbar[h * n + cols[q]];
+        int32_t mx = 0;
+        for (int64_t i = 0; i < m; ++i) {
+            const int8_t *a = abar + i * k;
+            int32_t s = 0;
+            for (int64_t h = 0; h < k; ++h) s += (int32_t)a[h] * (int32_t)bc[h];
+            mx = s > mx ? s : mx;
+        }
+        out[q] = mx;
+    }
+    free(bc);
+    return ORA_OK;
+}
+
+/* C entries (i, j) by the reference pipeline given the scaling exponents
+ * mu_i, nu_j: trunc (scaling.hpp:199-225), residues (crt.hpp:32-53), the N
+ * wrapped dot products and signed mod (crt.hpp:69-79), accumulate / Q /
+ * final_reduce (crt.hpp:91-150), inverse_scale (emulate.hpp:30-46).
+ * prec: 0 fp32 (C out as float), 1 fp64. */
+int ora_entries(int prec, const double *A, const double *B, int64_t k, int64_t n, const int16_t *mu,
+                const int16_t *nu, const int64_t *ri, const int64_t *cj, int64_t count, const ora_table *t,
+                void *out) {
+    const int N = t->n;
+    int8_t *ar = (int8_t *)xmalloc((size_t)k), *bc = (int8_t *)xmalloc((size_t)k);
+    for (int64_t q = 0; q < count; ++q) {
+        const int64_t i = ri[q], j = cj[q];
+        double c1 = 0.0, c2 = 0.0;
+        for (int l = 0; l < N; ++l) {
+            const int p = t->p[l];
+            for (int64_t h = 0; h < k; ++h) {
+                const double a = trunc(ldexp(A[i * k + h], mu[i]));
+                const double b = trunc(ldexp(B[h * n + j], nu[j]));
+                if (!isfinite(a) || !isfinite(b)) { free(ar); free(bc); return ORA_RANGE; }
+                ora_residue_of(a, p, &ar[h]);
+                ora_residue_of(b, p, &bc[h]);
+            }
+            uint32_t acc = 0;
+            for (int64_t h = 0; h < k; ++h) acc += (uint32_t)((int32_t)ar[h] * (int32_t)bc[h]);
+            long long v = signed_mod_ll((long long)(int32_t)acc, p);
+            if (2 * v == p) v = -v;
+            const double wv = (double)(int8_t)v;
+            c1 = fma(t->s1[l], wv, c1);
+            if (t->mode == 1) c2 = fma(t->s2[l], wv, c2);
+        }
+        const double qv = round_nearest_even(t->P_inv * c1);
+        const double t1 = fma(-qv, t->P1, c1);
+        const double t2 = t1 + c2;
+        const double cpp = fma(-qv, t->P2, t2);
+        if (prec == 0) {
+            const float x = ldexpf((float)cpp, -mu[i]);
+            ((float *)out)[q] = ldexpf(x, -nu[j]);
+        } else {
+            const double x = ldexp(cpp, -mu[i]);
+            ((double *)out)[q] = ldexp(x, -nu[j]);
+        }
+    }
+    free(ar); free(bc);
+    return ORA_OK;
+}

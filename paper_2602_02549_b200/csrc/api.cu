@@ -67,11 +67,30 @@ struct DevBuf {
     }
 };
 
+// Host-pointer calls on large problems are pipelined in row chunks of A / C
+// (see run_gemm): uploads of A overlap the row scan and the clearance GEMM,
+// and the download of each finished C row block overlaps the next block.
+constexpr int kPipeChunks = 8;
+
 struct Workspace {
     DevBuf A, B, C, abar, bbar, ares, bres, W, mup, nup, mu, nu, bmax, cmax_row, cmax_col, e, f, status;
     DevBuf x_cbar, x_cprod, x_c1, x_c2, x_q, x_cpp64, x_cpp32, x_ap, x_bp, x_bvec, x_bscr, x_bmax, x_bcheap, x_btight;
     std::map<std::pair<int, int>, ResidConsts*> rc;  // device copies of residue constants
     int num_sms = 0;
+    // copy streams / events of the pipelined host-pointer path
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_b = nullptr, ev_done = nullptr;
+    cudaEvent_t ev_a[kPipeChunks] = {}, ev_c[kPipeChunks] = {};
+    void ensure_streams() {
+        if (s_h2d) return;
+        CUDA_TRY(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&ev_start, &ev_b, &ev_done}) CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        for (int c = 0; c < kPipeChunks; ++c) {
+            CUDA_TRY(cudaEventCreateWithFlags(&ev_a[c], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&ev_c[c], cudaEventDisableTiming));
+        }
+    }
     void release() {
         for (DevBuf* b : {&A, &B, &C, &abar, &bbar, &ares, &bres, &W, &mup, &nup, &mu, &nu, &bmax, &cmax_row,
                           &cmax_col, &e, &f, &status, &x_cbar, &x_cprod, &x_c1, &x_c2, &x_q, &x_cpp64, &x_cpp32,
@@ -98,10 +117,13 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // 3-D uint8 tensor [planes][rows][kp] (kp contiguous), box {128, box_rows, 1}, 128-B swizzle.
-CUtensorMap make_plane_map(const void* base, int64_t kp, int64_t rows, int64_t planes, int box_rows) {
+// plane_stride (bytes) defaults to rows * kp; a larger stride addresses a row
+// block of every plane.
+CUtensorMap make_plane_map(const void* base, int64_t kp, int64_t rows, int64_t planes, int box_rows,
+                           int64_t plane_stride = 0) {
     CUtensorMap tm;
     cuuint64_t dims[3] = {(cuuint64_t)kp, (cuuint64_t)rows, (cuuint64_t)planes};
-    cuuint64_t strides[2] = {(cuuint64_t)kp, (cuuint64_t)(kp * rows)};
+    cuuint64_t strides[2] = {(cuuint64_t)kp, (cuuint64_t)(plane_stride ? plane_stride : kp * rows)};
     cuuint32_t box[3] = {128u, (cuuint32_t)box_rows, 1u};
     cuuint32_t estr[3] = {1u, 1u, 1u};
     CUresult r = get_encode()(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box,
@@ -236,13 +258,33 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     const void* dB = B;
     void* dC = C;
     int64_t lda_d = lda, ldb_d = ldb, ldc_d = ldc;
+    // pipelined host path: plain calls (no intermediates / multi-GPU hook) on large problems
+    const bool pipe = host && inter == nullptr && reduce_fn == nullptr && m >= 2048 && n >= 256;
+    const int64_t chunk_rows = pipe ? round_up((m + kPipeChunks - 1) / kPipeChunks, 256) : m;
+    const int nchunks = m > 0 ? (int)((m + chunk_rows - 1) / chunk_rows) : 1;
     if (host) {
         dA = ws.A.get(esz * (size_t)(m * k));
         dB = ws.B.get(esz * (size_t)(k * n));
         dC = ws.C.get(esz * (size_t)(m * n));
         lda_d = k; ldb_d = n; ldc_d = n;
-        if (m * k) CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dA), esz * k, A, esz * lda, esz * k, m, cudaMemcpyHostToDevice, stream));
-        if (k * n) CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dB), esz * n, B, esz * ldb, esz * n, k, cudaMemcpyHostToDevice, stream));
+        if (pipe) {
+            ws.ensure_streams();
+            CUDA_TRY(cudaEventRecord(ws.ev_start, stream));
+            CUDA_TRY(cudaStreamWaitEvent(ws.s_h2d, ws.ev_start, 0));
+            // B first: the column scan needs all of it
+            CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dB), esz * n, B, esz * ldb, esz * n, k, cudaMemcpyHostToDevice, ws.s_h2d));
+            CUDA_TRY(cudaEventRecord(ws.ev_b, ws.s_h2d));
+            for (int c = 0; c < nchunks; ++c) {
+                const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
+                CUDA_TRY(cudaMemcpy2DAsync((char*)const_cast<void*>(dA) + esz * (size_t)(r0 * k), esz * k,
+                                           (const char*)A + esz * (size_t)(r0 * lda), esz * lda, esz * k, rc,
+                                           cudaMemcpyHostToDevice, ws.s_h2d));
+                CUDA_TRY(cudaEventRecord(ws.ev_a[c], ws.s_h2d));
+            }
+        } else {
+            if (m * k) CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dA), esz * k, A, esz * lda, esz * k, m, cudaMemcpyHostToDevice, stream));
+            if (k * n) CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dB), esz * n, B, esz * ldb, esz * n, k, cudaMemcpyHostToDevice, stream));
+        }
     }
     tm.mark();
 
@@ -264,14 +306,12 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     if (m) CUDA_TRY(cudaMemsetAsync(cmax_row, 0, 4 * (size_t)m, stream));
     if (n) CUDA_TRY(cudaMemsetAsync(cmax_col, 0, 4 * (size_t)n, stream));
 
-    // ---- K1: pre-exponents and Abar / Bbar^T ----
-    CUDA_TRY(launch_row_scan_A(prec, dA, lda_d, m, k, kp, mup, abar, st, stream)); launches += m > 0;
+    // ---- K1 (B): column pre-exponents and Bbar^T ----
+    if (pipe) CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_b, 0));
     CUDA_TRY(launch_col_max_B(prec, dB, ldb_d, k, n, bmax, st, stream)); launches += n > 0;
     CUDA_TRY(launch_col_exp_B(bmax, n, nup, st, stream)); launches += n > 0;
     CUDA_TRY(launch_bbar_T(prec, dB, ldb_d, k, n, kp, nup, bbar, st, stream)); launches += n > 0;
-    tm.mark();
 
-    // ---- K2: clearance product, fused row/col maxima ----
     // tile shape: single-CTA 128x256 tiles or CTA-pair 256x256 tiles (cta_group::2)
     const bool pair = use_pair_gemm();
     const int BM = pair ? gemm_pair_tile_m() : gemm_tile_m();
@@ -283,32 +323,45 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     };
     GemmParams gp;
     std::memset(&gp, 0, sizeof gp);
-    gp.m = (int)m;
     gp.n = (int)n;
     gp.kblocks = (int)(kp / 128);
-    gp.tiles_m = (int)((m + BM - 1) / BM);
     gp.tiles_n = (int)((n + BN - 1) / BN);
-    gp.group_m = group_m_for(gp.tiles_m);
-    if (m > 0 && n > 0) {
-        const CUtensorMap tA = make_plane_map(abar, kp, m, 1, boxA);
-        const CUtensorMap tB = make_plane_map(bbar, kp, n, 1, boxB);
-        gp.planes = 1;
-        gp.rowmax = cmax_row;
-        gp.colmax = cmax_col;
-        CUDA_TRY(launch_gemm(EPI_MAX, tA, tB, gp)); ++launches;
-        if (inter && inter->Cbar) {
-            GemmParams g2 = gp;
-            g2.C32 = (int32_t*)ws.x_cbar.get(4 * (size_t)(m * n));
-            g2.ldc32 = n;
-            g2.cplane = m * n;
-            CUDA_TRY(launch_gemm(EPI_I32, tA, tB, g2)); ++launches;
+    auto set_rows = [&](GemmParams& g, int64_t rows) {
+        g.m = (int)rows;
+        g.tiles_m = (int)((rows + BM - 1) / BM);
+        g.group_m = group_m_for(g.tiles_m);
+    };
+
+    // ---- K1 (A) + K2 per row chunk: row pre-exponents, Abar, clearance product with fused maxima ----
+    for (int c = 0; c < nchunks; ++c) {
+        const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
+        if (pipe) CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_a[c], 0));
+        CUDA_TRY(launch_row_scan_A(prec, (const char*)dA + esz * (size_t)(r0 * lda_d), lda_d, rc, k, kp, mup + r0,
+                                   abar + r0 * kp, st, stream, r0)); launches += rc > 0;
+        if (nchunks == 1) tm.mark();  // end of the scaling scans
+        if (rc > 0 && n > 0) {
+            const CUtensorMap tA = make_plane_map(abar + r0 * kp, kp, rc, 1, boxA);
+            const CUtensorMap tB = make_plane_map(bbar, kp, n, 1, boxB);
+            set_rows(gp, rc);
+            gp.planes = 1;
+            gp.rowmax = cmax_row + r0;
+            gp.colmax = cmax_col;
+            CUDA_TRY(launch_gemm(EPI_MAX, tA, tB, gp)); ++launches;
+            if (inter && inter->Cbar) {
+                GemmParams g2 = gp;
+                g2.C32 = (int32_t*)ws.x_cbar.get(4 * (size_t)(m * n));
+                g2.ldc32 = n;
+                g2.cplane = m * n;
+                CUDA_TRY(launch_gemm(EPI_I32, tA, tB, g2)); ++launches;
+            }
         }
+        if (nchunks == 1) tm.mark();  // end of the clearance product
     }
+    if (nchunks > 1) { tm.mark(); tm.mark(); }
     if (reduce_fn) {
         if (reduce_fn(cmax_row, m, cmax_col, n, (void*)stream, reduce_user) != 0)
             throw Fail{OZ2G_CUDA_ERROR, "oz2g_gemm: reduce_maxima callback failed"};
     }
-    tm.mark();
 
     // ---- K3: scaling exponents ----
     CUDA_TRY(launch_exponents(cmax_row, m, cmax_col, n, mup, nup, tab.shift0, tab.nthr, tab.thr, mu, nu, ev, fv, st,
@@ -330,27 +383,6 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     int8_t* bres = (int8_t*)ws.bres.get((size_t)N * (size_t)(n * kp));
     CUDA_TRY(launch_resid_A(prec, dA, lda_d, m, k, kp, mu, rc_dev, N, ares, st, stream)); launches += m > 0;
     CUDA_TRY(launch_resid_BT(prec, dB, ldb_d, k, n, kp, nu, rc_dev, N, bres, st, stream)); launches += n > 0;
-    tm.mark();
-
-    // ---- K5: residue GEMMs with fused signed mod p ----
-    int8_t* W = (int8_t*)ws.W.get((size_t)N * (size_t)(m * ldw));
-    if (m > 0 && n > 0) {
-        const CUtensorMap tA = make_plane_map(ares, kp, m, N, boxA);
-        const CUtensorMap tB = make_plane_map(bres, kp, n, N, boxB);
-        gp.planes = N;
-        gp.W = W;
-        gp.ldw = ldw;
-        gp.wplane = m * ldw;
-        fill_gemm_moduli(gp, tab);
-        CUDA_TRY(launch_gemm(EPI_RESID, tA, tB, gp)); ++launches;
-        if (inter && inter->Cprod) {
-            GemmParams g2 = gp;
-            g2.C32 = (int32_t*)ws.x_cprod.get(4 * (size_t)N * (size_t)(m * n));
-            g2.ldc32 = n;
-            g2.cplane = m * n;
-            CUDA_TRY(launch_gemm(EPI_I32, tA, tB, g2)); ++launches;
-        }
-    }
     tm.mark();
 
     // ---- K6: CRT + inverse scaling ----
@@ -397,10 +429,47 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         if (bo->cheap) ex.bnd.cheap = bo->device ? bo->cheap : (double*)ws.x_bcheap.get(mn8);
         if (bo->tight) ex.bnd.tight = bo->device ? bo->tight : (double*)ws.x_btight.get(mn8);
     }
-    CUDA_TRY(launch_crt(prec, W, ldw, m * ldw, m, n, cc, mu, nu, dC, ldc_d, ex, st, stream)); launches += (m * n) > 0;
-    tm.mark();
-
-    if (host && m * n) CUDA_TRY(cudaMemcpy2DAsync(C, esz * ldc, dC, esz * n, esz * n, m, cudaMemcpyDeviceToHost, stream));
+    // ---- K5 + K6 per row block of C: residue GEMMs (fused signed mod p), CRT + unscale ----
+    int8_t* W = (int8_t*)ws.W.get((size_t)N * (size_t)(m * ldw));
+    fill_gemm_moduli(gp, tab);
+    gp.planes = N;
+    gp.ldw = ldw;
+    gp.wplane = m * ldw;
+    const CUtensorMap tBres = make_plane_map(bres, kp, n, N, boxB);
+    for (int c = 0; c < nchunks; ++c) {
+        const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
+        if (rc <= 0 || n <= 0) continue;
+        const CUtensorMap tA = make_plane_map(ares + r0 * kp, kp, rc, N, boxA, m * kp);
+        set_rows(gp, rc);
+        gp.W = W + r0 * ldw;
+        CUDA_TRY(launch_gemm(EPI_RESID, tA, tBres, gp)); ++launches;
+        if (inter && inter->Cprod) {
+            GemmParams g2 = gp;
+            g2.C32 = (int32_t*)ws.x_cprod.get(4 * (size_t)N * (size_t)(m * n));
+            g2.ldc32 = n;
+            g2.cplane = m * n;
+            CUDA_TRY(launch_gemm(EPI_I32, tA, tBres, g2)); ++launches;
+        }
+        if (nchunks == 1) tm.mark();  // end of the residue GEMMs
+        CUDA_TRY(launch_crt(prec, W + r0 * ldw, ldw, m * ldw, rc, n, cc, mu + r0, nu,
+                            (char*)dC + esz * (size_t)(r0 * ldc_d), ldc_d, ex, st, stream));
+        ++launches;
+        if (nchunks == 1) tm.mark();  // end of CRT + unscale
+        if (pipe) {  // download this C block while the next one computes
+            CUDA_TRY(cudaEventRecord(ws.ev_c[c], stream));
+            CUDA_TRY(cudaStreamWaitEvent(ws.s_d2h, ws.ev_c[c], 0));
+            CUDA_TRY(cudaMemcpy2DAsync((char*)C + esz * (size_t)(r0 * ldc), esz * ldc,
+                                       (const char*)dC + esz * (size_t)(r0 * n), esz * n, esz * n, rc,
+                                       cudaMemcpyDeviceToHost, ws.s_d2h));
+        }
+    }
+    if (nchunks > 1 || m * n == 0) { tm.mark(); tm.mark(); }
+    if (pipe) {
+        CUDA_TRY(cudaEventRecord(ws.ev_done, ws.s_d2h));
+        CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_done, 0));
+    } else if (host && m * n) {
+        CUDA_TRY(cudaMemcpy2DAsync(C, esz * ldc, dC, esz * n, esz * n, m, cudaMemcpyDeviceToHost, stream));
+    }
     tm.mark();
 
     // ---- intermediates (host copies) ----

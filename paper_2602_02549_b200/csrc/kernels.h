@@ -59,7 +59,7 @@ typedef ResidHeader ResidConsts;
 
 // Stage launchers (scale.cu).  T = float or double inputs; prec selects.
 cudaError_t launch_row_scan_A(int prec, const void* A, int64_t lda, int64_t m, int64_t k, int64_t kp,
-                              int32_t* mu_prime, int8_t* abar, DevStatus* st, cudaStream_t s);
+                              int32_t* mu_prime, int8_t* abar, DevStatus* st, cudaStream_t s, int64_t row0);
 cudaError_t launch_col_max_B(int prec, const void* B, int64_t ldb, int64_t k, int64_t n,
                              unsigned long long* bmax, DevStatus* st, cudaStream_t s);
 cudaError_t launch_col_exp_B(const unsigned long long* bmax, int64_t n, int32_t* nu_prime, DevStatus* st,

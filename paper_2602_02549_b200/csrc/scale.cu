@@ -33,8 +33,9 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
 template <class T>
 __global__ void __launch_bounds__(256) row_scan_A_kernel(const T* __restrict__ A, int64_t lda, int64_t k,
                                                          int64_t kp, int32_t* __restrict__ mu_prime,
-                                                         int8_t* __restrict__ abar, DevStatus* st) {
-    const int64_t i = blockIdx.x;
+                                                         int8_t* __restrict__ abar, DevStatus* st,
+                                                         int64_t row0) {
+    const int64_t i = blockIdx.x;  // row within this launch; row0 + i in the whole matrix
     const T* row = A + i * lda;
     unsigned long long mx = 0;
     bool bad = false;
@@ -46,7 +47,7 @@ __global__ void __launch_bounds__(256) row_scan_A_kernel(const T* __restrict__ A
         mx = b > mx ? b : mx;
     }
     if (__syncthreads_or(bad)) {
-        if (threadIdx.x == 0) { flag(st, ERR_A_NONFINITE); atomicMin((unsigned long long*)&st->first_row, i); }
+        if (threadIdx.x == 0) { flag(st, ERR_A_NONFINITE); atomicMin((unsigned long long*)&st->first_row, row0 + i); }
         return;
     }
 #pragma unroll
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(256) row_scan_A_kernel(const T* __restrict__ A
         int mup = 0;
         if (m2 == 0) {
             flag(st, ERR_A_ZERO_ROW);
-            atomicMin((unsigned long long*)&st->first_row, i);
+            atomicMin((unsigned long long*)&st->first_row, row0 + i);
         } else {
             mup = 5 - ilogb_exact(__longlong_as_double((long long)m2));
         }
@@ -178,10 +179,10 @@ inline unsigned blocks_for(int64_t work, int per) { return (unsigned)((work + pe
 }  // namespace
 
 cudaError_t launch_row_scan_A(int prec, const void* A, int64_t lda, int64_t m, int64_t k, int64_t kp,
-                              int32_t* mu_prime, int8_t* abar, DevStatus* st, cudaStream_t s) {
+                              int32_t* mu_prime, int8_t* abar, DevStatus* st, cudaStream_t s, int64_t row0) {
     if (m == 0) return cudaSuccess;
-    if (prec) row_scan_A_kernel<double><<<(unsigned)m, 256, 0, s>>>((const double*)A, lda, k, kp, mu_prime, abar, st);
-    else row_scan_A_kernel<float><<<(unsigned)m, 256, 0, s>>>((const float*)A, lda, k, kp, mu_prime, abar, st);
+    if (prec) row_scan_A_kernel<double><<<(unsigned)m, 256, 0, s>>>((const double*)A, lda, k, kp, mu_prime, abar, st, row0);
+    else row_scan_A_kernel<float><<<(unsigned)m, 256, 0, s>>>((const float*)A, lda, k, kp, mu_prime, abar, st, row0);
     return cudaGetLastError();
 }
 

@@ -138,7 +138,7 @@ def _is_torch_cuda(x) -> bool:
 
 
 def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = False, out=None,
-          stream=None, timing: bool = False, bounds=False,
+          stream=None, timing: bool = False, bounds=False, vectors: bool = False,
           reduce_maxima: Optional[Callable] = None) -> EmulationResult:
     """C ~ A*B by Ozaki-II accurate mode with `n` moduli (emulate.hpp:54-88).
 
@@ -146,7 +146,9 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
     (row-major, unit column stride).  The precision of the call follows the
     dtype, like os_ii<float> / os_ii<double>.  `keep_intermediates` returns the
     reference's ScalingOutput/CrtIntermediates fields; `evidence` also returns
-    the residue planes and wrapped INT32 products.  `bounds=True` evaluates the
+    the residue planes and wrapped INT32 products; `vectors` returns only the
+    O(m+n) scaling vectors (mu, nu, mu', nu', e, f, clearance maxima).
+    `bounds=True` evaluates the
     paper's error bounds (bounds.hpp) and returns their maxima;
     `bounds="full"` also returns the m x n cheap / tight bound matrices (same
     memory space as the inputs).  `reduce_maxima(row_ptr, m, col_ptr, n,
@@ -199,7 +201,7 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
     inter_c = None
     sc, cr = ScalingOutput(), CrtIntermediates()
     keep = {}
-    if keep_intermediates or evidence:
+    if keep_intermediates or evidence or vectors:
         inter_c = _lib.Intermediates()
         N = int(n)
         spec = dict(mu=(sc, (m,), np.int16), nu=(sc, (nn,), np.int16), mu_prime=(sc, (m,), np.int16),

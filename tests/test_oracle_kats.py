@@ -438,3 +438,21 @@ def test_oracle_reproduces_reference_golden(oracle):
         assert ours.tobytes() == g[f"gen{idx}"].tobytes()
     for idx in range(3):
         assert np.array_equal(oracle.gemm_i8_wrap(g[f"gemm{idx}_a"], g[f"gemm{idx}_b"]), g[f"gemm{idx}_c"])
+
+
+def test_sampled_pieces_equal_full_oracle(oracle):
+    """The sampled full-size checkers reproduce the full oracle exactly."""
+    for phi, dt in ((2.0, np.float64), (0.5, np.float32)):
+        A = oracle.gen_matrix(40, 50, phi, 1, dt)
+        B = oracle.gen_matrix(50, 30, phi, 2, dt)
+        r = oracle.os_ii(A, B, 16, keep_intermediates=True)
+        A64, B64 = A.astype(np.float64), B.astype(np.float64)
+        mup = oracle.pre_exponents(A64, False)
+        nup = oracle.pre_exponents(B64, True)
+        assert np.array_equal(mup, r.inter["mu_prime"]) and np.array_equal(nup, r.inter["nu_prime"])
+        ab, bb = oracle.ceil_scale(A64, mup, False), oracle.ceil_scale(B64, nup, True)
+        assert np.array_equal(oracle.cbar_row_max(ab, bb, np.arange(40)), r.inter["cmax_row"])
+        assert np.array_equal(oracle.cbar_col_max(ab, bb, np.arange(30)), r.inter["cmax_col"])
+        ri, cj = np.repeat(np.arange(40), 30), np.tile(np.arange(30), 40)
+        e = oracle.entries(A64, B64, 16, r.inter["mu"], r.inter["nu"], ri, cj, prec=1 if dt == np.float64 else 0)
+        assert e.reshape(40, 30).tobytes() == r.C.tobytes()
