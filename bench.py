@@ -97,6 +97,30 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
+def _ncu_traffic(m: int, nmod: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the residue GEMM launch
+    from the committed `ncu --set full` capture of this configuration (one
+    launch), or None when no capture matches."""
+    import csv
+    path = os.path.join(ROOT, "profiles", f"r01_ncu_full_residue_gemm_{m}.csv")
+    if nmod != 16 or not os.path.exists(path):
+        return None
+    try:
+        rows = list(csv.reader(open(path)))
+        h, units = rows[0], rows[1]
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+        for r in rows[2:]:
+            if "gemm_i8_tc_kernel<1>" in r[h.index("Kernel Name")]:
+                tot = 0.0
+                for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    i = h.index(key)
+                    tot += float(r[i].replace(",", "")) * scale.get(units[i], 1.0)
+                return tot
+    except Exception:
+        return None
+    return None
+
+
 def gen_device(rows, cols, phi, seed, dtype, device):
     """The reference generator's distribution, (u - 1/2) * exp(g * phi) with
     u uniform on (0, 1] and g standard normal (gen.hpp:15-31), drawn on the GPU
@@ -166,7 +190,7 @@ def main():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--moduli", type=int, default=16)
     ap.add_argument("--phi", type=float, default=0.0)
-    ap.add_argument("--cpu-sample", type=int, default=96, help="rows/cols of the bounded CPU sample")
+    ap.add_argument("--cpu-sample", type=int, default=512, help="rows/cols of the bounded CPU sample (~10 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-native", action="store_true")
@@ -341,8 +365,10 @@ def main():
     gemm_avg = float(np.mean(gemm_ms))
     achieved = ops / (gemm_avg * 1e-3) / 1e12
     int8_peak = 2.0 * peaks["bf16_tflops"]
+    traffic = _ncu_traffic(m, args.moduli) if world == 1 else None
     roof = {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s", "frac": achieved / int8_peak,
-            "traffic": None, "kernel": "gemm_i8_tc_kernel<EPI_RESID> (N residue GEMMs, one launch)",
+            "traffic": traffic, "traffic_unit": "bytes per launch (ncu --set full, profiles/)",
+            "kernel": "gemm_i8_tc_kernel<EPI_RESID> (N residue GEMMs, one launch)",
             "peak_note": f"dense INT8 = 2 x {peak_kind} bf16 burst ({peaks['bf16_tflops']} TF/s); int8 ops counted as FLOPs",
             "algorithmic_ops_per_launch": ops, "launch_ms": gemm_avg}
 

@@ -169,12 +169,31 @@ int oz2g_shift_of_cmax(int n, int64_t c);
  * can compare it exhaustively with the host libm (log2_fp32, softfp.hpp:147). */
 int oz2g_device_log2f(const float *x_dev, float *out_dev, int64_t count, void *stream);
 
+/* suggest_n (bounds.hpp:217-243): the smallest N in [2, 49] (fp32: [2, 16])
+ * whose cheap-bound maximum (bounds.hpp:198-206) is <= `target` (absolute).
+ * *n_out = 0 when no N achieves it; *bound_max = the cheap-bound maximum at
+ * the returned N (or at the cap).  One clearance pass; A, B as in oz2g_gemm. */
+int oz2g_suggest_n(int prec, int64_t m, int64_t n, int64_t k, const void *A, int64_t lda, const void *B, int64_t ldb,
+                   double target, unsigned flags, void *stream, int *n_out, double *bound_max);
+
 /* Double-double reference product C = A B (hi + lo) for DEVICE fp64
  * matrices: every product exact (TwoProd), the k-term sum in double-double
  * (error <= ~k 2^-104 sum|a||b|).  Used to measure the emulation error
  * against the paper's bounds (the role of error_matrix, oracle.hpp:164-172). */
 int oz2g_dd_gemm(int64_t m, int64_t n, int64_t k, const double *A, int64_t lda, const double *B, int64_t ldb,
                  double *Chi, double *Clo, int64_t ldc, void *stream);
+
+/* Experiment-harness pieces:
+ *  oz2g_gen_matrix   the reference's synthetic stream (gen.hpp:15-31, prng.hpp),
+ *                    host memory, bit-identical to the reference for a seed;
+ *  oz2g_derive_seed  experiment.hpp:83-88;
+ *  oz2g_native_gemm  the "native" working-precision GEMM of the error report
+ *                    (experiment.hpp:55-68: sequential loop, separate RN mul
+ *                    and add), DEVICE pointers. */
+int oz2g_gen_matrix(int prec, int64_t rows, int64_t cols, double phi, uint64_t seed, void *out);
+uint64_t oz2g_derive_seed(uint64_t seed, uint64_t trial, uint64_t role);
+int oz2g_native_gemm(int prec, int64_t m, int64_t n, int64_t k, const void *A, int64_t lda, const void *B,
+                     int64_t ldb, void *C, int64_t ldc, void *stream);
 
 /* Library information (compiled arch, number of SMs used, version). */
 int oz2g_version(void);

@@ -85,3 +85,18 @@ def exact_product(A: np.ndarray, B: np.ndarray):
     Af = [[Fraction(float(x)) for x in row] for row in A]
     Bf = [[Fraction(float(x)) for x in row] for row in B]
     return [[sum(Af[i][h] * Bf[h][j] for h in range(k)) for j in range(nn)] for i in range(m)]
+
+
+def suggest_n(A: np.ndarray, B: np.ndarray, target: float, cmax_row, cmax_col):
+    """bounds.hpp:217-243 with the cheap bound restated above (mpmath); the
+    clearance maxima do not depend on N (bounds.hpp:214-216)."""
+    mode = M.F64 if A.dtype == np.float64 else M.F32
+    n_max = M.fp32_safe_moduli_max() if mode == M.F32 else M.K_MAX_MODULI
+    last = None
+    for n in range(2, n_max + 1):
+        cheap, _ = bounds(A, B, n, cmax_row, cmax_col)
+        mx = max(max(row) for row in cheap)
+        last = mx
+        if mx <= target:
+            return True, n, mx
+    return False, 0, last

@@ -42,7 +42,8 @@ REDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C
 
 EXPORTED = ("oz2g_gemm", "oz2g_dgemm", "oz2g_sgemm", "oz2g_last_error", "oz2g_table_for",
             "oz2g_fp32_safe_moduli_max", "oz2g_shift_of_cmax", "oz2g_device_log2f", "oz2g_version",
-            "oz2g_release_workspace", "oz2g_dd_gemm")
+            "oz2g_release_workspace", "oz2g_dd_gemm", "oz2g_suggest_n", "oz2g_gen_matrix", "oz2g_derive_seed",
+            "oz2g_native_gemm")
 
 _LIB = None
 
@@ -68,5 +69,13 @@ def load() -> C.CDLL:
     L.oz2g_device_log2f.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
     L.oz2g_dd_gemm.argtypes = [C.c_int64] * 3 + [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
                                                  C.c_void_p, C.c_int64, C.c_void_p]
+    L.oz2g_suggest_n.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                                 C.c_int64, C.c_double, C.c_uint, C.c_void_p, C.POINTER(C.c_int),
+                                 C.POINTER(C.c_double)]
+    L.oz2g_gen_matrix.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_uint64, C.c_void_p]
+    L.oz2g_derive_seed.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
+    L.oz2g_derive_seed.restype = C.c_uint64
+    L.oz2g_native_gemm.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                                   C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]
     _LIB = L
     return L

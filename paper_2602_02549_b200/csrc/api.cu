@@ -197,6 +197,19 @@ bool use_pair_gemm() {
     return v;
 }
 
+// TMA L2 policies (CUTLASS CacheHintSm90 encodings).  Default EVICT_NORMAL for
+// both operands: measured at 16384^3, EVICT_LAST on A / EVICT_FIRST on B doubled
+// the residue GEMM's DRAM reads (81 -> 156 GB: B tiles are shared by the CTAs of
+// a wave and were evicted before reuse).  OZ2G_L2HINT=1 re-enables for study.
+void set_l2_hints(GemmParams& g) {
+    static const bool on = [] {
+        const char* s = std::getenv("OZ2G_L2HINT");
+        return s && std::strcmp(s, "1") == 0;
+    }();
+    g.hintA = on ? 0x14F0000000000000ull /*EVICT_LAST*/ : 0x1000000000000000ull /*EVICT_NORMAL*/;
+    g.hintB = on ? 0x12F0000000000000ull /*EVICT_FIRST*/ : 0x1000000000000000ull;
+}
+
 // Raster group height: one wave of persistent CTAs covers group_m tile-rows,
 // so B tiles are streamed from HBM about tiles_m / group_m times per plane.
 int group_m_for(int tiles_m) {
@@ -326,6 +339,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     gp.n = (int)n;
     gp.kblocks = (int)(kp / 128);
     gp.tiles_n = (int)((n + BN - 1) / BN);
+    set_l2_hints(gp);
     auto set_rows = [&](GemmParams& g, int64_t rows) {
         g.m = (int)rows;
         g.tiles_m = (int)((rows + BM - 1) / BM);
@@ -588,6 +602,103 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     return OZ2G_OK;
 }
 
+// suggest_n (bounds.hpp:217-243): one clearance pass (Cbar does not depend on
+// N), then the cheap bound's maximum for N = 2, 3, ... until it meets the
+// absolute target.  fp32 candidates stop at the format's safe ceiling.
+int run_suggest_n(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
+                  double target, unsigned flags, cudaStream_t stream, int* n_out, double* bound_out) {
+    if (prec != OZ2G_FP32 && prec != OZ2G_FP64) throw Fail{OZ2G_INVALID_ARGUMENT, "suggest_n: bad precision"};
+    if (!(target > 0)) throw Fail{OZ2G_DOMAIN_ERROR, "suggest_n: target must be positive"};
+    if (m < 0 || n < 0 || k < 0 || lda < k || ldb < n) throw Fail{OZ2G_INVALID_ARGUMENT, "dimension mismatch: suggest_n"};
+    if (k > OZ2G_MAX_INNER_DIM) throw Fail{OZ2G_DOMAIN_ERROR, "os_ii: k exceeds 2^17"};
+    if (k == 0 && m > 0) throw Fail{OZ2G_DOMAIN_ERROR, "row_pre_exponents: zero row 0"};
+    if (k == 0 && n > 0) throw Fail{OZ2G_DOMAIN_ERROR, "col_pre_exponents: zero column 0"};
+    *n_out = 0;
+    *bound_out = 0.0;
+    if (m == 0 || n == 0) return OZ2G_OK;
+    const bool host = (flags & OZ2G_DEVICE_PTRS) == 0;
+    const size_t esz = prec ? 8 : 4;
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> dev_lock(device_mutex(dev));
+    Workspace& ws = workspace(dev);
+    const int64_t kp = round_up(k, 128);
+    const void* dA = A;
+    const void* dB = B;
+    int64_t lda_d = lda, ldb_d = ldb;
+    if (host) {
+        dA = ws.A.get(esz * (size_t)(m * k));
+        dB = ws.B.get(esz * (size_t)(k * n));
+        lda_d = k; ldb_d = n;
+        CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dA), esz * k, A, esz * lda, esz * k, m, cudaMemcpyHostToDevice, stream));
+        CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dB), esz * n, B, esz * ldb, esz * n, k, cudaMemcpyHostToDevice, stream));
+    }
+    DevStatus* st = (DevStatus*)ws.status.get(sizeof(DevStatus));
+    CUDA_TRY(cudaMemsetAsync(st, 0, 8, stream));
+    CUDA_TRY(cudaMemsetAsync(&st->first_row, 0x7f, 16, stream));
+    int32_t* mup = (int32_t*)ws.mup.get(4 * (size_t)m);
+    int32_t* nup = (int32_t*)ws.nup.get(4 * (size_t)n);
+    unsigned long long* bmax = (unsigned long long*)ws.bmax.get(8 * (size_t)n);
+    int32_t* cmax_row = (int32_t*)ws.cmax_row.get(4 * (size_t)m);
+    int32_t* cmax_col = (int32_t*)ws.cmax_col.get(4 * (size_t)n);
+    int8_t* abar = (int8_t*)ws.abar.get((size_t)(m * kp));
+    int8_t* bbar = (int8_t*)ws.bbar.get((size_t)(n * kp));
+    CUDA_TRY(cudaMemsetAsync(bmax, 0, 8 * (size_t)n, stream));
+    CUDA_TRY(cudaMemsetAsync(cmax_row, 0, 4 * (size_t)m, stream));
+    CUDA_TRY(cudaMemsetAsync(cmax_col, 0, 4 * (size_t)n, stream));
+    CUDA_TRY(launch_col_max_B(prec, dB, ldb_d, k, n, bmax, st, stream));
+    CUDA_TRY(launch_col_exp_B(bmax, n, nup, st, stream));
+    CUDA_TRY(launch_bbar_T(prec, dB, ldb_d, k, n, kp, nup, bbar, st, stream));
+    CUDA_TRY(launch_row_scan_A(prec, dA, lda_d, m, k, kp, mup, abar, st, stream, 0));
+    GemmParams gp;
+    std::memset(&gp, 0, sizeof gp);
+    gp.m = (int)m;
+    gp.n = (int)n;
+    gp.kblocks = (int)(kp / 128);
+    gp.tiles_m = (int)((m + gemm_tile_m() - 1) / gemm_tile_m());
+    gp.tiles_n = (int)((n + gemm_tile_n() - 1) / gemm_tile_n());
+    gp.group_m = group_m_for(gp.tiles_m);
+    set_l2_hints(gp);
+    gp.planes = 1;
+    gp.rowmax = cmax_row;
+    gp.colmax = cmax_col;
+    CUDA_TRY(launch_gemm_i8(EPI_MAX, make_plane_map(abar, kp, m, 1, gemm_tile_m()),
+                            make_plane_map(bbar, kp, n, 1, gemm_tile_n()), gp, ws.num_sms, stream));
+    // exponent_stats (bounds.hpp:32-60) as the per-row / per-column factors with t = 1
+    double* vec = (double*)ws.x_bvec.get(8 * (size_t)(2 * (m + n)) + 4 * (size_t)(m + n) + 16);
+    BoundVecs v;
+    v.RA = vec; v.PA = vec + m; v.CB = vec + 2 * m; v.PB = vec + 2 * m + n;
+    v.ea = reinterpret_cast<int32_t*>(vec + 2 * (m + n));
+    v.eb = v.ea + m;
+    double* scratch = (double*)ws.x_bscr.get(8 * bound_scratch_doubles(m, n, k));
+    CUDA_TRY(launch_bound_vectors(prec, dA, lda_d, m, dB, ldb_d, k, n, cmax_row, cmax_col, mup, nup, 1.0, scratch, v,
+                                  stream));
+    DevStatus hs;
+    CUDA_TRY(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    if (hs.err & (ERR_A_NONFINITE | ERR_B_NONFINITE)) throw Fail{OZ2G_DOMAIN_ERROR, "matrix entry is not finite"};
+    if (hs.err & (ERR_A_ZERO_ROW | ERR_B_ZERO_COL)) throw Fail{OZ2G_DOMAIN_ERROR, "exponent_stats: zero row"};
+    unsigned long long* bits = (unsigned long long*)ws.x_bmax.get(16);
+    const int n_max = prec == OZ2G_FP32 ? fp32_safe_moduli_max() : kMaxModuli;
+    for (int nm = 2; nm <= n_max; ++nm) {
+        const BoundScalars bs = bound_scalars(table_for(nm, prec), k);
+        CUDA_TRY(cudaMemsetAsync(bits, 0, 8, stream));
+        CUDA_TRY(launch_cheap_bound_max(v, m, n, bs.t_up, __builtin_nextafter(bs.kpr_cheap_up * bs.t2_up, 1e308), bits,
+                                        ws.num_sms, stream));
+        unsigned long long hb = 0;
+        CUDA_TRY(cudaMemcpyAsync(&hb, bits, 8, cudaMemcpyDeviceToHost, stream));
+        CUDA_TRY(cudaStreamSynchronize(stream));
+        double mx;
+        std::memcpy(&mx, &hb, 8);
+        *bound_out = mx;
+        if (mx <= target) {
+            *n_out = nm;
+            return OZ2G_OK;
+        }
+    }
+    return OZ2G_OK;  // not achievable: n_out = 0, bound_out = bound max at the cap
+}
+
 template <class F>
 int guarded(F&& f) {
     g_last_error.clear();
@@ -683,12 +794,29 @@ int oz2g_device_log2f(const float* x_dev, float* out_dev, int64_t count, void* s
     });
 }
 
+int oz2g_suggest_n(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
+                   double target, unsigned flags, void* stream, int* n_out, double* bound_max) {
+    return guarded([&] {
+        return run_suggest_n(prec, m, n, k, A, lda, B, ldb, target, flags, (cudaStream_t)stream, n_out, bound_max);
+    });
+}
+
 int oz2g_dd_gemm(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B, int64_t ldb,
                  double* Chi, double* Clo, int64_t ldc, void* stream) {
     return guarded([&] {
         if (m < 0 || n < 0 || k < 0 || lda < k || ldb < n || ldc < n)
             throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_dd_gemm: bad dimensions"};
         CUDA_TRY(launch_dd_gemm(A, lda, B, ldb, m, n, k, Chi, Clo, ldc, (cudaStream_t)stream));
+        return OZ2G_OK;
+    });
+}
+
+int oz2g_native_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
+                     int64_t ldb, void* C, int64_t ldc, void* stream) {
+    return guarded([&] {
+        if (m < 0 || n < 0 || k < 0 || lda < k || ldb < n || ldc < n)
+            throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_native_gemm: bad dimensions"};
+        CUDA_TRY(launch_native_gemm(prec, A, lda, B, ldb, m, n, k, C, ldc, (cudaStream_t)stream));
         return OZ2G_OK;
     });
 }

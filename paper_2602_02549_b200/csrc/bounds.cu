@@ -155,9 +155,70 @@ __global__ void __launch_bounds__(256) dd_gemm_kernel(const double* __restrict__
         }
 }
 
+// max_ij of the cheap bound for one N (bounds.hpp:198-206), every operation
+// rounded up; used by suggest_n (bounds.hpp:217-243).
+__global__ void __launch_bounds__(256) cheap_bound_max_kernel(BoundVecs v, int64_t m, int64_t n, double t_up,
+                                                              double kt2_up, unsigned long long* out_bits) {
+    unsigned long long best = 0;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m * n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / n, j = e - i * n;
+        // RA/CB hold t_ref*(|A|v), t_ref*(v^T|B|) for t_ref = 1; scale by this N's t
+        const double b1 = ldexp_ru(__dmul_ru(__dmul_ru(t_up, v.RA[i]), v.PB[j]), v.eb[j]);
+        const double b2 = ldexp_ru(__dmul_ru(__dmul_ru(t_up, v.CB[j]), v.PA[i]), v.ea[i]);
+        const double b3 = ldexp_ru(__dmul_ru(kt2_up, __dmul_ru(v.PA[i], v.PB[j])), v.ea[i] + v.eb[j]);
+        const double bnd = __dadd_ru(__dadd_ru(b1, b2), b3);
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(bnd);
+        best = bits > best ? bits : best;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+        best = t > best ? t : best;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(out_bits, best);
+}
+
+// The experiment harness's "native" GEMM (experiment.hpp:55-68): per entry a
+// sequential loop h = 0..k-1 with a separate RN multiply and RN add in the
+// working precision T (no FMA), exactly the reference's err_native reference.
+template <class T>
+__global__ void native_gemm_kernel(const T* __restrict__ A, int64_t lda, const T* __restrict__ B, int64_t ldb,
+                                   int64_t m, int64_t n, int64_t k, T* __restrict__ C, int64_t ldc) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m * n) return;
+    const int64_t i = t / n, j = t - i * n;
+    T acc = 0;
+    for (int64_t h = 0; h < k; ++h) {
+        if constexpr (sizeof(T) == 8) acc = __dadd_rn(acc, __dmul_rn(A[i * lda + h], B[h * ldb + j]));
+        else acc = __fadd_rn(acc, __fmul_rn(A[i * lda + h], B[h * ldb + j]));
+    }
+    C[i * ldc + j] = acc;
+}
+
 inline unsigned blocks_for(int64_t work, int per) { return (unsigned)((work + per - 1) / per); }
 
 }  // namespace
+
+cudaError_t launch_native_gemm(int prec, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m,
+                               int64_t n, int64_t k, void* C, int64_t ldc, cudaStream_t s) {
+    if (m * n == 0) return cudaSuccess;
+    if (prec)
+        native_gemm_kernel<double><<<blocks_for(m * n, 128), 128, 0, s>>>((const double*)A, lda, (const double*)B, ldb,
+                                                                         m, n, k, (double*)C, ldc);
+    else
+        native_gemm_kernel<float><<<blocks_for(m * n, 128), 128, 0, s>>>((const float*)A, lda, (const float*)B, ldb, m,
+                                                                        n, k, (float*)C, ldc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cheap_bound_max(const BoundVecs& v, int64_t m, int64_t n, double t_up, double kt2_up,
+                                   unsigned long long* out_bits, int num_sms, cudaStream_t s) {
+    if (m * n == 0) return cudaSuccess;
+    const int64_t want = (m * n + 255) / 256;
+    const unsigned grid = (unsigned)(want < (int64_t)num_sms * 8 ? want : (int64_t)num_sms * 8);
+    cheap_bound_max_kernel<<<grid, 256, 0, s>>>(v, m, n, t_up, kt2_up, out_bits);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_bound_vectors(int prec, const void* A, int64_t lda, int64_t m, const void* B, int64_t ldb,
                                  int64_t k, int64_t n, const int32_t* cmax_row, const int32_t* cmax_col,

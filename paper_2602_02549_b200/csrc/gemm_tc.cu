@@ -106,8 +106,9 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&v)[32], int row,
         int8_t* dst = P.W + (int64_t)l * P.wplane + (int64_t)row * P.ldw + col0;
         if (col0 + 32 <= P.n) {
             uint4* d4 = reinterpret_cast<uint4*>(dst);
-            d4[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-            d4[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+            // streaming stores: W is read once by the CRT pass, keep it from evicting operands in L2
+            __stcs(d4, make_uint4(packed[0], packed[1], packed[2], packed[3]));
+            __stcs(d4 + 1, make_uint4(packed[4], packed[5], packed[6], packed[7]));
         } else {
             for (int c = 0; c < 32 && col0 + c < P.n; ++c) dst[c] = (int8_t)((packed[c >> 2] >> (8 * (c & 3))) & 0xff);
         }
@@ -160,8 +161,10 @@ __global__ void __launch_bounds__(256, 1)
                 mbar_wait(&empty[stage], phase ^ 1u);
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
-                    tma_load_3d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, tc.tm * BM, tc.l, kEvictNormal);
-                    tma_load_3d(sB + stage * B_BYTES, &tmB, &full[stage], kb * BK, tc.tn * BN, tc.l, kEvictNormal);
+                    // A row groups are reused by every wave of a raster group: keep them in L2;
+                    // B tiles stream through
+                    tma_load_3d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, tc.tm * BM, tc.l, P.hintA);
+                    tma_load_3d(sB + stage * B_BYTES, &tmB, &full[stage], kb * BK, tc.tn * BN, tc.l, P.hintB);
                 }
                 __syncwarp();
                 if (++stage == STAGES) { stage = 0; phase ^= 1u; }
@@ -301,8 +304,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                 mbar_wait(&empty[stage], phase ^ 1u);
                 if (lane == 0) {
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
-                    tma_load_3d_pair(sA + stage * P_HALF * BK, &tmA, &full[stage], kb * BK, arow, tc.l, kEvictNormal);
-                    tma_load_3d_pair(sB + stage * P_HALF * BK, &tmB, &full[stage], kb * BK, brow, tc.l, kEvictNormal);
+                    tma_load_3d_pair(sA + stage * P_HALF * BK, &tmA, &full[stage], kb * BK, arow, tc.l, P.hintA);
+                    tma_load_3d_pair(sB + stage * P_HALF * BK, &tmB, &full[stage], kb * BK, brow, tc.l, P.hintB);
                 }
                 __syncwarp();
                 if (++stage == P_STAGES) { stage = 0; phase ^= 1u; }

@@ -17,6 +17,7 @@ struct GemmParams {
     int planes;               // number of (A_l, B_l) pairs
     int tiles_m, tiles_n;
     int group_m;              // tile-rows per raster group (L2 reuse of the B operand)
+    uint64_t hintA, hintB;    // TMA L2 cache policies for the A / B operand loads
     // EPI_MAX
     int32_t* rowmax;
     int32_t* colmax;
@@ -91,8 +92,12 @@ cudaError_t launch_bound_vectors(int prec, const void* A, int64_t lda, int64_t m
                                  const int32_t* mu_prime, const int32_t* nu_prime, double t_up, double* scratch,
                                  const BoundVecs& v, cudaStream_t s);
 size_t bound_scratch_doubles(int64_t m, int64_t n, int64_t k);
+cudaError_t launch_cheap_bound_max(const BoundVecs& v, int64_t m, int64_t n, double t_up, double kt2_up,
+                                   unsigned long long* out_bits, int num_sms, cudaStream_t s);
 cudaError_t launch_dd_gemm(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t m, int64_t n,
                            int64_t k, double* Chi, double* Clo, int64_t ldc, cudaStream_t s);
+cudaError_t launch_native_gemm(int prec, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m,
+                               int64_t n, int64_t k, void* C, int64_t ldc, cudaStream_t s);
 
 // CRT + inverse scaling (crt.cu).
 struct CrtConsts {

@@ -29,9 +29,10 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
 
 // ---------------------------------------------------------------------------
 // A: one CTA per row (two passes; the second re-reads the row from L2).
+// blockDim is 256 or 1024 (launcher); the reductions below handle both.
 // ---------------------------------------------------------------------------
 template <class T>
-__global__ void __launch_bounds__(256) row_scan_A_kernel(const T* __restrict__ A, int64_t lda, int64_t k,
+__global__ void __launch_bounds__(1024) row_scan_A_kernel(const T* __restrict__ A, int64_t lda, int64_t k,
                                                          int64_t kp, int32_t* __restrict__ mu_prime,
                                                          int8_t* __restrict__ abar, DevStatus* st,
                                                          int64_t row0) {
@@ -55,7 +56,7 @@ __global__ void __launch_bounds__(256) row_scan_A_kernel(const T* __restrict__ A
         const unsigned long long t = __shfl_xor_sync(0xffffffffu, mx, o);
         mx = t > mx ? t : mx;
     }
-    __shared__ unsigned long long red[8];
+    __shared__ unsigned long long red[32];
     __shared__ int s_mup;
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
     __syncthreads();
@@ -181,8 +182,11 @@ inline unsigned blocks_for(int64_t work, int per) { return (unsigned)((work + pe
 cudaError_t launch_row_scan_A(int prec, const void* A, int64_t lda, int64_t m, int64_t k, int64_t kp,
                               int32_t* mu_prime, int8_t* abar, DevStatus* st, cudaStream_t s, int64_t row0) {
     if (m == 0) return cudaSuccess;
-    if (prec) row_scan_A_kernel<double><<<(unsigned)m, 256, 0, s>>>((const double*)A, lda, k, kp, mu_prime, abar, st, row0);
-    else row_scan_A_kernel<float><<<(unsigned)m, 256, 0, s>>>((const float*)A, lda, k, kp, mu_prime, abar, st, row0);
+    // 1024 threads per row keep ~2 rows per SM in flight, so the second pass
+    // over a row (<= 1 MiB) is served from L2 instead of HBM
+    const unsigned threads = k >= 4096 ? 1024u : 256u;
+    if (prec) row_scan_A_kernel<double><<<(unsigned)m, threads, 0, s>>>((const double*)A, lda, k, kp, mu_prime, abar, st, row0);
+    else row_scan_A_kernel<float><<<(unsigned)m, threads, 0, s>>>((const float*)A, lda, k, kp, mu_prime, abar, st, row0);
     return cudaGetLastError();
 }
 

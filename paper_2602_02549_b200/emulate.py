@@ -287,3 +287,43 @@ def device_log2f(x_dev, out_dev, stream=None) -> None:
         stream = torch.cuda.current_stream(x_dev.device).cuda_stream
     _check(_lib.load().oz2g_device_log2f(x_dev.data_ptr(), out_dev.data_ptr(), x_dev.numel(),
                                          C.c_void_p(int(stream))))
+
+
+@dataclass
+class SuggestResult:
+    """bounds.hpp:208-212."""
+    achievable: bool
+    n: int
+    bound_max: float
+
+
+def suggest_n(a, b, target: float) -> SuggestResult:
+    """Smallest N whose cheap error bound (bounds.hpp:198-206) is <= `target`
+    everywhere (bounds.hpp:217-243); host numpy arrays or CUDA tensors."""
+    L = _lib.load()
+    if _is_torch_cuda(a):
+        import torch
+        prec = F64 if a.dtype == torch.float64 else F32
+        m, k = a.shape
+        nn = b.shape[1]
+        pa, pb, lda, ldb = a.data_ptr(), b.data_ptr(), a.stride(0), b.stride(0)
+        flags = _lib.OZ2G_DEVICE_PTRS
+        stream = torch.cuda.current_stream(a.device).cuda_stream
+    else:
+        a = np.ascontiguousarray(a)
+        b = np.ascontiguousarray(b)
+        if a.dtype != b.dtype or a.dtype not in (np.float32, np.float64):
+            raise TypeError("suggest_n: A and B must both be float32 or float64")
+        prec = F64 if a.dtype == np.float64 else F32
+        m, k = a.shape
+        nn = b.shape[1]
+        pa, pb, lda, ldb = a.ctypes.data, b.ctypes.data, k, nn
+        flags = _lib.OZ2G_HOST_PTRS
+        stream = 0
+    if a.shape[1] != b.shape[0]:
+        raise InvalidArgument("dimension mismatch: suggest_n inner dimension")
+    n_out = C.c_int()
+    bmax = C.c_double()
+    _check(L.oz2g_suggest_n(prec, m, nn, k, pa, lda, pb, ldb, float(target), flags, C.c_void_p(int(stream)),
+                            C.byref(n_out), C.byref(bmax)))
+    return SuggestResult(achievable=n_out.value > 0, n=n_out.value, bound_max=bmax.value)

@@ -75,3 +75,21 @@ def test_bounds_device_tensors(cuda, oracle):
     assert bool((r.bounds["tight"] <= r.bounds["cheap"]).all())
     host = oz.os_ii(A, B, 16, bounds=True)
     assert host.bounds["tight_max"] == float(r.bounds["tight"].max())
+
+
+@pytest.mark.parametrize("phi,target,dt", [(0.0, 1e-12, np.float64), (2.0, 1e-9, np.float64),
+                                           (0.5, 1e-14, np.float64), (0.0, 1e-4, np.float32),
+                                           (8.0, 1e-30, np.float64)])
+def test_suggest_n_matches_oracle(cuda, oracle, phi, target, dt):
+    """suggest_n (bounds.hpp:217-243): same N as the restated cheap bound; at
+    that N the bound holds and one N less fails (minimality)."""
+    from oracle import bounds as OB
+    A = oracle.gen_matrix(10, 48, phi, 71, dt)
+    B = oracle.gen_matrix(48, 9, phi, 72, dt)
+    r = oracle.os_ii(A, B, 8, want_cmax=True)
+    ok, n_or, mx_or = OB.suggest_n(A, B, target, r.inter["cmax_row"], r.inter["cmax_col"])
+    got = oz.suggest_n(A, B, target)
+    assert got.achievable == ok
+    assert got.n == n_or
+    if ok:
+        assert got.bound_max <= target and mpmath.mpf(got.bound_max) >= mx_or

@@ -24,7 +24,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def test_library_exports_header_symbols():
     L = oz.load_library()
     header = open(os.path.join(ROOT, "include", "oz2g.h")).read()
-    declared = set(re.findall(r"^\s*(?:int|void|const char \*)\s*\**\s*(oz2g_\w+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:int|void|uint64_t|const char \*)\s*\**\s*(oz2g_\w+)\s*\(", header, re.M))
     assert declared, "no declarations parsed"
     assert declared == set(_lib.EXPORTED)
     for name in declared:
