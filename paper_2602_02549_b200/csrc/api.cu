@@ -141,21 +141,22 @@ std::vector<uint8_t> build_resid_consts(const Table& t) {
     for (int l = 0; l < t.n; ++l) {
         const uint32_t p = (uint32_t)t.p[l];
         h->p[l] = p;
-        h->magic[l] = (uint32_t)((0x100000000ull + p - 1) / p);  // ceil(2^32 / p)
-        h->offh[l] = p * (((1u << 18) + p - 1) / p) + p / 2;
-        h->h4[l] = (p / 2) * 0x01010101u;
-        h->negp[l] = 0u - p;
-        for (int E = 0; E < kResidE; ++E) {
-            uint32_t w[8];
-            for (int b = 0; b < 8; ++b) {  // symmetric representative of 2^(8b + E) mod p, as a byte
-                uint32_t v = 1 % p;
-                for (int s = 0; s < 8 * b + E; ++s) v = (v * 2u) % p;
-                const int rep = (2 * v > p) ? (int)v - (int)p : (int)v;  // p = 256: 128 stays (byte -128)
-                w[b] = (uint32_t)rep & 0xffu;
+        h->inv_p[l] = (float)(1.0 / (double)p);  // any value within 2^-20 relative of 1/p works (resid.cu)
+        h->pf[l] = (float)p;
+        for (int G = 0; G < kResidE8; ++G) {
+            for (int sg = 0; sg < 2; ++sg) {
+                uint32_t w[8];
+                for (int b = 0; b < 8; ++b) {  // symmetric representative of +-2^(8(b + G)) mod p, as a byte
+                    uint32_t v = 1 % p;
+                    for (int s = 0; s < 8 * (b + G); ++s) v = (v * 2u) % p;
+                    int rep = (2 * v > p) ? (int)v - (int)p : (int)v;  // p = 256: 128 (byte -128)
+                    if (sg) rep = -rep;                                  // -128 == 128 (mod 256)
+                    w[b] = (uint32_t)rep & 0xffu;
+                }
+                uint32_t* cell = tab + 2 * (((size_t)l * kResidE8 + G) * 2 + sg);  // [l][G][sign]
+                cell[0] = w[0] | (w[1] << 8) | (w[2] << 16) | (w[3] << 24);
+                cell[1] = w[4] | (w[5] << 8) | (w[6] << 16) | (w[7] << 24);
             }
-            uint32_t* cell = tab + 2 * ((size_t)l * kResidE + E);  // layout [l][E]: lanes with different E hit different banks
-            cell[0] = w[0] | (w[1] << 8) | (w[2] << 16) | (w[3] << 24);
-            cell[1] = w[4] | (w[5] << 8) | (w[6] << 16) | (w[7] << 24);
         }
     }
     return buf;
@@ -217,7 +218,7 @@ int group_m_for(int tiles_m) {
         const char* s = std::getenv("OZ2G_GROUP_M");
         return s ? std::atoi(s) : 0;
     }();
-    int g = env > 0 ? env : 32;
+    int g = env > 0 ? env : 16;  // best of {8, 12, 16, 24, 32} at 16384^3 (interleaved A/B)
     return g < tiles_m ? g : (tiles_m > 0 ? tiles_m : 1);
 }
 

@@ -16,6 +16,7 @@
 // Optionally (BND) the same pass evaluates the cheap and tight error bounds
 // of bounds.hpp:143-206 for every entry (see bounds.cu for the derivation).
 #include <cfloat>
+#include <cstdlib>
 
 #include "device_common.cuh"
 #include "kernels.h"
@@ -35,7 +36,17 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
     return v;
 }
 
-template <class T, bool DD, bool BND>
+// Exact int8 -> fp64 on the fp64 pipe instead of the conversion (XU) pipe: the
+// double with bits 0x43300000:(w ^ 0x80) is 2^52 + w + 128, and subtracting
+// 2^52 + 128 is exact.  wx = the packed word with every byte XORed by 0x80.
+__device__ __forceinline__ double i8_to_f64_fp(uint32_t wx, int b) {
+    const uint32_t lo = __byte_perm(wx, 0u, 0x4440u | (uint32_t)b);
+    return __dsub_rn(__hiloint2double(0x43300000, (int)lo), 4503599627370624.0);
+}
+
+// NFP of the CV columns convert through i8_to_f64_fp, the rest with I2F (XU):
+// XU converts 16 values/clk/SM, the fp64 pipe 64, so splitting balances them.
+template <class T, bool DD, bool BND, int NFP>
 __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, int64_t ldw, int64_t wplane,
                                                   int64_t m, int64_t n, const CrtConsts cc,
                                                   const int32_t* __restrict__ mu, const int32_t* __restrict__ nu,
@@ -58,19 +69,28 @@ __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, 
         auto fold = [&](const uint2 word, int l) {
             const double s1 = cc.s1[l];
             const double s2 = cc.s2[l];
+            const uint32_t xx = word.x ^ 0x80808080u, xy = word.y ^ 0x80808080u;
 #pragma unroll
             for (int b = 0; b < CV; ++b) {
                 const uint32_t w32 = b < 4 ? word.x : word.y;
-                const double wv = (double)(int8_t)((w32 >> (8 * (b & 3))) & 0xffu);
+                const double wv = b >= CV - NFP ? i8_to_f64_fp(b < 4 ? xx : xy, b & 3)
+                                                : (double)(int8_t)((w32 >> (8 * (b & 3))) & 0xffu);
                 c1[b] = __fma_rn(s1, wv, c1[b]);
                 if (DD) c2[b] = __fma_rn(s2, wv, c2[b]);
             }
         };
         int l = 0;
+        for (; l + 8 <= cc.n; l += 8) {  // 8 plane loads in flight per thread
+            uint2 wv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) wv[u] = __ldcs(reinterpret_cast<const uint2*>(wp + (int64_t)(l + u) * wplane));
+#pragma unroll
+            for (int u = 0; u < 8; ++u) fold(wv[u], l + u);
+        }
         for (; l + 4 <= cc.n; l += 4) {
             uint2 wv[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) wv[u] = __ldg(reinterpret_cast<const uint2*>(wp + (int64_t)(l + u) * wplane));
+            for (int u = 0; u < 4; ++u) wv[u] = __ldcs(reinterpret_cast<const uint2*>(wp + (int64_t)(l + u) * wplane));
 #pragma unroll
             for (int u = 0; u < 4; ++u) fold(wv[u], l + u);
         }
@@ -144,12 +164,32 @@ __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, 
     }
 }
 
+template <class T, bool DD, int NFP>
+void launch_n(unsigned grid, cudaStream_t s, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
+              const CrtConsts& cc, const int32_t* mu, const int32_t* nu, T* C, int64_t ldc, const CrtExtra& ex,
+              DevStatus* st) {
+    if (ex.bnd.on) crt_kernel<T, DD, true, NFP><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+    else crt_kernel<T, DD, false, NFP><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+}
+
+int crt_nfp() {
+    static const int v = [] {
+        const char* e = getenv("OZ2G_CRT_NFP");
+        return e ? atoi(e) : 3;
+    }();
+    return v;
+}
+
 template <class T, bool DD>
 void launch_t(unsigned grid, cudaStream_t s, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
               const CrtConsts& cc, const int32_t* mu, const int32_t* nu, T* C, int64_t ldc, const CrtExtra& ex,
               DevStatus* st) {
-    if (ex.bnd.on) crt_kernel<T, DD, true><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
-    else crt_kernel<T, DD, false><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+    switch (crt_nfp()) {
+        case 0: launch_n<T, DD, 0>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st); break;
+        case 5: launch_n<T, DD, 5>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st); break;
+        case 8: launch_n<T, DD, 8>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st); break;
+        default: launch_n<T, DD, 3>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st); break;
+    }
 }
 
 }  // namespace

@@ -106,9 +106,8 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&v)[32], int row,
         int8_t* dst = P.W + (int64_t)l * P.wplane + (int64_t)row * P.ldw + col0;
         if (col0 + 32 <= P.n) {
             uint4* d4 = reinterpret_cast<uint4*>(dst);
-            // streaming stores: W is read once by the CRT pass, keep it from evicting operands in L2
-            __stcs(d4, make_uint4(packed[0], packed[1], packed[2], packed[3]));
-            __stcs(d4 + 1, make_uint4(packed[4], packed[5], packed[6], packed[7]));
+            d4[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+            d4[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
         } else {
             for (int c = 0; c < 32 && col0 + c < P.n; ++c) dst[c] = (int8_t)((packed[c >> 2] >> (8 * (c & 3))) & 0xff);
         }

@@ -43,19 +43,18 @@ cudaError_t launch_gemm_i8_pair(int mode, const CUtensorMap& tmA, const CUtensor
                                 int num_sms, cudaStream_t stream);
 
 // Residue constants for the residue kernels (uploaded once per table): a
-// header followed by the weight table w[l][E] (E in [0, kResidE)) of two packed
-// words whose signed bytes are the symmetric representatives of
-// 2^(8t + E) mod p_l, t = 0..7 (resid.cu explains the arithmetic).
+// header followed by the weight table w[l][G][s] (G in [0, kResidE8), s = sign)
+// of two packed words whose signed bytes are the symmetric representatives of
+// (-1)^s 2^(8 (t + G)) mod p_l, t = 0..7 (resid.cu explains the arithmetic).
 struct alignas(16) ResidHeader {  // size a multiple of 16: the table that follows is read as int2/uint4
     int n, pad;
     uint32_t p[49];
-    uint32_t magic[49];  // ceil(2^32 / p): floor(U / p) == umulhi(U, magic) for U < 2^24
-    uint32_t offh[49];   // p * ceil(2^18 / p) + floor(p / 2)
-    uint32_t h4[49];     // floor(p / 2) replicated in 4 bytes
-    uint32_t negp[49];   // -p (mod 2^32)
+    float inv_p[49];  // RN32(1 / p)
+    float pf[49];     // p as float
 };
-constexpr int kResidE = 128;  // E' <= 124: |A'| < 2^(6 + P') and P' < 171 for N <= 49
-__host__ __device__ inline size_t resid_consts_bytes(int n) { return sizeof(ResidHeader) + (size_t)kResidE * n * 8; }
+constexpr int kResidE8 = 16;  // E' / 8 <= 15: |A'| < 2^(6 + P') and P' < 171 for N <= 49
+constexpr int kResidRow = kResidE8 * 2 * 8;  // bytes per modulus: [G][sign][8 bytes]
+__host__ __device__ inline size_t resid_consts_bytes(int n) { return sizeof(ResidHeader) + (size_t)kResidRow * n; }
 typedef ResidHeader ResidConsts;
 
 // Stage launchers (scale.cu).  T = float or double inputs; prec selects.

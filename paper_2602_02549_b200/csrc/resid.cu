@@ -10,16 +10,24 @@
 //   bbar_T       ceil_abs_scale_cols (scaling.hpp:122-131) -> Bbar^T [n][kp].
 //
 // Residue arithmetic.  |A'| = m' * 2^E' with m' < 2^53 (m' = mant >> -E if
-// E < 0, E' = max(E, 0)).  With the signed byte weights
-//   w[l][E'][t] = symmetric representative of 2^(8t + E') mod p_l (|w| <= 128),
-//   S = sum_t byte_t(m') * w[l][E'][t]          (two dp4a.u32.s32, |S| < 2^18)
-// is congruent to |A'| mod p_l.  U = sgn(x) * S + OFF_l with OFF_l = a multiple
-// of p_l above 2^18 plus h_l = floor(p_l / 2) lies in [0, 2^20), so
-//   r = U - p_l * umulhi(U, ceil(2^32 / p_l))  in [0, p_l)   (exact for U < 2^24)
-// and r - h_l is the reference's representative of A' mod p_l
-// (crt.hpp:48-52): symmetric for odd p; for p = 256 the byte of r - 128 equals
-// A' mod 256 as int8, which is how the reference stores the class 128 (-128).
-// The subtraction of h_l is done per byte on the packed word (vsub4).
+// E < 0, E' = max(E, 0)); write it as g * 2^(8 G) with g = m' << (E' mod 8)
+// < 2^60 and G = E' / 8.  With the signed byte weights
+//   w[l][G][s][t] = symmetric representative of (-1)^s 2^(8 (t + G)) mod p_l
+//   S = sum_t byte_t(g) * w[l][G][sgn(x)][t]     (two dp4a.u32.s32, |S| < 2^18)
+// is congruent to A' mod p_l.  The dp4a accumulator starts at the bit pattern
+// of M = 1.5 * 2^23, so the integer result is the bit pattern of the float
+// M + S (exact: the float has ulp 1 on [2^23, 2^24)).  Then, in fp32,
+//   q = round(S / p) = RN(S * RN(1/p) + M) - M      (|error| < 2^-13.5, while
+//       S / p is >= 1/(2p) > 2^-9 away from a half-integer for odd p;
+//       for p = 256 the product is exact)
+//   M + r = (M + S) - q * p                         (exact, integers < 2^24)
+// and the low byte of the bit pattern of M + r is r as int8: r is the
+// reference's representative of A' mod p_l (crt.hpp:48-52), symmetric for odd
+// p; for p = 256, r = +-128 both give the byte 0x80, which is how the
+// reference stores the class 128 (-128).  Per (element, modulus): one LDS.64,
+// two IDP, four fp32 operations, and 3/4 of a PRMT to pack.  Bucketing E' by 8
+// keeps the table small (256 B per modulus) and the lanes of a warp on one or
+// two entries, so the weight loads are broadcasts.
 #include "device_common.cuh"
 #include "kernels.h"
 
@@ -33,13 +41,12 @@ template <class T>
 __device__ __forceinline__ double ld_d(const T* p) { return (double)__ldg(p); }
 
 struct ElemDec {
-    uint32_t lo, hi;  // bytes 0-3 / 4-7 of m'
-    uint32_t off;     // 8 * E': byte offset into the weight row of a modulus
-    int32_t sgn;      // +1, -1, or 0 for x == 0
+    uint32_t lo, hi;  // bytes 0-3 / 4-7 of m' << (E' mod 8)  (< 2^60)
+    uint32_t off;     // byte offset of the weights: 16 * (E' / 8) (+ 8 for x < 0)
 };
 
 __device__ __forceinline__ ElemDec elem_dec(double x, int shift, bool& overflow) {
-    ElemDec d{0u, 0u, 0u, 0};
+    ElemDec d{0u, 0u, 0u};
     if (x == 0.0) return d;
     uint64_t mant; int e2;
     decompose(x, mant, e2);
@@ -49,12 +56,12 @@ __device__ __forceinline__ ElemDec elem_dec(double x, int shift, bool& overflow)
     uint64_t mp = mant;
     int Ep = E;
     if (E < 0) { mp = (-E >= 64) ? 0ull : (mant >> (-E)); Ep = 0; }
-    // |A'| < 2^(6 + P') < 2^177 for every valid input, so E' <= 124 < kResidE
-    if (Ep > kResidE - 1) { overflow = true; Ep = kResidE - 1; }
+    // |A'| < 2^(6 + P') < 2^177 for every valid input, so E' <= 124 < 8 * kResidE8
+    if (Ep > 8 * kResidE8 - 1) { overflow = true; Ep = 8 * kResidE8 - 1; }
+    mp <<= (Ep & 7);
     d.lo = (uint32_t)mp;
     d.hi = (uint32_t)(mp >> 32);
-    d.off = (uint32_t)Ep * 8u;
-    d.sgn = x < 0.0 ? -1 : 1;
+    d.off = (uint32_t)(Ep >> 3) * 16u + (x < 0.0 ? 8u : 0u);
     return d;
 }
 
@@ -65,17 +72,22 @@ __device__ __forceinline__ int dp4a_us(uint32_t a, int32_t b, int32_t c) {
 }
 
 struct ModC {
-    uint32_t magic, offh, h4, negp;
+    float inv_p, pf;
 };
 
-// r in [0, p) with r - h == residue of sgn * m' * 2^E' (see the file header)
-__device__ __forceinline__ uint32_t resid_r(const ElemDec& d, const uint8_t* __restrict__ row_l, const ModC& c) {
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23 (bits 0x4B400000): ulp 1 on [2^23, 2^24)
+
+// Word whose low byte is the reference's representative of sgn * m' * 2^E' mod p
+// (see the file header).  All four fp32 operations are exact except the one
+// rounding to an integer, which yields round(S / p) for |S| < 2^18.
+__device__ __forceinline__ uint32_t resid_w(const ElemDec& d, const uint8_t* __restrict__ row_l, const ModC& c) {
     const int2 w = *reinterpret_cast<const int2*>(row_l + d.off);
-    int S = dp4a_us(d.lo, w.x, 0);
-    S = dp4a_us(d.hi, w.y, S);
-    const uint32_t U = (uint32_t)(S * d.sgn) + c.offh;
-    const uint32_t q = __umulhi(U, c.magic);
-    return U + q * c.negp;
+    const int bits = dp4a_us(d.hi, w.y, dp4a_us(d.lo, w.x, 0x4B400000));  // bits of the float M + S
+    const float fU = __int_as_float(bits);
+    const float u = __fsub_rn(fU, kMagic);                 // S
+    const float t = __fmaf_rn(u, c.inv_p, kMagic);         // M + round(S / p)
+    const float nq = __fsub_rn(kMagic, t);                 // -round(S / p)
+    return __float_as_uint(__fmaf_rn(nq, c.pf, fU));       // M + S - p round(S / p)
 }
 
 __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
@@ -91,18 +103,13 @@ __device__ __forceinline__ void load_resid_consts(const ResidHeader* __restrict_
     for (int t = threadIdx.x; t < words; t += blockDim.x) dst[t] = src[t];
 }
 
-__device__ __forceinline__ ModC modc(const ResidHeader& hd, int l) {
-    ModC c;
-    c.magic = hd.magic[l];
-    c.offh = hd.offh[l];
-    c.h4 = hd.h4[l];
-    c.negp = hd.negp[l];
-    return c;
-}
+__device__ __forceinline__ ModC modc(const ResidHeader& hd, int l) { return ModC{hd.inv_p[l], hd.pf[l]}; }
 
 // ---------------------------------------------------------------------------
 // A: each thread owns 8 consecutive columns of one row (one 8-byte store per
-// plane, 16-byte vector loads).
+// plane, 16-byte vector loads).  grid.x covers the 2048-column chunks of a
+// row; a CTA walks rows blockIdx.y, blockIdx.y + gridDim.y, ... so the weight
+// table is loaded once per CTA instead of once per row chunk.
 // ---------------------------------------------------------------------------
 constexpr int RA_E = 8;
 
@@ -114,54 +121,57 @@ __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, i
     extern __shared__ __align__(16) uint8_t sh[];
     load_resid_consts(rc_g, nmod, sh);
     __syncthreads();
-    const int64_t i = blockIdx.y;
-    const int64_t h0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * RA_E;
-    if (h0 >= kp) return;
     const ResidHeader& hd = *reinterpret_cast<const ResidHeader*>(sh);
     const uint8_t* tab = sh + sizeof(ResidHeader);
-    const int sft = mu[i];
-    const T* row = A + i * lda + h0;
-    ElemDec d[RA_E];
+    const int64_t plane = m * kp;
+    const int64_t h0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * RA_E;
     bool ovf = false;
-    if (sizeof(T) == 8 && h0 + RA_E <= k && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
+    for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
+        if (h0 >= kp) break;
+        const int sft = mu[i];
+        const T* row = A + i * lda + h0;
+        ElemDec d[RA_E];
+        if (sizeof(T) == 8 && h0 + RA_E <= k && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
 #pragma unroll
-        for (int j = 0; j < RA_E; j += 2) {
-            const double2 v = __ldg(reinterpret_cast<const double2*>(row + j));
-            d[j] = elem_dec(v.x, sft, ovf);
-            d[j + 1] = elem_dec(v.y, sft, ovf);
+            for (int j = 0; j < RA_E; j += 2) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(row + j));
+                d[j] = elem_dec(v.x, sft, ovf);
+                d[j + 1] = elem_dec(v.y, sft, ovf);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < RA_E; ++j) d[j] = elem_dec(h0 + j < k ? ld_d(row + j) : 0.0, sft, ovf);
         }
-    } else {
-#pragma unroll
-        for (int j = 0; j < RA_E; ++j) d[j] = elem_dec(h0 + j < k ? ld_d(row + j) : 0.0, sft, ovf);
+        int8_t* out = planes + i * kp + h0;
+#pragma unroll 2
+        for (int l = 0; l < nmod; ++l) {
+            const ModC c = modc(hd, l);
+            const uint8_t* rl = tab + (size_t)l * kResidRow;
+            const uint32_t w0 = pack4(resid_w(d[0], rl, c), resid_w(d[1], rl, c), resid_w(d[2], rl, c),
+                                      resid_w(d[3], rl, c));
+            const uint32_t w1 = pack4(resid_w(d[4], rl, c), resid_w(d[5], rl, c), resid_w(d[6], rl, c),
+                                      resid_w(d[7], rl, c));
+            *reinterpret_cast<uint2*>(out + (int64_t)l * plane) = make_uint2(w0, w1);
+        }
     }
     if (ovf) flag(st, ERR_TRUNC_A_RANGE);
-    const int64_t plane = m * kp;
-    int8_t* out = planes + i * kp + h0;
-#pragma unroll 2
-    for (int l = 0; l < nmod; ++l) {
-        const ModC c = modc(hd, l);
-        const uint8_t* rl = tab + (size_t)l * kResidE * 8;
-        const uint32_t w0 = __vsub4(pack4(resid_r(d[0], rl, c), resid_r(d[1], rl, c), resid_r(d[2], rl, c),
-                                          resid_r(d[3], rl, c)), c.h4);
-        const uint32_t w1 = __vsub4(pack4(resid_r(d[4], rl, c), resid_r(d[5], rl, c), resid_r(d[6], rl, c),
-                                          resid_r(d[7], rl, c)), c.h4);
-        *reinterpret_cast<uint2*>(out + (int64_t)l * plane) = make_uint2(w0, w1);
-    }
 }
 
 // ---------------------------------------------------------------------------
-// B transposed writers: tile 64 (h) x 64 (j), output [plane][j][kp].
+// B transposed writers: tile 32 (h) x 64 (j), 8 rows per thread, output
+// [plane][j][kp] through a shared-memory transpose, one tile per CTA.
 //   OP 0: Bbar^T = ceil(|B| 2^nu')   OP 1: residue planes of trunc(B 2^nu)
 // ---------------------------------------------------------------------------
-constexpr int TB = 64;
-constexpr int TROW = TB + 16;  // padded smem row (bytes) to spread banks
+constexpr int TB = 64;         // columns j per tile
+constexpr int THR = 32;        // rows h per tile
+constexpr int TROW = THR + 8;  // padded smem row (bytes): 8-byte stores of 16 lanes hit distinct banks
 constexpr int TCH = 8;         // moduli per smem round
 
 template <class T, int OP>
-__global__ void __launch_bounds__(256, 2) transpose_B_kernel(const T* __restrict__ B, int64_t ldb, int64_t k,
-                                                             int64_t n, int64_t kp, const int32_t* __restrict__ shift,
-                                                             const ResidHeader* __restrict__ rc_g, int nmod,
-                                                             int8_t* __restrict__ out, DevStatus* st) {
+__global__ void __launch_bounds__(256) transpose_B_kernel(const T* __restrict__ B, int64_t ldb, int64_t k,
+                                                          int64_t n, int64_t kp, const int32_t* __restrict__ shift,
+                                                          const ResidHeader* __restrict__ rc_g, int nmod,
+                                                          int8_t* __restrict__ out, DevStatus* st) {
     extern __shared__ __align__(16) uint8_t sh[];
     uint8_t* tile = sh;  // [TCH][TB][TROW]
     uint8_t* rcs = sh + TCH * TB * TROW;
@@ -169,62 +179,64 @@ __global__ void __launch_bounds__(256, 2) transpose_B_kernel(const T* __restrict
     const ResidHeader& hd = *reinterpret_cast<const ResidHeader*>(rcs);
     const uint8_t* tab = rcs + sizeof(ResidHeader);
     const int tx = threadIdx.x & 63;  // column within tile
-    const int ty = threadIdx.x >> 6;  // 4 groups of 16 rows
-    const int64_t j = (int64_t)blockIdx.x * TB + tx;
-    const int64_t hbase = (int64_t)blockIdx.y * TB + ty * 16;
-    const bool jok = j < n;
-    const int sft = jok ? shift[j] : 0;
-    double x[16];
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-        const int64_t h = hbase + r;
-        x[r] = (jok && h < k) ? ld_d(B + h * ldb + j) : 0.0;
-    }
-    __syncthreads();
+    const int ty = threadIdx.x >> 6;  // 4 groups of 8 rows
     const int nplanes = OP == 0 ? 1 : nmod;
     const int64_t plane = n * kp;
-    ElemDec d[16];
     bool flagbit = false;
-    if (OP == 1) {
+    {
+        const int64_t tj = blockIdx.x, th = blockIdx.y;
+        const int64_t j = tj * TB + tx;
+        const int64_t hbase = th * THR + ty * 8;
+        const bool jok = j < n;
+        const int sft = jok ? shift[j] : 0;
+        double x[8];
 #pragma unroll
-        for (int r = 0; r < 16; ++r) d[r] = elem_dec(x[r], sft, flagbit);
-    }
-    for (int l0 = 0; l0 < nplanes; l0 += TCH) {
-        const int lc = nplanes - l0 < TCH ? nplanes - l0 : TCH;
+        for (int r = 0; r < 8; ++r) {
+            const int64_t h = hbase + r;
+            x[r] = (jok && h < k) ? ld_d(B + h * ldb + j) : 0.0;
+        }
+        __syncthreads();  // weight table loaded
+        ElemDec d[8];
+        if (OP == 1) {
+#pragma unroll
+            for (int r = 0; r < 8; ++r) d[r] = elem_dec(x[r], sft, flagbit);
+        }
+        for (int l0 = 0; l0 < nplanes; l0 += TCH) {
+            const int lc = nplanes - l0 < TCH ? nplanes - l0 : TCH;
 #pragma unroll 1
-        for (int c = 0; c < lc; ++c) {
-            uint32_t w[4] = {0, 0, 0, 0};
-            if (OP == 0) {
+            for (int c = 0; c < lc; ++c) {
+                uint32_t w[2] = {0, 0};
+                if (OP == 0) {
 #pragma unroll
-                for (int r = 0; r < 16; ++r) {
-                    const int v = ceil_abs_scaled(x[r], sft);
-                    flagbit |= v < 0;
-                    w[r >> 2] |= (uint32_t)(v & 0xff) << (8 * (r & 3));
+                    for (int r = 0; r < 8; ++r) {
+                        const int v = ceil_abs_scaled(x[r], sft);
+                        flagbit |= v < 0;
+                        w[r >> 2] |= (uint32_t)(v & 0xff) << (8 * (r & 3));
+                    }
+                } else {
+                    const ModC mc = modc(hd, l0 + c);
+                    const uint8_t* rl = tab + (size_t)(l0 + c) * kResidRow;
+#pragma unroll
+                    for (int q = 0; q < 2; ++q)
+                        w[q] = pack4(resid_w(d[4 * q], rl, mc), resid_w(d[4 * q + 1], rl, mc),
+                                     resid_w(d[4 * q + 2], rl, mc), resid_w(d[4 * q + 3], rl, mc));
                 }
-            } else {
-                const ModC mc = modc(hd, l0 + c);
-                const uint8_t* rl = tab + (size_t)(l0 + c) * kResidE * 8;
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    w[q] = __vsub4(pack4(resid_r(d[4 * q], rl, mc), resid_r(d[4 * q + 1], rl, mc),
-                                         resid_r(d[4 * q + 2], rl, mc), resid_r(d[4 * q + 3], rl, mc)),
-                                   mc.h4);
+                *reinterpret_cast<uint2*>(tile + (c * TB + tx) * TROW + ty * 8) = make_uint2(w[0], w[1]);
             }
-            *reinterpret_cast<uint4*>(tile + (c * TB + tx) * TROW + ty * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+            __syncthreads();
+            // write out: per (c, row jj) 32 contiguous bytes = 4 x 8 B (one full sector)
+            for (int idx = threadIdx.x; idx < lc * TB * 4; idx += blockDim.x) {
+                const int q = idx & 3;
+                const int jj = (idx >> 2) % TB;
+                const int c = (idx >> 2) / TB;
+                const int64_t jg = tj * TB + jj;
+                if (jg >= n) continue;
+                const int64_t hg = th * THR + q * 8;
+                const uint2 val = *reinterpret_cast<const uint2*>(tile + (c * TB + jj) * TROW + q * 8);
+                *reinterpret_cast<uint2*>(out + (int64_t)(l0 + c) * plane + jg * kp + hg) = val;
+            }
+            if (l0 + TCH < nplanes) __syncthreads();
         }
-        __syncthreads();
-        // write out: per (c, row jj) 64 contiguous bytes = 4 x 16 B
-        for (int idx = threadIdx.x; idx < lc * TB * 4; idx += blockDim.x) {
-            const int q = idx & 3;
-            const int jj = (idx >> 2) % TB;
-            const int c = (idx >> 2) / TB;
-            const int64_t jg = (int64_t)blockIdx.x * TB + jj;
-            if (jg >= n) continue;
-            const int64_t hg = (int64_t)blockIdx.y * TB + q * 16;
-            const uint4 val = *reinterpret_cast<const uint4*>(tile + (c * TB + jj) * TROW + q * 16);
-            *reinterpret_cast<uint4*>(out + (int64_t)(l0 + c) * plane + jg * kp + hg) = val;
-        }
-        __syncthreads();
     }
     if (flagbit) flag(st, OP == 0 ? ERR_CEIL_LOGIC : ERR_TRUNC_B_RANGE);
 }
@@ -240,12 +252,31 @@ cudaError_t set_smem(K kernel, size_t bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+// resid_A grid: x = column chunks, y = enough row strides for kResidWaves waves
+// of resident CTAs (each CTA then loads the weight table once for m / y rows).
+constexpr int kResidWaves = 4;
+
+template <class K>
+cudaError_t resid_A_grid(K kernel, size_t smem, int64_t m, unsigned chunks, dim3& grid) {
+    cudaError_t err = set_smem(kernel, smem);
+    if (err != cudaSuccess) return err;
+    int dev = 0, sms = 0, per_sm = 0;
+    if ((err = cudaGetDevice(&dev)) != cudaSuccess) return err;
+    if ((err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return err;
+    if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem)) != cudaSuccess) return err;
+    const int64_t ctas = (int64_t)sms * (per_sm > 0 ? per_sm : 1) * kResidWaves;
+    int64_t rows = (ctas + chunks - 1) / chunks;
+    rows = rows < m ? rows : m;
+    grid = dim3(chunks, (unsigned)(rows < 65535 ? rows : 65535));
+    return cudaSuccess;
+}
+
 }  // namespace
 
 cudaError_t launch_bbar_T(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp,
                           const int32_t* nu_prime, int8_t* bbar_t, DevStatus* st, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    dim3 grid(blocks_for(n, TB), (unsigned)(kp / TB));
+    const dim3 grid(blocks_for(n, TB), (unsigned)(kp / THR));
     const size_t sm = transpose_smem(0, 1);
     if (prec)
         transpose_B_kernel<double, 0><<<grid, 256, sm, s>>>((const double*)B, ldb, k, n, kp, nu_prime, nullptr, 1, bbar_t, st);
@@ -258,7 +289,7 @@ cudaError_t launch_resid_BT(int prec, const void* B, int64_t ldb, int64_t k, int
                             const int32_t* nu, const ResidConsts* rc_dev, int nmod, int8_t* planes,
                             DevStatus* st, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    dim3 grid(blocks_for(n, TB), (unsigned)(kp / TB));
+    const dim3 grid(blocks_for(n, TB), (unsigned)(kp / THR));
     const size_t sm = transpose_smem(1, nmod);
     cudaError_t err;
     if (prec) {
@@ -275,14 +306,15 @@ cudaError_t launch_resid_A(int prec, const void* A, int64_t lda, int64_t m, int6
                            const int32_t* mu, const ResidConsts* rc_dev, int nmod, int8_t* planes,
                            DevStatus* st, cudaStream_t s) {
     if (m == 0) return cudaSuccess;
-    dim3 grid(blocks_for(kp, 256 * RA_E), (unsigned)m);
+    const unsigned chunks = blocks_for(kp, 256 * RA_E);
     const size_t sm = resid_consts_bytes(nmod);
+    dim3 grid;
     cudaError_t err;
     if (prec) {
-        if ((err = set_smem(resid_A_kernel<double>, sm)) != cudaSuccess) return err;
+        if ((err = resid_A_grid(resid_A_kernel<double>, sm, m, chunks, grid)) != cudaSuccess) return err;
         resid_A_kernel<double><<<grid, 256, sm, s>>>((const double*)A, lda, m, k, kp, mu, rc_dev, nmod, planes, st);
     } else {
-        if ((err = set_smem(resid_A_kernel<float>, sm)) != cudaSuccess) return err;
+        if ((err = resid_A_grid(resid_A_kernel<float>, sm, m, chunks, grid)) != cudaSuccess) return err;
         resid_A_kernel<float><<<grid, 256, sm, s>>>((const float*)A, lda, m, k, kp, mu, rc_dev, nmod, planes, st);
     }
     return cudaGetLastError();

@@ -1,4 +1,7 @@
-"""Summarise an ncu --metrics gpu__time_duration.sum CSV launch list."""
+"""Summarise an ncu --metrics CSV launch list (one or more metrics per launch).
+
+Prints per kernel: launches, mean/min duration (ms) and, when captured, mean
+DRAM read/write GB per launch."""
 import csv
 import sys
 from collections import OrderedDict
@@ -6,13 +9,25 @@ from collections import OrderedDict
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 h = rows[hdr]
-ki, vi = h.index("Kernel Name"), h.index("Metric Value")
-agg = OrderedDict()
+ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
+launch = OrderedDict()  # launch id -> (name, {metric: value})
 for r in rows[hdr + 1:]:
-    if len(r) > vi:
-        name = r[ki].split("(")[0].replace("void ", "").replace("oz2g::<unnamed>::", "")
-        agg.setdefault(name, []).append(float(r[vi].replace(",", "")) / 1e6)
-tot = sum(sum(v) for k, v in agg.items() if "oz2g" in k or "gemm_i8" in k or "kernel" in k)
-print(f"{'kernel':60s} {'n':>3s} {'mean ms':>9s} {'min ms':>9s}")
+    if len(r) <= vi:
+        continue
+    name = r[ki].split("(")[0].replace("void ", "").replace("oz2g::<unnamed>::", "")
+    launch.setdefault(r[ii], (name, {}))[1][r[mi]] = float(r[vi].replace(",", ""))
+agg = OrderedDict()
+for name, met in launch.values():
+    agg.setdefault(name, []).append(met)
+
+
+def col(v, key, scale):
+    xs = [m[key] for m in v if key in m]
+    return (sum(xs) / len(xs) / scale) if xs else float("nan")
+
+
+print(f"{'kernel':56s} {'n':>3s} {'mean ms':>9s} {'min ms':>9s} {'rd GB':>8s} {'wr GB':>8s}")
 for k, v in agg.items():
-    print(f"{k[:60]:60s} {len(v):3d} {sum(v)/len(v):9.3f} {min(v):9.3f}")
+    ts = [m["gpu__time_duration.sum"] / 1e6 for m in v if "gpu__time_duration.sum" in m]
+    print(f"{k[:56]:56s} {len(v):3d} {sum(ts)/len(ts):9.3f} {min(ts):9.3f} "
+          f"{col(v, 'dram__bytes_read.sum', 1e9):8.2f} {col(v, 'dram__bytes_write.sum', 1e9):8.2f}")
