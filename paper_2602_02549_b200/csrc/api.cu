@@ -213,11 +213,17 @@ void set_l2_hints(GemmParams& g) {
 
 // Raster group height: one wave of persistent CTAs covers group_m tile-rows,
 // so B tiles are streamed from HBM about tiles_m / group_m times per plane.
-int group_m_for(int tiles_m) {
+// OZ2G_GROUP_N > 0 groups tile-columns instead (returned negated).
+int group_m_for(int tiles_m, int tiles_n) {
     static const int env = [] {
         const char* s = std::getenv("OZ2G_GROUP_M");
         return s ? std::atoi(s) : 0;
     }();
+    static const int env_n = [] {
+        const char* s = std::getenv("OZ2G_GROUP_N");
+        return s ? std::atoi(s) : 0;
+    }();
+    if (env_n > 0) return -(env_n < tiles_n ? env_n : (tiles_n > 0 ? tiles_n : 1));
     int g = env > 0 ? env : 16;  // best of {8, 12, 16, 24, 32} at 16384^3 (interleaved A/B)
     return g < tiles_m ? g : (tiles_m > 0 ? tiles_m : 1);
 }
@@ -344,7 +350,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     auto set_rows = [&](GemmParams& g, int64_t rows) {
         g.m = (int)rows;
         g.tiles_m = (int)((rows + BM - 1) / BM);
-        g.group_m = group_m_for(g.tiles_m);
+        g.group_m = group_m_for(g.tiles_m, g.tiles_n);
     };
 
     // ---- K1 (A) + K2 per row chunk: row pre-exponents, Abar, clearance product with fused maxima ----
@@ -658,7 +664,7 @@ int run_suggest_n(int prec, int64_t m, int64_t n, int64_t k, const void* A, int6
     gp.kblocks = (int)(kp / 128);
     gp.tiles_m = (int)((m + gemm_tile_m() - 1) / gemm_tile_m());
     gp.tiles_n = (int)((n + gemm_tile_n() - 1) / gemm_tile_n());
-    gp.group_m = group_m_for(gp.tiles_m);
+    gp.group_m = group_m_for(gp.tiles_m, gp.tiles_n);
     set_l2_hints(gp);
     gp.planes = 1;
     gp.rowmax = cmax_row;

@@ -16,7 +16,6 @@
 // Optionally (BND) the same pass evaluates the cheap and tight error bounds
 // of bounds.hpp:143-206 for every entry (see bounds.cu for the derivation).
 #include <cfloat>
-#include <cstdlib>
 
 #include "device_common.cuh"
 #include "kernels.h"
@@ -172,24 +171,14 @@ void launch_n(unsigned grid, cudaStream_t s, const int8_t* W, int64_t ldw, int64
     else crt_kernel<T, DD, false, NFP><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
 }
 
-int crt_nfp() {
-    static const int v = [] {
-        const char* e = getenv("OZ2G_CRT_NFP");
-        return e ? atoi(e) : 3;
-    }();
-    return v;
-}
+// 3 of 8 conversions on the fp64 pipe: measured best of {0, 3, 5, 8} at 16384^2, N = 16
+constexpr int kCrtNfp = 3;
 
 template <class T, bool DD>
 void launch_t(unsigned grid, cudaStream_t s, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
               const CrtConsts& cc, const int32_t* mu, const int32_t* nu, T* C, int64_t ldc, const CrtExtra& ex,
               DevStatus* st) {
-    switch (crt_nfp()) {
-        case 0: launch_n<T, DD, 0>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st); break;
-        case 5: launch_n<T, DD, 5>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st); break;
-        case 8: launch_n<T, DD, 8>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st); break;
-        default: launch_n<T, DD, 3>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st); break;
-    }
+    launch_n<T, DD, kCrtNfp>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
 }
 
 }  // namespace

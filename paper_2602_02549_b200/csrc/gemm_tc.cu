@@ -27,6 +27,8 @@
 //   warp 2      TMEM allocator;
 //   warps 4..7  epilogue: tcgen05.ld 32 lanes x 32 columns, fused reduction.
 // Operands are K-major (A planes [l][m][kp], B planes [l][n][kp]).
+#include <cstdlib>
+
 #include "device_common.cuh"
 #include "kernels.h"
 
@@ -42,18 +44,32 @@ constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /
 
 struct TileCoord { int l, tm, tn; };
 
+// Grouped raster: group_m > 0 walks groups of group_m tile-rows column by
+// column (B tiles reused across the group); group_m < 0 walks groups of
+// -group_m tile-columns row by row (A tiles reused).
 __device__ __forceinline__ TileCoord decode_unit(int u, int tiles_m, int tiles_n, int group_m) {
     const int per_plane = tiles_m * tiles_n;
     TileCoord c;
     c.l = u / per_plane;
     const int t = u - c.l * per_plane;
-    const int group = group_m * tiles_n;
-    const int g = t / group;
-    const int first_m = g * group_m;
-    const int gm = min(tiles_m - first_m, group_m);
-    const int r = t - g * group;
-    c.tm = first_m + r % gm;
-    c.tn = r / gm;
+    if (group_m > 0) {
+        const int group = group_m * tiles_n;
+        const int g = t / group;
+        const int first_m = g * group_m;
+        const int gm = min(tiles_m - first_m, group_m);
+        const int r = t - g * group;
+        c.tm = first_m + r % gm;
+        c.tn = r / gm;
+    } else {
+        const int group_n = -group_m;
+        const int group = group_n * tiles_m;
+        const int g = t / group;
+        const int first_n = g * group_n;
+        const int gn = min(tiles_n - first_n, group_n);
+        const int r = t - g * group;
+        c.tn = first_n + r % gn;
+        c.tm = r / gn;
+    }
     return c;
 }
 
@@ -250,12 +266,11 @@ __global__ void __launch_bounds__(256, 1)
 // ---------------------------------------------------------------------------
 constexpr int P_BM = 256, P_BN = 256;     // pair tile
 constexpr int P_HALF = 128;               // rows of A and of B^T per CTA
-constexpr int P_STAGES = 6;
 constexpr int P_STAGE_BYTES = 2 * P_HALF * BK;  // 32 KB per CTA per stage
 constexpr uint32_t P_IDESC = idesc_i8(P_BM, P_BN);
-constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+constexpr int p_smem_bytes(int stages) { return stages * P_STAGE_BYTES + 1024 + 256; }
 
-template <int MODE>
+template <int MODE, int P_STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_i8_tc_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                            const __grid_constant__ GemmParams P) {
@@ -423,34 +438,40 @@ int gemm_pair_tile_m() { return P_BM; }
 int gemm_pair_tile_n() { return P_BN; }
 int gemm_pair_box_rows() { return P_HALF; }
 
+template <int MODE, int ST>
+cudaError_t launch_pair_t(int grid, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& P,
+                          cudaStream_t stream) {
+    cudaError_t err = cudaFuncSetAttribute(gemm_i8_tc_pair_kernel<MODE, ST>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_bytes(ST));
+    if (err != cudaSuccess) return err;
+    gemm_i8_tc_pair_kernel<MODE, ST><<<grid, 256, p_smem_bytes(ST), stream>>>(tmA, tmB, P);
+    return cudaGetLastError();
+}
+
+template <int ST>
+cudaError_t launch_pair_s(int mode, int grid, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& P,
+                          cudaStream_t stream) {
+    switch (mode) {
+        case EPI_MAX: return launch_pair_t<EPI_MAX, ST>(grid, tmA, tmB, P, stream);
+        case EPI_RESID: return launch_pair_t<EPI_RESID, ST>(grid, tmA, tmB, P, stream);
+        default: return launch_pair_t<EPI_I32, ST>(grid, tmA, tmB, P, stream);
+    }
+}
+
 cudaError_t launch_gemm_i8_pair(int mode, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& P,
                                 int num_sms, cudaStream_t stream) {
     const int total = P.planes * P.tiles_m * P.tiles_n;  // pair tiles
     if (total == 0) return cudaSuccess;
     const int pairs = num_sms / 2;
     const int grid = 2 * (total < pairs ? total : pairs);
-    cudaError_t err = cudaSuccess;
-    switch (mode) {
-        case EPI_MAX:
-            err = cudaFuncSetAttribute(gemm_i8_tc_pair_kernel<EPI_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       P_SMEM_BYTES);
-            if (err != cudaSuccess) return err;
-            gemm_i8_tc_pair_kernel<EPI_MAX><<<grid, 256, P_SMEM_BYTES, stream>>>(tmA, tmB, P);
-            break;
-        case EPI_RESID:
-            err = cudaFuncSetAttribute(gemm_i8_tc_pair_kernel<EPI_RESID>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
-            if (err != cudaSuccess) return err;
-            gemm_i8_tc_pair_kernel<EPI_RESID><<<grid, 256, P_SMEM_BYTES, stream>>>(tmA, tmB, P);
-            break;
-        default:
-            err = cudaFuncSetAttribute(gemm_i8_tc_pair_kernel<EPI_I32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       P_SMEM_BYTES);
-            if (err != cudaSuccess) return err;
-            gemm_i8_tc_pair_kernel<EPI_I32><<<grid, 256, P_SMEM_BYTES, stream>>>(tmA, tmB, P);
-            break;
-    }
-    return cudaGetLastError();
+    static const int stages = [] {
+        const char* e = getenv("OZ2G_PAIR_STAGES");
+        return e ? atoi(e) : 4;
+    }();
+    // deeper pipelines let the clusters drift apart and lose L2 sharing:
+    // DRAM reads 82 GB (4 stages), 245 GB (6), 250 GB (7) at 16384^3, N = 16
+    if (stages == 6) return launch_pair_s<6>(mode, grid, tmA, tmB, P, stream);
+    return launch_pair_s<4>(mode, grid, tmA, tmB, P, stream);
 }
 
 }  // namespace oz2g

@@ -126,8 +126,8 @@ __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, i
     const int64_t plane = m * kp;
     const int64_t h0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * RA_E;
     bool ovf = false;
+    if (h0 >= kp) return;
     for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
-        if (h0 >= kp) break;
         const int sft = mu[i];
         const T* row = A + i * lda + h0;
         ElemDec d[RA_E];
@@ -158,14 +158,17 @@ __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, i
 }
 
 // ---------------------------------------------------------------------------
-// B transposed writers: tile 32 (h) x 64 (j), 8 rows per thread, output
-// [plane][j][kp] through a shared-memory transpose, one tile per CTA.
+// B transposed writers, output [plane][j][kp] (K-major).  A warp covers 8
+// columns x 32 rows: lane = 4 * column + row group, each lane 8 consecutive
+// rows of one column, so the 4 lanes of a column hold its 32 consecutive
+// output bytes and every warp store writes 8 full 32-byte sectors — no shared
+// memory transpose.  Loads read 64-byte row segments (full sectors).  A CTA (8
+// warps, 64 columns) walks TB_H consecutive 32-row tiles.
 //   OP 0: Bbar^T = ceil(|B| 2^nu')   OP 1: residue planes of trunc(B 2^nu)
 // ---------------------------------------------------------------------------
-constexpr int TB = 64;         // columns j per tile
-constexpr int THR = 32;        // rows h per tile
-constexpr int TROW = THR + 8;  // padded smem row (bytes): 8-byte stores of 16 lanes hit distinct banks
-constexpr int TCH = 8;         // moduli per smem round
+constexpr int TB = 64;    // columns j per CTA
+constexpr int THR = 32;   // rows h per tile
+constexpr int TB_H = 8;   // tiles per CTA
 
 template <class T, int OP>
 __global__ void __launch_bounds__(256) transpose_B_kernel(const T* __restrict__ B, int64_t ldb, int64_t k,
@@ -173,69 +176,58 @@ __global__ void __launch_bounds__(256) transpose_B_kernel(const T* __restrict__ 
                                                           const ResidHeader* __restrict__ rc_g, int nmod,
                                                           int8_t* __restrict__ out, DevStatus* st) {
     extern __shared__ __align__(16) uint8_t sh[];
-    uint8_t* tile = sh;  // [TCH][TB][TROW]
-    uint8_t* rcs = sh + TCH * TB * TROW;
-    if (OP == 1) load_resid_consts(rc_g, nmod, rcs);
-    const ResidHeader& hd = *reinterpret_cast<const ResidHeader*>(rcs);
-    const uint8_t* tab = rcs + sizeof(ResidHeader);
-    const int tx = threadIdx.x & 63;  // column within tile
-    const int ty = threadIdx.x >> 6;  // 4 groups of 8 rows
-    const int nplanes = OP == 0 ? 1 : nmod;
+    if (OP == 1) {
+        load_resid_consts(rc_g, nmod, sh);
+        __syncthreads();
+    }
+    const ResidHeader& hd = *reinterpret_cast<const ResidHeader*>(sh);
+    const uint8_t* tab = sh + sizeof(ResidHeader);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t j = (int64_t)blockIdx.y * TB + warp * 8 + (lane >> 2);
+    if (j >= n) return;
+    const int sft = shift[j];
     const int64_t plane = n * kp;
     bool flagbit = false;
-    {
-        const int64_t tj = blockIdx.x, th = blockIdx.y;
-        const int64_t j = tj * TB + tx;
-        const int64_t hbase = th * THR + ty * 8;
-        const bool jok = j < n;
-        const int sft = jok ? shift[j] : 0;
+    const int64_t hend = (int64_t)(blockIdx.x + 1) * TB_H * THR;
+    const int64_t hmax = kp < hend ? kp : hend;
+    int64_t h0 = (int64_t)blockIdx.x * TB_H * THR + (lane & 3) * 8;
+    // the next tile's rows are loaded while this one computes (latency hiding)
+    double xn[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) xn[r] = h0 + r < k ? ld_d(B + (h0 + r) * ldb + j) : 0.0;
+    for (; h0 < hmax; h0 += THR) {
         double x[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const int64_t h = hbase + r;
-            x[r] = (jok && h < k) ? ld_d(B + h * ldb + j) : 0.0;
+        for (int r = 0; r < 8; ++r) x[r] = xn[r];
+        const int64_t h1 = h0 + THR;
+        if (h1 < hmax) {
+#pragma unroll
+            for (int r = 0; r < 8; ++r) xn[r] = h1 + r < k ? ld_d(B + (h1 + r) * ldb + j) : 0.0;
         }
-        __syncthreads();  // weight table loaded
-        ElemDec d[8];
-        if (OP == 1) {
+        int8_t* o = out + j * kp + h0;
+        if (OP == 0) {
+            uint32_t w[2] = {0, 0};
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int v = ceil_abs_scaled(x[r], sft);
+                flagbit |= v < 0;
+                w[r >> 2] |= (uint32_t)(v & 0xff) << (8 * (r & 3));
+            }
+            *reinterpret_cast<uint2*>(o) = make_uint2(w[0], w[1]);
+        } else {
+            ElemDec d[8];
 #pragma unroll
             for (int r = 0; r < 8; ++r) d[r] = elem_dec(x[r], sft, flagbit);
-        }
-        for (int l0 = 0; l0 < nplanes; l0 += TCH) {
-            const int lc = nplanes - l0 < TCH ? nplanes - l0 : TCH;
-#pragma unroll 1
-            for (int c = 0; c < lc; ++c) {
-                uint32_t w[2] = {0, 0};
-                if (OP == 0) {
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) {
-                        const int v = ceil_abs_scaled(x[r], sft);
-                        flagbit |= v < 0;
-                        w[r >> 2] |= (uint32_t)(v & 0xff) << (8 * (r & 3));
-                    }
-                } else {
-                    const ModC mc = modc(hd, l0 + c);
-                    const uint8_t* rl = tab + (size_t)(l0 + c) * kResidRow;
-#pragma unroll
-                    for (int q = 0; q < 2; ++q)
-                        w[q] = pack4(resid_w(d[4 * q], rl, mc), resid_w(d[4 * q + 1], rl, mc),
-                                     resid_w(d[4 * q + 2], rl, mc), resid_w(d[4 * q + 3], rl, mc));
-                }
-                *reinterpret_cast<uint2*>(tile + (c * TB + tx) * TROW + ty * 8) = make_uint2(w[0], w[1]);
+#pragma unroll 2
+            for (int l = 0; l < nmod; ++l) {
+                const ModC mc = modc(hd, l);
+                const uint8_t* rl = tab + (size_t)l * kResidRow;
+                const uint32_t w0 = pack4(resid_w(d[0], rl, mc), resid_w(d[1], rl, mc), resid_w(d[2], rl, mc),
+                                          resid_w(d[3], rl, mc));
+                const uint32_t w1 = pack4(resid_w(d[4], rl, mc), resid_w(d[5], rl, mc), resid_w(d[6], rl, mc),
+                                          resid_w(d[7], rl, mc));
+                *reinterpret_cast<uint2*>(o + (int64_t)l * plane) = make_uint2(w0, w1);
             }
-            __syncthreads();
-            // write out: per (c, row jj) 32 contiguous bytes = 4 x 8 B (one full sector)
-            for (int idx = threadIdx.x; idx < lc * TB * 4; idx += blockDim.x) {
-                const int q = idx & 3;
-                const int jj = (idx >> 2) % TB;
-                const int c = (idx >> 2) / TB;
-                const int64_t jg = tj * TB + jj;
-                if (jg >= n) continue;
-                const int64_t hg = th * THR + q * 8;
-                const uint2 val = *reinterpret_cast<const uint2*>(tile + (c * TB + jj) * TROW + q * 8);
-                *reinterpret_cast<uint2*>(out + (int64_t)(l0 + c) * plane + jg * kp + hg) = val;
-            }
-            if (l0 + TCH < nplanes) __syncthreads();
         }
     }
     if (flagbit) flag(st, OP == 0 ? ERR_CEIL_LOGIC : ERR_TRUNC_B_RANGE);
@@ -243,9 +235,7 @@ __global__ void __launch_bounds__(256) transpose_B_kernel(const T* __restrict__ 
 
 inline unsigned blocks_for(int64_t work, int per) { return (unsigned)((work + per - 1) / per); }
 
-size_t transpose_smem(int op, int nmod) {
-    return (size_t)TCH * TB * TROW + (op == 1 ? resid_consts_bytes(nmod) : 0);
-}
+size_t transpose_smem(int op, int nmod) { return op == 1 ? resid_consts_bytes(nmod) : 0; }
 
 template <class K>
 cudaError_t set_smem(K kernel, size_t bytes) {
@@ -276,7 +266,7 @@ cudaError_t resid_A_grid(K kernel, size_t smem, int64_t m, unsigned chunks, dim3
 cudaError_t launch_bbar_T(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp,
                           const int32_t* nu_prime, int8_t* bbar_t, DevStatus* st, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    const dim3 grid(blocks_for(n, TB), (unsigned)(kp / THR));
+    const dim3 grid(blocks_for(kp, TB_H * THR), blocks_for(n, TB));
     const size_t sm = transpose_smem(0, 1);
     if (prec)
         transpose_B_kernel<double, 0><<<grid, 256, sm, s>>>((const double*)B, ldb, k, n, kp, nu_prime, nullptr, 1, bbar_t, st);
@@ -289,7 +279,7 @@ cudaError_t launch_resid_BT(int prec, const void* B, int64_t ldb, int64_t k, int
                             const int32_t* nu, const ResidConsts* rc_dev, int nmod, int8_t* planes,
                             DevStatus* st, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    const dim3 grid(blocks_for(n, TB), (unsigned)(kp / THR));
+    const dim3 grid(blocks_for(kp, TB_H * THR), blocks_for(n, TB));
     const size_t sm = transpose_smem(1, nmod);
     cudaError_t err;
     if (prec) {
