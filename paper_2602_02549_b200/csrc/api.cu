@@ -71,6 +71,9 @@ struct DevBuf {
 // (see run_gemm): uploads of A overlap the row scan and the clearance GEMM,
 // and the download of each finished C row block overlaps the next block.
 constexpr int kPipeChunks = 8;
+// The last C row block is split in this many pieces so that only a small
+// download follows the last kernel.
+constexpr int kTailSplit = 4;
 
 struct Workspace {
     DevBuf A, B, C, abar, bbar, ares, bres, W, mup, nup, mu, nu, bmax, cmax_row, cmax_col, e, f, status;
@@ -80,16 +83,15 @@ struct Workspace {
     // copy streams / events of the pipelined host-pointer path
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_start = nullptr, ev_b = nullptr, ev_done = nullptr;
-    cudaEvent_t ev_a[kPipeChunks] = {}, ev_c[kPipeChunks] = {};
+    cudaEvent_t ev_a[kPipeChunks] = {}, ev_c[kPipeChunks + kTailSplit] = {};
     void ensure_streams() {
         if (s_h2d) return;
         CUDA_TRY(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking));
         CUDA_TRY(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking));
         for (cudaEvent_t* e : {&ev_start, &ev_b, &ev_done}) CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-        for (int c = 0; c < kPipeChunks; ++c) {
-            CUDA_TRY(cudaEventCreateWithFlags(&ev_a[c], cudaEventDisableTiming));
+        for (int c = 0; c < kPipeChunks; ++c) CUDA_TRY(cudaEventCreateWithFlags(&ev_a[c], cudaEventDisableTiming));
+        for (int c = 0; c < kPipeChunks + kTailSplit; ++c)
             CUDA_TRY(cudaEventCreateWithFlags(&ev_c[c], cudaEventDisableTiming));
-        }
     }
     void release() {
         for (DevBuf* b : {&A, &B, &C, &abar, &bbar, &ares, &bres, &W, &mup, &nup, &mu, &nu, &bmax, &cmax_row,
@@ -353,7 +355,24 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         g.group_m = group_m_for(g.tiles_m, g.tiles_n);
     };
 
+    // residue constants (uploaded once per table) and planes
+    const int N = tab.n;
+    const auto key = std::make_pair(tab.n, tab.mode);
+    if (!ws.rc.count(key)) {
+        const std::vector<uint8_t> h = build_resid_consts(tab);
+        ResidConsts* d = nullptr;
+        CUDA_TRY(cudaMalloc(&d, h.size()));
+        CUDA_TRY(cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice));
+        ws.rc[key] = d;
+    }
+    const ResidConsts* rc_dev = ws.rc[key];
+    int8_t* ares = (int8_t*)ws.ares.get((size_t)N * (size_t)(m * kp));
+    int8_t* bres = (int8_t*)ws.bres.get((size_t)N * (size_t)(n * kp));
+
     // ---- K1 (A) + K2 per row chunk: row pre-exponents, Abar, clearance product with fused maxima ----
+    // Pipelined: B is complete before the first chunk, so a chunk's row maxima
+    // are final after its clearance GEMM and its mu and A residues follow at
+    // once, overlapping the upload of the next chunks.
     for (int c = 0; c < nchunks; ++c) {
         const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
         if (pipe) CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_a[c], 0));
@@ -377,6 +396,12 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             }
         }
         if (nchunks == 1) tm.mark();  // end of the clearance product
+        if (pipe && rc > 0) {
+            CUDA_TRY(launch_exponents(cmax_row + r0, rc, cmax_col, 0, mup + r0, nup, tab.shift0, tab.nthr, tab.thr,
+                                      mu + r0, nu, ev + r0, fv, st, stream)); ++launches;
+            CUDA_TRY(launch_resid_A(prec, (const char*)dA + esz * (size_t)(r0 * lda_d), lda_d, rc, k, kp, mu + r0,
+                                    rc_dev, N, ares + r0 * kp, m * kp, st, stream)); ++launches;
+        }
     }
     if (nchunks > 1) { tm.mark(); tm.mark(); }
     if (reduce_fn) {
@@ -384,25 +409,18 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             throw Fail{OZ2G_CUDA_ERROR, "oz2g_gemm: reduce_maxima callback failed"};
     }
 
-    // ---- K3: scaling exponents ----
-    CUDA_TRY(launch_exponents(cmax_row, m, cmax_col, n, mup, nup, tab.shift0, tab.nthr, tab.thr, mu, nu, ev, fv, st,
-                              stream)); ++launches;
-    tm.mark();
-
-    // ---- K4: residue planes ----
-    const int N = tab.n;
-    const auto key = std::make_pair(tab.n, tab.mode);
-    if (!ws.rc.count(key)) {
-        const std::vector<uint8_t> h = build_resid_consts(tab);
-        ResidConsts* d = nullptr;
-        CUDA_TRY(cudaMalloc(&d, h.size()));
-        CUDA_TRY(cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice));
-        ws.rc[key] = d;
+    // ---- K3: scaling exponents; K4: residue planes ----
+    if (pipe) {  // row exponents and A residues were produced per chunk during the upload
+        CUDA_TRY(launch_exponents(cmax_row, 0, cmax_col, n, mup, nup, tab.shift0, tab.nthr, tab.thr, mu, nu, ev, fv,
+                                  st, stream)); ++launches;
+    } else {
+        CUDA_TRY(launch_exponents(cmax_row, m, cmax_col, n, mup, nup, tab.shift0, tab.nthr, tab.thr, mu, nu, ev, fv,
+                                  st, stream)); ++launches;
     }
-    const ResidConsts* rc_dev = ws.rc[key];
-    int8_t* ares = (int8_t*)ws.ares.get((size_t)N * (size_t)(m * kp));
-    int8_t* bres = (int8_t*)ws.bres.get((size_t)N * (size_t)(n * kp));
-    CUDA_TRY(launch_resid_A(prec, dA, lda_d, m, k, kp, mu, rc_dev, N, ares, st, stream)); launches += m > 0;
+    tm.mark();
+    if (!pipe) {
+        CUDA_TRY(launch_resid_A(prec, dA, lda_d, m, k, kp, mu, rc_dev, N, ares, 0, st, stream)); launches += m > 0;
+    }
     CUDA_TRY(launch_resid_BT(prec, dB, ldb_d, k, n, kp, nu, rc_dev, N, bres, st, stream)); launches += n > 0;
     tm.mark();
 
@@ -457,9 +475,20 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     gp.ldw = ldw;
     gp.wplane = m * ldw;
     const CUtensorMap tBres = make_plane_map(bres, kp, n, N, boxB);
+    std::vector<std::pair<int64_t, int64_t>> blocks;  // (first row, rows) of C per GEMM + CRT launch
     for (int c = 0; c < nchunks; ++c) {
         const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
-        if (rc <= 0 || n <= 0) continue;
+        if (rc <= 0) continue;
+        if (pipe && c == nchunks - 1 && rc >= 2 * 128) {
+            const int64_t sub = round_up((rc + kTailSplit - 1) / kTailSplit, 128);
+            for (int64_t q = r0; q < r0 + rc; q += sub) blocks.emplace_back(q, std::min<int64_t>(sub, r0 + rc - q));
+        } else {
+            blocks.emplace_back(r0, rc);
+        }
+    }
+    for (size_t bi = 0; bi < blocks.size(); ++bi) {
+        const int64_t r0 = blocks[bi].first, rc = blocks[bi].second;
+        if (n <= 0) continue;
         const CUtensorMap tA = make_plane_map(ares + r0 * kp, kp, rc, N, boxA, m * kp);
         set_rows(gp, rc);
         gp.W = W + r0 * ldw;
@@ -477,8 +506,8 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         ++launches;
         if (nchunks == 1) tm.mark();  // end of CRT + unscale
         if (pipe) {  // download this C block while the next one computes
-            CUDA_TRY(cudaEventRecord(ws.ev_c[c], stream));
-            CUDA_TRY(cudaStreamWaitEvent(ws.s_d2h, ws.ev_c[c], 0));
+            CUDA_TRY(cudaEventRecord(ws.ev_c[bi], stream));
+            CUDA_TRY(cudaStreamWaitEvent(ws.s_d2h, ws.ev_c[bi], 0));
             CUDA_TRY(cudaMemcpy2DAsync((char*)C + esz * (size_t)(r0 * ldc), esz * ldc,
                                        (const char*)dC + esz * (size_t)(r0 * n), esz * n, esz * n, rc,
                                        cudaMemcpyDeviceToHost, ws.s_d2h));

@@ -117,13 +117,12 @@ template <class T>
 __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t k,
                                                       int64_t kp, const int32_t* __restrict__ mu,
                                                       const ResidHeader* __restrict__ rc_g, int nmod,
-                                                      int8_t* __restrict__ planes, DevStatus* st) {
+                                                      int8_t* __restrict__ planes, int64_t plane, DevStatus* st) {
     extern __shared__ __align__(16) uint8_t sh[];
     load_resid_consts(rc_g, nmod, sh);
     __syncthreads();
     const ResidHeader& hd = *reinterpret_cast<const ResidHeader*>(sh);
     const uint8_t* tab = sh + sizeof(ResidHeader);
-    const int64_t plane = m * kp;
     const int64_t h0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * RA_E;
     bool ovf = false;
     if (h0 >= kp) return;
@@ -294,18 +293,19 @@ cudaError_t launch_resid_BT(int prec, const void* B, int64_t ldb, int64_t k, int
 
 cudaError_t launch_resid_A(int prec, const void* A, int64_t lda, int64_t m, int64_t k, int64_t kp,
                            const int32_t* mu, const ResidConsts* rc_dev, int nmod, int8_t* planes,
-                           DevStatus* st, cudaStream_t s) {
+                           int64_t plane_stride, DevStatus* st, cudaStream_t s) {
     if (m == 0) return cudaSuccess;
+    const int64_t plane = plane_stride ? plane_stride : m * kp;
     const unsigned chunks = blocks_for(kp, 256 * RA_E);
     const size_t sm = resid_consts_bytes(nmod);
     dim3 grid;
     cudaError_t err;
     if (prec) {
         if ((err = resid_A_grid(resid_A_kernel<double>, sm, m, chunks, grid)) != cudaSuccess) return err;
-        resid_A_kernel<double><<<grid, 256, sm, s>>>((const double*)A, lda, m, k, kp, mu, rc_dev, nmod, planes, st);
+        resid_A_kernel<double><<<grid, 256, sm, s>>>((const double*)A, lda, m, k, kp, mu, rc_dev, nmod, planes, plane, st);
     } else {
         if ((err = resid_A_grid(resid_A_kernel<float>, sm, m, chunks, grid)) != cudaSuccess) return err;
-        resid_A_kernel<float><<<grid, 256, sm, s>>>((const float*)A, lda, m, k, kp, mu, rc_dev, nmod, planes, st);
+        resid_A_kernel<float><<<grid, 256, sm, s>>>((const float*)A, lda, m, k, kp, mu, rc_dev, nmod, planes, plane, st);
     }
     return cudaGetLastError();
 }
