@@ -129,6 +129,31 @@ int oz2g_gemm(int prec, int64_t m, int64_t n, int64_t k, const void *A, int64_t 
               oz2g_intermediates *inter, oz2g_diag *diag, oz2g_reduce_maxima_fn reduce_fn, void *reduce_user);
 
 /* Convenience wrappers mirroring os_ii<double>/os_ii<float>. */
+/*
+ * One emulated GEMM tiled over several devices of this process:
+ * C is split into an R x Cg grid of tiles (count 1 -> 1x1, 2 -> 2x1, 4 -> 2x2,
+ * 8 -> 2x4, otherwise count x 1; oz2g_grid_shape), tile t = (t / Cg, t % Cg)
+ * runs on devices[t], and the clearance maxima are max-reduced across tiles
+ * before the scaling exponents, so C equals the single-device result bit for
+ * bit.  Host pointers only (each device uploads its own blocks); a device may
+ * be listed more than once.  Errors: the one the single-device call reports.
+ * Replaces os_ii<T> (emulate.hpp:54-88) for callers that own several GPUs.
+ */
+int oz2g_gemm_multi(int prec, int64_t m, int64_t n, int64_t k, const void *A, int64_t lda, const void *B,
+                    int64_t ldb, void *C, int64_t ldc, int nmod, unsigned flags, const int *devices, int count,
+                    oz2g_diag *diag);
+
+/* The tile grid oz2g_gemm_multi uses for `count` devices. */
+int oz2g_grid_shape(int count, int *rows, int *cols);
+
+/*
+ * Optional warm-up: create the workspaces and streams of the listed devices
+ * and upload the residue constants of every table (N = 2..49, fp32 and fp64),
+ * the work the first call on a device would otherwise do (moduli.hpp:145-153
+ * builds tables lazily the same way).
+ */
+int oz2g_init(const int *devices, int count);
+
 int oz2g_dgemm(int64_t m, int64_t n, int64_t k, const double *A, int64_t lda, const double *B, int64_t ldb,
                double *C, int64_t ldc, int nmod, unsigned flags, void *stream, oz2g_diag *diag);
 int oz2g_sgemm(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda, const float *B, int64_t ldb,

@@ -17,11 +17,13 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <condition_variable>
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/oz2g.h"
@@ -37,6 +39,11 @@ thread_local std::string g_last_error;
 struct Fail {
     int code;
     std::string what;
+    // multi-device calls report the failure the single-device call would:
+    // the smallest (order, index) — order = position in the reference's
+    // pipeline, index = the global row / column for zero-row / zero-column errors
+    int order = 200;
+    int64_t index = 0;
 };
 
 #define CUDA_TRY(expr)                                                                         \
@@ -80,12 +87,15 @@ struct Workspace {
     DevBuf x_cbar, x_cprod, x_c1, x_c2, x_q, x_cpp64, x_cpp32, x_ap, x_bp, x_bvec, x_bscr, x_bmax, x_bcheap, x_btight;
     std::map<std::pair<int, int>, ResidConsts*> rc;  // device copies of residue constants
     int num_sms = 0;
+    std::mutex mtx;                     // calls on one workspace are serialised
+    cudaStream_t s_main = nullptr;      // compute stream of oz2g_gemm_multi tiles
     // copy streams / events of the pipelined host-pointer path
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_start = nullptr, ev_b = nullptr, ev_done = nullptr;
     cudaEvent_t ev_a[kPipeChunks] = {}, ev_c[kPipeChunks + kTailSplit] = {};
     void ensure_streams() {
         if (s_h2d) return;
+        CUDA_TRY(cudaStreamCreateWithFlags(&s_main, cudaStreamNonBlocking));
         CUDA_TRY(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking));
         CUDA_TRY(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking));
         for (cudaEvent_t* e : {&ev_start, &ev_b, &ev_done}) CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -104,7 +114,7 @@ struct Workspace {
 };
 
 std::mutex g_ws_mtx;
-std::map<int, Workspace*> g_ws;  // per device; calls on one device are serialised
+std::map<int, Workspace*> g_ws;  // key device * 256 + slot
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -173,20 +183,18 @@ void fill_gemm_moduli(GemmParams& P, const Table& t) {
     }
 }
 
-Workspace& workspace(int dev) {
+// One workspace per (device, slot): slot 0 serves oz2g_gemm; oz2g_gemm_multi
+// gives tile t slot t, so a device listed twice gets two independent workspaces.
+Workspace& workspace(int dev, int slot = 0) {
     std::lock_guard<std::mutex> lk(g_ws_mtx);
-    auto it = g_ws.find(dev);
+    const int key = dev * 256 + slot;
+    auto it = g_ws.find(key);
     if (it == g_ws.end()) {
         Workspace* w = new Workspace();
         CUDA_TRY(cudaDeviceGetAttribute(&w->num_sms, cudaDevAttrMultiProcessorCount, dev));
-        it = g_ws.emplace(dev, w).first;
+        it = g_ws.emplace(key, w).first;
     }
     return *it->second;
-}
-
-std::mutex& device_mutex(int dev) {
-    static std::mutex mtx[64];
-    return mtx[dev & 63];
 }
 
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
@@ -246,9 +254,12 @@ struct Timer {
     }
 };
 
+// row_base / col_base: global index of the first row / column of this call's
+// tile (error messages of oz2g_gemm_multi); slot: workspace slot.
 int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
              void* C, int64_t ldc, int nmod, unsigned flags, cudaStream_t stream, oz2g_intermediates* inter,
-             oz2g_diag* diag, oz2g_reduce_maxima_fn reduce_fn, void* reduce_user) {
+             oz2g_diag* diag, oz2g_reduce_maxima_fn reduce_fn, void* reduce_user, int64_t row_base = 0,
+             int64_t col_base = 0, int slot = 0) {
     if (prec != OZ2G_FP32 && prec != OZ2G_FP64) throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_gemm: prec must be OZ2G_FP32 or OZ2G_FP64"};
     if (m < 0 || n < 0 || k < 0) throw Fail{OZ2G_INVALID_ARGUMENT, "Matrix: negative dimension"};
     if (lda < k || ldb < n || ldc < n) throw Fail{OZ2G_INVALID_ARGUMENT, "dimension mismatch: leading dimension"};
@@ -265,8 +276,8 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     const size_t esz = prec ? 8 : 4;
     int dev = 0;
     CUDA_TRY(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> dev_lock(device_mutex(dev));
-    Workspace& ws = workspace(dev);
+    Workspace& ws = workspace(dev, slot);
+    std::lock_guard<std::mutex> dev_lock(ws.mtx);
     int launches = 0;
 
     Timer tm;
@@ -406,7 +417,11 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     if (nchunks > 1) { tm.mark(); tm.mark(); }
     if (reduce_fn) {
         if (reduce_fn(cmax_row, m, cmax_col, n, (void*)stream, reduce_user) != 0)
-            throw Fail{OZ2G_CUDA_ERROR, "oz2g_gemm: reduce_maxima callback failed"};
+        {
+            Fail f{OZ2G_CUDA_ERROR, "oz2g_gemm: reduce_maxima callback failed"};
+            f.order = 201;  // a peer's own failure (multi-device) is the one to report
+            throw f;
+        }
     }
 
     // ---- K3: scaling exponents; K4: residue planes ----
@@ -617,24 +632,31 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
 
     const uint32_t e = hs.err;
     char buf[160];
+    auto fail = [](int code, std::string what, int order, int64_t index = 0) {
+        Fail f{code, std::move(what)};
+        f.order = order;
+        f.index = index;
+        return f;
+    };
     if (e & (ERR_A_NONFINITE | ERR_A_ZERO_ROW)) {
-        if (e & ERR_A_NONFINITE) throw Fail{OZ2G_DOMAIN_ERROR, "matrix entry is not finite"};
-        snprintf(buf, sizeof buf, "row_pre_exponents: zero row %lld", (long long)hs.first_row);
-        throw Fail{OZ2G_DOMAIN_ERROR, buf};
+        if (e & ERR_A_NONFINITE) throw fail(OZ2G_DOMAIN_ERROR, "matrix entry is not finite", 0, -1);
+        snprintf(buf, sizeof buf, "row_pre_exponents: zero row %lld", (long long)(hs.first_row + row_base));
+        throw fail(OZ2G_DOMAIN_ERROR, buf, 0, hs.first_row + row_base);
     }
-    if (e & ERR_B_NONFINITE) throw Fail{OZ2G_DOMAIN_ERROR, "matrix entry is not finite"};
+    if (e & ERR_B_NONFINITE) throw fail(OZ2G_DOMAIN_ERROR, "matrix entry is not finite", 1, -1);
     if (e & ERR_B_ZERO_COL) {
-        snprintf(buf, sizeof buf, "col_pre_exponents: zero column %lld", (long long)hs.first_col);
-        throw Fail{OZ2G_DOMAIN_ERROR, buf};
+        snprintf(buf, sizeof buf, "col_pre_exponents: zero column %lld", (long long)(hs.first_col + col_base));
+        throw fail(OZ2G_DOMAIN_ERROR, buf, 1, hs.first_col + col_base);
     }
-    if (e & ERR_CEIL_LOGIC) throw Fail{OZ2G_LOGIC_ERROR, "ceil_abs_scaled: entry above row/column max"};
-    if (e & ERR_E_LOGIC) throw Fail{OZ2G_LOGIC_ERROR, "scaling_exponents: e_i >= 31"};
-    if (e & ERR_MU_RANGE) throw Fail{OZ2G_RANGE_ERROR, "mu: exceeds 16-bit range"};
-    if (e & ERR_NU_RANGE) throw Fail{OZ2G_RANGE_ERROR, "nu: exceeds 16-bit range"};
-    if (e & ERR_TRUNC_A_RANGE) throw Fail{OZ2G_RANGE_ERROR, "truncate_scaled: 2^mu*a overflow"};
-    if (e & ERR_TRUNC_B_RANGE) throw Fail{OZ2G_RANGE_ERROR, "truncate_scaled: b*2^nu overflow"};
-    if (e & ERR_FR_RANGE) throw Fail{OZ2G_RANGE_ERROR, "final_reduce: single(C'') overflows fp32 (N too large for fp32 mode)"};
-    if (e & ERR_INV_RANGE) throw Fail{OZ2G_RANGE_ERROR, "os_ii: inverse scaling overflow"};
+    if (e & ERR_CEIL_LOGIC) throw fail(OZ2G_LOGIC_ERROR, "ceil_abs_scaled: entry above row/column max", 2);
+    if (e & ERR_E_LOGIC) throw fail(OZ2G_LOGIC_ERROR, "scaling_exponents: e_i >= 31", 3);
+    if (e & ERR_MU_RANGE) throw fail(OZ2G_RANGE_ERROR, "mu: exceeds 16-bit range", 4);
+    if (e & ERR_NU_RANGE) throw fail(OZ2G_RANGE_ERROR, "nu: exceeds 16-bit range", 5);
+    if (e & ERR_TRUNC_A_RANGE) throw fail(OZ2G_RANGE_ERROR, "truncate_scaled: 2^mu*a overflow", 6);
+    if (e & ERR_TRUNC_B_RANGE) throw fail(OZ2G_RANGE_ERROR, "truncate_scaled: b*2^nu overflow", 7);
+    if (e & ERR_FR_RANGE)
+        throw fail(OZ2G_RANGE_ERROR, "final_reduce: single(C'') overflows fp32 (N too large for fp32 mode)", 8);
+    if (e & ERR_INV_RANGE) throw fail(OZ2G_RANGE_ERROR, "os_ii: inverse scaling overflow", 9);
     return OZ2G_OK;
 }
 
@@ -656,8 +678,8 @@ int run_suggest_n(int prec, int64_t m, int64_t n, int64_t k, const void* A, int6
     const size_t esz = prec ? 8 : 4;
     int dev = 0;
     CUDA_TRY(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> dev_lock(device_mutex(dev));
     Workspace& ws = workspace(dev);
+    std::lock_guard<std::mutex> dev_lock(ws.mtx);
     const int64_t kp = round_up(k, 128);
     const void* dA = A;
     const void* dB = B;
@@ -735,6 +757,162 @@ int run_suggest_n(int prec, int64_t m, int64_t n, int64_t k, const void* A, int6
     return OZ2G_OK;  // not achievable: n_out = 0, bound_out = bound max at the cap
 }
 
+// ---------------------------------------------------------------------------
+// Single-process multi-device tiling (oz2g_gemm_multi): the C grid
+// R x Cg over the listed devices (1 -> 1x1, 2 -> 2x1, 4 -> 2x2, 8 -> 2x4, else
+// count x 1; the same grid as paper_2602_02549_b200/dist.py), one host thread
+// per tile.  Tile (r, c) gets the row block r of A and the column block c of B
+// (all of k).  The clearance maxima are max-reduced across tiles on the host
+// between the clearance product and the scaling exponents — the reduce hook of
+// oz2g_gemm — so every tile scales exactly as the single-device call does and
+// C is bit-identical.  Inputs are host pointers (each device uploads its own
+// blocks over its own link).
+// ---------------------------------------------------------------------------
+void grid_shape(int count, int& R, int& Cg) {
+    switch (count) {
+        case 1: R = 1; Cg = 1; break;
+        case 2: R = 2; Cg = 1; break;
+        case 4: R = 2; Cg = 2; break;
+        case 8: R = 2; Cg = 4; break;
+        default: R = count; Cg = 1; break;
+    }
+}
+
+struct MultiCtx {
+    std::mutex mtx;
+    std::condition_variable cv;
+    int count = 0, arrived = 0, generation = 0;
+    bool broken = false;
+    std::vector<int32_t> rowmax, colmax;  // global clearance maxima
+    // barrier that a failing tile can break (the others then fail fast)
+    bool wait() {
+        std::unique_lock<std::mutex> lk(mtx);
+        if (broken) return false;
+        const int gen = generation;
+        if (++arrived == count) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+            return true;
+        }
+        cv.wait(lk, [&] { return broken || generation != gen; });
+        return generation != gen;
+    }
+    void breakit() {
+        std::lock_guard<std::mutex> lk(mtx);
+        broken = true;
+        cv.notify_all();
+    }
+};
+
+struct MultiTile {
+    MultiCtx* ctx;
+    int64_t r0, c0;
+};
+
+int multi_reduce_hook(int32_t* rowp, int64_t m, int32_t* colp, int64_t n, void* stream, void* user) {
+    MultiTile* t = static_cast<MultiTile*>(user);
+    MultiCtx* x = t->ctx;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::vector<int32_t> hr((size_t)m), hc((size_t)n);
+    bool ok = true;
+    if (m) ok &= cudaMemcpyAsync(hr.data(), rowp, 4 * (size_t)m, cudaMemcpyDeviceToHost, s) == cudaSuccess;
+    if (n) ok &= cudaMemcpyAsync(hc.data(), colp, 4 * (size_t)n, cudaMemcpyDeviceToHost, s) == cudaSuccess;
+    ok &= cudaStreamSynchronize(s) == cudaSuccess;
+    if (!ok) { x->breakit(); return -1; }
+    {
+        std::lock_guard<std::mutex> lk(x->mtx);
+        for (int64_t i = 0; i < m; ++i) x->rowmax[(size_t)(t->r0 + i)] = std::max(x->rowmax[(size_t)(t->r0 + i)], hr[(size_t)i]);
+        for (int64_t j = 0; j < n; ++j) x->colmax[(size_t)(t->c0 + j)] = std::max(x->colmax[(size_t)(t->c0 + j)], hc[(size_t)j]);
+    }
+    if (!x->wait()) return -1;
+    {
+        std::lock_guard<std::mutex> lk(x->mtx);
+        for (int64_t i = 0; i < m; ++i) hr[(size_t)i] = x->rowmax[(size_t)(t->r0 + i)];
+        for (int64_t j = 0; j < n; ++j) hc[(size_t)j] = x->colmax[(size_t)(t->c0 + j)];
+    }
+    if (m) ok &= cudaMemcpyAsync(rowp, hr.data(), 4 * (size_t)m, cudaMemcpyHostToDevice, s) == cudaSuccess;
+    if (n) ok &= cudaMemcpyAsync(colp, hc.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, s) == cudaSuccess;
+    ok &= cudaStreamSynchronize(s) == cudaSuccess;
+    return ok ? 0 : -1;
+}
+
+int run_gemm_multi(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
+                   void* C, int64_t ldc, int nmod, unsigned flags, const int* devices, int count, oz2g_diag* diag) {
+    if (!devices || count < 1) throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_gemm_multi: empty device list"};
+    if (count > 256) throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_gemm_multi: at most 256 tiles"};
+    if (flags & OZ2G_DEVICE_PTRS) throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_gemm_multi: host pointers required"};
+    if (prec != OZ2G_FP32 && prec != OZ2G_FP64) throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_gemm: prec must be OZ2G_FP32 or OZ2G_FP64"};
+    if (m < 0 || n < 0 || k < 0) throw Fail{OZ2G_INVALID_ARGUMENT, "Matrix: negative dimension"};
+    if (lda < k || ldb < n || ldc < n) throw Fail{OZ2G_INVALID_ARGUMENT, "dimension mismatch: leading dimension"};
+    if (k > OZ2G_MAX_INNER_DIM) throw Fail{OZ2G_DOMAIN_ERROR, "os_ii: k exceeds 2^17"};
+    (void)table_for(nmod, prec);  // std::domain_error for N outside [2, 49]
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    for (int t = 0; t < count; ++t)
+        if (devices[t] < 0 || devices[t] >= ndev) throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_gemm_multi: no such device"};
+    if (diag) std::memset(diag, 0, sizeof *diag);
+    const size_t esz = prec ? 8 : 4;
+    int R = 1, Cg = 1;
+    grid_shape(count, R, Cg);
+    const int64_t mb = (m + R - 1) / R, nb = (n + Cg - 1) / Cg;
+    MultiCtx ctx;
+    ctx.count = count;
+    ctx.rowmax.assign((size_t)m, 0);
+    ctx.colmax.assign((size_t)n, 0);
+    std::vector<MultiTile> tiles((size_t)count);
+    std::vector<Fail> fails((size_t)count, Fail{OZ2G_OK, ""});
+    std::vector<oz2g_diag> diags((size_t)count);
+    int caller_dev = 0;
+    CUDA_TRY(cudaGetDevice(&caller_dev));
+    auto body = [&](int t) {
+        const int r = t / Cg, c = t % Cg;
+        const int64_t r0 = std::min(m, r * mb), r1 = std::min(m, (r + 1) * mb);
+        const int64_t c0 = std::min(n, c * nb), c1 = std::min(n, (c + 1) * nb);
+        tiles[(size_t)t] = MultiTile{&ctx, r0, c0};
+        try {
+            CUDA_TRY(cudaSetDevice(devices[t]));
+            Workspace& ws = workspace(devices[t], t);
+            {
+                std::lock_guard<std::mutex> lk(ws.mtx);
+                ws.ensure_streams();
+            }
+            run_gemm(prec, r1 - r0, c1 - c0, k, (const char*)A + esz * (size_t)(r0 * lda), lda,
+                     (const char*)B + esz * (size_t)c0, ldb, (char*)C + esz * (size_t)(r0 * ldc + c0), ldc, nmod,
+                     flags & OZ2G_TIMING, ws.s_main, nullptr, diag ? &diags[(size_t)t] : nullptr, multi_reduce_hook,
+                     &tiles[(size_t)t], r0, c0, t);
+        } catch (const Fail& f) {
+            fails[(size_t)t] = f;
+            ctx.breakit();
+        } catch (const std::exception& e) {
+            fails[(size_t)t] = Fail{OZ2G_CUDA_ERROR, e.what()};
+            ctx.breakit();
+        }
+    };
+    if (count == 1) {
+        body(0);
+    } else {
+        std::vector<std::thread> th;
+        th.reserve((size_t)count);
+        for (int t = 0; t < count; ++t) th.emplace_back(body, t);
+        for (auto& x : th) x.join();
+    }
+    cudaSetDevice(caller_dev);
+    const Fail* worst = nullptr;
+    for (const Fail& f : fails)
+        if (f.code != OZ2G_OK && (!worst || f.order < worst->order || (f.order == worst->order && f.index < worst->index)))
+            worst = &f;
+    if (worst) throw *worst;
+    if (diag) {
+        for (const oz2g_diag& d : diags) {
+            diag->subnormal |= d.subnormal;
+            diag->kernels_launched += d.kernels_launched;
+            for (int q = 0; q < 8; ++q) diag->stage_ms[q] = std::max(diag->stage_ms[q], d.stage_ms[q]);
+        }
+    }
+    return OZ2G_OK;
+}
+
 template <class F>
 int guarded(F&& f) {
     g_last_error.clear();
@@ -785,6 +963,46 @@ int oz2g_dgemm(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, co
 int oz2g_sgemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B, int64_t ldb,
                float* C, int64_t ldc, int nmod, unsigned flags, void* stream, oz2g_diag* diag) {
     return oz2g_gemm(OZ2G_FP32, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, stream, nullptr, diag, nullptr, nullptr);
+}
+
+int oz2g_gemm_multi(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
+                    void* C, int64_t ldc, int nmod, unsigned flags, const int* devices, int count, oz2g_diag* diag) {
+    return guarded([&] {
+        return run_gemm_multi(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, devices, count, diag);
+    });
+}
+
+int oz2g_grid_shape(int count, int* rows, int* cols) {
+    if (count < 1 || !rows || !cols) return OZ2G_INVALID_ARGUMENT;
+    grid_shape(count, *rows, *cols);
+    return OZ2G_OK;
+}
+
+int oz2g_init(const int* devices, int count) {
+    return guarded([&] {
+        if (count < 0 || (count > 0 && !devices)) throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_init: bad device list"};
+        int caller = 0;
+        CUDA_TRY(cudaGetDevice(&caller));
+        for (int t = 0; t < count; ++t) {
+            CUDA_TRY(cudaSetDevice(devices[t]));
+            Workspace& ws = workspace(devices[t], 0);
+            std::lock_guard<std::mutex> lk(ws.mtx);
+            ws.ensure_streams();
+            for (int mode : {OZ2G_FP32, OZ2G_FP64})
+                for (int nm = 2; nm <= 49; ++nm) {
+                    const Table& tab = table_for(nm, mode);
+                    const auto key = std::make_pair(tab.n, tab.mode);
+                    if (ws.rc.count(key)) continue;
+                    const std::vector<uint8_t> h = build_resid_consts(tab);
+                    ResidConsts* d = nullptr;
+                    CUDA_TRY(cudaMalloc(&d, h.size()));
+                    CUDA_TRY(cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice));
+                    ws.rc[key] = d;
+                }
+        }
+        CUDA_TRY(cudaSetDevice(caller));
+        return OZ2G_OK;
+    });
 }
 
 const char* oz2g_last_error(void) { return g_last_error.c_str(); }
@@ -863,8 +1081,11 @@ void oz2g_release_workspace(void) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return;
     std::lock_guard<std::mutex> lk(g_ws_mtx);
-    auto it = g_ws.find(dev);
-    if (it != g_ws.end()) it->second->release();
+    for (auto& kv : g_ws)
+        if (kv.first / 256 == dev) {
+            std::lock_guard<std::mutex> wl(kv.second->mtx);
+            kv.second->release();
+        }
 }
 
 }  // extern "C"

@@ -139,7 +139,7 @@ def _is_torch_cuda(x) -> bool:
 
 def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = False, out=None,
           stream=None, timing: bool = False, bounds=False, vectors: bool = False,
-          reduce_maxima: Optional[Callable] = None) -> EmulationResult:
+          reduce_maxima: Optional[Callable] = None, devices=None) -> EmulationResult:
     """C ~ A*B by Ozaki-II accurate mode with `n` moduli (emulate.hpp:54-88).
 
     `a`, `b`: 2-D float32/float64 numpy arrays (host) or CUDA torch tensors
@@ -152,7 +152,9 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
     paper's error bounds (bounds.hpp) and returns their maxima;
     `bounds="full"` also returns the m x n cheap / tight bound matrices (same
     memory space as the inputs).  `reduce_maxima(row_ptr, m, col_ptr, n,
-    stream)` is the multi-GPU hook of oz2g.h.
+    stream)` is the multi-GPU hook of oz2g.h.  `devices=[d0, d1, ...]` tiles
+    one call over those devices of this process (oz2g_gemm_multi; host arrays,
+    C only) with a result identical to the single-device call.
     """
     L = _lib.load()
     dev = _is_torch_cuda(a)
@@ -197,6 +199,19 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
         flags = _lib.OZ2G_HOST_PTRS
     if timing:
         flags |= _lib.OZ2G_TIMING
+    if devices is not None:
+        if dev:
+            raise InvalidArgument("os_ii: devices= takes host arrays (each device uploads its own blocks)")
+        if keep_intermediates or evidence or vectors or bounds or reduce_maxima is not None:
+            raise InvalidArgument("os_ii: devices= returns C only")
+        devs = [int(d) for d in devices]
+        ds = (C.c_int * max(1, len(devs)))(*devs)
+        diag = _lib.Diag()
+        _check(L.oz2g_gemm_multi(prec, m, nn, k, pa, lda, pb, ldb, pc, ldc, int(n), flags, ds, len(devs),
+                                 C.byref(diag)))
+        return EmulationResult(C=C_out, scaling=ScalingOutput(), crt=CrtIntermediates(), table=table_for(n, prec),
+                               subnormal=bool(diag.subnormal), kernels_launched=diag.kernels_launched,
+                               stage_ms=tuple(diag.stage_ms))
 
     inter_c = None
     sc, cr = ScalingOutput(), CrtIntermediates()

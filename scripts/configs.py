@@ -81,9 +81,10 @@ def main():
     rows = [
         run("cfg1 1024^3 N=14 (the reference's CPU case)", 1024, 1024, 1024, 14, torch.float64, reps=20),
         run("cfg2 SGEMM 4096^3 N=6", 4096, 4096, 4096, 6, torch.float32, reps=10),
+        run("cfg2 SGEMM 4096^3 N=7", 4096, 4096, 4096, 7, torch.float32, reps=10),
         run("cfg2 SGEMM 4096^3 N=8", 4096, 4096, 4096, 8, torch.float32, reps=10),
     ]
-    for phi in (0.0, 1.0, 2.0, 4.0):
+    for phi in (0.0, 0.5, 2.0, 8.0):  # the reference's sweep {0.5, 2, 8}, plus phi = 0
         for nmod in (8, 12, 16, 20):
             rows.append(run(f"cfg3 8192^3 phi={phi} N={nmod}", 8192, 8192, 8192, nmod, torch.float64, phi=phi,
                             reps=3, accuracy=True))
