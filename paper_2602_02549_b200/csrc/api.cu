@@ -90,7 +90,16 @@ struct Workspace {
     std::mutex mtx;                     // calls on one workspace are serialised
     cudaStream_t s_main = nullptr;      // compute stream of oz2g_gemm_multi tiles
     // copy streams / events of the pipelined host-pointer path
-    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr, s_aux = nullptr;
+    std::vector<cudaEvent_t> ev_pool;  // per-block events of the overlapped CRT
+    cudaEvent_t pool_event(size_t i) {
+        while (ev_pool.size() <= i) {
+            cudaEvent_t e = nullptr;
+            CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ev_pool.push_back(e);
+        }
+        return ev_pool[i];
+    }
     cudaEvent_t ev_start = nullptr, ev_b = nullptr, ev_done = nullptr;
     cudaEvent_t ev_a[kPipeChunks] = {}, ev_c[kPipeChunks + kTailSplit] = {};
     void ensure_streams() {
@@ -98,6 +107,7 @@ struct Workspace {
         CUDA_TRY(cudaStreamCreateWithFlags(&s_main, cudaStreamNonBlocking));
         CUDA_TRY(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking));
         CUDA_TRY(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&s_aux, cudaStreamNonBlocking));
         for (cudaEvent_t* e : {&ev_start, &ev_b, &ev_done}) CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         for (int c = 0; c < kPipeChunks; ++c) CUDA_TRY(cudaEventCreateWithFlags(&ev_a[c], cudaEventDisableTiming));
         for (int c = 0; c < kPipeChunks + kTailSplit; ++c)
@@ -212,13 +222,29 @@ bool use_pair_gemm() {
 // both operands: measured at 16384^3, EVICT_LAST on A / EVICT_FIRST on B doubled
 // the residue GEMM's DRAM reads (81 -> 156 GB: B tiles are shared by the CTAs of
 // a wave and were evicted before reuse).  OZ2G_L2HINT=1 re-enables for study.
+// TMA L2 eviction hints of the GEMM operand loads (OZ2G_L2HINT):
+//   0 normal/normal (default), 1 A last / B first, 2 A last / B normal,
+//   3 A normal / B first
 void set_l2_hints(GemmParams& g) {
-    static const bool on = [] {
+    static const int mode = [] {
         const char* s = std::getenv("OZ2G_L2HINT");
-        return s && std::strcmp(s, "1") == 0;
+        return s ? std::atoi(s) : 0;
     }();
-    g.hintA = on ? 0x14F0000000000000ull /*EVICT_LAST*/ : 0x1000000000000000ull /*EVICT_NORMAL*/;
-    g.hintB = on ? 0x12F0000000000000ull /*EVICT_FIRST*/ : 0x1000000000000000ull;
+    constexpr uint64_t kNormal = 0x1000000000000000ull, kLast = 0x14F0000000000000ull,
+                       kFirst = 0x12F0000000000000ull;
+    g.hintA = (mode == 1 || mode == 2) ? kLast : kNormal;
+    g.hintB = (mode == 1 || mode == 3) ? kFirst : kNormal;
+}
+
+// OZ2G_CRT_OVERLAP = B > 0: the residue GEMMs + CRT of a large call run in B
+// row blocks and each block's CRT runs on a side stream while the next
+// block's GEMM computes (the CRT CTAs fit beside the persistent GEMM CTAs).
+int crt_overlap_blocks() {
+    static const int v = [] {
+        const char* s = std::getenv("OZ2G_CRT_OVERLAP");
+        return s ? std::atoi(s) : 0;
+    }();
+    return v;
 }
 
 // Raster group height: one wave of persistent CTAs covers group_m tile-rows,
@@ -491,16 +517,23 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     gp.wplane = m * ldw;
     const CUtensorMap tBres = make_plane_map(bres, kp, n, N, boxB);
     std::vector<std::pair<int64_t, int64_t>> blocks;  // (first row, rows) of C per GEMM + CRT launch
+    const int ovb = crt_overlap_blocks();
+    const bool overlap = ovb > 1 && !inter && m >= 2048;
+    if (overlap) ws.ensure_streams();
     for (int c = 0; c < nchunks; ++c) {
         const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
         if (rc <= 0) continue;
         if (pipe && c == nchunks - 1 && rc >= 2 * 128) {
             const int64_t sub = round_up((rc + kTailSplit - 1) / kTailSplit, 128);
             for (int64_t q = r0; q < r0 + rc; q += sub) blocks.emplace_back(q, std::min<int64_t>(sub, r0 + rc - q));
+        } else if (overlap && !pipe) {
+            const int64_t sub = round_up((rc + ovb - 1) / ovb, 128);
+            for (int64_t q = r0; q < r0 + rc; q += sub) blocks.emplace_back(q, std::min<int64_t>(sub, r0 + rc - q));
         } else {
             blocks.emplace_back(r0, rc);
         }
     }
+    const bool marks = nchunks == 1 && blocks.size() == 1;
     for (size_t bi = 0; bi < blocks.size(); ++bi) {
         const int64_t r0 = blocks[bi].first, rc = blocks[bi].second;
         if (n <= 0) continue;
@@ -515,19 +548,33 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             g2.cplane = m * n;
             CUDA_TRY(launch_gemm(EPI_I32, tA, tBres, g2)); ++launches;
         }
-        if (nchunks == 1) tm.mark();  // end of the residue GEMMs
+        if (marks) tm.mark();  // end of the residue GEMMs
+        cudaStream_t crt_stream = stream;
+        if (overlap) {  // this block's CRT beside the next block's GEMM
+            const cudaEvent_t eg = ws.pool_event(2 * bi);
+            CUDA_TRY(cudaEventRecord(eg, stream));
+            CUDA_TRY(cudaStreamWaitEvent(ws.s_aux, eg, 0));
+            crt_stream = ws.s_aux;
+        }
         CUDA_TRY(launch_crt(prec, W + r0 * ldw, ldw, m * ldw, rc, n, cc, mu + r0, nu,
-                            (char*)dC + esz * (size_t)(r0 * ldc_d), ldc_d, ex, st, stream));
+                            (char*)dC + esz * (size_t)(r0 * ldc_d), ldc_d, ex, st, crt_stream));
         ++launches;
-        if (nchunks == 1) tm.mark();  // end of CRT + unscale
+        if (marks) tm.mark();  // end of CRT + unscale
         if (pipe) {  // download this C block while the next one computes
-            CUDA_TRY(cudaEventRecord(ws.ev_c[bi], stream));
-            CUDA_TRY(cudaStreamWaitEvent(ws.s_d2h, ws.ev_c[bi], 0));
+            const cudaEvent_t ec = overlap ? ws.pool_event(2 * bi + 1) : ws.ev_c[bi];
+            CUDA_TRY(cudaEventRecord(ec, crt_stream));
+            CUDA_TRY(cudaStreamWaitEvent(ws.s_d2h, ec, 0));
             CUDA_TRY(cudaMemcpy2DAsync((char*)C + esz * (size_t)(r0 * ldc), esz * ldc,
                                        (const char*)dC + esz * (size_t)(r0 * n), esz * n, esz * n, rc,
                                        cudaMemcpyDeviceToHost, ws.s_d2h));
         }
     }
+    if (overlap) {  // join the side stream
+        const cudaEvent_t ej = ws.pool_event(2 * blocks.size());
+        CUDA_TRY(cudaEventRecord(ej, ws.s_aux));
+        CUDA_TRY(cudaStreamWaitEvent(stream, ej, 0));
+    }
+    if (!marks && nchunks == 1 && m * n != 0) { tm.mark(); tm.mark(); }
     if (nchunks > 1 || m * n == 0) { tm.mark(); tm.mark(); }
     if (pipe) {
         CUDA_TRY(cudaEventRecord(ws.ev_done, ws.s_d2h));

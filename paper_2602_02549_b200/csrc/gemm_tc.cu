@@ -471,6 +471,7 @@ cudaError_t launch_gemm_i8_pair(int mode, const CUtensorMap& tmA, const CUtensor
     // deeper pipelines let the clusters drift apart and lose L2 sharing:
     // DRAM reads 82 GB (4 stages), 245 GB (6), 250 GB (7) at 16384^3, N = 16
     if (stages == 6) return launch_pair_s<6>(mode, grid, tmA, tmB, P, stream);
+    if (stages == 5) return launch_pair_s<5>(mode, grid, tmA, tmB, P, stream);
     return launch_pair_s<4>(mode, grid, tmA, tmB, P, stream);
 }
 
