@@ -137,6 +137,15 @@ __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, i
                 d[j] = elem_dec(v.x, sft, ovf);
                 d[j + 1] = elem_dec(v.y, sft, ovf);
             }
+        } else if (sizeof(T) == 4 && h0 + RA_E <= k && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
+#pragma unroll
+            for (int j = 0; j < RA_E; j += 4) {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(row + j));
+                d[j] = elem_dec((double)v.x, sft, ovf);
+                d[j + 1] = elem_dec((double)v.y, sft, ovf);
+                d[j + 2] = elem_dec((double)v.z, sft, ovf);
+                d[j + 3] = elem_dec((double)v.w, sft, ovf);
+            }
         } else {
 #pragma unroll
             for (int j = 0; j < RA_E; ++j) d[j] = elem_dec(h0 + j < k ? ld_d(row + j) : 0.0, sft, ovf);
@@ -167,13 +176,13 @@ __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, i
 // ---------------------------------------------------------------------------
 constexpr int TB = 64;    // columns j per CTA
 constexpr int THR = 32;   // rows h per tile
-constexpr int TB_H = 8;   // tiles per CTA
+constexpr int TB_H = 8;   // at most this many tiles per CTA (fewer on small matrices)
 
 template <class T, int OP>
 __global__ void __launch_bounds__(256) transpose_B_kernel(const T* __restrict__ B, int64_t ldb, int64_t k,
                                                           int64_t n, int64_t kp, const int32_t* __restrict__ shift,
                                                           const ResidHeader* __restrict__ rc_g, int nmod,
-                                                          int8_t* __restrict__ out, DevStatus* st) {
+                                                          int8_t* __restrict__ out, int tb_h, DevStatus* st) {
     extern __shared__ __align__(16) uint8_t sh[];
     if (OP == 1) {
         load_resid_consts(rc_g, nmod, sh);
@@ -187,21 +196,22 @@ __global__ void __launch_bounds__(256) transpose_B_kernel(const T* __restrict__ 
     const int sft = shift[j];
     const int64_t plane = n * kp;
     bool flagbit = false;
-    const int64_t hend = (int64_t)(blockIdx.x + 1) * TB_H * THR;
+    const int64_t hend = (int64_t)(blockIdx.x + 1) * tb_h * THR;
     const int64_t hmax = kp < hend ? kp : hend;
-    int64_t h0 = (int64_t)blockIdx.x * TB_H * THR + (lane & 3) * 8;
-    // the next tile's rows are loaded while this one computes (latency hiding)
-    double xn[8];
+    int64_t h0 = (int64_t)blockIdx.x * tb_h * THR + (lane & 3) * 8;
+    // the next tile's rows are loaded while this one computes (latency hiding);
+    // the buffer keeps the input type (half the registers for float)
+    T xn[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) xn[r] = h0 + r < k ? ld_d(B + (h0 + r) * ldb + j) : 0.0;
+    for (int r = 0; r < 8; ++r) xn[r] = h0 + r < k ? __ldg(B + (h0 + r) * ldb + j) : T(0);
     for (; h0 < hmax; h0 += THR) {
         double x[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) x[r] = xn[r];
+        for (int r = 0; r < 8; ++r) x[r] = (double)xn[r];
         const int64_t h1 = h0 + THR;
         if (h1 < hmax) {
 #pragma unroll
-            for (int r = 0; r < 8; ++r) xn[r] = h1 + r < k ? ld_d(B + (h1 + r) * ldb + j) : 0.0;
+            for (int r = 0; r < 8; ++r) xn[r] = h1 + r < k ? __ldg(B + (h1 + r) * ldb + j) : T(0);
         }
         int8_t* o = out + j * kp + h0;
         if (OP == 0) {
@@ -236,6 +246,15 @@ inline unsigned blocks_for(int64_t work, int per) { return (unsigned)((work + pe
 
 size_t transpose_smem(int op, int nmod) { return op == 1 ? resid_consts_bytes(nmod) : 0; }
 
+// tiles per CTA: up to TB_H, fewer when that leaves under ~16 CTAs per SM
+// (short per-CTA chains keep enough loads in flight on mid-size matrices)
+int transpose_tiles_per_cta(int64_t kp, int64_t n) {
+    const int64_t tiles = (kp / THR) * blocks_for(n, TB);
+    int t = TB_H;
+    while (t > 1 && tiles / t < 16 * 148) t /= 2;
+    return t;
+}
+
 template <class K>
 cudaError_t set_smem(K kernel, size_t bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -265,12 +284,13 @@ cudaError_t resid_A_grid(K kernel, size_t smem, int64_t m, unsigned chunks, dim3
 cudaError_t launch_bbar_T(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp,
                           const int32_t* nu_prime, int8_t* bbar_t, DevStatus* st, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    const dim3 grid(blocks_for(kp, TB_H * THR), blocks_for(n, TB));
+    const int tb = transpose_tiles_per_cta(kp, n);
+    const dim3 grid(blocks_for(kp, tb * THR), blocks_for(n, TB));
     const size_t sm = transpose_smem(0, 1);
     if (prec)
-        transpose_B_kernel<double, 0><<<grid, 256, sm, s>>>((const double*)B, ldb, k, n, kp, nu_prime, nullptr, 1, bbar_t, st);
+        transpose_B_kernel<double, 0><<<grid, 256, sm, s>>>((const double*)B, ldb, k, n, kp, nu_prime, nullptr, 1, bbar_t, tb, st);
     else
-        transpose_B_kernel<float, 0><<<grid, 256, sm, s>>>((const float*)B, ldb, k, n, kp, nu_prime, nullptr, 1, bbar_t, st);
+        transpose_B_kernel<float, 0><<<grid, 256, sm, s>>>((const float*)B, ldb, k, n, kp, nu_prime, nullptr, 1, bbar_t, tb, st);
     return cudaGetLastError();
 }
 
@@ -278,15 +298,16 @@ cudaError_t launch_resid_BT(int prec, const void* B, int64_t ldb, int64_t k, int
                             const int32_t* nu, const ResidConsts* rc_dev, int nmod, int8_t* planes,
                             DevStatus* st, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    const dim3 grid(blocks_for(kp, TB_H * THR), blocks_for(n, TB));
+    const int tb = transpose_tiles_per_cta(kp, n);
+    const dim3 grid(blocks_for(kp, tb * THR), blocks_for(n, TB));
     const size_t sm = transpose_smem(1, nmod);
     cudaError_t err;
     if (prec) {
         if ((err = set_smem(transpose_B_kernel<double, 1>, sm)) != cudaSuccess) return err;
-        transpose_B_kernel<double, 1><<<grid, 256, sm, s>>>((const double*)B, ldb, k, n, kp, nu, rc_dev, nmod, planes, st);
+        transpose_B_kernel<double, 1><<<grid, 256, sm, s>>>((const double*)B, ldb, k, n, kp, nu, rc_dev, nmod, planes, tb, st);
     } else {
         if ((err = set_smem(transpose_B_kernel<float, 1>, sm)) != cudaSuccess) return err;
-        transpose_B_kernel<float, 1><<<grid, 256, sm, s>>>((const float*)B, ldb, k, n, kp, nu, rc_dev, nmod, planes, st);
+        transpose_B_kernel<float, 1><<<grid, 256, sm, s>>>((const float*)B, ldb, k, n, kp, nu, rc_dev, nmod, planes, tb, st);
     }
     return cudaGetLastError();
 }
