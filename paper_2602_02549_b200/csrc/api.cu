@@ -264,21 +264,43 @@ int group_m_for(int tiles_m, int tiles_n) {
     return g < tiles_m ? g : (tiles_m > 0 ? tiles_m : 1);
 }
 
+// Per-stage device time (OZ2G_TIMING): every launch or copy is bracketed by
+// events on the stream it runs on and the intervals are summed per stage, so
+// the numbers are right for row-blocked and pipelined calls too (where stages
+// overlap, a stage's figure is its busy time).
 struct Timer {
     bool on = false;
-    cudaStream_t s = nullptr;
-    std::vector<cudaEvent_t> ev;
-    void mark() {
-        if (!on) return;
-        cudaEvent_t e;
+    struct Interval { int stage; cudaEvent_t a, b; };
+    std::vector<Interval> iv;
+    std::vector<cudaEvent_t> owned;
+    cudaEvent_t rec(cudaStream_t s) {
+        cudaEvent_t e = nullptr;
         cudaEventCreate(&e);
         cudaEventRecord(e, s);
-        ev.push_back(e);
+        owned.push_back(e);
+        return e;
+    }
+    template <class F>
+    void span(int stage, cudaStream_t s, F&& f) {
+        if (!on) { f(); return; }
+        cudaEvent_t a = rec(s);
+        f();
+        iv.push_back({stage, a, rec(s)});
+    }
+    void collect(double* out) {
+        for (const Interval& x : iv) {
+            float ms = 0;
+            if (cudaEventElapsedTime(&ms, x.a, x.b) == cudaSuccess) out[x.stage] += ms;
+        }
     }
     ~Timer() {
-        for (auto e : ev) cudaEventDestroy(e);
+        for (auto e : owned) cudaEventDestroy(e);
     }
 };
+
+// Row block of the residue GEMMs + CRT: one raster group (16 x 128 rows), so
+// W (N int8 planes) is held for one block only.
+constexpr int64_t kWBlockRows = 2048;
 
 // row_base / col_base: global index of the first row / column of this call's
 // tile (error messages of oz2g_gemm_multi); slot: workspace slot.
@@ -308,8 +330,6 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
 
     Timer tm;
     tm.on = diag && (flags & OZ2G_TIMING);
-    tm.s = stream;
-    tm.mark();
 
     const int64_t kp = round_up(k, 128);
     const int64_t ldw = round_up(n > 0 ? n : 1, 16);
@@ -331,21 +351,27 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             CUDA_TRY(cudaEventRecord(ws.ev_start, stream));
             CUDA_TRY(cudaStreamWaitEvent(ws.s_h2d, ws.ev_start, 0));
             // B first: the column scan needs all of it
-            CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dB), esz * n, B, esz * ldb, esz * n, k, cudaMemcpyHostToDevice, ws.s_h2d));
+            tm.span(0, ws.s_h2d, [&] {
+                CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dB), esz * n, B, esz * ldb, esz * n, k,
+                                           cudaMemcpyHostToDevice, ws.s_h2d));
+            });
             CUDA_TRY(cudaEventRecord(ws.ev_b, ws.s_h2d));
             for (int c = 0; c < nchunks; ++c) {
                 const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
-                CUDA_TRY(cudaMemcpy2DAsync((char*)const_cast<void*>(dA) + esz * (size_t)(r0 * k), esz * k,
-                                           (const char*)A + esz * (size_t)(r0 * lda), esz * lda, esz * k, rc,
-                                           cudaMemcpyHostToDevice, ws.s_h2d));
+                tm.span(0, ws.s_h2d, [&] {
+                    CUDA_TRY(cudaMemcpy2DAsync((char*)const_cast<void*>(dA) + esz * (size_t)(r0 * k), esz * k,
+                                               (const char*)A + esz * (size_t)(r0 * lda), esz * lda, esz * k, rc,
+                                               cudaMemcpyHostToDevice, ws.s_h2d));
+                });
                 CUDA_TRY(cudaEventRecord(ws.ev_a[c], ws.s_h2d));
             }
         } else {
-            if (m * k) CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dA), esz * k, A, esz * lda, esz * k, m, cudaMemcpyHostToDevice, stream));
-            if (k * n) CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dB), esz * n, B, esz * ldb, esz * n, k, cudaMemcpyHostToDevice, stream));
+            tm.span(0, stream, [&] {
+                if (m * k) CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dA), esz * k, A, esz * lda, esz * k, m, cudaMemcpyHostToDevice, stream));
+                if (k * n) CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dB), esz * n, B, esz * ldb, esz * n, k, cudaMemcpyHostToDevice, stream));
+            });
         }
     }
-    tm.mark();
 
     DevStatus* st = (DevStatus*)ws.status.get(sizeof(DevStatus));
     CUDA_TRY(cudaMemsetAsync(st, 0, 8, stream));
@@ -367,9 +393,11 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
 
     // ---- K1 (B): column pre-exponents and Bbar^T ----
     if (pipe) CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_b, 0));
-    CUDA_TRY(launch_col_max_B(prec, dB, ldb_d, k, n, bmax, st, stream)); launches += n > 0;
-    CUDA_TRY(launch_col_exp_B(bmax, n, nup, st, stream)); launches += n > 0;
-    CUDA_TRY(launch_bbar_T(prec, dB, ldb_d, k, n, kp, nup, bbar, st, stream)); launches += n > 0;
+    tm.span(1, stream, [&] {
+        CUDA_TRY(launch_col_max_B(prec, dB, ldb_d, k, n, bmax, st, stream)); launches += n > 0;
+        CUDA_TRY(launch_col_exp_B(bmax, n, nup, st, stream)); launches += n > 0;
+        CUDA_TRY(launch_bbar_T(prec, dB, ldb_d, k, n, kp, nup, bbar, st, stream)); launches += n > 0;
+    });
 
     // tile shape: single-CTA 128x256 tiles or CTA-pair 256x256 tiles (cta_group::2)
     const bool pair = use_pair_gemm();
@@ -413,10 +441,12 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     for (int c = 0; c < nchunks; ++c) {
         const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
         if (pipe) CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_a[c], 0));
-        CUDA_TRY(launch_row_scan_A(prec, (const char*)dA + esz * (size_t)(r0 * lda_d), lda_d, rc, k, kp, mup + r0,
-                                   abar + r0 * kp, st, stream, r0)); launches += rc > 0;
-        if (nchunks == 1) tm.mark();  // end of the scaling scans
-        if (rc > 0 && n > 0) {
+        tm.span(1, stream, [&] {
+            CUDA_TRY(launch_row_scan_A(prec, (const char*)dA + esz * (size_t)(r0 * lda_d), lda_d, rc, k, kp,
+                                       mup + r0, abar + r0 * kp, st, stream, r0));
+        });
+        launches += rc > 0;
+        if (rc > 0 && n > 0) tm.span(2, stream, [&] {
             const CUtensorMap tA = make_plane_map(abar + r0 * kp, kp, rc, 1, boxA);
             const CUtensorMap tB = make_plane_map(bbar, kp, n, 1, boxB);
             set_rows(gp, rc);
@@ -431,16 +461,19 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
                 g2.cplane = m * n;
                 CUDA_TRY(launch_gemm(EPI_I32, tA, tB, g2)); ++launches;
             }
-        }
-        if (nchunks == 1) tm.mark();  // end of the clearance product
+        });
         if (pipe && rc > 0) {
-            CUDA_TRY(launch_exponents(cmax_row + r0, rc, cmax_col, 0, mup + r0, nup, tab.shift0, tab.nthr, tab.thr,
-                                      mu + r0, nu, ev + r0, fv, st, stream)); ++launches;
-            CUDA_TRY(launch_resid_A(prec, (const char*)dA + esz * (size_t)(r0 * lda_d), lda_d, rc, k, kp, mu + r0,
-                                    rc_dev, N, ares + r0 * kp, m * kp, st, stream)); ++launches;
+            tm.span(3, stream, [&] {
+                CUDA_TRY(launch_exponents(cmax_row + r0, rc, cmax_col, 0, mup + r0, nup, tab.shift0, tab.nthr,
+                                          tab.thr, mu + r0, nu, ev + r0, fv, st, stream));
+            });
+            tm.span(4, stream, [&] {
+                CUDA_TRY(launch_resid_A(prec, (const char*)dA + esz * (size_t)(r0 * lda_d), lda_d, rc, k, kp,
+                                        mu + r0, rc_dev, N, ares + r0 * kp, m * kp, st, stream));
+            });
+            launches += 2;
         }
     }
-    if (nchunks > 1) { tm.mark(); tm.mark(); }
     if (reduce_fn) {
         if (reduce_fn(cmax_row, m, cmax_col, n, (void*)stream, reduce_user) != 0)
         {
@@ -451,19 +484,18 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     }
 
     // ---- K3: scaling exponents; K4: residue planes ----
-    if (pipe) {  // row exponents and A residues were produced per chunk during the upload
-        CUDA_TRY(launch_exponents(cmax_row, 0, cmax_col, n, mup, nup, tab.shift0, tab.nthr, tab.thr, mu, nu, ev, fv,
-                                  st, stream)); ++launches;
-    } else {
-        CUDA_TRY(launch_exponents(cmax_row, m, cmax_col, n, mup, nup, tab.shift0, tab.nthr, tab.thr, mu, nu, ev, fv,
-                                  st, stream)); ++launches;
-    }
-    tm.mark();
-    if (!pipe) {
-        CUDA_TRY(launch_resid_A(prec, dA, lda_d, m, k, kp, mu, rc_dev, N, ares, 0, st, stream)); launches += m > 0;
-    }
-    CUDA_TRY(launch_resid_BT(prec, dB, ldb_d, k, n, kp, nu, rc_dev, N, bres, st, stream)); launches += n > 0;
-    tm.mark();
+    // (pipelined: row exponents and A residues were produced per chunk during the upload)
+    tm.span(3, stream, [&] {
+        CUDA_TRY(launch_exponents(cmax_row, pipe ? 0 : m, cmax_col, n, mup, nup, tab.shift0, tab.nthr, tab.thr, mu,
+                                  nu, ev, fv, st, stream));
+    });
+    ++launches;
+    tm.span(4, stream, [&] {
+        if (!pipe) {
+            CUDA_TRY(launch_resid_A(prec, dA, lda_d, m, k, kp, mu, rc_dev, N, ares, 0, st, stream)); launches += m > 0;
+        }
+        CUDA_TRY(launch_resid_BT(prec, dB, ldb_d, k, n, kp, nu, rc_dev, N, bres, st, stream)); launches += n > 0;
+    });
 
     // ---- K6: CRT + inverse scaling ----
     CrtConsts cc;
@@ -510,37 +542,41 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         if (bo->tight) ex.bnd.tight = bo->device ? bo->tight : (double*)ws.x_btight.get(mn8);
     }
     // ---- K5 + K6 per row block of C: residue GEMMs (fused signed mod p), CRT + unscale ----
-    int8_t* W = (int8_t*)ws.W.get((size_t)N * (size_t)(m * ldw));
-    fill_gemm_moduli(gp, tab);
-    gp.planes = N;
-    gp.ldw = ldw;
-    gp.wplane = m * ldw;
-    const CUtensorMap tBres = make_plane_map(bres, kp, n, N, boxB);
-    std::vector<std::pair<int64_t, int64_t>> blocks;  // (first row, rows) of C per GEMM + CRT launch
     const int ovb = crt_overlap_blocks();
     const bool overlap = ovb > 1 && !inter && m >= 2048;
     if (overlap) ws.ensure_streams();
+    // W holds one row block (all N planes) unless every plane of the whole
+    // matrix is wanted (intermediates) or blocks overlap (side-stream CRT)
+    const bool w_full = inter || overlap;
+    const int64_t wrows = w_full ? m : std::min<int64_t>(m, kWBlockRows);
+    int8_t* W = (int8_t*)ws.W.get((size_t)N * (size_t)(wrows * ldw));
+    fill_gemm_moduli(gp, tab);
+    gp.planes = N;
+    gp.ldw = ldw;
+    gp.wplane = wrows * ldw;
+    const CUtensorMap tBres = make_plane_map(bres, kp, n, N, boxB);
+    std::vector<std::pair<int64_t, int64_t>> blocks;  // (first row, rows) of C per GEMM + CRT launch
+    auto split = [&](int64_t r0, int64_t rc, int64_t sub) {
+        for (int64_t q = r0; q < r0 + rc; q += sub) blocks.emplace_back(q, std::min<int64_t>(sub, r0 + rc - q));
+    };
+    const int64_t max_block = w_full ? (overlap ? round_up((m + ovb - 1) / ovb, 128) : m) : kWBlockRows;
     for (int c = 0; c < nchunks; ++c) {
         const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
         if (rc <= 0) continue;
-        if (pipe && c == nchunks - 1 && rc >= 2 * 128) {
-            const int64_t sub = round_up((rc + kTailSplit - 1) / kTailSplit, 128);
-            for (int64_t q = r0; q < r0 + rc; q += sub) blocks.emplace_back(q, std::min<int64_t>(sub, r0 + rc - q));
-        } else if (overlap && !pipe) {
-            const int64_t sub = round_up((rc + ovb - 1) / ovb, 128);
-            for (int64_t q = r0; q < r0 + rc; q += sub) blocks.emplace_back(q, std::min<int64_t>(sub, r0 + rc - q));
-        } else {
-            blocks.emplace_back(r0, rc);
-        }
+        if (pipe && c == nchunks - 1 && rc >= 2 * 128)
+            split(r0, rc, std::min<int64_t>(max_block, round_up((rc + kTailSplit - 1) / kTailSplit, 128)));
+        else
+            split(r0, rc, max_block);
     }
-    const bool marks = nchunks == 1 && blocks.size() == 1;
     for (size_t bi = 0; bi < blocks.size(); ++bi) {
         const int64_t r0 = blocks[bi].first, rc = blocks[bi].second;
         if (n <= 0) continue;
         const CUtensorMap tA = make_plane_map(ares + r0 * kp, kp, rc, N, boxA, m * kp);
+        int8_t* Wb = w_full ? W + r0 * ldw : W;
         set_rows(gp, rc);
-        gp.W = W + r0 * ldw;
-        CUDA_TRY(launch_gemm(EPI_RESID, tA, tBres, gp)); ++launches;
+        gp.W = Wb;
+        tm.span(5, stream, [&] { CUDA_TRY(launch_gemm(EPI_RESID, tA, tBres, gp)); });
+        ++launches;
         if (inter && inter->Cprod) {
             GemmParams g2 = gp;
             g2.C32 = (int32_t*)ws.x_cprod.get(4 * (size_t)N * (size_t)(m * n));
@@ -548,7 +584,6 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             g2.cplane = m * n;
             CUDA_TRY(launch_gemm(EPI_I32, tA, tBres, g2)); ++launches;
         }
-        if (marks) tm.mark();  // end of the residue GEMMs
         cudaStream_t crt_stream = stream;
         if (overlap) {  // this block's CRT beside the next block's GEMM
             const cudaEvent_t eg = ws.pool_event(2 * bi);
@@ -556,17 +591,20 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             CUDA_TRY(cudaStreamWaitEvent(ws.s_aux, eg, 0));
             crt_stream = ws.s_aux;
         }
-        CUDA_TRY(launch_crt(prec, W + r0 * ldw, ldw, m * ldw, rc, n, cc, mu + r0, nu,
-                            (char*)dC + esz * (size_t)(r0 * ldc_d), ldc_d, ex, st, crt_stream));
+        tm.span(6, crt_stream, [&] {
+            CUDA_TRY(launch_crt(prec, Wb, ldw, wrows * ldw, rc, n, cc, mu + r0, nu,
+                                (char*)dC + esz * (size_t)(r0 * ldc_d), ldc_d, ex, st, crt_stream));
+        });
         ++launches;
-        if (marks) tm.mark();  // end of CRT + unscale
         if (pipe) {  // download this C block while the next one computes
-            const cudaEvent_t ec = overlap ? ws.pool_event(2 * bi + 1) : ws.ev_c[bi];
+            const cudaEvent_t ec = ws.pool_event(2 * bi + 1);
             CUDA_TRY(cudaEventRecord(ec, crt_stream));
             CUDA_TRY(cudaStreamWaitEvent(ws.s_d2h, ec, 0));
-            CUDA_TRY(cudaMemcpy2DAsync((char*)C + esz * (size_t)(r0 * ldc), esz * ldc,
-                                       (const char*)dC + esz * (size_t)(r0 * n), esz * n, esz * n, rc,
-                                       cudaMemcpyDeviceToHost, ws.s_d2h));
+            tm.span(7, ws.s_d2h, [&] {
+                CUDA_TRY(cudaMemcpy2DAsync((char*)C + esz * (size_t)(r0 * ldc), esz * ldc,
+                                           (const char*)dC + esz * (size_t)(r0 * n), esz * n, esz * n, rc,
+                                           cudaMemcpyDeviceToHost, ws.s_d2h));
+            });
         }
     }
     if (overlap) {  // join the side stream
@@ -574,15 +612,14 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         CUDA_TRY(cudaEventRecord(ej, ws.s_aux));
         CUDA_TRY(cudaStreamWaitEvent(stream, ej, 0));
     }
-    if (!marks && nchunks == 1 && m * n != 0) { tm.mark(); tm.mark(); }
-    if (nchunks > 1 || m * n == 0) { tm.mark(); tm.mark(); }
     if (pipe) {
         CUDA_TRY(cudaEventRecord(ws.ev_done, ws.s_d2h));
         CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_done, 0));
     } else if (host && m * n) {
-        CUDA_TRY(cudaMemcpy2DAsync(C, esz * ldc, dC, esz * n, esz * n, m, cudaMemcpyDeviceToHost, stream));
+        tm.span(7, stream, [&] {
+            CUDA_TRY(cudaMemcpy2DAsync(C, esz * ldc, dC, esz * n, esz * n, m, cudaMemcpyDeviceToHost, stream));
+        });
     }
-    tm.mark();
 
     // ---- intermediates (host copies) ----
     std::vector<int32_t> tmp32;
@@ -666,14 +703,10 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     if (diag) {
         diag->subnormal = hs.subnormal ? 1 : 0;
         diag->kernels_launched = launches;
-        if (tm.on && tm.ev.size() >= 2) {
+        if (tm.on) {
             // stage order: 0 H2D, 1 K1 scale, 2 clearance GEMM, 3 exponents, 4 residues,
             //              5 residue GEMMs, 6 CRT, 7 D2H
-            for (size_t s = 0; s + 1 < tm.ev.size() && s < 8; ++s) {
-                float ms = 0;
-                cudaEventElapsedTime(&ms, tm.ev[s], tm.ev[s + 1]);
-                diag->stage_ms[s] = ms;
-            }
+            tm.collect(diag->stage_ms);
         }
     }
 

@@ -45,7 +45,7 @@ __device__ __forceinline__ double i8_to_f64_fp(uint32_t wx, int b) {
 
 // NFP of the CV columns convert through i8_to_f64_fp, the rest with I2F (XU):
 // XU converts 16 values/clk/SM, the fp64 pipe 64, so splitting balances them.
-template <class T, bool DD, bool BND, int NFP>
+template <class T, bool DD, bool BND, int NFP, bool INTER>
 __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, int64_t ldw, int64_t wplane,
                                                   int64_t m, int64_t n, const CrtConsts cc,
                                                   const int32_t* __restrict__ mu, const int32_t* __restrict__ nu,
@@ -109,10 +109,12 @@ __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, 
             const double t2 = __dadd_rn(t1, c2[b]);
             const double cpp = __fma_rn(-q, cc.P2, t2);
             const int64_t o = i * n + j;
-            if (ex.C1) ex.C1[o] = c1[b];
-            if (ex.C2) ex.C2[o] = c2[b];
-            if (ex.Q) ex.Q[o] = q;
-            if (ex.Cpp64) ex.Cpp64[o] = cpp;
+            if (INTER) {
+                if (ex.C1) ex.C1[o] = c1[b];
+                if (ex.C2) ex.C2[o] = c2[b];
+                if (ex.Q) ex.Q[o] = q;
+                if (ex.Cpp64) ex.Cpp64[o] = cpp;
+            }
             const int nuj = __ldg(nu + j);
             if (BND) {
                 const BoundCtx& bc = ex.bnd;
@@ -135,7 +137,7 @@ __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, 
             if constexpr (sizeof(T) == 4) {
                 if (fabs(cpp) >= 0x1.ffffffp+127) { fr_range = true; continue; }  // crt.hpp:144-145
                 const float c32 = __double2float_rn(cpp);
-                if (ex.Cpp32) ex.Cpp32[o] = c32;
+                if (INTER && ex.Cpp32) ex.Cpp32[o] = c32;
                 const float x = ldexpf_rn(c32, -mui);                             // emulate.hpp:37-38
                 const float y = ldexpf_rn(x, -nuj);
                 inv_range |= !isfinite(x) || !isfinite(y);
@@ -163,22 +165,27 @@ __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, 
     }
 }
 
-template <class T, bool DD, int NFP>
+template <class T, bool DD, int NFP, bool INTER>
 void launch_n(unsigned grid, cudaStream_t s, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
               const CrtConsts& cc, const int32_t* mu, const int32_t* nu, T* C, int64_t ldc, const CrtExtra& ex,
               DevStatus* st) {
-    if (ex.bnd.on) crt_kernel<T, DD, true, NFP><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
-    else crt_kernel<T, DD, false, NFP><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+    if (ex.bnd.on)
+        crt_kernel<T, DD, true, NFP, INTER><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+    else
+        crt_kernel<T, DD, false, NFP, INTER><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
 }
 
-// 3 of 8 conversions on the fp64 pipe: measured best of {0, 3, 5, 8} at 16384^2, N = 16
-constexpr int kCrtNfp = 3;
-
+// Conversions on the fp64 pipe: 3 of 8 with the double-double chain (two DFMA
+// per byte; measured best of {0, 3, 5, 8} at 16384^2, N = 16), 6 of 8 with the
+// single chain of fp32 mode (one DFMA per byte).
 template <class T, bool DD>
 void launch_t(unsigned grid, cudaStream_t s, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
               const CrtConsts& cc, const int32_t* mu, const int32_t* nu, T* C, int64_t ldc, const CrtExtra& ex,
               DevStatus* st) {
-    launch_n<T, DD, kCrtNfp>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+    constexpr int NFP = DD ? 3 : 6;
+    const bool inter = ex.C1 || ex.C2 || ex.Q || ex.Cpp64 || ex.Cpp32;
+    if (inter) launch_n<T, DD, NFP, true>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+    else launch_n<T, DD, NFP, false>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
 }
 
 }  // namespace
