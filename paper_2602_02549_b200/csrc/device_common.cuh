@@ -357,4 +357,18 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
            | ((uint32_t)(M >> 4) << 24);   // M / 16
 }
 
+// SM count of the current device (cached per device); launch shapes aim for a
+// number of CTAs per SM.
+inline int current_sm_count() {
+    static int cache[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (!cache[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = v > 0 ? v : 148;
+    }
+    return cache[dev];
+}
+
 }  // namespace oz2g

@@ -251,7 +251,7 @@ size_t transpose_smem(int op, int nmod) { return op == 1 ? resid_consts_bytes(nm
 int transpose_tiles_per_cta(int64_t kp, int64_t n) {
     const int64_t tiles = (kp / THR) * blocks_for(n, TB);
     int t = TB_H;
-    while (t > 1 && tiles / t < 16 * 148) t /= 2;
+    while (t > 1 && tiles / t < 16 * current_sm_count()) t /= 2;
     return t;
 }
 

@@ -273,7 +273,7 @@ cudaError_t launch_col_max_B(int prec, const void* B, int64_t ldb, int64_t k, in
     // 64 rows per CTA, fewer when that leaves under ~16 CTAs per SM
     const int64_t cols = blocks_for(n, 256);
     int rows = 64;
-    while (rows > 8 && cols * blocks_for(k, rows) < 16 * 148) rows /= 2;
+    while (rows > 8 && cols * blocks_for(k, rows) < 16 * current_sm_count()) rows /= 2;
     dim3 grid((unsigned)cols, blocks_for(k, rows));
     if (prec) col_max_B_kernel<double><<<grid, 256, 0, s>>>((const double*)B, ldb, k, n, rows, bmax, st);
     else col_max_B_kernel<float><<<grid, 256, 0, s>>>((const float*)B, ldb, k, n, rows, bmax, st);
