@@ -20,12 +20,13 @@
 //   q = round(S / p) = RN(S * RN(1/p) + M) - M      (|error| < 2^-13.5, while
 //       S / p is >= 1/(2p) > 2^-9 away from a half-integer for odd p;
 //       for p = 256 the product is exact)
-//   M + r = (M + S) - q * p                         (exact, integers < 2^24)
-// and the low byte of the bit pattern of M + r is r as int8: r is the
-// reference's representative of A' mod p_l (crt.hpp:48-52), symmetric for odd
-// p; for p = 256, r = +-128 both give the byte 0x80, which is how the
-// reference stores the class 128 (-128).  Per (element, modulus): one LDS.64,
-// two IDP, four fp32 operations, and 3/4 of a PRMT to pack.  Bucketing E' by 8
+// and r = S - p q is read off the integer bit patterns: bits(M + S) -
+// p * bits(M + q) = r + 0x4B400000 (1 - p), whose low byte is r as int8
+// because 0x4B400000 is a multiple of 256.  r is the reference's
+// representative of A' mod p_l (crt.hpp:48-52), symmetric for odd p; for
+// p = 256, r = +-128 both give the byte 0x80, which is how the reference
+// stores the class 128 (-128).  Per (element, modulus): one LDS.64, two IDP,
+// one FADD, one FFMA, one IMAD, and 3/4 of a PRMT to pack.  Bucketing E' by 8
 // keeps the table small (256 B per modulus) and the lanes of a warp on one or
 // two entries, so the weight loads are broadcasts.
 #include "device_common.cuh"
@@ -72,22 +73,23 @@ __device__ __forceinline__ int dp4a_us(uint32_t a, int32_t b, int32_t c) {
 }
 
 struct ModC {
-    float inv_p, pf;
+    float inv_p;
+    uint32_t p;
 };
 
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23 (bits 0x4B400000): ulp 1 on [2^23, 2^24)
 
 // Word whose low byte is the reference's representative of sgn * m' * 2^E' mod p
-// (see the file header).  All four fp32 operations are exact except the one
-// rounding to an integer, which yields round(S / p) for |S| < 2^18.
+// (see the file header).  bits = bits(M + S) = 0x4B400000 + S and
+// bits(t) = 0x4B400000 + q with q = round(S / p) (the only inexact fp32 step
+// rounds to that integer), so bits - p * bits(t) = S - p q + 0x4B400000 (1 - p),
+// whose low byte is r = S - p q: 0x4B400000 is a multiple of 256.
 __device__ __forceinline__ uint32_t resid_w(const ElemDec& d, const uint8_t* __restrict__ row_l, const ModC& c) {
     const int2 w = *reinterpret_cast<const int2*>(row_l + d.off);
     const int bits = dp4a_us(d.hi, w.y, dp4a_us(d.lo, w.x, 0x4B400000));  // bits of the float M + S
-    const float fU = __int_as_float(bits);
-    const float u = __fsub_rn(fU, kMagic);                 // S
-    const float t = __fmaf_rn(u, c.inv_p, kMagic);         // M + round(S / p)
-    const float nq = __fsub_rn(kMagic, t);                 // -round(S / p)
-    return __float_as_uint(__fmaf_rn(nq, c.pf, fU));       // M + S - p round(S / p)
+    const float u = __fsub_rn(__int_as_float(bits), kMagic);              // S
+    const float t = __fmaf_rn(u, c.inv_p, kMagic);                         // M + round(S / p)
+    return (uint32_t)bits - (uint32_t)__float_as_int(t) * c.p;
 }
 
 __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
@@ -103,7 +105,7 @@ __device__ __forceinline__ void load_resid_consts(const ResidHeader* __restrict_
     for (int t = threadIdx.x; t < words; t += blockDim.x) dst[t] = src[t];
 }
 
-__device__ __forceinline__ ModC modc(const ResidHeader& hd, int l) { return ModC{hd.inv_p[l], hd.pf[l]}; }
+__device__ __forceinline__ ModC modc(const ResidHeader& hd, int l) { return ModC{hd.inv_p[l], hd.p[l]}; }
 
 // ---------------------------------------------------------------------------
 // A: each thread owns 8 consecutive columns of one row (one 8-byte store per
