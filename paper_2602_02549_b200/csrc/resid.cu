@@ -46,23 +46,24 @@ struct ElemDec {
     uint32_t off;     // byte offset of the weights: 16 * (E' / 8) (+ 8 for x < 0)
 };
 
+// Branch-free: x = mant * 2^(max(ef, 1) - 1075) holds for normals, subnormals
+// (ef = 0, no hidden bit) and zero (mant = 0, which gives S = 0 for any table
+// row), so no case needs separate code.
 __device__ __forceinline__ ElemDec elem_dec(double x, int shift, bool& overflow) {
-    ElemDec d{0u, 0u, 0u};
-    if (x == 0.0) return d;
-    uint64_t mant; int e2;
-    decompose(x, mant, e2);
-    const int E = e2 + shift;
-    // ldexp(x, shift) overflows iff |x| 2^shift >= 2^1024 (scaling.hpp:206/220)
-    overflow |= E + 53 > 1024;
-    uint64_t mp = mant;
-    int Ep = E;
-    if (E < 0) { mp = (-E >= 64) ? 0ull : (mant >> (-E)); Ep = 0; }
+    const uint64_t bits = (uint64_t)__double_as_longlong(x);
+    const int ef = (int)((bits >> 52) & 0x7ff);
+    const uint64_t mant = (bits & 0x000fffffffffffffull) | ((uint64_t)(ef != 0) << 52);
+    const int E = max(ef, 1) - 1075 + shift;
+    // ldexp(x, shift) overflows iff |x| 2^shift >= 2^1024 (scaling.hpp:206/220);
     // |A'| < 2^(6 + P') < 2^177 for every valid input, so E' <= 124 < 8 * kResidE8
-    if (Ep > 8 * kResidE8 - 1) { overflow = true; Ep = 8 * kResidE8 - 1; }
-    mp <<= (Ep & 7);
-    d.lo = (uint32_t)mp;
-    d.hi = (uint32_t)(mp >> 32);
-    d.off = (uint32_t)(Ep >> 3) * 16u + (x < 0.0 ? 8u : 0u);
+    const int Ep = max(E, 0);
+    overflow |= mant != 0 && (E > 1024 - 53 || Ep > 8 * kResidE8 - 1);
+    const int Ec = min(Ep, 8 * kResidE8 - 1);
+    const uint64_t g = (mant >> min(max(-E, 0), 63)) << (Ec & 7);  // trunc for E < 0, then E' mod 8
+    ElemDec d;
+    d.lo = (uint32_t)g;
+    d.hi = (uint32_t)(g >> 32);
+    d.off = (uint32_t)(Ec >> 3) * 16u + (uint32_t)(bits >> 63) * 8u;
     return d;
 }
 
