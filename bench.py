@@ -377,8 +377,10 @@ def main():
     peaks, peak_kind = _peaks()
     # dominant kernel: the N residue GEMMs (one launch); algorithmic int8 ops = 2*N*m_loc*n_loc*k
     ops = 2.0 * args.moduli * A.shape[0] * B.shape[1] * k
-    gemm_avg = float(np.mean(gemm_ms))
+    gemm_avg = float(np.mean(gemm_ms))   # all residue-GEMM launches of one step
     achieved = ops / (gemm_avg * 1e-3) / 1e12
+    # the residue GEMMs run per 2048-row block of C (W is held per block): equal launches
+    n_gemm_launches = -(-A.shape[0] // 2048)
     # the residue GEMM is timed inside back-to-back steps: the sustained (power-capped) figure applies
     int8_peak = 2.0 * peaks["bf16_tflops_sustained"]
     int8_burst = 2.0 * peaks["bf16_tflops"]
@@ -386,10 +388,11 @@ def main():
     roof = {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s", "frac": achieved / int8_peak,
             "frac_of_burst": achieved / int8_burst,
             "traffic": traffic, "traffic_unit": "bytes per launch (ncu --set full, profiles/)",
-            "kernel": "gemm_i8_tc_kernel<EPI_RESID> (N residue GEMMs, one launch)",
+            "kernel": "gemm_i8_tc_kernel<EPI_RESID> (N residue GEMMs of one 2048-row block of C per launch)",
             "peak_note": f"of {peak_kind}: dense INT8 = 2 x bf16 sustained ({peaks['bf16_tflops_sustained']} TF/s, "
                          f"burst {peaks['bf16_tflops']}); int8 ops counted as FLOPs",
-            "algorithmic_ops_per_launch": ops, "launch_ms": gemm_avg}
+            "algorithmic_ops_per_launch": ops / n_gemm_launches, "launch_ms": gemm_avg / n_gemm_launches,
+            "launches_per_step": n_gemm_launches}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:

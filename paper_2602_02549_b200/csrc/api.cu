@@ -209,11 +209,15 @@ Workspace& workspace(int dev, int slot = 0) {
 
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
-// GEMM variant: OZ2G_GEMM=pair selects the CTA-pair (cta_group::2) kernel.
-bool use_pair_gemm() {
-    static const bool v = [] {
+// GEMM variant (OZ2G_GEMM): 0 single-CTA 128x256 tiles (default), 1 "pair"
+// CTA-pair cta_group::2 256x256 tiles, 2 "mcast" 2-CTA clusters sharing a
+// multicast B tile.
+int gemm_variant() {
+    static const int v = [] {
         const char* s = std::getenv("OZ2G_GEMM");
-        return s && std::strcmp(s, "pair") == 0;
+        if (s && std::strcmp(s, "pair") == 0) return 1;
+        if (s && std::strcmp(s, "mcast") == 0) return 2;
+        return 0;
     }();
     return v;
 }
@@ -399,14 +403,18 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         CUDA_TRY(launch_bbar_T(prec, dB, ldb_d, k, n, kp, nup, bbar, st, stream)); launches += n > 0;
     });
 
-    // tile shape: single-CTA 128x256 tiles or CTA-pair 256x256 tiles (cta_group::2)
-    const bool pair = use_pair_gemm();
+    // tile shape: single-CTA 128x256 tiles, CTA-pair 256x256 tiles (cta_group::2),
+    // or 128x256 tiles in 2-CTA clusters with a multicast B tile
+    const int variant = gemm_variant();
+    const bool pair = variant == 1;
     const int BM = pair ? gemm_pair_tile_m() : gemm_tile_m();
     const int BN = pair ? gemm_pair_tile_n() : gemm_tile_n();
-    const int boxA = pair ? gemm_pair_box_rows() : BM, boxB = pair ? gemm_pair_box_rows() : BN;
+    const int boxA = pair ? gemm_pair_box_rows() : BM;
+    const int boxB = pair ? gemm_pair_box_rows() : variant == 2 ? BN / 2 : BN;
     auto launch_gemm = [&](int mode, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& g) {
-        return pair ? launch_gemm_i8_pair(mode, ta, tb, g, ws.num_sms, stream)
-                    : launch_gemm_i8(mode, ta, tb, g, ws.num_sms, stream);
+        if (variant == 1) return launch_gemm_i8_pair(mode, ta, tb, g, ws.num_sms, stream);
+        if (variant == 2) return launch_gemm_i8_mc(mode, ta, tb, g, ws.num_sms, stream);
+        return launch_gemm_i8(mode, ta, tb, g, ws.num_sms, stream);
     };
     GemmParams gp;
     std::memset(&gp, 0, sizeof gp);

@@ -314,6 +314,27 @@ __device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uin
 }
 // Arrive on the barrier at the same smem offset in every CTA of `mask` once
 // the pair's previously issued MMAs complete.
+// ---- cluster multicast with single-CTA MMAs ----
+// TMA load whose bytes land at the same smem offset in every CTA of `mask`,
+// each signalling its own mbarrier at the offset of `bar`.
+__device__ __forceinline__ void tma_load_3d_mc(void* smem_dst, const CUtensorMap* desc, uint64_t* bar, int c0, int c1,
+                                               int c2, uint16_t mask, uint64_t cache_hint) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6, %7;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask),
+        "l"(cache_hint)
+        : "memory");
+}
+// MMA completion arriving on the mbarrier at the offset of `bar` in every CTA of `mask`
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+
 __device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(

@@ -255,6 +255,149 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Multicast variant: a cluster of 2 CTAs computes two vertically adjacent
+// 128 x 256 tiles that share one B tile.  Each CTA loads its own A tile and
+// HALF of the B tile with .multicast::cluster into both CTAs' shared memory,
+// so B crosses L2 -> SM once per pair; MMAs stay cta_group::1 (each CTA owns
+// its accumulator).  A stage may be refilled only when both CTAs' MMAs have
+// read it: every MMA commit arrives on the empty barrier of both CTAs.
+// ---------------------------------------------------------------------------
+constexpr int MC_HALF_B = B_BYTES / 2;  // 128 rows of B^T x 128 B
+
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm_i8_tc_mc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ GemmParams P) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 2); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
+    if (warp == 2) { tmem_alloc(tmem_slot, 512); tmem_relinquish(); }
+    tc_fence_before();
+    cluster_sync_all();  // the peer's barriers exist before any multicast reaches them
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int clusters = gridDim.x >> 1;
+    const int cid = blockIdx.x >> 1;
+    const int tiles_m2 = (P.tiles_m + 1) >> 1;  // tile-row pairs
+    const int total = P.planes * tiles_m2 * P.tiles_n;
+    const int group2 = P.group_m > 1 ? P.group_m >> 1 : 1;
+
+    if (warp == 0) {
+        // ===== TMA producer (both CTAs) =====
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int u = cid; u < total; u += clusters) {
+            const TileCoord tc = decode_unit(u, tiles_m2, P.tiles_n, group2);
+            const int arow = (2 * tc.tm + (int)rank) * BM;  // rows past m are TMA zero fill
+            const int brow = tc.tn * BN + (int)rank * (BN / 2);
+            for (int kb = 0; kb < P.kblocks; ++kb) {
+                mbar_wait(&empty[stage], phase ^ 1u);
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
+                    tma_load_3d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, arow, tc.l, P.hintA);
+                    tma_load_3d_mc(sB + stage * B_BYTES + (int)rank * MC_HALF_B, &tmB, &full[stage], kb * BK, brow,
+                                   tc.l, (uint16_t)0x3, P.hintB);
+                }
+                __syncwarp();
+                if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+            }
+        }
+        // producer tail: every stage released by both CTAs before the cluster
+        // may exit (the peer's last commits target our barriers)
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer (each CTA, its own accumulator) =====
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int u = cid; u < total; u += clusters, ++it) {
+            const int acc = it & 1;
+            const uint32_t aph = (uint32_t)((it >> 1) & 1);
+            mbar_wait(&tempty[acc], aph ^ 1u);
+            tc_fence_after();
+            const uint32_t dtmem = tmem_base + (uint32_t)(acc * BN);
+            for (int kb = 0; kb < P.kblocks; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
+                    const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / 32; ++k)
+                        mma_i8(dtmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), IDESC,
+                               (kb | k) != 0 ? 1u : 0u);
+                    mma_commit_mc(&empty[stage], (uint16_t)0x3);
+                }
+                __syncwarp();
+                if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+            }
+            if (lane == 0) mma_commit(&tfull[acc]);
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        // ===== Epilogue =====
+        const int wq = warp - 4;
+        int it = 0;
+        for (int u = cid; u < total; u += clusters, ++it) {
+            const TileCoord tc = decode_unit(u, tiles_m2, P.tiles_n, group2);
+            const int acc = it & 1;
+            const uint32_t aph = (uint32_t)((it >> 1) & 1);
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            const int row = (2 * tc.tm + (int)rank) * BM + wq * 32 + lane;
+            int32_t rowmax = 0;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld32(tmem_base + ((uint32_t)(wq * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
+                tmem_ld_wait();
+                const int col0 = tc.tn * BN + c * 32;
+                if constexpr (MODE == EPI_MAX) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) rowmax = max(rowmax, (int32_t)v[j]);
+                }
+                epilogue_chunk<MODE>(v, row, col0, tc.l, P);
+            }
+            if constexpr (MODE == EPI_MAX) {
+                if (row < P.m) atomicMax(&P.rowmax[row], rowmax);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+    }
+
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 512);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // CTA-pair variant: a cluster of 2 CTAs computes a 256 x 256 tile with
 // tcgen05.mma.cta_group::2 (M = 256, N = 256).  Each CTA loads its 128-row half
 // of A and its 128-row half of B^T per stage (32 KB instead of 48 KB for the
@@ -429,6 +572,36 @@ cudaError_t launch_gemm_i8(int mode, const CUtensorMap& tmA, const CUtensorMap& 
                                        SMEM_BYTES);
             if (err != cudaSuccess) return err;
             gemm_i8_tc_kernel<EPI_I32><<<grid, 256, SMEM_BYTES, stream>>>(tmA, tmB, P);
+            break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_i8_mc(int mode, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& P,
+                              int num_sms, cudaStream_t stream) {
+    const int total = P.planes * ((P.tiles_m + 1) / 2) * P.tiles_n;  // tile pairs
+    if (total == 0) return cudaSuccess;
+    const int pairs = num_sms / 2;
+    const int grid = 2 * (total < pairs ? total : pairs);
+    cudaError_t err = cudaSuccess;
+    switch (mode) {
+        case EPI_MAX:
+            err = cudaFuncSetAttribute(gemm_i8_tc_mc_kernel<EPI_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       SMEM_BYTES);
+            if (err != cudaSuccess) return err;
+            gemm_i8_tc_mc_kernel<EPI_MAX><<<grid, 256, SMEM_BYTES, stream>>>(tmA, tmB, P);
+            break;
+        case EPI_RESID:
+            err = cudaFuncSetAttribute(gemm_i8_tc_mc_kernel<EPI_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       SMEM_BYTES);
+            if (err != cudaSuccess) return err;
+            gemm_i8_tc_mc_kernel<EPI_RESID><<<grid, 256, SMEM_BYTES, stream>>>(tmA, tmB, P);
+            break;
+        default:
+            err = cudaFuncSetAttribute(gemm_i8_tc_mc_kernel<EPI_I32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       SMEM_BYTES);
+            if (err != cudaSuccess) return err;
+            gemm_i8_tc_mc_kernel<EPI_I32><<<grid, 256, SMEM_BYTES, stream>>>(tmA, tmB, P);
             break;
     }
     return cudaGetLastError();

@@ -36,6 +36,9 @@ int gemm_tile_n();
 int gemm_tile_k();
 cudaError_t launch_gemm_i8(int mode, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& P,
                            int num_sms, cudaStream_t stream);
+// cluster of 2 CTAs, 128 x 256 tiles each, B tile multicast (tmB box: 128 rows)
+cudaError_t launch_gemm_i8_mc(int mode, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& P,
+                              int num_sms, cudaStream_t stream);
 int gemm_pair_tile_m();
 int gemm_pair_tile_n();
 int gemm_pair_box_rows();
