@@ -160,4 +160,23 @@ EmulationResult<T> os_ii(const Matrix<T>& a, const Matrix<T>& b, int n, bool kee
     return r;
 }
 
+// The same emulation tiled over several CUDA devices of this process
+// (oz2g_gemm_multi): C is bit-identical to os_ii<T>; the result carries C,
+// the subnormal flag and the table (no per-stage intermediates).
+template <class T>
+EmulationResult<T> os_ii_multi(const Matrix<T>& a, const Matrix<T>& b, int n, const std::vector<int>& devices) {
+    static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>);
+    require_dims(a.cols() == b.rows(), "os_ii inner dimension");
+    const std::int64_t m = a.rows(), k = a.cols(), nn = b.cols();
+    const int prec = std::is_same_v<T, double> ? OZ2G_FP64 : OZ2G_FP32;
+    EmulationResult<T> r;
+    r.C = Matrix<T>(m, nn);
+    oz2g_diag diag;
+    detail::throw_status(oz2g_gemm_multi(prec, m, nn, k, a.data(), k, b.data(), nn, r.C.data(), nn, n,
+                                         OZ2G_HOST_PTRS, devices.data(), static_cast<int>(devices.size()), &diag));
+    r.subnormal = diag.subnormal != 0;
+    detail::throw_status(oz2g_table_for(n, prec, &r.table));
+    return r;
+}
+
 }  // namespace oz2

@@ -342,7 +342,12 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     void* dC = C;
     int64_t lda_d = lda, ldb_d = ldb, ldc_d = ldc;
     // pipelined host path: plain calls (no intermediates / multi-GPU hook) on large problems
-    const bool pipe = host && inter == nullptr && reduce_fn == nullptr && m >= 2048 && n >= 256;
+    // Matrix-sized intermediates need whole-matrix buffers; the O(m + n) scaling
+    // vectors (which the reference returns even with keep = false) do not.
+    const bool inter_mats = inter && (inter->Aprime || inter->Bprime || inter->Cbar || inter->Dbar || inter->W ||
+                                      inter->C1 || inter->C2 || inter->Q || inter->Cpp64 || inter->Cpp32 ||
+                                      inter->Ares || inter->Bres || inter->Cprod || inter->bounds);
+    const bool pipe = host && !inter_mats && reduce_fn == nullptr && m >= 2048 && n >= 256;
     const int64_t chunk_rows = pipe ? round_up((m + kPipeChunks - 1) / kPipeChunks, 256) : m;
     const int nchunks = m > 0 ? (int)((m + chunk_rows - 1) / chunk_rows) : 1;
     if (host) {
@@ -551,11 +556,11 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     }
     // ---- K5 + K6 per row block of C: residue GEMMs (fused signed mod p), CRT + unscale ----
     const int ovb = crt_overlap_blocks();
-    const bool overlap = ovb > 1 && !inter && m >= 2048;
+    const bool overlap = ovb > 1 && !inter_mats && m >= 2048;
     if (overlap) ws.ensure_streams();
     // W holds one row block (all N planes) unless every plane of the whole
     // matrix is wanted (intermediates) or blocks overlap (side-stream CRT)
-    const bool w_full = inter || overlap;
+    const bool w_full = (inter && inter->W) || overlap;
     const int64_t wrows = w_full ? m : std::min<int64_t>(m, kWBlockRows);
     int8_t* W = (int8_t*)ws.W.get((size_t)N * (size_t)(wrows * ldw));
     fill_gemm_moduli(gp, tab);

@@ -57,6 +57,28 @@ int main() {
     for (int i = 0; i < 4; ++i)
         for (int j = 0; j < 4; ++j)
             CHECK(std::ldexp(std::ldexp(res.C(i, j), res.scaling.mu[i]), res.scaling.nu[j]) == res.crt.Cpp64(i, j));
+    // multi-device tiling (the device listed twice): C identical to os_ii
+    {
+        Matrix<double> X(40, 33), Y(33, 27);
+        for (int i = 0; i < 40 * 33; ++i) X.data()[i] = std::sin(0.3 * i) * std::exp(0.01 * (i % 17));
+        for (int i = 0; i < 33 * 27; ++i) Y.data()[i] = std::cos(0.7 * i) - 0.25;
+        const auto single = os_ii(X, Y, 14);
+        const auto tiled = os_ii_multi(X, Y, 14, {0, 0});
+        CHECK(std::memcmp(single.C.data(), tiled.C.data(), sizeof(double) * 40 * 27) == 0);
+        CHECK(throws_as<std::invalid_argument>([&] { os_ii_multi(X, Y, 14, {}); }));
+    }
+    // large call through the drop-in (pipelined host path even though the
+    // scaling vectors are returned): same C as the device-pointer path
+    {
+        const std::int64_t m = 2304, k = 96, n = 300;
+        Matrix<double> X(m, k), Y(k, n);
+        for (std::int64_t i = 0; i < m * k; ++i) X.data()[i] = std::sin(0.001 * i) + 0.5 * std::cos(0.37 * i);
+        for (std::int64_t i = 0; i < k * n; ++i) Y.data()[i] = std::cos(0.002 * i) - 0.1;
+        const auto r = os_ii(X, Y, 16);
+        CHECK(static_cast<std::int64_t>(r.scaling.mu.size()) == m && static_cast<std::int64_t>(r.scaling.nu.size()) == n);
+        const auto t = os_ii_multi(X, Y, 16, {0});
+        CHECK(std::memcmp(r.C.data(), t.C.data(), sizeof(double) * m * n) == 0);
+    }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
     return failures ? 1 : 0;
 }
