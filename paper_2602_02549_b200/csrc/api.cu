@@ -560,7 +560,13 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     if (overlap) ws.ensure_streams();
     // W holds one row block (all N planes) unless every plane of the whole
     // matrix is wanted (intermediates) or blocks overlap (side-stream CRT)
-    const bool w_full = (inter && inter->W) || overlap;
+    // W per block only when the whole-matrix W would be large (more launches
+    // cost more than the memory saves on mid-size problems)
+    static const int64_t w_block_min = [] {
+        const char* e = std::getenv("OZ2G_WBLOCK_MIN_MB");
+        return (int64_t)(e ? std::atoll(e) : 2048) << 20;
+    }();
+    const bool w_full = (inter && inter->W) || overlap || (int64_t)N * m * ldw < w_block_min;
     const int64_t wrows = w_full ? m : std::min<int64_t>(m, kWBlockRows);
     int8_t* W = (int8_t*)ws.W.get((size_t)N * (size_t)(wrows * ldw));
     fill_gemm_moduli(gp, tab);

@@ -78,13 +78,26 @@ __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, 
                 if (DD) c2[b] = __fma_rn(s2, wv, c2[b]);
             }
         };
+        // planes in groups of 8, the next group's loads issued before this
+        // group is folded (8-16 loads in flight per thread)
         int l = 0;
-        for (; l + 8 <= cc.n; l += 8) {  // 8 plane loads in flight per thread
-            uint2 wv[8];
+        const int nfull = cc.n & ~7;
+        if (nfull) {
+            uint2 cur[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) wv[u] = __ldcs(reinterpret_cast<const uint2*>(wp + (int64_t)(l + u) * wplane));
+            for (int u = 0; u < 8; ++u) cur[u] = __ldcs(reinterpret_cast<const uint2*>(wp + (int64_t)u * wplane));
+            for (; l < nfull; l += 8) {
+                uint2 nxt[8];
+                if (l + 8 < nfull) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) fold(wv[u], l + u);
+                    for (int u = 0; u < 8; ++u)
+                        nxt[u] = __ldcs(reinterpret_cast<const uint2*>(wp + (int64_t)(l + 8 + u) * wplane));
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) fold(cur[u], l + u);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
+            }
         }
         for (; l + 4 <= cc.n; l += 4) {
             uint2 wv[4];
