@@ -63,7 +63,7 @@ class ClockSampler:
                  "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -296,10 +296,15 @@ def main():
         te = torch.tensor([(time.perf_counter() - t0) / e_steps], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        st_e2e = oz.os_ii(a_np, b_np, args.moduli, out=c_np, reduce_maxima=reduce_cb, timing=True).stage_ms
         e2e = {"value": flops / float(te.item()) / 1e12, "unit": UNIT,
                "h2d_bytes_per_step": int(8 * (A.numel() + B.numel()) * world),
                "d2h_bytes_per_step": int(8 * Cout.numel() * world),
-               "timing": "wall clock around blocking os_ii calls (host pointers; copies inside)"}
+               "timing": "wall clock around blocking os_ii calls (host pointers; copies inside)",
+               # one call's per-stage device busy time (stages overlap in the pipelined host path)
+               "stages_busy_ms": {nm: round(v, 3) for nm, v in zip(
+                   ["h2d", "scale", "clearance_gemm", "exponents", "residues", "residue_gemms", "crt_unscale",
+                    "d2h"], st_e2e)}}
         if not torch.equal(torch.from_numpy(c_np).to(dev), Cout):
             e2e["mismatch_vs_device_path"] = True
         # PCIe reference: plain pinned copies of the same bytes (what bounds e2e from below
