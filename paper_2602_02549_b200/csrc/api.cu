@@ -610,9 +610,25 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             CUDA_TRY(cudaStreamWaitEvent(ws.s_aux, eg, 0));
             crt_stream = ws.s_aux;
         }
+        // the CRT indexes rows from the block's first row: offset the optional
+        // per-entry outputs and the per-row bound vectors to this block
+        CrtExtra exb = ex;
+        const int64_t eo = r0 * n;
+        if (exb.C1) exb.C1 += eo;
+        if (exb.C2) exb.C2 += eo;
+        if (exb.Q) exb.Q += eo;
+        if (exb.Cpp64) exb.Cpp64 += eo;
+        if (exb.Cpp32) exb.Cpp32 += eo;
+        if (exb.bnd.on) {
+            exb.bnd.v.RA += r0;
+            exb.bnd.v.PA += r0;
+            exb.bnd.v.ea += r0;
+            if (exb.bnd.cheap) exb.bnd.cheap += eo;
+            if (exb.bnd.tight) exb.bnd.tight += eo;
+        }
         tm.span(6, crt_stream, [&] {
             CUDA_TRY(launch_crt(prec, Wb, ldw, wrows * ldw, rc, n, cc, mu + r0, nu,
-                                (char*)dC + esz * (size_t)(r0 * ldc_d), ldc_d, ex, st, crt_stream));
+                                (char*)dC + esz * (size_t)(r0 * ldc_d), ldc_d, exb, st, crt_stream));
         });
         ++launches;
         if (pipe) {  // download this C block while the next one computes
