@@ -596,9 +596,9 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         gp.W = Wb;
         tm.span(5, stream, [&] { CUDA_TRY(launch_gemm(EPI_RESID, tA, tBres, gp)); });
         ++launches;
-        if (inter && inter->Cprod) {
+        if (inter && inter->Cprod) {  // rows of this block of the m x n planes
             GemmParams g2 = gp;
-            g2.C32 = (int32_t*)ws.x_cprod.get(4 * (size_t)N * (size_t)(m * n));
+            g2.C32 = (int32_t*)ws.x_cprod.get(4 * (size_t)N * (size_t)(m * n)) + r0 * n;
             g2.ldc32 = n;
             g2.cplane = m * n;
             CUDA_TRY(launch_gemm(EPI_I32, tA, tBres, g2)); ++launches;

@@ -3,8 +3,8 @@ that the CRT writes per entry, and the per-row bound vectors it reads, must be
 addressed from the block's first row.  Blocking normally starts at 2 GB of W;
 a subprocess lowers the threshold (OZ2G_WBLOCK_MIN_MB=0) so a 4500-row problem
 runs as three blocks, and its outputs are compared with the unblocked call and
-the oracle: C, the cheap / tight bound matrices, and C1, C2, Q, C'' requested
-without W through the C ABI."""
+the oracle: C, the cheap / tight bound matrices, and C1, C2, Q, C'' and the
+wrapped INT32 products requested without W through the C ABI."""
 import os
 import subprocess
 import sys
@@ -31,6 +31,8 @@ it = _lib.Intermediates()
 arrs = {nm: np.zeros((m, n)) for nm in ("C1", "C2", "Q", "Cpp64")}
 for nm, a in arrs.items():
     setattr(it, nm, a.ctypes.data)
+cprod = np.zeros((14, m, n), dtype=np.int32)
+it.Cprod = cprod.ctypes.data
 Cc = np.zeros((m, n)); diag = _lib.Diag()
 rc = L.oz2g_gemm(_lib.OZ2G_FP64, m, n, k, A.ctypes.data, k, B.ctypes.data, n, Cc.ctypes.data, n, 14,
                  _lib.OZ2G_HOST_PTRS, None, C.byref(it), C.byref(diag), _lib.REDUCE_FN(), None)
@@ -38,6 +40,7 @@ assert rc == 0, L.oz2g_last_error()
 np.save("C_abi.npy", Cc)
 for nm, a in arrs.items():
     np.save(nm + ".npy", a)
+np.save("Cprod.npy", cprod)
 """.replace("ROOT", repr(ROOT))
 
 
@@ -63,3 +66,6 @@ def test_row_blocked_crt_outputs(cuda, oracle, tmp_path):
     same(np.load(tmp_path / "tight.npy"), ref.bounds["tight"])
     for nm in ("C1", "C2", "Q", "Cpp64"):  # intermediates: equal values (+0.0 == -0.0, as in test_parity_gpu)
         assert np.array_equal(np.load(tmp_path / f"{nm}.npy"), ora.inter[nm]), nm
+    # wrapped INT32 residue products of every block, against the unblocked evidence export
+    ev = oz.os_ii(A[:, :], B, 14, evidence=True)
+    assert np.array_equal(np.load(tmp_path / "Cprod.npy"), ev.crt.Cprod)
