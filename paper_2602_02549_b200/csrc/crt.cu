@@ -16,6 +16,7 @@
 // Optionally (BND) the same pass evaluates the cheap and tight error bounds
 // of bounds.hpp:143-206 for every entry (see bounds.cu for the derivation).
 #include <cfloat>
+#include <cstdlib>
 
 #include "device_common.cuh"
 #include "kernels.h"
@@ -24,7 +25,19 @@ namespace oz2g {
 
 namespace {
 
-constexpr int CV = 8;  // consecutive columns per thread (one 8-byte load per modulus plane)
+// CV consecutive columns per thread: one 8-byte (CV = 8) or 4-byte (CV = 4)
+// load per modulus plane
+template <int CV> struct WordOf;
+template <> struct WordOf<8> {
+    using T = uint2;
+    static __device__ __forceinline__ uint32_t lo(uint2 w) { return w.x; }
+    static __device__ __forceinline__ uint32_t hi(uint2 w) { return w.y; }
+};
+template <> struct WordOf<4> {
+    using T = uint32_t;
+    static __device__ __forceinline__ uint32_t lo(uint32_t w) { return w; }
+    static __device__ __forceinline__ uint32_t hi(uint32_t) { return 0u; }
+};
 
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
 #pragma unroll
@@ -45,7 +58,7 @@ __device__ __forceinline__ double i8_to_f64_fp(uint32_t wx, int b) {
 
 // NFP of the CV columns convert through i8_to_f64_fp, the rest with I2F (XU):
 // XU converts 16 values/clk/SM, the fp64 pipe 64, so splitting balances them.
-template <class T, bool DD, bool BND, int NFP, bool INTER>
+template <class T, bool DD, bool BND, int NFP, bool INTER, int CV>
 __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, int64_t ldw, int64_t wplane,
                                                   int64_t m, int64_t n, const CrtConsts cc,
                                                   const int32_t* __restrict__ mu, const int32_t* __restrict__ nu,
@@ -65,13 +78,15 @@ __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, 
         const int8_t* wp = W + i * ldw + j0;
         // crt.hpp:99-104: acc = fma(s_l, W_l, acc) in the fixed order l = 0..N-1.
         // Loads are issued 4 planes ahead of their use to keep HBM busy.
-        auto fold = [&](const uint2 word, int l) {
+        using Wt = typename WordOf<CV>::T;
+        auto fold = [&](const Wt word, int l) {
             const double s1 = cc.s1[l];
             const double s2 = cc.s2[l];
-            const uint32_t xx = word.x ^ 0x80808080u, xy = word.y ^ 0x80808080u;
+            const uint32_t wlo = WordOf<CV>::lo(word), whi = WordOf<CV>::hi(word);
+            const uint32_t xx = wlo ^ 0x80808080u, xy = whi ^ 0x80808080u;
 #pragma unroll
             for (int b = 0; b < CV; ++b) {
-                const uint32_t w32 = b < 4 ? word.x : word.y;
+                const uint32_t w32 = b < 4 ? wlo : whi;
                 const double wv = b >= CV - NFP ? i8_to_f64_fp(b < 4 ? xx : xy, b & 3)
                                                 : (double)(int8_t)((w32 >> (8 * (b & 3))) & 0xffu);
                 c1[b] = __fma_rn(s1, wv, c1[b]);
@@ -83,15 +98,15 @@ __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, 
         int l = 0;
         const int nfull = cc.n & ~7;
         if (nfull) {
-            uint2 cur[8];
+            Wt cur[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) cur[u] = __ldcs(reinterpret_cast<const uint2*>(wp + (int64_t)u * wplane));
+            for (int u = 0; u < 8; ++u) cur[u] = __ldcs(reinterpret_cast<const Wt*>(wp + (int64_t)u * wplane));
             for (; l < nfull; l += 8) {
-                uint2 nxt[8];
+                Wt nxt[8];
                 if (l + 8 < nfull) {
 #pragma unroll
                     for (int u = 0; u < 8; ++u)
-                        nxt[u] = __ldcs(reinterpret_cast<const uint2*>(wp + (int64_t)(l + 8 + u) * wplane));
+                        nxt[u] = __ldcs(reinterpret_cast<const Wt*>(wp + (int64_t)(l + 8 + u) * wplane));
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) fold(cur[u], l + u);
@@ -100,13 +115,13 @@ __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, 
             }
         }
         for (; l + 4 <= cc.n; l += 4) {
-            uint2 wv[4];
+            Wt wv[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) wv[u] = __ldcs(reinterpret_cast<const uint2*>(wp + (int64_t)(l + u) * wplane));
+            for (int u = 0; u < 4; ++u) wv[u] = __ldcs(reinterpret_cast<const Wt*>(wp + (int64_t)(l + u) * wplane));
 #pragma unroll
             for (int u = 0; u < 4; ++u) fold(wv[u], l + u);
         }
-        for (; l < cc.n; ++l) fold(__ldg(reinterpret_cast<const uint2*>(wp + (int64_t)l * wplane)), l);
+        for (; l < cc.n; ++l) fold(__ldg(reinterpret_cast<const Wt*>(wp + (int64_t)l * wplane)), l);
 
         const int mui = mu[i];
         double RAi = 0, PAi = 0;
@@ -178,27 +193,43 @@ __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, 
     }
 }
 
-template <class T, bool DD, int NFP, bool INTER>
-void launch_n(unsigned grid, cudaStream_t s, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
+template <class T, bool DD, int NFP, bool INTER, int CV>
+void launch_n(cudaStream_t s, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
               const CrtConsts& cc, const int32_t* mu, const int32_t* nu, T* C, int64_t ldc, const CrtExtra& ex,
               DevStatus* st) {
+    const int64_t work = m * ((n + CV - 1) / CV);
+    const unsigned grid = (unsigned)((work + 255) / 256);
     if (ex.bnd.on)
-        crt_kernel<T, DD, true, NFP, INTER><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+        crt_kernel<T, DD, true, NFP, INTER, CV><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
     else
-        crt_kernel<T, DD, false, NFP, INTER><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+        crt_kernel<T, DD, false, NFP, INTER, CV><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+}
+
+int crt_cv() {
+    static const int v = [] {
+        const char* e = std::getenv("OZ2G_CRT_CV");
+        return e && std::atoi(e) == 4 ? 4 : 8;
+    }();
+    return v;
 }
 
 // Conversions on the fp64 pipe: 3 of 8 with the double-double chain (two DFMA
 // per byte; measured best of {0, 3, 5, 8} at 16384^2, N = 16), 6 of 8 with the
-// single chain of fp32 mode (one DFMA per byte).
+// single chain of fp32 mode (one DFMA per byte); half of that with 4 columns.
 template <class T, bool DD>
-void launch_t(unsigned grid, cudaStream_t s, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
+void launch_t(cudaStream_t s, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
               const CrtConsts& cc, const int32_t* mu, const int32_t* nu, T* C, int64_t ldc, const CrtExtra& ex,
               DevStatus* st) {
-    constexpr int NFP = DD ? 3 : 6;
     const bool inter = ex.C1 || ex.C2 || ex.Q || ex.Cpp64 || ex.Cpp32;
-    if (inter) launch_n<T, DD, NFP, true>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
-    else launch_n<T, DD, NFP, false>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+    if (crt_cv() == 4) {
+        constexpr int NFP = DD ? 2 : 3;
+        if (inter) launch_n<T, DD, NFP, true, 4>(s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+        else launch_n<T, DD, NFP, false, 4>(s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+    } else {
+        constexpr int NFP = DD ? 3 : 6;
+        if (inter) launch_n<T, DD, NFP, true, 8>(s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+        else launch_n<T, DD, NFP, false, 8>(s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+    }
 }
 
 }  // namespace
@@ -206,14 +237,12 @@ void launch_t(unsigned grid, cudaStream_t s, const int8_t* W, int64_t ldw, int64
 cudaError_t launch_crt(int prec, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
                        const CrtConsts& cc, const int32_t* mu, const int32_t* nu, void* C, int64_t ldc,
                        const CrtExtra& extra, DevStatus* st, cudaStream_t s) {
-    const int64_t work = m * ((n + CV - 1) / CV);
-    if (work == 0) return cudaSuccess;
-    const unsigned grid = (unsigned)((work + 255) / 256);
+    if (m * n == 0) return cudaSuccess;
     if (prec) {
-        if (cc.mode == 1) launch_t<double, true>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, (double*)C, ldc, extra, st);
-        else launch_t<double, false>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, (double*)C, ldc, extra, st);
+        if (cc.mode == 1) launch_t<double, true>(s, W, ldw, wplane, m, n, cc, mu, nu, (double*)C, ldc, extra, st);
+        else launch_t<double, false>(s, W, ldw, wplane, m, n, cc, mu, nu, (double*)C, ldc, extra, st);
     } else {
-        launch_t<float, false>(grid, s, W, ldw, wplane, m, n, cc, mu, nu, (float*)C, ldc, extra, st);
+        launch_t<float, false>(s, W, ldw, wplane, m, n, cc, mu, nu, (float*)C, ldc, extra, st);
     }
     return cudaGetLastError();
 }
