@@ -164,7 +164,6 @@ std::vector<uint8_t> build_resid_consts(const Table& t) {
         const uint32_t p = (uint32_t)t.p[l];
         h->p[l] = p;
         h->inv_p[l] = (float)(1.0 / (double)p);  // any value within 2^-20 relative of 1/p works (resid.cu)
-        h->pf[l] = (float)p;
         for (int G = 0; G < kResidE8; ++G) {
             for (int sg = 0; sg < 2; ++sg) {
                 uint32_t w[8];

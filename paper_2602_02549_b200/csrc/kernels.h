@@ -53,7 +53,6 @@ struct alignas(16) ResidHeader {  // size a multiple of 16: the table that follo
     int n, pad;
     uint32_t p[49];
     float inv_p[49];  // RN32(1 / p)
-    float pf[49];     // p as float
 };
 constexpr int kResidE8 = 16;  // E' / 8 <= 15: |A'| < 2^(6 + P') and P' < 171 for N <= 49
 constexpr int kResidRow = kResidE8 * 2 * 8;  // bytes per modulus: [G][sign][8 bytes]
