@@ -46,6 +46,7 @@ extern "C" {
 #define OZ2G_HOST_PTRS 0u    /* A, B, C are host pointers (copies are done inside) */
 #define OZ2G_DEVICE_PTRS 1u  /* A, B, C are device pointers on the current device */
 #define OZ2G_TIMING 2u       /* fill oz2g_diag::stage_ms with per-stage CUDA-event times */
+#define OZ2G_ASYNC 4u        /* enqueue and return (see oz2g_synchronize); C only, no timing */
 
 /* Limits (int8gemm.hpp:12, moduli.hpp:38). */
 #define OZ2G_MAX_INNER_DIM (1LL << 17)
@@ -128,7 +129,6 @@ int oz2g_gemm(int prec, int64_t m, int64_t n, int64_t k, const void *A, int64_t 
               int64_t ldb, void *C, int64_t ldc, int nmod, unsigned flags, void *stream,
               oz2g_intermediates *inter, oz2g_diag *diag, oz2g_reduce_maxima_fn reduce_fn, void *reduce_user);
 
-/* Convenience wrappers mirroring os_ii<double>/os_ii<float>. */
 /*
  * One emulated GEMM tiled over several devices of this process:
  * C is split into an R x Cg grid of tiles (count 1 -> 1x1, 2 -> 2x1, 4 -> 2x2,
@@ -154,6 +154,7 @@ int oz2g_grid_shape(int count, int *rows, int *cols);
  */
 int oz2g_init(const int *devices, int count);
 
+/* Convenience wrappers mirroring os_ii<double>/os_ii<float>. */
 int oz2g_dgemm(int64_t m, int64_t n, int64_t k, const double *A, int64_t lda, const double *B, int64_t ldb,
                double *C, int64_t ldc, int nmod, unsigned flags, void *stream, oz2g_diag *diag);
 int oz2g_sgemm(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda, const float *B, int64_t ldb,
@@ -222,6 +223,17 @@ int oz2g_native_gemm(int prec, int64_t m, int64_t n, int64_t k, const void *A, i
 
 /* Library information (compiled arch, number of SMs used, version). */
 int oz2g_version(void);
+
+/*
+ * Complete every OZ2G_ASYNC call enqueued on the current device: wait for
+ * them, then report the first failure in call order (the status the blocking
+ * call would have returned; later calls' C are still written).  With
+ * OZ2G_ASYNC, host buffers (A, B, C) must stay valid and C must not be read
+ * until this returns; the next call's uploads overlap the previous call's
+ * residue GEMMs, so a stream of calls is bounded by PCIe rather than by
+ * upload + compute.
+ */
+int oz2g_synchronize(void);
 
 /* Release cached device workspaces of this thread's current device. */
 void oz2g_release_workspace(void);

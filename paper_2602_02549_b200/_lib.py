@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(HERE, "liboz2g.so")
 
 OZ2G_OK, OZ2G_INVALID_ARGUMENT, OZ2G_DOMAIN_ERROR, OZ2G_RANGE_ERROR, OZ2G_LOGIC_ERROR, OZ2G_CUDA_ERROR = range(6)
 OZ2G_FP32, OZ2G_FP64 = 0, 1
-OZ2G_HOST_PTRS, OZ2G_DEVICE_PTRS, OZ2G_TIMING = 0, 1, 2
+OZ2G_HOST_PTRS, OZ2G_DEVICE_PTRS, OZ2G_TIMING, OZ2G_ASYNC = 0, 1, 2, 4
 
 
 class Intermediates(C.Structure):
@@ -43,7 +43,7 @@ REDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C
 EXPORTED = ("oz2g_gemm", "oz2g_dgemm", "oz2g_sgemm", "oz2g_last_error", "oz2g_table_for",
             "oz2g_fp32_safe_moduli_max", "oz2g_shift_of_cmax", "oz2g_device_log2f", "oz2g_version",
             "oz2g_release_workspace", "oz2g_dd_gemm", "oz2g_suggest_n", "oz2g_gen_matrix", "oz2g_derive_seed",
-            "oz2g_native_gemm", "oz2g_gemm_multi", "oz2g_grid_shape", "oz2g_init")
+            "oz2g_native_gemm", "oz2g_gemm_multi", "oz2g_grid_shape", "oz2g_init", "oz2g_synchronize")
 
 _LIB = None
 

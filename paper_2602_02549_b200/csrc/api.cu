@@ -91,6 +91,12 @@ struct Workspace {
     cudaStream_t s_main = nullptr;      // compute stream of oz2g_gemm_multi tiles
     // copy streams / events of the pipelined host-pointer path
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr, s_aux = nullptr;
+    // OZ2G_ASYNC: one status slot per call in flight, completed by oz2g_synchronize
+    struct Pending { int slot; int64_t row_base, col_base; cudaStream_t stream; };
+    DevBuf status_ring;
+    int ring_next = 0;
+    std::vector<Pending> pending;
+    cudaEvent_t ev_inputs_free = nullptr;  // the last read of the device copies of A and B
     std::vector<cudaEvent_t> ev_pool;  // per-block events of the overlapped CRT
     cudaEvent_t pool_event(size_t i) {
         while (ev_pool.size() <= i) {
@@ -108,7 +114,8 @@ struct Workspace {
         CUDA_TRY(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking));
         CUDA_TRY(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking));
         CUDA_TRY(cudaStreamCreateWithFlags(&s_aux, cudaStreamNonBlocking));
-        for (cudaEvent_t* e : {&ev_start, &ev_b, &ev_done}) CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        for (cudaEvent_t* e : {&ev_start, &ev_b, &ev_done, &ev_inputs_free})
+            CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         for (int c = 0; c < kPipeChunks; ++c) CUDA_TRY(cudaEventCreateWithFlags(&ev_a[c], cudaEventDisableTiming));
         for (int c = 0; c < kPipeChunks + kTailSplit; ++c)
             CUDA_TRY(cudaEventCreateWithFlags(&ev_c[c], cudaEventDisableTiming));
@@ -116,7 +123,7 @@ struct Workspace {
     void release() {
         for (DevBuf* b : {&A, &B, &C, &abar, &bbar, &ares, &bres, &W, &mup, &nup, &mu, &nu, &bmax, &cmax_row,
                           &cmax_col, &e, &f, &status, &x_cbar, &x_cprod, &x_c1, &x_c2, &x_q, &x_cpp64, &x_cpp32,
-                          &x_ap, &x_bp, &x_bvec, &x_bscr, &x_bmax, &x_bcheap, &x_btight})
+                          &x_ap, &x_bp, &x_bvec, &x_bscr, &x_bmax, &x_bcheap, &x_btight, &status_ring})
             b->release();
         for (auto& kv : rc) cudaFree(kv.second);
         rc.clear();
@@ -267,6 +274,60 @@ int group_m_for(int tiles_m, int tiles_n) {
     return g < tiles_m ? g : (tiles_m > 0 ? tiles_m : 1);
 }
 
+constexpr int kStatusRing = 64;
+
+// The failure the reference would raise for a device status word, in its
+// pipeline order (false when the status is clean).
+bool status_failure(const DevStatus& hs, int64_t row_base, int64_t col_base, Fail& out) {
+    const uint32_t e = hs.err;
+    char buf[160];
+    auto fail = [&](int code, std::string what, int order, int64_t index = 0) {
+        out = Fail{code, std::move(what)};
+        out.order = order;
+        out.index = index;
+        return true;
+    };
+    if (e & (ERR_A_NONFINITE | ERR_A_ZERO_ROW)) {
+        if (e & ERR_A_NONFINITE) return fail(OZ2G_DOMAIN_ERROR, "matrix entry is not finite", 0, -1);
+        snprintf(buf, sizeof buf, "row_pre_exponents: zero row %lld", (long long)(hs.first_row + row_base));
+        return fail(OZ2G_DOMAIN_ERROR, buf, 0, hs.first_row + row_base);
+    }
+    if (e & ERR_B_NONFINITE) return fail(OZ2G_DOMAIN_ERROR, "matrix entry is not finite", 1, -1);
+    if (e & ERR_B_ZERO_COL) {
+        snprintf(buf, sizeof buf, "col_pre_exponents: zero column %lld", (long long)(hs.first_col + col_base));
+        return fail(OZ2G_DOMAIN_ERROR, buf, 1, hs.first_col + col_base);
+    }
+    if (e & ERR_CEIL_LOGIC) return fail(OZ2G_LOGIC_ERROR, "ceil_abs_scaled: entry above row/column max", 2);
+    if (e & ERR_E_LOGIC) return fail(OZ2G_LOGIC_ERROR, "scaling_exponents: e_i >= 31", 3);
+    if (e & ERR_MU_RANGE) return fail(OZ2G_RANGE_ERROR, "mu: exceeds 16-bit range", 4);
+    if (e & ERR_NU_RANGE) return fail(OZ2G_RANGE_ERROR, "nu: exceeds 16-bit range", 5);
+    if (e & ERR_TRUNC_A_RANGE) return fail(OZ2G_RANGE_ERROR, "truncate_scaled: 2^mu*a overflow", 6);
+    if (e & ERR_TRUNC_B_RANGE) return fail(OZ2G_RANGE_ERROR, "truncate_scaled: b*2^nu overflow", 7);
+    if (e & ERR_FR_RANGE)
+        return fail(OZ2G_RANGE_ERROR, "final_reduce: single(C'') overflows fp32 (N too large for fp32 mode)", 8);
+    if (e & ERR_INV_RANGE) return fail(OZ2G_RANGE_ERROR, "os_ii: inverse scaling overflow", 9);
+    return false;
+}
+
+// Wait for every pending OZ2G_ASYNC call of `ws` and return the first failure
+// in call order (caller holds ws.mtx).
+bool complete_pending(Workspace& ws, Fail& first) {
+    bool failed = false;
+    if (ws.pending.empty()) return false;
+    for (const auto& p : ws.pending) CUDA_TRY(cudaStreamSynchronize(p.stream));
+    std::vector<DevStatus> hs(kStatusRing);
+    CUDA_TRY(cudaMemcpy(hs.data(), ws.status_ring.p, sizeof(DevStatus) * kStatusRing, cudaMemcpyDeviceToHost));
+    for (const auto& p : ws.pending) {
+        Fail f{OZ2G_OK, ""};
+        if (!failed && status_failure(hs[(size_t)p.slot], p.row_base, p.col_base, f)) {
+            first = f;
+            failed = true;
+        }
+    }
+    ws.pending.clear();
+    return failed;
+}
+
 // Per-stage device time (OZ2G_TIMING): every launch or copy is bracketed by
 // events on the stream it runs on and the intervals are summed per stage, so
 // the numbers are right for row-blocked and pipelined calls too (where stages
@@ -324,12 +385,19 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         return OZ2G_OK;
     }
     const bool host = (flags & OZ2G_DEVICE_PTRS) == 0;
+    const bool async = (flags & OZ2G_ASYNC) != 0;
+    if (async && (inter || reduce_fn || (flags & OZ2G_TIMING)))
+        throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_gemm: OZ2G_ASYNC computes C only (no intermediates, hook or timing)"};
     const size_t esz = prec ? 8 : 4;
     int dev = 0;
     CUDA_TRY(cudaGetDevice(&dev));
     Workspace& ws = workspace(dev, slot);
     std::lock_guard<std::mutex> dev_lock(ws.mtx);
     int launches = 0;
+    if (!async && !ws.pending.empty()) {  // a blocking call completes earlier async calls first
+        Fail f{OZ2G_OK, ""};
+        if (complete_pending(ws, f)) throw f;
+    }
 
     Timer tm;
     tm.on = diag && (flags & OZ2G_TIMING);
@@ -356,8 +424,9 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         lda_d = k; ldb_d = n; ldc_d = n;
         if (pipe) {
             ws.ensure_streams();
-            CUDA_TRY(cudaEventRecord(ws.ev_start, stream));
-            CUDA_TRY(cudaStreamWaitEvent(ws.s_h2d, ws.ev_start, 0));
+            // the device copies of A and B are free once the previous call's last
+            // reader ran (its residue GEMMs may still be running: uploads overlap them)
+            CUDA_TRY(cudaStreamWaitEvent(ws.s_h2d, ws.ev_inputs_free, 0));
             // B first: the column scan needs all of it
             tm.span(0, ws.s_h2d, [&] {
                 CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dB), esz * n, B, esz * ldb, esz * n, k,
@@ -381,7 +450,20 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         }
     }
 
-    DevStatus* st = (DevStatus*)ws.status.get(sizeof(DevStatus));
+    DevStatus* st;
+    int ring_slot = -1;
+    if (async) {
+        ws.ensure_streams();
+        if ((int)ws.pending.size() >= kStatusRing) {  // ring full: complete the oldest calls first
+            Fail f{OZ2G_OK, ""};
+            if (complete_pending(ws, f)) throw f;
+        }
+        ring_slot = ws.ring_next;
+        ws.ring_next = (ws.ring_next + 1) % kStatusRing;
+        st = (DevStatus*)ws.status_ring.get(sizeof(DevStatus) * kStatusRing) + ring_slot;
+    } else {
+        st = (DevStatus*)ws.status.get(sizeof(DevStatus));
+    }
     CUDA_TRY(cudaMemsetAsync(st, 0, 8, stream));
     CUDA_TRY(cudaMemsetAsync(&st->first_row, 0x7f, 16, stream));
     int32_t* mup = (int32_t*)ws.mup.get(4 * (size_t)m);
@@ -553,6 +635,8 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         if (bo->cheap) ex.bnd.cheap = bo->device ? bo->cheap : (double*)ws.x_bcheap.get(mn8);
         if (bo->tight) ex.bnd.tight = bo->device ? bo->tight : (double*)ws.x_btight.get(mn8);
     }
+    // every read of the device copies of A and B is enqueued by now
+    if (host && ws.ev_inputs_free) CUDA_TRY(cudaEventRecord(ws.ev_inputs_free, stream));
     // ---- K5 + K6 per row block of C: residue GEMMs (fused signed mod p), CRT + unscale ----
     const int ovb = crt_overlap_blocks();
     const bool overlap = ovb > 1 && !inter_mats && m >= 2048;
@@ -713,6 +797,13 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         }
     }
 
+    if (async) {
+        CUDA_TRY(cudaGetLastError());
+        ws.pending.push_back({ring_slot, row_base, col_base, stream});
+        if (diag) diag->kernels_launched = launches;
+        return OZ2G_OK;
+    }
+
     unsigned long long bmax_host[2] = {0, 0};
     if (bo && bmax_dev) {
         CUDA_TRY(cudaMemcpyAsync(bmax_host, bmax_dev, 16, cudaMemcpyDeviceToHost, stream));
@@ -744,33 +835,8 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         }
     }
 
-    const uint32_t e = hs.err;
-    char buf[160];
-    auto fail = [](int code, std::string what, int order, int64_t index = 0) {
-        Fail f{code, std::move(what)};
-        f.order = order;
-        f.index = index;
-        return f;
-    };
-    if (e & (ERR_A_NONFINITE | ERR_A_ZERO_ROW)) {
-        if (e & ERR_A_NONFINITE) throw fail(OZ2G_DOMAIN_ERROR, "matrix entry is not finite", 0, -1);
-        snprintf(buf, sizeof buf, "row_pre_exponents: zero row %lld", (long long)(hs.first_row + row_base));
-        throw fail(OZ2G_DOMAIN_ERROR, buf, 0, hs.first_row + row_base);
-    }
-    if (e & ERR_B_NONFINITE) throw fail(OZ2G_DOMAIN_ERROR, "matrix entry is not finite", 1, -1);
-    if (e & ERR_B_ZERO_COL) {
-        snprintf(buf, sizeof buf, "col_pre_exponents: zero column %lld", (long long)(hs.first_col + col_base));
-        throw fail(OZ2G_DOMAIN_ERROR, buf, 1, hs.first_col + col_base);
-    }
-    if (e & ERR_CEIL_LOGIC) throw fail(OZ2G_LOGIC_ERROR, "ceil_abs_scaled: entry above row/column max", 2);
-    if (e & ERR_E_LOGIC) throw fail(OZ2G_LOGIC_ERROR, "scaling_exponents: e_i >= 31", 3);
-    if (e & ERR_MU_RANGE) throw fail(OZ2G_RANGE_ERROR, "mu: exceeds 16-bit range", 4);
-    if (e & ERR_NU_RANGE) throw fail(OZ2G_RANGE_ERROR, "nu: exceeds 16-bit range", 5);
-    if (e & ERR_TRUNC_A_RANGE) throw fail(OZ2G_RANGE_ERROR, "truncate_scaled: 2^mu*a overflow", 6);
-    if (e & ERR_TRUNC_B_RANGE) throw fail(OZ2G_RANGE_ERROR, "truncate_scaled: b*2^nu overflow", 7);
-    if (e & ERR_FR_RANGE)
-        throw fail(OZ2G_RANGE_ERROR, "final_reduce: single(C'') overflows fp32 (N too large for fp32 mode)", 8);
-    if (e & ERR_INV_RANGE) throw fail(OZ2G_RANGE_ERROR, "os_ii: inverse scaling overflow", 9);
+    Fail f{OZ2G_OK, ""};
+    if (status_failure(hs, row_base, col_base, f)) throw f;
     return OZ2G_OK;
 }
 
@@ -794,6 +860,10 @@ int run_suggest_n(int prec, int64_t m, int64_t n, int64_t k, const void* A, int6
     CUDA_TRY(cudaGetDevice(&dev));
     Workspace& ws = workspace(dev);
     std::lock_guard<std::mutex> dev_lock(ws.mtx);
+    if (!ws.pending.empty()) {  // complete earlier OZ2G_ASYNC calls (they may still read ws.A / ws.B)
+        Fail f{OZ2G_OK, ""};
+        if (complete_pending(ws, f)) throw f;
+    }
     const int64_t kp = round_up(k, 128);
     const void* dA = A;
     const void* dB = B;
@@ -1119,6 +1189,18 @@ int oz2g_init(const int* devices, int count) {
     });
 }
 
+int oz2g_synchronize(void) {
+    return guarded([&] {
+        int dev = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        Workspace& ws = workspace(dev, 0);
+        std::lock_guard<std::mutex> lk(ws.mtx);
+        Fail f{OZ2G_OK, ""};
+        if (complete_pending(ws, f)) throw f;
+        return OZ2G_OK;
+    });
+}
+
 const char* oz2g_last_error(void) { return g_last_error.c_str(); }
 
 int oz2g_table_for(int n, int mode, oz2g_table* out) {
@@ -1198,6 +1280,8 @@ void oz2g_release_workspace(void) {
     for (auto& kv : g_ws)
         if (kv.first / 256 == dev) {
             std::lock_guard<std::mutex> wl(kv.second->mtx);
+            for (const auto& p : kv.second->pending) cudaStreamSynchronize(p.stream);
+            kv.second->pending.clear();
             kv.second->release();
         }
 }

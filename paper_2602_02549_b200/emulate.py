@@ -139,7 +139,7 @@ def _is_torch_cuda(x) -> bool:
 
 def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = False, out=None,
           stream=None, timing: bool = False, bounds=False, vectors: bool = False,
-          reduce_maxima: Optional[Callable] = None, devices=None) -> EmulationResult:
+          reduce_maxima: Optional[Callable] = None, devices=None, blocking: bool = True) -> EmulationResult:
     """C ~ A*B by Ozaki-II accurate mode with `n` moduli (emulate.hpp:54-88).
 
     `a`, `b`: 2-D float32/float64 numpy arrays (host) or CUDA torch tensors
@@ -155,6 +155,10 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
     stream)` is the multi-GPU hook of oz2g.h.  `devices=[d0, d1, ...]` tiles
     one call over those devices of this process (oz2g_gemm_multi; host arrays,
     C only) with a result identical to the single-device call.
+    `blocking=False` enqueues the call and returns at once (C only): A, B and
+    the output must stay alive and C must not be read until `synchronize()`,
+    which raises the first failure among the pending calls.  Back-to-back
+    host-array calls then overlap the next upload with the previous GEMMs.
     """
     L = _lib.load()
     dev = _is_torch_cuda(a)
@@ -199,6 +203,17 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
         flags = _lib.OZ2G_HOST_PTRS
     if timing:
         flags |= _lib.OZ2G_TIMING
+    if not blocking:
+        if keep_intermediates or evidence or vectors or bounds or reduce_maxima is not None or timing:
+            raise InvalidArgument("os_ii: blocking=False returns C only (no intermediates, bounds, hook or timing)")
+        if devices is not None:
+            raise InvalidArgument("os_ii: blocking=False is single-device")
+        flags |= _lib.OZ2G_ASYNC
+        diag = _lib.Diag()
+        _check(L.oz2g_gemm(prec, m, nn, k, pa, lda, pb, ldb, pc, ldc, int(n), flags,
+                           C.c_void_p(int(stream) if stream else 0), None, C.byref(diag), _lib.REDUCE_FN(), None))
+        return EmulationResult(C=C_out, scaling=ScalingOutput(), crt=CrtIntermediates(), table=table_for(n, prec),
+                               subnormal=False, kernels_launched=diag.kernels_launched)
     if devices is not None:
         if dev:
             raise InvalidArgument("os_ii: devices= takes host arrays (each device uploads its own blocks)")
@@ -279,6 +294,12 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
         bres = dict(cheap_max=bnd_c.cheap_max, tight_max=bnd_c.tight_max, **bnd_arrays)
     return EmulationResult(C=C_out, scaling=sc, crt=cr, table=table_for(n, prec), subnormal=bool(diag.subnormal),
                            kernels_launched=diag.kernels_launched, stage_ms=tuple(diag.stage_ms), bounds=bres)
+
+
+def synchronize() -> None:
+    """Complete every blocking=False call on the current device and raise the
+    first failure among them in call order (oz2g_synchronize)."""
+    _check(_lib.load().oz2g_synchronize())
 
 
 def dd_gemm(a, b):
