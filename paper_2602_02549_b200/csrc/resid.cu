@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(256) transpose_B_kernel(const T* __restrict__ 
             ElemDec d[8];
 #pragma unroll
             for (int r = 0; r < 8; ++r) d[r] = elem_dec(x[r], sft, flagbit);
-#pragma unroll 2
+#pragma unroll 1
             for (int l = 0; l < nmod; ++l) {
                 const ModC mc = modc(hd, l);
                 const uint8_t* rl = tab + (size_t)l * kResidRow;
