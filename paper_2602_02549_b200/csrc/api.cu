@@ -162,6 +162,23 @@ CUtensorMap make_plane_map(const void* base, int64_t kp, int64_t rows, int64_t p
     return tm;
 }
 
+// 3-D uint8 tensor [planes][rows][cols] read as MN-major B tiles: box {128
+// columns, 128 rows, 1}, 128-B swizzle; `pitch` = bytes between rows (16-byte
+// multiple), columns past `cols` read as zeros.
+CUtensorMap make_plane_map_mn(const void* base, int64_t cols, int64_t pitch, int64_t rows, int64_t planes,
+                              int64_t plane_stride) {
+    CUtensorMap tm;
+    cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)plane_stride};
+    cuuint32_t box[3] = {128u, 128u, 1u};
+    cuuint32_t estr[3] = {1u, 1u, 1u};
+    CUresult r = get_encode()(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Fail{OZ2G_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
+    return tm;
+}
+
 std::vector<uint8_t> build_resid_consts(const Table& t) {
     std::vector<uint8_t> buf(resid_consts_bytes(t.n), 0);
     ResidHeader* h = reinterpret_cast<ResidHeader*>(buf.data());
@@ -404,6 +421,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
 
     const int64_t kp = round_up(k, 128);
     const int64_t ldw = round_up(n > 0 ? n : 1, 16);
+    const int64_t ldn = ldw;  // row pitch of Bbar and of the B residue planes [kp][ldn]
     const void* dA = A;
     const void* dB = B;
     void* dC = C;
@@ -476,7 +494,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     float* ev = (float*)ws.e.get(4 * (size_t)m);
     float* fv = (float*)ws.f.get(4 * (size_t)n);
     int8_t* abar = (int8_t*)ws.abar.get((size_t)(m * kp));
-    int8_t* bbar = (int8_t*)ws.bbar.get((size_t)(n * kp));
+    int8_t* bbar = (int8_t*)ws.bbar.get((size_t)(kp * ldn));
     if (n) CUDA_TRY(cudaMemsetAsync(bmax, 0, 8 * (size_t)n, stream));
     if (m) CUDA_TRY(cudaMemsetAsync(cmax_row, 0, 4 * (size_t)m, stream));
     if (n) CUDA_TRY(cudaMemsetAsync(cmax_col, 0, 4 * (size_t)n, stream));
@@ -486,7 +504,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     tm.span(1, stream, [&] {
         CUDA_TRY(launch_col_max_B(prec, dB, ldb_d, k, n, bmax, st, stream)); launches += n > 0;
         CUDA_TRY(launch_col_exp_B(bmax, n, nup, st, stream)); launches += n > 0;
-        CUDA_TRY(launch_bbar_T(prec, dB, ldb_d, k, n, kp, nup, bbar, st, stream)); launches += n > 0;
+        CUDA_TRY(launch_bbar_rows(prec, dB, ldb_d, k, n, kp, ldn, nup, bbar, st, stream)); launches += n > 0;
     });
 
     // tile shape: single-CTA 128x256 tiles, CTA-pair 256x256 tiles (cta_group::2),
@@ -496,7 +514,6 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     const int BM = pair ? gemm_pair_tile_m() : gemm_tile_m();
     const int BN = pair ? gemm_pair_tile_n() : gemm_tile_n();
     const int boxA = pair ? gemm_pair_box_rows() : BM;
-    const int boxB = pair ? gemm_pair_box_rows() : variant == 2 ? BN / 2 : BN;
     auto launch_gemm = [&](int mode, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& g) {
         if (variant == 1) return launch_gemm_i8_pair(mode, ta, tb, g, ws.num_sms, stream);
         if (variant == 2) return launch_gemm_i8_mc(mode, ta, tb, g, ws.num_sms, stream);
@@ -526,7 +543,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     }
     const ResidConsts* rc_dev = ws.rc[key];
     int8_t* ares = (int8_t*)ws.ares.get((size_t)N * (size_t)(m * kp));
-    int8_t* bres = (int8_t*)ws.bres.get((size_t)N * (size_t)(n * kp));
+    int8_t* bres = (int8_t*)ws.bres.get((size_t)N * (size_t)(kp * ldn));
 
     // ---- K1 (A) + K2 per row chunk: row pre-exponents, Abar, clearance product with fused maxima ----
     // Pipelined: B is complete before the first chunk, so a chunk's row maxima
@@ -542,7 +559,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         launches += rc > 0;
         if (rc > 0 && n > 0) tm.span(2, stream, [&] {
             const CUtensorMap tA = make_plane_map(abar + r0 * kp, kp, rc, 1, boxA);
-            const CUtensorMap tB = make_plane_map(bbar, kp, n, 1, boxB);
+            const CUtensorMap tB = make_plane_map_mn(bbar, n, ldn, kp, 1, kp * ldn);
             set_rows(gp, rc);
             gp.planes = 1;
             gp.rowmax = cmax_row + r0;
@@ -588,7 +605,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         if (!pipe) {
             CUDA_TRY(launch_resid_A(prec, dA, lda_d, m, k, kp, mu, rc_dev, N, ares, 0, st, stream)); launches += m > 0;
         }
-        CUDA_TRY(launch_resid_BT(prec, dB, ldb_d, k, n, kp, nu, rc_dev, N, bres, st, stream)); launches += n > 0;
+        CUDA_TRY(launch_resid_B_rows(prec, dB, ldb_d, k, n, kp, ldn, nu, rc_dev, N, bres, st, stream)); launches += n > 0;
     });
 
     // ---- K6: CRT + inverse scaling ----
@@ -656,7 +673,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     gp.planes = N;
     gp.ldw = ldw;
     gp.wplane = wrows * ldw;
-    const CUtensorMap tBres = make_plane_map(bres, kp, n, N, boxB);
+    const CUtensorMap tBres = make_plane_map_mn(bres, n, ldn, kp, N, kp * ldn);
     std::vector<std::pair<int64_t, int64_t>> blocks;  // (first row, rows) of C per GEMM + CRT launch
     auto split = [&](int64_t r0, int64_t rc, int64_t sub) {
         for (int64_t q = r0; q < r0 + rc; q += sub) blocks.emplace_back(q, std::min<int64_t>(sub, r0 + rc - q));
@@ -784,17 +801,11 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             for (int l = 0; l < N; ++l)
                 CUDA_TRY(cudaMemcpy2DAsync(inter->Ares + (size_t)l * (size_t)(m * k), (size_t)k, ares + (size_t)l * (size_t)(m * kp),
                                            (size_t)kp, (size_t)k, (size_t)m, cudaMemcpyDeviceToHost, stream));
-        if (inter->Bres && k * n) {
-            // device planes are B'^T [n][kp]; the reference layout is k x n
-            std::vector<int8_t> t((size_t)(n * kp));
-            for (int l = 0; l < N; ++l) {
-                CUDA_TRY(cudaMemcpyAsync(t.data(), bres + (size_t)l * (size_t)(n * kp), (size_t)(n * kp), cudaMemcpyDeviceToHost, stream));
-                CUDA_TRY(cudaStreamSynchronize(stream));
-                int8_t* dst = inter->Bres + (size_t)l * (size_t)(k * n);
-                for (int64_t h = 0; h < k; ++h)
-                    for (int64_t j = 0; j < n; ++j) dst[h * n + j] = t[(size_t)(j * kp + h)];
-            }
-        }
+        if (inter->Bres && k * n)  // device planes are [kp][ldn], the reference layout k x n
+            for (int l = 0; l < N; ++l)
+                CUDA_TRY(cudaMemcpy2DAsync(inter->Bres + (size_t)l * (size_t)(k * n), (size_t)n,
+                                           bres + (size_t)l * (size_t)(kp * ldn), (size_t)ldn, (size_t)n, (size_t)k,
+                                           cudaMemcpyDeviceToHost, stream));
     }
 
     if (async) {
@@ -884,13 +895,14 @@ int run_suggest_n(int prec, int64_t m, int64_t n, int64_t k, const void* A, int6
     int32_t* cmax_row = (int32_t*)ws.cmax_row.get(4 * (size_t)m);
     int32_t* cmax_col = (int32_t*)ws.cmax_col.get(4 * (size_t)n);
     int8_t* abar = (int8_t*)ws.abar.get((size_t)(m * kp));
-    int8_t* bbar = (int8_t*)ws.bbar.get((size_t)(n * kp));
+    const int64_t ldn = round_up(n, 16);
+    int8_t* bbar = (int8_t*)ws.bbar.get((size_t)(kp * ldn));
     CUDA_TRY(cudaMemsetAsync(bmax, 0, 8 * (size_t)n, stream));
     CUDA_TRY(cudaMemsetAsync(cmax_row, 0, 4 * (size_t)m, stream));
     CUDA_TRY(cudaMemsetAsync(cmax_col, 0, 4 * (size_t)n, stream));
     CUDA_TRY(launch_col_max_B(prec, dB, ldb_d, k, n, bmax, st, stream));
     CUDA_TRY(launch_col_exp_B(bmax, n, nup, st, stream));
-    CUDA_TRY(launch_bbar_T(prec, dB, ldb_d, k, n, kp, nup, bbar, st, stream));
+    CUDA_TRY(launch_bbar_rows(prec, dB, ldb_d, k, n, kp, ldn, nup, bbar, st, stream));
     CUDA_TRY(launch_row_scan_A(prec, dA, lda_d, m, k, kp, mup, abar, st, stream, 0));
     GemmParams gp;
     std::memset(&gp, 0, sizeof gp);
@@ -905,7 +917,7 @@ int run_suggest_n(int prec, int64_t m, int64_t n, int64_t k, const void* A, int6
     gp.rowmax = cmax_row;
     gp.colmax = cmax_col;
     CUDA_TRY(launch_gemm_i8(EPI_MAX, make_plane_map(abar, kp, m, 1, gemm_tile_m()),
-                            make_plane_map(bbar, kp, n, 1, gemm_tile_n()), gp, ws.num_sms, stream));
+                            make_plane_map_mn(bbar, n, ldn, kp, 1, kp * ldn), gp, ws.num_sms, stream));
     // exponent_stats (bounds.hpp:32-60) as the per-row / per-column factors with t = 1
     double* vec = (double*)ws.x_bvec.get(8 * (size_t)(2 * (m + n)) + 4 * (size_t)(m + n) + 16);
     BoundVecs v;

@@ -370,10 +370,27 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
     return d;
 }
 
-// Instruction descriptor for kind::i8: s8 x s8 -> s32, both K-major.
-__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+// MN-major operand with 128-byte swizzle (canonical layout, in 16-byte units,
+// ((8, n), (8, k)) : ((1, LBO), (8, SBO))): every K-row holds 128 contiguous
+// bytes along N, 8 K-rows form a 1 KB swizzle atom (SBO = 1024 B), and the
+// next 128 columns of N start `lbo_bytes` further on.  Advancing K by 32 rows
+// adds 32 * 128 B to the start address.
+__device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo_bytes) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;  // LBO: between 128-column chunks of N
+    d |= (uint64_t)(1024 >> 4) << 32;                  // SBO: between 8-row groups of K
+    d |= (uint64_t)1 << 46;                            // descriptor version
+    d |= (uint64_t)2 << 61;                            // SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor for kind::i8: s8 x s8 -> s32, A K-major, B K-major or
+// (b_mn) MN-major (valid for INT8 operands).
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool b_mn = false) {
     return (2u << 4)                       // D format S32
            | (1u << 7) | (1u << 10)        // A, B signed int8
+           | ((b_mn ? 1u : 0u) << 16)      // B major: 0 K, 1 MN
            | ((uint32_t)(N >> 3) << 17)    // N / 8
            | ((uint32_t)(M >> 4) << 24);   // M / 16
 }

@@ -21,12 +21,16 @@
 //
 // Kernel shape: persistent, one CTA per SM, 256 threads —
 //   warp 0      TMA producer (one elected lane): A tile 128x128 B and
-//               B tile 256x128 B per stage, 128-byte swizzle, 4 stages;
+//               B tile 128 rows x 256 columns per stage (two 128-column
+//               boxes), 128-byte swizzle, 4 stages;
 //   warp 1      MMA issuer (one lane): 4 x tcgen05.mma 128x256x32 per stage
 //               into a TMEM accumulator (2 x 256 columns, double-buffered);
 //   warp 2      TMEM allocator;
 //   warps 4..7  epilogue: tcgen05.ld 32 lanes x 32 columns, fused reduction.
-// Operands are K-major (A planes [l][m][kp], B planes [l][n][kp]).
+// A is K-major (planes [l][m][kp]); B is MN-major in its own row-major layout
+// (planes [l][kp][ldn], ldn = n rounded to 16), which tcgen05 accepts for INT8
+// (instruction-descriptor bit 16), so B's planes are written without a
+// transpose.
 #include <cstdlib>
 
 #include "device_common.cuh"
@@ -39,7 +43,10 @@ namespace {
 constexpr int BM = 128, BN = 256, BK = 128, STAGES = 4;
 constexpr int A_BYTES = BM * BK;  // 16 KB
 constexpr int B_BYTES = BN * BK;  // 32 KB
-constexpr uint32_t IDESC = idesc_i8(BM, BN);
+// B is MN-major ([plane][k][n] in HBM, B's own layout): a B tile is two TMA
+// boxes of 128 columns x BK rows, B_CHUNK bytes apart in shared memory
+constexpr int B_CHUNK = 128 * BK;  // 16 KB
+constexpr uint32_t IDESC = idesc_i8(BM, BN, true);
 constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
 
 struct TileCoord { int l, tm, tn; };
@@ -179,7 +186,9 @@ __global__ void __launch_bounds__(256, 1)
                     // A row groups are reused by every wave of a raster group: keep them in L2;
                     // B tiles stream through
                     tma_load_3d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, tc.tm * BM, tc.l, P.hintA);
-                    tma_load_3d(sB + stage * B_BYTES, &tmB, &full[stage], kb * BK, tc.tn * BN, tc.l, P.hintB);
+                    tma_load_3d(sB + stage * B_BYTES, &tmB, &full[stage], tc.tn * BN, kb * BK, tc.l, P.hintB);
+                    tma_load_3d(sB + stage * B_BYTES + B_CHUNK, &tmB, &full[stage], tc.tn * BN + 128, kb * BK, tc.l,
+                                P.hintB);
                 }
                 __syncwarp();
                 if (++stage == STAGES) { stage = 0; phase ^= 1u; }
@@ -204,7 +213,7 @@ __global__ void __launch_bounds__(256, 1)
                     const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
 #pragma unroll
                     for (int k = 0; k < BK / 32; ++k)
-                        mma_i8(dtmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), IDESC,
+                        mma_i8(dtmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128_mn(b0 + k * 32 * 128, B_CHUNK), IDESC,
                                (kb | k) != 0 ? 1u : 0u);
                     mma_commit(&empty[stage]);
                 }
@@ -262,7 +271,7 @@ __global__ void __launch_bounds__(256, 1)
 // its accumulator).  A stage may be refilled only when both CTAs' MMAs have
 // read it: every MMA commit arrives on the empty barrier of both CTAs.
 // ---------------------------------------------------------------------------
-constexpr int MC_HALF_B = B_BYTES / 2;  // 128 rows of B^T x 128 B
+constexpr int MC_HALF_B = B_CHUNK;  // 128 columns of B x BK rows
 
 template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
@@ -308,13 +317,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         for (int u = cid; u < total; u += clusters) {
             const TileCoord tc = decode_unit(u, tiles_m2, P.tiles_n, group2);
             const int arow = (2 * tc.tm + (int)rank) * BM;  // rows past m are TMA zero fill
-            const int brow = tc.tn * BN + (int)rank * (BN / 2);
+            const int bcol = tc.tn * BN + (int)rank * (BN / 2);
             for (int kb = 0; kb < P.kblocks; ++kb) {
                 mbar_wait(&empty[stage], phase ^ 1u);
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
                     tma_load_3d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, arow, tc.l, P.hintA);
-                    tma_load_3d_mc(sB + stage * B_BYTES + (int)rank * MC_HALF_B, &tmB, &full[stage], kb * BK, brow,
+                    tma_load_3d_mc(sB + stage * B_BYTES + (int)rank * MC_HALF_B, &tmB, &full[stage], bcol, kb * BK,
                                    tc.l, (uint16_t)0x3, P.hintB);
                 }
                 __syncwarp();
@@ -346,7 +355,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                     const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
 #pragma unroll
                     for (int k = 0; k < BK / 32; ++k)
-                        mma_i8(dtmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), IDESC,
+                        mma_i8(dtmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128_mn(b0 + k * 32 * 128, B_CHUNK), IDESC,
                                (kb | k) != 0 ? 1u : 0u);
                     mma_commit_mc(&empty[stage], (uint16_t)0x3);
                 }
@@ -408,9 +417,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 // accumulator stage on the leader's tmem-empty barrier.
 // ---------------------------------------------------------------------------
 constexpr int P_BM = 256, P_BN = 256;     // pair tile
-constexpr int P_HALF = 128;               // rows of A and of B^T per CTA
+constexpr int P_HALF = 128;               // rows of A and columns of B per CTA
 constexpr int P_STAGE_BYTES = 2 * P_HALF * BK;  // 32 KB per CTA per stage
-constexpr uint32_t P_IDESC = idesc_i8(P_BM, P_BN);
+constexpr uint32_t P_IDESC = idesc_i8(P_BM, P_BN, true);
 constexpr int p_smem_bytes(int stages) { return stages * P_STAGE_BYTES + 1024 + 256; }
 
 template <int MODE, int P_STAGES>
@@ -456,13 +465,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         for (int u = cid; u < total; u += clusters) {
             const TileCoord tc = decode_unit(u, P.tiles_m, P.tiles_n, P.group_m);
             const int arow = tc.tm * P_BM + (int)rank * P_HALF;
-            const int brow = tc.tn * P_BN + (int)rank * P_HALF;
+            const int bcol = tc.tn * P_BN + (int)rank * P_HALF;  // this CTA's 128 columns of B
             for (int kb = 0; kb < P.kblocks; ++kb) {
                 mbar_wait(&empty[stage], phase ^ 1u);
                 if (lane == 0) {
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
                     tma_load_3d_pair(sA + stage * P_HALF * BK, &tmA, &full[stage], kb * BK, arow, tc.l, P.hintA);
-                    tma_load_3d_pair(sB + stage * P_HALF * BK, &tmB, &full[stage], kb * BK, brow, tc.l, P.hintB);
+                    tma_load_3d_pair(sB + stage * P_HALF * BK, &tmB, &full[stage], bcol, kb * BK, tc.l, P.hintB);
                 }
                 __syncwarp();
                 if (++stage == P_STAGES) { stage = 0; phase ^= 1u; }
@@ -488,7 +497,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                         const uint32_t b0 = smem_u32(sB + stage * P_HALF * BK);
 #pragma unroll
                         for (int k = 0; k < BK / 32; ++k)
-                            mma_i8_pair(dtmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), P_IDESC,
+                            mma_i8_pair(dtmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128_mn(b0 + k * 32 * 128, P_HALF * BK), P_IDESC,
                                         (kb | k) != 0 ? 1u : 0u);
                         mma_commit_pair(&empty[stage], (uint16_t)0x3);
                     }

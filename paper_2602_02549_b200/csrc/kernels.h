@@ -66,8 +66,9 @@ cudaError_t launch_col_max_B(int prec, const void* B, int64_t ldb, int64_t k, in
                              unsigned long long* bmax, DevStatus* st, cudaStream_t s);
 cudaError_t launch_col_exp_B(const unsigned long long* bmax, int64_t n, int32_t* nu_prime, DevStatus* st,
                              cudaStream_t s);
-cudaError_t launch_bbar_T(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp,
-                          const int32_t* nu_prime, int8_t* bbar_t, DevStatus* st, cudaStream_t s);
+// Bbar = ceil(|B| 2^nu') in B's layout [kp][ldn] (rows k..kp and columns n..ldn zero)
+cudaError_t launch_bbar_rows(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp, int64_t ldn,
+                             const int32_t* nu_prime, int8_t* bbar, DevStatus* st, cudaStream_t s);
 cudaError_t launch_exponents(const int32_t* cmax_row, int64_t m, const int32_t* cmax_col, int64_t n,
                              const int32_t* mu_prime, const int32_t* nu_prime, int shift0, int nthr,
                              const int32_t* thr, int32_t* mu, int32_t* nu, float* e, float* f, DevStatus* st,
@@ -77,9 +78,10 @@ cudaError_t launch_exponents(const int32_t* cmax_row, int64_t m, const int32_t* 
 cudaError_t launch_resid_A(int prec, const void* A, int64_t lda, int64_t m, int64_t k, int64_t kp,
                            const int32_t* mu, const ResidConsts* rc_dev, int nmod, int8_t* planes,
                            int64_t plane_stride, DevStatus* st, cudaStream_t s);
-cudaError_t launch_resid_BT(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp,
-                            const int32_t* nu, const ResidConsts* rc_dev, int nmod, int8_t* planes,
-                            DevStatus* st, cudaStream_t s);
+// residue planes of trunc(B 2^nu) in B's layout, [l][kp][ldn]
+cudaError_t launch_resid_B_rows(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp, int64_t ldn,
+                                const int32_t* nu, const ResidConsts* rc_dev, int nmod, int8_t* planes,
+                                DevStatus* st, cudaStream_t s);
 cudaError_t launch_trunc_scaled(int prec, const void* X, int64_t ldx, int64_t rows, int64_t cols,
                                 const int32_t* shift, int by_col, double* out, cudaStream_t s);
 cudaError_t launch_log2f(const float* x, float* out, int64_t count, cudaStream_t s);

@@ -5,9 +5,9 @@
 //                (crt.hpp:20-65) for every modulus: A' = trunc(2^mu A) is never
 //                materialised; each element is decomposed once and all N int8
 //                planes [l][m][kp] (K-major) are written in the same pass.
-//   resid_BT     the same for B (truncate_scaled_cols, scaling.hpp:213-225),
-//                written transposed to K-major planes [l][n][kp].
-//   bbar_T       ceil_abs_scale_cols (scaling.hpp:122-131) -> Bbar^T [n][kp].
+//   resid_B      the same for B (truncate_scaled_cols, scaling.hpp:213-225)
+//                in B's own layout, planes [l][kp][ldn] (MN-major for the GEMM).
+//   bbar         ceil_abs_scale_cols (scaling.hpp:122-131) -> Bbar [kp][ldn].
 //
 // Residue arithmetic.  |A'| = m' * 2^E' with m' < 2^53 (m' = mant >> -E if
 // E < 0, E' = max(E, 0)); write it as g * 2^(8 G) with g = m' << (E' mod 8)
@@ -109,13 +109,20 @@ __device__ __forceinline__ void load_resid_consts(const ResidHeader* __restrict_
 __device__ __forceinline__ ModC modc(const ResidHeader& hd, int l) { return ModC{hd.inv_p[l], hd.p[l]}; }
 
 // ---------------------------------------------------------------------------
-// A: each thread owns 8 consecutive columns of one row (one 8-byte store per
-// plane, 16-byte vector loads).  grid.x covers the 2048-column chunks of a
-// row; a CTA walks rows blockIdx.y, blockIdx.y + gridDim.y, ... so the weight
-// table is loaded once per CTA instead of once per row chunk.
+// Row-major writers (A and B alike): each thread owns 8 consecutive columns of
+// one row (16-byte vector loads, one 8-byte store per output plane); grid.x
+// covers the 2048-column chunks of a row and a CTA walks rows blockIdx.y,
+// blockIdx.y + gridDim.y, ... so the weight table is loaded once per CTA.
+//   A residues: rows m, shift mu per row, planes [l][m][kp] (K-major for the GEMM)
+//   B residues: rows kp (k real, the rest zero), shift nu per column, planes
+//               [l][kp][ldn] (B's own layout, read MN-major by the GEMM)
+//   Bbar (OP 0): ceil(|b| 2^nu'_j) into [kp][ldn] (scaling.hpp:122-131)
+// Columns past the valid ones (up to the padded width) are written as zeros.
 // ---------------------------------------------------------------------------
 constexpr int RA_E = 8;
 
+// A: the row-shift case of the writer below, kept as its own kernel (48
+// registers, 5 CTAs per SM; the general one needs 60).
 template <class T>
 __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t k,
                                                       int64_t kp, const int32_t* __restrict__ mu,
@@ -168,24 +175,13 @@ __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, i
     if (ovf) flag(st, ERR_TRUNC_A_RANGE);
 }
 
-// ---------------------------------------------------------------------------
-// B transposed writers, output [plane][j][kp] (K-major).  A warp covers 8
-// columns x 32 rows: lane = 4 * column + row group, each lane 8 consecutive
-// rows of one column, so the 4 lanes of a column hold its 32 consecutive
-// output bytes and every warp store writes 8 full 32-byte sectors — no shared
-// memory transpose.  Loads read 64-byte row segments (full sectors).  A CTA (8
-// warps, 64 columns) walks TB_H consecutive 32-row tiles.
-//   OP 0: Bbar^T = ceil(|B| 2^nu')   OP 1: residue planes of trunc(B 2^nu)
-// ---------------------------------------------------------------------------
-constexpr int TB = 64;    // columns j per CTA
-constexpr int THR = 32;   // rows h per tile
-constexpr int TB_H = 8;   // at most this many tiles per CTA (fewer on small matrices)
-
-template <class T, int OP>
-__global__ void __launch_bounds__(256) transpose_B_kernel(const T* __restrict__ B, int64_t ldb, int64_t k,
-                                                          int64_t n, int64_t kp, const int32_t* __restrict__ shift,
-                                                          const ResidHeader* __restrict__ rc_g, int nmod,
-                                                          int8_t* __restrict__ out, int tb_h, DevStatus* st) {
+template <class T, bool COLSHIFT, int OP>
+__global__ void __launch_bounds__(256) resid_rows_kernel(const T* __restrict__ X, int64_t ldx, int64_t rows_valid,
+                                                         int64_t rows_total, int64_t cols_valid, int64_t ld_out,
+                                                         const int32_t* __restrict__ shift,
+                                                         const ResidHeader* __restrict__ rc_g, int nmod,
+                                                         int8_t* __restrict__ planes, int64_t plane, uint32_t err_bit,
+                                                         DevStatus* st) {
     extern __shared__ __align__(16) uint8_t sh[];
     if (OP == 1) {
         load_resid_consts(rc_g, nmod, sh);
@@ -193,126 +189,150 @@ __global__ void __launch_bounds__(256) transpose_B_kernel(const T* __restrict__ 
     }
     const ResidHeader& hd = *reinterpret_cast<const ResidHeader*>(sh);
     const uint8_t* tab = sh + sizeof(ResidHeader);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t j = (int64_t)blockIdx.y * TB + warp * 8 + (lane >> 2);
-    if (j >= n) return;
-    const int sft = shift[j];
-    const int64_t plane = n * kp;
-    bool flagbit = false;
-    const int64_t hend = (int64_t)(blockIdx.x + 1) * tb_h * THR;
-    const int64_t hmax = kp < hend ? kp : hend;
-    int64_t h0 = (int64_t)blockIdx.x * tb_h * THR + (lane & 3) * 8;
-    // the next tile's rows are loaded while this one computes (latency hiding);
-    // the buffer keeps the input type (half the registers for float)
-    T xn[8];
+    const int64_t h0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * RA_E;
+    if (h0 >= ld_out) return;
+    bool bad = false;
+    int csft[RA_E];  // per-column shifts (B): the same for every row
+    if (COLSHIFT) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) xn[r] = h0 + r < k ? __ldg(B + (h0 + r) * ldb + j) : T(0);
-    for (; h0 < hmax; h0 += THR) {
-        double x[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) x[r] = (double)xn[r];
-        const int64_t h1 = h0 + THR;
-        if (h1 < hmax) {
-#pragma unroll
-            for (int r = 0; r < 8; ++r) xn[r] = h1 + r < k ? __ldg(B + (h1 + r) * ldb + j) : T(0);
+        for (int j = 0; j < RA_E; ++j) csft[j] = h0 + j < cols_valid ? __ldg(shift + h0 + j) : 0;
+    }
+    const bool full = h0 + RA_E <= cols_valid;
+    const int nplanes = OP == 0 ? 1 : nmod;
+    for (int64_t i = blockIdx.y; i < rows_total; i += gridDim.y) {
+        int8_t* out = planes + i * ld_out + h0;
+        if (i >= rows_valid) {  // zero padding rows (B: k .. kp)
+            for (int l = 0; l < nplanes; ++l) *reinterpret_cast<uint2*>(out + (int64_t)l * plane) = make_uint2(0u, 0u);
+            continue;
         }
-        int8_t* o = out + j * kp + h0;
+        const T* row = X + i * ldx + h0;
+        const int rsft = COLSHIFT ? 0 : __ldg(shift + i);
+        const bool vec = full && ((reinterpret_cast<uintptr_t>(row) & 15) == 0);
         if (OP == 0) {
-            uint32_t w[2] = {0, 0};
+            double x[RA_E];
+            if (vec && sizeof(T) == 8) {
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                const int v = ceil_abs_scaled(x[r], sft);
-                flagbit |= v < 0;
-                w[r >> 2] |= (uint32_t)(v & 0xff) << (8 * (r & 3));
+                for (int j = 0; j < RA_E; j += 2) {
+                    const double2 t = __ldg(reinterpret_cast<const double2*>(row + j));
+                    x[j] = t.x;
+                    x[j + 1] = t.y;
+                }
+            } else if (vec && sizeof(T) == 4) {
+#pragma unroll
+                for (int j = 0; j < RA_E; j += 4) {
+                    const float4 t = __ldg(reinterpret_cast<const float4*>(row + j));
+                    x[j] = t.x; x[j + 1] = t.y; x[j + 2] = t.z; x[j + 3] = t.w;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < RA_E; ++j) x[j] = h0 + j < cols_valid ? (double)__ldg(row + j) : 0.0;
             }
-            *reinterpret_cast<uint2*>(o) = make_uint2(w[0], w[1]);
+            uint32_t w[2] = {0u, 0u};
+#pragma unroll
+            for (int j = 0; j < RA_E; ++j) {
+                const int c = ceil_abs_scaled(x[j], COLSHIFT ? csft[j] : rsft);
+                bad |= c < 0;
+                w[j >> 2] |= (uint32_t)(c & 0xff) << (8 * (j & 3));
+            }
+            *reinterpret_cast<uint2*>(out) = make_uint2(w[0], w[1]);
+            continue;
+        }
+        // decode straight from the loads (no staging array: fewer live registers)
+        ElemDec d[RA_E];
+        if (vec && sizeof(T) == 8) {
+#pragma unroll
+            for (int j = 0; j < RA_E; j += 2) {
+                const double2 t = __ldg(reinterpret_cast<const double2*>(row + j));
+                d[j] = elem_dec(t.x, COLSHIFT ? csft[j] : rsft, bad);
+                d[j + 1] = elem_dec(t.y, COLSHIFT ? csft[j + 1] : rsft, bad);
+            }
+        } else if (vec && sizeof(T) == 4) {
+#pragma unroll
+            for (int j = 0; j < RA_E; j += 4) {
+                const float4 t = __ldg(reinterpret_cast<const float4*>(row + j));
+                d[j] = elem_dec((double)t.x, COLSHIFT ? csft[j] : rsft, bad);
+                d[j + 1] = elem_dec((double)t.y, COLSHIFT ? csft[j + 1] : rsft, bad);
+                d[j + 2] = elem_dec((double)t.z, COLSHIFT ? csft[j + 2] : rsft, bad);
+                d[j + 3] = elem_dec((double)t.w, COLSHIFT ? csft[j + 3] : rsft, bad);
+            }
         } else {
-            ElemDec d[8];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) d[r] = elem_dec(x[r], sft, flagbit);
-#pragma unroll 1
-            for (int l = 0; l < nmod; ++l) {
-                const ModC mc = modc(hd, l);
-                const uint8_t* rl = tab + (size_t)l * kResidRow;
-                const uint32_t w0 = pack4(resid_w(d[0], rl, mc), resid_w(d[1], rl, mc), resid_w(d[2], rl, mc),
-                                          resid_w(d[3], rl, mc));
-                const uint32_t w1 = pack4(resid_w(d[4], rl, mc), resid_w(d[5], rl, mc), resid_w(d[6], rl, mc),
-                                          resid_w(d[7], rl, mc));
-                *reinterpret_cast<uint2*>(o + (int64_t)l * plane) = make_uint2(w0, w1);
-            }
+            for (int j = 0; j < RA_E; ++j)
+                d[j] = elem_dec(h0 + j < cols_valid ? (double)__ldg(row + j) : 0.0, COLSHIFT ? csft[j] : rsft, bad);
+        }
+#pragma unroll 2
+        for (int l = 0; l < nmod; ++l) {
+            const ModC c = modc(hd, l);
+            const uint8_t* rl = tab + (size_t)l * kResidRow;
+            const uint32_t w0 = pack4(resid_w(d[0], rl, c), resid_w(d[1], rl, c), resid_w(d[2], rl, c),
+                                      resid_w(d[3], rl, c));
+            const uint32_t w1 = pack4(resid_w(d[4], rl, c), resid_w(d[5], rl, c), resid_w(d[6], rl, c),
+                                      resid_w(d[7], rl, c));
+            *reinterpret_cast<uint2*>(out + (int64_t)l * plane) = make_uint2(w0, w1);
         }
     }
-    if (flagbit) flag(st, OP == 0 ? ERR_CEIL_LOGIC : ERR_TRUNC_B_RANGE);
+    if (bad) flag(st, err_bit);
 }
 
 inline unsigned blocks_for(int64_t work, int per) { return (unsigned)((work + per - 1) / per); }
-
-size_t transpose_smem(int op, int nmod) { return op == 1 ? resid_consts_bytes(nmod) : 0; }
-
-// tiles per CTA: up to TB_H, fewer when that leaves under ~16 CTAs per SM
-// (short per-CTA chains keep enough loads in flight on mid-size matrices)
-int transpose_tiles_per_cta(int64_t kp, int64_t n) {
-    const int64_t tiles = (kp / THR) * blocks_for(n, TB);
-    int t = TB_H;
-    while (t > 1 && tiles / t < 16 * current_sm_count()) t /= 2;
-    return t;
-}
 
 template <class K>
 cudaError_t set_smem(K kernel, size_t bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-// resid_A grid: x = column chunks, y = enough row strides for kResidWaves waves
-// of resident CTAs (each CTA then loads the weight table once for m / y rows).
+// grid: x = column chunks, y = enough row strides for kResidWaves waves of
+// resident CTAs (each CTA then loads the weight table once for rows / y rows).
 constexpr int kResidWaves = 4;
 
 template <class K>
-cudaError_t resid_A_grid(K kernel, size_t smem, int64_t m, unsigned chunks, dim3& grid) {
+cudaError_t rows_grid(K kernel, size_t smem, int64_t rows, unsigned chunks, dim3& grid) {
     cudaError_t err = set_smem(kernel, smem);
     if (err != cudaSuccess) return err;
-    int dev = 0, sms = 0, per_sm = 0;
-    if ((err = cudaGetDevice(&dev)) != cudaSuccess) return err;
-    if ((err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return err;
+    int per_sm = 0;
     if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem)) != cudaSuccess) return err;
-    const int64_t ctas = (int64_t)sms * (per_sm > 0 ? per_sm : 1) * kResidWaves;
-    int64_t rows = (ctas + chunks - 1) / chunks;
-    rows = rows < m ? rows : m;
-    grid = dim3(chunks, (unsigned)(rows < 65535 ? rows : 65535));
+    const int64_t ctas = (int64_t)current_sm_count() * (per_sm > 0 ? per_sm : 1) * kResidWaves;
+    int64_t r = (ctas + chunks - 1) / chunks;
+    r = r < rows ? r : rows;
+    grid = dim3(chunks, (unsigned)(r < 65535 ? (r > 0 ? r : 1) : 65535));
     return cudaSuccess;
+}
+
+template <class T, bool COLSHIFT, int OP>
+cudaError_t launch_rows(const void* X, int64_t ldx, int64_t rows_valid, int64_t rows_total, int64_t cols_valid,
+                        int64_t ld_out, const int32_t* shift, const ResidConsts* rc, int nmod, int8_t* planes,
+                        int64_t plane, uint32_t err_bit, DevStatus* st, cudaStream_t s) {
+    if (rows_total == 0 || ld_out == 0) return cudaSuccess;
+    const unsigned chunks = blocks_for(ld_out, 256 * RA_E);
+    const size_t sm = OP == 1 ? resid_consts_bytes(nmod) : 0;
+    dim3 grid;
+    cudaError_t err = rows_grid(resid_rows_kernel<T, COLSHIFT, OP>, sm, rows_total, chunks, grid);
+    if (err != cudaSuccess) return err;
+    resid_rows_kernel<T, COLSHIFT, OP><<<grid, 256, sm, s>>>((const T*)X, ldx, rows_valid, rows_total, cols_valid,
+                                                            ld_out, shift, rc, nmod, planes, plane, err_bit, st);
+    return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_bbar_T(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp,
-                          const int32_t* nu_prime, int8_t* bbar_t, DevStatus* st, cudaStream_t s) {
+cudaError_t launch_bbar_rows(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp, int64_t ldn,
+                             const int32_t* nu_prime, int8_t* bbar, DevStatus* st, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    const int tb = transpose_tiles_per_cta(kp, n);
-    const dim3 grid(blocks_for(kp, tb * THR), blocks_for(n, TB));
-    const size_t sm = transpose_smem(0, 1);
-    if (prec)
-        transpose_B_kernel<double, 0><<<grid, 256, sm, s>>>((const double*)B, ldb, k, n, kp, nu_prime, nullptr, 1, bbar_t, tb, st);
-    else
-        transpose_B_kernel<float, 0><<<grid, 256, sm, s>>>((const float*)B, ldb, k, n, kp, nu_prime, nullptr, 1, bbar_t, tb, st);
-    return cudaGetLastError();
+    return prec ? launch_rows<double, true, 0>(B, ldb, k, kp, n, ldn, nu_prime, nullptr, 1, bbar, 0, ERR_CEIL_LOGIC,
+                                               st, s)
+                : launch_rows<float, true, 0>(B, ldb, k, kp, n, ldn, nu_prime, nullptr, 1, bbar, 0, ERR_CEIL_LOGIC,
+                                              st, s);
 }
 
-cudaError_t launch_resid_BT(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp,
-                            const int32_t* nu, const ResidConsts* rc_dev, int nmod, int8_t* planes,
-                            DevStatus* st, cudaStream_t s) {
+cudaError_t launch_resid_B_rows(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp, int64_t ldn,
+                                const int32_t* nu, const ResidConsts* rc_dev, int nmod, int8_t* planes,
+                                DevStatus* st, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    const int tb = transpose_tiles_per_cta(kp, n);
-    const dim3 grid(blocks_for(kp, tb * THR), blocks_for(n, TB));
-    const size_t sm = transpose_smem(1, nmod);
-    cudaError_t err;
-    if (prec) {
-        if ((err = set_smem(transpose_B_kernel<double, 1>, sm)) != cudaSuccess) return err;
-        transpose_B_kernel<double, 1><<<grid, 256, sm, s>>>((const double*)B, ldb, k, n, kp, nu, rc_dev, nmod, planes, tb, st);
-    } else {
-        if ((err = set_smem(transpose_B_kernel<float, 1>, sm)) != cudaSuccess) return err;
-        transpose_B_kernel<float, 1><<<grid, 256, sm, s>>>((const float*)B, ldb, k, n, kp, nu, rc_dev, nmod, planes, tb, st);
-    }
-    return cudaGetLastError();
+    const int64_t plane = kp * ldn;
+    return prec ? launch_rows<double, true, 1>(B, ldb, k, kp, n, ldn, nu, rc_dev, nmod, planes, plane,
+                                               ERR_TRUNC_B_RANGE, st, s)
+                : launch_rows<float, true, 1>(B, ldb, k, kp, n, ldn, nu, rc_dev, nmod, planes, plane,
+                                              ERR_TRUNC_B_RANGE, st, s);
 }
 
 cudaError_t launch_resid_A(int prec, const void* A, int64_t lda, int64_t m, int64_t k, int64_t kp,
@@ -325,10 +345,10 @@ cudaError_t launch_resid_A(int prec, const void* A, int64_t lda, int64_t m, int6
     dim3 grid;
     cudaError_t err;
     if (prec) {
-        if ((err = resid_A_grid(resid_A_kernel<double>, sm, m, chunks, grid)) != cudaSuccess) return err;
+        if ((err = rows_grid(resid_A_kernel<double>, sm, m, chunks, grid)) != cudaSuccess) return err;
         resid_A_kernel<double><<<grid, 256, sm, s>>>((const double*)A, lda, m, k, kp, mu, rc_dev, nmod, planes, plane, st);
     } else {
-        if ((err = resid_A_grid(resid_A_kernel<float>, sm, m, chunks, grid)) != cudaSuccess) return err;
+        if ((err = rows_grid(resid_A_kernel<float>, sm, m, chunks, grid)) != cudaSuccess) return err;
         resid_A_kernel<float><<<grid, 256, sm, s>>>((const float*)A, lda, m, k, kp, mu, rc_dev, nmod, planes, plane, st);
     }
     return cudaGetLastError();
