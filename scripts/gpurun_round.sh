@@ -12,4 +12,4 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
     --log-file gpurun_out/r_launches.csv python bench.py $B > /dev/null 2>&1; echo launches=$?
 B1="--steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-native"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:gemm_i8_tc -s 1 -c 1 -o gpurun_out/r_gemm python bench.py $B1 > /dev/null 2>&1; echo gemm=$?
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"row_scan|col_max|transpose_B|resid_A|crt" -c 6 -o gpurun_out/r_aux python bench.py $B1 > /dev/null 2>&1; echo aux=$?
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"row_scan|col_max|resid_rows|resid_A|crt" -c 6 -o gpurun_out/r_aux python bench.py $B1 > /dev/null 2>&1; echo aux=$?
