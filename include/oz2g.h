@@ -143,6 +143,17 @@ int oz2g_gemm_multi(int prec, int64_t m, int64_t n, int64_t k, const void *A, in
                     int64_t ldb, void *C, int64_t ldc, int nmod, unsigned flags, const int *devices, int count,
                     oz2g_diag *diag);
 
+/*
+ * The same A, B emulated for several moduli counts (the N sweep of the
+ * paper's experiments): the scaling scans and the clearance product do not
+ * depend on N and are computed once.  C[i] (leading dimension ldc) receives
+ * the result for nmods[i], bit-identical to oz2g_gemm with nmods[i].  Host or
+ * device pointers (flags); no OZ2G_ASYNC / OZ2G_TIMING.
+ */
+int oz2g_gemm_sweep(int prec, int64_t m, int64_t n, int64_t k, const void *A, int64_t lda, const void *B,
+                    int64_t ldb, void *const *C, int64_t ldc, const int *nmods, int count, unsigned flags,
+                    void *stream, oz2g_diag *diag);
+
 /* The tile grid oz2g_gemm_multi uses for `count` devices. */
 int oz2g_grid_shape(int count, int *rows, int *cols);
 

@@ -43,7 +43,8 @@ REDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C
 EXPORTED = ("oz2g_gemm", "oz2g_dgemm", "oz2g_sgemm", "oz2g_last_error", "oz2g_table_for",
             "oz2g_fp32_safe_moduli_max", "oz2g_shift_of_cmax", "oz2g_device_log2f", "oz2g_version",
             "oz2g_release_workspace", "oz2g_dd_gemm", "oz2g_suggest_n", "oz2g_gen_matrix", "oz2g_derive_seed",
-            "oz2g_native_gemm", "oz2g_gemm_multi", "oz2g_grid_shape", "oz2g_init", "oz2g_synchronize")
+            "oz2g_native_gemm", "oz2g_gemm_multi", "oz2g_grid_shape", "oz2g_init", "oz2g_synchronize",
+            "oz2g_gemm_sweep")
 
 _LIB = None
 
@@ -81,6 +82,9 @@ def load() -> C.CDLL:
                                   C.c_int64, C.c_void_p, C.c_int64, C.c_int, C.c_uint, C.POINTER(C.c_int), C.c_int,
                                   C.POINTER(Diag)]
     L.oz2g_grid_shape.argtypes = [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    L.oz2g_gemm_sweep.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                                  C.c_int64, C.POINTER(C.c_void_p), C.c_int64, C.POINTER(C.c_int), C.c_int, C.c_uint,
+                                  C.c_void_p, C.POINTER(Diag)]
     L.oz2g_init.argtypes = [C.POINTER(C.c_int), C.c_int]
     _LIB = L
     return L

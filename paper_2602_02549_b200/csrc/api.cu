@@ -388,7 +388,7 @@ constexpr int64_t kWBlockRows = 2048;
 int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
              void* C, int64_t ldc, int nmod, unsigned flags, cudaStream_t stream, oz2g_intermediates* inter,
              oz2g_diag* diag, oz2g_reduce_maxima_fn reduce_fn, void* reduce_user, int64_t row_base = 0,
-             int64_t col_base = 0, int slot = 0) {
+             int64_t col_base = 0, int slot = 0, bool reuse_scaling = false) {
     if (prec != OZ2G_FP32 && prec != OZ2G_FP64) throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_gemm: prec must be OZ2G_FP32 or OZ2G_FP64"};
     if (m < 0 || n < 0 || k < 0) throw Fail{OZ2G_INVALID_ARGUMENT, "Matrix: negative dimension"};
     if (lda < k || ldb < n || ldc < n) throw Fail{OZ2G_INVALID_ARGUMENT, "dimension mismatch: leading dimension"};
@@ -495,13 +495,17 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     float* fv = (float*)ws.f.get(4 * (size_t)n);
     int8_t* abar = (int8_t*)ws.abar.get((size_t)(m * kp));
     int8_t* bbar = (int8_t*)ws.bbar.get((size_t)(kp * ldn));
-    if (n) CUDA_TRY(cudaMemsetAsync(bmax, 0, 8 * (size_t)n, stream));
-    if (m) CUDA_TRY(cudaMemsetAsync(cmax_row, 0, 4 * (size_t)m, stream));
-    if (n) CUDA_TRY(cudaMemsetAsync(cmax_col, 0, 4 * (size_t)n, stream));
+    // reuse_scaling (oz2g_gemm_sweep, device pointers): mu', nu' and the
+    // clearance maxima of the previous call on these same inputs are still in
+    // the workspace — they do not depend on N — so K1 / K2 are skipped
+    const bool scan = !reuse_scaling;
+    if (scan && n) CUDA_TRY(cudaMemsetAsync(bmax, 0, 8 * (size_t)n, stream));
+    if (scan && m) CUDA_TRY(cudaMemsetAsync(cmax_row, 0, 4 * (size_t)m, stream));
+    if (scan && n) CUDA_TRY(cudaMemsetAsync(cmax_col, 0, 4 * (size_t)n, stream));
 
     // ---- K1 (B): column pre-exponents and Bbar^T ----
     if (pipe) CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_b, 0));
-    tm.span(1, stream, [&] {
+    if (scan) tm.span(1, stream, [&] {
         CUDA_TRY(launch_col_max_B(prec, dB, ldb_d, k, n, bmax, st, stream)); launches += n > 0;
         CUDA_TRY(launch_col_exp_B(bmax, n, nup, st, stream)); launches += n > 0;
         CUDA_TRY(launch_bbar_rows(prec, dB, ldb_d, k, n, kp, ldn, nup, bbar, st, stream)); launches += n > 0;
@@ -549,7 +553,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     // Pipelined: B is complete before the first chunk, so a chunk's row maxima
     // are final after its clearance GEMM and its mu and A residues follow at
     // once, overlapping the upload of the next chunks.
-    for (int c = 0; c < nchunks; ++c) {
+    for (int c = 0; c < (scan ? nchunks : 0); ++c) {
         const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
         if (pipe) CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_a[c], 0));
         tm.span(1, stream, [&] {
@@ -1109,6 +1113,56 @@ int run_gemm_multi(int prec, int64_t m, int64_t n, int64_t k, const void* A, int
     return OZ2G_OK;
 }
 
+// Several N on the same A, B (the cfg3 sweep): the pre-exponents,
+// Abar / Bbar and the clearance maxima do not depend on N, so they are
+// computed once; each N then runs exponents, residues, residue GEMMs and CRT.
+// C[i] (ldc) receives the result for nmods[i]; every C[i] equals
+// oz2g_gemm(..., nmods[i]) bit for bit.
+int run_gemm_sweep(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
+                   void* const* C, int64_t ldc, const int* nmods, int count, unsigned flags, cudaStream_t stream,
+                   oz2g_diag* diag) {
+    if (count < 1 || !nmods || !C) throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_gemm_sweep: empty moduli list"};
+    if (flags & (OZ2G_ASYNC | OZ2G_TIMING)) throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_gemm_sweep: no async / timing"};
+    if (prec != OZ2G_FP32 && prec != OZ2G_FP64) throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_gemm: prec must be OZ2G_FP32 or OZ2G_FP64"};
+    if (m < 0 || n < 0 || k < 0) throw Fail{OZ2G_INVALID_ARGUMENT, "Matrix: negative dimension"};
+    if (lda < k || ldb < n || ldc < n) throw Fail{OZ2G_INVALID_ARGUMENT, "dimension mismatch: leading dimension"};
+    for (int i = 0; i < count; ++i) (void)table_for(nmods[i], prec);  // every N valid before any work
+    const bool host = (flags & OZ2G_DEVICE_PTRS) == 0;
+    const size_t esz = prec ? 8 : 4;
+    if (diag) std::memset(diag, 0, sizeof *diag);
+    const void* dA = A;
+    const void* dB = B;
+    void* dC = nullptr;
+    int64_t lda_d = lda, ldb_d = ldb, ldc_d = ldc;
+    DevBuf bufA, bufB, bufC;  // sweep-private device copies for host inputs / outputs
+    if (host) {
+        dA = bufA.get(esz * (size_t)(m * k));
+        dB = bufB.get(esz * (size_t)(k * n));
+        dC = bufC.get(esz * (size_t)(m * n));
+        lda_d = k; ldb_d = n; ldc_d = n;
+        if (m * k) CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dA), esz * k, A, esz * lda, esz * k, m, cudaMemcpyHostToDevice, stream));
+        if (k * n) CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dB), esz * n, B, esz * ldb, esz * n, k, cudaMemcpyHostToDevice, stream));
+    }
+    struct Release {
+        DevBuf *a, *b, *c;
+        ~Release() { a->release(); b->release(); c->release(); }
+    } rel{&bufA, &bufB, &bufC};
+    for (int i = 0; i < count; ++i) {
+        void* Ci = host ? dC : C[i];
+        oz2g_diag d;
+        run_gemm(prec, m, n, k, dA, lda_d, dB, ldb_d, Ci, ldc_d, nmods[i], OZ2G_DEVICE_PTRS, stream, nullptr,
+                 diag ? &d : nullptr, nullptr, nullptr, 0, 0, 0, /*reuse_scaling=*/i > 0);
+        if (diag) {
+            diag->subnormal |= d.subnormal;
+            diag->kernels_launched += d.kernels_launched;
+        }
+        if (host && m * n)
+            CUDA_TRY(cudaMemcpy2DAsync(C[i], esz * ldc, dC, esz * n, esz * n, m, cudaMemcpyDeviceToHost, stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    return OZ2G_OK;
+}
+
 template <class F>
 int guarded(F&& f) {
     g_last_error.clear();
@@ -1165,6 +1219,14 @@ int oz2g_gemm_multi(int prec, int64_t m, int64_t n, int64_t k, const void* A, in
                     void* C, int64_t ldc, int nmod, unsigned flags, const int* devices, int count, oz2g_diag* diag) {
     return guarded([&] {
         return run_gemm_multi(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, devices, count, diag);
+    });
+}
+
+int oz2g_gemm_sweep(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
+                    void* const* C, int64_t ldc, const int* nmods, int count, unsigned flags, void* stream,
+                    oz2g_diag* diag) {
+    return guarded([&] {
+        return run_gemm_sweep(prec, m, n, k, A, lda, B, ldb, C, ldc, nmods, count, flags, (cudaStream_t)stream, diag);
     });
 }
 

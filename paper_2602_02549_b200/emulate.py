@@ -296,6 +296,54 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
                            kernels_launched=diag.kernels_launched, stage_ms=tuple(diag.stage_ms), bounds=bres)
 
 
+def os_ii_sweep(a, b, ns, stream=None) -> list:
+    """os_ii(a, b, n).C for every n in `ns` with the scaling scans and the
+    clearance product computed once (they do not depend on N): the N sweep of
+    the paper's experiments (oz2g_gemm_sweep).  Host arrays or CUDA tensors;
+    returns the list of C, each bit-identical to os_ii(a, b, n).C."""
+    L = _lib.load()
+    ns = [int(x) for x in ns]
+    dev = _is_torch_cuda(a)
+    if dev != _is_torch_cuda(b):
+        raise InvalidArgument("os_ii_sweep: A and B must both be host arrays or both CUDA tensors")
+    if dev:
+        import torch
+        if a.dtype != b.dtype or a.dtype not in (torch.float32, torch.float64):
+            raise TypeError("os_ii_sweep: A and B must both be float32 or float64")
+        if a.stride(1) != 1 or b.stride(1) != 1:
+            raise InvalidArgument("os_ii_sweep: unit column stride required (row-major)")
+        prec = F64 if a.dtype == torch.float64 else F32
+        m, k = a.shape
+        nn = b.shape[1]
+        if b.shape[0] != k:
+            raise InvalidArgument("dimension mismatch: os_ii inner dimension")
+        outs = [torch.empty((m, nn), dtype=a.dtype, device=a.device) for _ in ns]
+        pa, pb, lda, ldb = a.data_ptr(), b.data_ptr(), max(a.stride(0), k), max(b.stride(0), nn)
+        ptrs = [o.data_ptr() for o in outs]
+        flags = _lib.OZ2G_DEVICE_PTRS
+        if stream is None:
+            stream = torch.cuda.current_stream(a.device).cuda_stream
+    else:
+        a = np.ascontiguousarray(a)
+        b = np.ascontiguousarray(b)
+        if a.dtype != b.dtype or a.dtype not in (np.float32, np.float64):
+            raise TypeError("os_ii_sweep: A and B must both be float32 or float64")
+        if a.ndim != 2 or b.ndim != 2 or a.shape[1] != b.shape[0]:
+            raise InvalidArgument("dimension mismatch: os_ii inner dimension")
+        prec = F64 if a.dtype == np.float64 else F32
+        m, k = a.shape
+        nn = b.shape[1]
+        outs = [np.empty((m, nn), dtype=a.dtype) for _ in ns]
+        pa, pb, lda, ldb = a.ctypes.data, b.ctypes.data, k, nn
+        ptrs = [o.ctypes.data for o in outs]
+        flags = _lib.OZ2G_HOST_PTRS
+    cp = (C.c_void_p * max(1, len(ptrs)))(*ptrs)
+    cn = (C.c_int * max(1, len(ns)))(*ns)
+    _check(L.oz2g_gemm_sweep(prec, m, nn, k, pa, lda, pb, ldb, cp, nn, cn, len(ns), flags,
+                             C.c_void_p(int(stream) if stream else 0), None))
+    return outs
+
+
 def synchronize() -> None:
     """Complete every blocking=False call on the current device and raise the
     first failure among them in call order (oz2g_synchronize)."""
