@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define OZ2G_API_VERSION 1
+#define OZ2G_API_VERSION 2
 
 /* Status codes (return value of every entry point). */
 #define OZ2G_OK 0
@@ -105,6 +105,9 @@ typedef struct oz2g_diag {
     int kernels_launched;   /* device kernels launched by this call */
     double stage_ms[8];     /* with OZ2G_TIMING: 0 H2D, 1 scale (K1), 2 clearance GEMM, 3 exponents,
                                4 residues, 5 residue GEMMs, 6 CRT + unscale, 7 D2H (ms) */
+    int speculation;        /* pipelined host-pointer calls (speculated column exponents): 0 not used,
+                               1 confirmed, 2 some column tiles recomputed, 3 every stage after the
+                               upload redone; C is the same in every case */
 } oz2g_diag;
 
 /*

@@ -28,7 +28,8 @@ class Bounds(C.Structure):
 
 
 class Diag(C.Structure):
-    _fields_ = [("subnormal", C.c_int), ("kernels_launched", C.c_int), ("stage_ms", C.c_double * 8)]
+    _fields_ = [("subnormal", C.c_int), ("kernels_launched", C.c_int), ("stage_ms", C.c_double * 8),
+                ("speculation", C.c_int)]
 
 
 class TableC(C.Structure):

@@ -85,9 +85,27 @@ constexpr int kTailSplit = 4;
 struct Workspace {
     DevBuf A, B, C, abar, bbar, ares, bres, W, mup, nup, mu, nu, bmax, cmax_row, cmax_col, e, f, status;
     DevBuf x_cbar, x_cprod, x_c1, x_c2, x_q, x_cpp64, x_cpp32, x_ap, x_bp, x_bvec, x_bscr, x_bmax, x_bcheap, x_btight;
+    DevBuf spec_st;  // speculated column exponents: per-stage statuses
+    // changed-tile flags of the speculation checks: mapped pinned host memory
+    // written by the check kernel, read by the host after an event
+    int32_t* spec_changed = nullptr;
+    size_t spec_changed_cap = 0;
+    cudaEvent_t ev_check = nullptr;
+    int32_t* changed_flags(size_t count) {
+        if (count > spec_changed_cap) {
+            if (spec_changed) cudaFreeHost(spec_changed);
+            spec_changed = nullptr;
+            spec_changed_cap = 0;
+            CUDA_TRY(cudaHostAlloc((void**)&spec_changed, 4 * count, cudaHostAllocMapped));
+            spec_changed_cap = count;
+        }
+        if (!ev_check) CUDA_TRY(cudaEventCreateWithFlags(&ev_check, cudaEventDisableTiming));
+        return spec_changed;
+    }
     std::map<std::pair<int, int>, ResidConsts*> rc;  // device copies of residue constants
     int num_sms = 0;
-    std::mutex mtx;                     // calls on one workspace are serialised
+    std::recursive_mutex mtx;           // calls on one workspace are serialised (re-entered by the
+                                        // speculation fallback of run_gemm)
     cudaStream_t s_main = nullptr;      // compute stream of oz2g_gemm_multi tiles
     // copy streams / events of the pipelined host-pointer path
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr, s_aux = nullptr;
@@ -123,8 +141,11 @@ struct Workspace {
     void release() {
         for (DevBuf* b : {&A, &B, &C, &abar, &bbar, &ares, &bres, &W, &mup, &nup, &mu, &nu, &bmax, &cmax_row,
                           &cmax_col, &e, &f, &status, &x_cbar, &x_cprod, &x_c1, &x_c2, &x_q, &x_cpp64, &x_cpp32,
-                          &x_ap, &x_bp, &x_bvec, &x_bscr, &x_bmax, &x_bcheap, &x_btight, &status_ring})
+                          &x_ap, &x_bp, &x_bvec, &x_bscr, &x_bmax, &x_bcheap, &x_btight, &status_ring, &spec_st})
             b->release();
+        if (spec_changed) cudaFreeHost(spec_changed);
+        spec_changed = nullptr;
+        spec_changed_cap = 0;
         for (auto& kv : rc) cudaFree(kv.second);
         rc.clear();
     }
@@ -274,6 +295,13 @@ int crt_overlap_blocks() {
     return v;
 }
 
+// Speculative column exponents on the pipelined host path (run_gemm);
+// OZ2G_SPEC=0 turns them off (read per call).
+bool speculation_enabled() {
+    const char* s = std::getenv("OZ2G_SPEC");
+    return !(s && s[0] == '0');
+}
+
 // Raster group height: one wave of persistent CTAs covers group_m tile-rows,
 // so B tiles are streamed from HBM about tiles_m / group_m times per plane.
 // OZ2G_GROUP_N > 0 groups tile-columns instead (returned negated).
@@ -409,7 +437,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     int dev = 0;
     CUDA_TRY(cudaGetDevice(&dev));
     Workspace& ws = workspace(dev, slot);
-    std::lock_guard<std::mutex> dev_lock(ws.mtx);
+    std::lock_guard<std::recursive_mutex> dev_lock(ws.mtx);
     int launches = 0;
     if (!async && !ws.pending.empty()) {  // a blocking call completes earlier async calls first
         Fail f{OZ2G_OK, ""};
@@ -549,70 +577,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     int8_t* ares = (int8_t*)ws.ares.get((size_t)N * (size_t)(m * kp));
     int8_t* bres = (int8_t*)ws.bres.get((size_t)N * (size_t)(kp * ldn));
 
-    // ---- K1 (A) + K2 per row chunk: row pre-exponents, Abar, clearance product with fused maxima ----
-    // Pipelined: B is complete before the first chunk, so a chunk's row maxima
-    // are final after its clearance GEMM and its mu and A residues follow at
-    // once, overlapping the upload of the next chunks.
-    for (int c = 0; c < (scan ? nchunks : 0); ++c) {
-        const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
-        if (pipe) CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_a[c], 0));
-        tm.span(1, stream, [&] {
-            CUDA_TRY(launch_row_scan_A(prec, (const char*)dA + esz * (size_t)(r0 * lda_d), lda_d, rc, k, kp,
-                                       mup + r0, abar + r0 * kp, st, stream, r0));
-        });
-        launches += rc > 0;
-        if (rc > 0 && n > 0) tm.span(2, stream, [&] {
-            const CUtensorMap tA = make_plane_map(abar + r0 * kp, kp, rc, 1, boxA);
-            const CUtensorMap tB = make_plane_map_mn(bbar, n, ldn, kp, 1, kp * ldn);
-            set_rows(gp, rc);
-            gp.planes = 1;
-            gp.rowmax = cmax_row + r0;
-            gp.colmax = cmax_col;
-            CUDA_TRY(launch_gemm(EPI_MAX, tA, tB, gp)); ++launches;
-            if (inter && inter->Cbar) {
-                GemmParams g2 = gp;
-                g2.C32 = (int32_t*)ws.x_cbar.get(4 * (size_t)(m * n));
-                g2.ldc32 = n;
-                g2.cplane = m * n;
-                CUDA_TRY(launch_gemm(EPI_I32, tA, tB, g2)); ++launches;
-            }
-        });
-        if (pipe && rc > 0) {
-            tm.span(3, stream, [&] {
-                CUDA_TRY(launch_exponents(cmax_row + r0, rc, cmax_col, 0, mup + r0, nup, tab.shift0, tab.nthr,
-                                          tab.thr, mu + r0, nu, ev + r0, fv, st, stream));
-            });
-            tm.span(4, stream, [&] {
-                CUDA_TRY(launch_resid_A(prec, (const char*)dA + esz * (size_t)(r0 * lda_d), lda_d, rc, k, kp,
-                                        mu + r0, rc_dev, N, ares + r0 * kp, m * kp, st, stream));
-            });
-            launches += 2;
-        }
-    }
-    if (reduce_fn) {
-        if (reduce_fn(cmax_row, m, cmax_col, n, (void*)stream, reduce_user) != 0)
-        {
-            Fail f{OZ2G_CUDA_ERROR, "oz2g_gemm: reduce_maxima callback failed"};
-            f.order = 201;  // a peer's own failure (multi-device) is the one to report
-            throw f;
-        }
-    }
-
-    // ---- K3: scaling exponents; K4: residue planes ----
-    // (pipelined: row exponents and A residues were produced per chunk during the upload)
-    tm.span(3, stream, [&] {
-        CUDA_TRY(launch_exponents(cmax_row, pipe ? 0 : m, cmax_col, n, mup, nup, tab.shift0, tab.nthr, tab.thr, mu,
-                                  nu, ev, fv, st, stream));
-    });
-    ++launches;
-    tm.span(4, stream, [&] {
-        if (!pipe) {
-            CUDA_TRY(launch_resid_A(prec, dA, lda_d, m, k, kp, mu, rc_dev, N, ares, 0, st, stream)); launches += m > 0;
-        }
-        CUDA_TRY(launch_resid_B_rows(prec, dB, ldb_d, k, n, kp, ldn, nu, rc_dev, N, bres, st, stream)); launches += n > 0;
-    });
-
-    // ---- K6: CRT + inverse scaling ----
+    // ---- CRT constants, W and the row blocks of C (host-side set-up) ----
     CrtConsts cc;
     std::memset(&cc, 0, sizeof cc);
     cc.n = N;
@@ -631,39 +596,11 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         if (inter->Cpp64) ex.Cpp64 = (double*)ws.x_cpp64.get(mn8);
         if (inter->Cpp32 && prec == OZ2G_FP32) ex.Cpp32 = (float*)ws.x_cpp32.get(mn8 / 2);
     }
-    if (bo && m * n) {
-        // bounds.hpp:143-206 evaluated in the CRT pass
-        const BoundScalars bs = bound_scalars(tab, k);
-        double* vec = (double*)ws.x_bvec.get(8 * (size_t)(2 * (m + n)) + 4 * (size_t)(m + n) + 16);
-        BoundVecs v;
-        v.RA = vec; v.PA = vec + m; v.CB = vec + 2 * m; v.PB = vec + 2 * m + n;
-        v.ea = reinterpret_cast<int32_t*>(vec + 2 * (m + n));
-        v.eb = v.ea + m;
-        double* scratch = (double*)ws.x_bscr.get(8 * bound_scratch_doubles(m, n, k));
-        CUDA_TRY(launch_bound_vectors(prec, dA, lda_d, m, dB, ldb_d, k, n, cmax_row, cmax_col, mup, nup, bs.t_up,
-                                      scratch, v, stream));
-        launches += 5;
-        bmax_dev = (unsigned long long*)ws.x_bmax.get(16);
-        CUDA_TRY(cudaMemsetAsync(bmax_dev, 0, 16, stream));
-        ex.bnd.on = 1;
-        ex.bnd.v = v;
-        ex.bnd.t2_up = bs.t2_up;
-        ex.bnd.rconst_up = bs.rconst_up;
-        ex.bnd.ucoef = bs.ucoef;
-        ex.bnd.kpr_cheap_up = bs.kpr_cheap_up;
-        ex.bnd.k_rconst_up = bs.k_rconst_up;
-        ex.bnd.max_bits = bmax_dev;
-        if (bo->cheap) ex.bnd.cheap = bo->device ? bo->cheap : (double*)ws.x_bcheap.get(mn8);
-        if (bo->tight) ex.bnd.tight = bo->device ? bo->tight : (double*)ws.x_btight.get(mn8);
-    }
-    // every read of the device copies of A and B is enqueued by now
-    if (host && ws.ev_inputs_free) CUDA_TRY(cudaEventRecord(ws.ev_inputs_free, stream));
-    // ---- K5 + K6 per row block of C: residue GEMMs (fused signed mod p), CRT + unscale ----
     const int ovb = crt_overlap_blocks();
     const bool overlap = ovb > 1 && !inter_mats && m >= 2048;
     if (overlap) ws.ensure_streams();
     // W holds one row block (all N planes) unless every plane of the whole
-    // matrix is wanted (intermediates) or blocks overlap (side-stream CRT)
+    // matrix is wanted (intermediates) or blocks overlap (side-stream CRT).
     // W per block only when the whole-matrix W would be large (more launches
     // cost more than the memory saves on mid-size problems)
     static const int64_t w_block_min = [] {
@@ -674,42 +611,79 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     const int64_t wrows = w_full ? m : std::min<int64_t>(m, kWBlockRows);
     int8_t* W = (int8_t*)ws.W.get((size_t)N * (size_t)(wrows * ldw));
     fill_gemm_moduli(gp, tab);
-    gp.planes = N;
-    gp.ldw = ldw;
-    gp.wplane = wrows * ldw;
-    const CUtensorMap tBres = make_plane_map_mn(bres, n, ldn, kp, N, kp * ldn);
-    std::vector<std::pair<int64_t, int64_t>> blocks;  // (first row, rows) of C per GEMM + CRT launch
-    auto split = [&](int64_t r0, int64_t rc, int64_t sub) {
-        for (int64_t q = r0; q < r0 + rc; q += sub) blocks.emplace_back(q, std::min<int64_t>(sub, r0 + rc - q));
-    };
+    struct Block { int64_t r0, rows; int chunk; };
+    std::vector<Block> blocks;  // row blocks of C, one residue-GEMM + CRT launch each
     const int64_t max_block = w_full ? (overlap ? round_up((m + ovb - 1) / ovb, 128) : m) : kWBlockRows;
     for (int c = 0; c < nchunks; ++c) {
         const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
         if (rc <= 0) continue;
-        if (pipe && c == nchunks - 1 && rc >= 2 * 128)
-            split(r0, rc, std::min<int64_t>(max_block, round_up((rc + kTailSplit - 1) / kTailSplit, 128)));
-        else
-            split(r0, rc, max_block);
+        const int64_t sub = (pipe && c == nchunks - 1 && rc >= 2 * 128)
+                                ? std::min<int64_t>(max_block, round_up((rc + kTailSplit - 1) / kTailSplit, 128))
+                                : max_block;
+        for (int64_t q = r0; q < r0 + rc; q += sub) blocks.push_back({q, std::min<int64_t>(sub, r0 + rc - q), c});
     }
-    for (size_t bi = 0; bi < blocks.size(); ++bi) {
-        const int64_t r0 = blocks[bi].first, rc = blocks[bi].second;
-        if (n <= 0) continue;
+    const CUtensorMap tBres = make_plane_map_mn(bres, n, ldn, kp, N, kp * ldn);
+
+    // Speculative column exponents (blocking host-pointer calls).  nu_j needs
+    // the clearance maxima of column j over every row of A, i.e. the whole
+    // upload, and every residue GEMM needs the B residues, which need nu.  nu
+    // is a step function of those maxima (thresholds 4x apart), so it is taken
+    // from the maxima of the first uploaded row chunk, and the B residues and
+    // the residue GEMMs + CRT of each chunk run while the rest of A is still
+    // uploading.  After every later chunk's clearance product the exponents
+    // are re-derived from the maxima so far; where one moved, the B residues
+    // are recomputed and the 256-column tiles holding moved columns are redone
+    // for every block already computed.  After the last chunk nu is final, so C
+    // is the unspeculated C bit for bit.  Status flags of the stages that read
+    // nu (B residues, CRT) are kept per stage / block so that flags raised with
+    // a superseded nu are dropped; a repaired block whose first CRT raised any
+    // flag makes the call redo every stage after the upload unspeculated.
+    const bool spec = pipe && !async && scan && !overlap && n > 0 && speculation_enabled();
+    const size_t nb = blocks.size();
+    const int64_t ntiles = (n + 255) / 256;
+    DevStatus* sx = nullptr;       // [0] discarded, [1] B residues, [2 + b] CRT of block b, [2 + nb + b] its repairs
+    int32_t* changed_h = nullptr;  // [0] any column moved, [1 + t] a column of tile t moved (host view)
+    int32_t* changed = nullptr;    // its device alias
+    std::vector<char> repaired;
+    int spec_state = spec ? 1 : 0;
+    if (spec) {
+        ws.ensure_streams();
+        sx = (DevStatus*)ws.spec_st.get(sizeof(DevStatus) * (2 + 2 * nb));
+        CUDA_TRY(cudaMemsetAsync(sx, 0, sizeof(DevStatus) * (2 + 2 * nb), stream));
+        changed_h = ws.changed_flags((size_t)(1 + ntiles));
+        CUDA_TRY(cudaHostGetDevicePointer((void**)&changed, changed_h, 0));
+        repaired.assign(nb, 0);
+    }
+    size_t evn = 0;  // per-call event index (downloads wait for their CRT)
+
+    // ---- K5 + K6 of one row block of C (columns c0 .. c0 + nc): residue GEMMs
+    //      (fused signed mod p), CRT + unscale, download ----
+    auto run_block = [&](size_t bi, int64_t c0, int64_t nc, DevStatus* sb) {
+        const int64_t r0 = blocks[bi].r0, rc = blocks[bi].rows;
+        if (nc <= 0) return;
+        GemmParams g = gp;
+        g.planes = N;
+        g.ldw = ldw;
+        g.wplane = wrows * ldw;
+        g.n = (int)nc;
+        g.tiles_n = (int)((nc + BN - 1) / BN);
         const CUtensorMap tA = make_plane_map(ares + r0 * kp, kp, rc, N, boxA, m * kp);
-        int8_t* Wb = w_full ? W + r0 * ldw : W;
-        set_rows(gp, rc);
-        gp.W = Wb;
-        tm.span(5, stream, [&] { CUDA_TRY(launch_gemm(EPI_RESID, tA, tBres, gp)); });
+        const CUtensorMap tB = (c0 == 0 && nc == n) ? tBres : make_plane_map_mn(bres + c0, nc, ldn, kp, N, kp * ldn);
+        int8_t* Wb = (w_full ? W + r0 * ldw : W) + c0;
+        set_rows(g, rc);
+        g.W = Wb;
+        tm.span(5, stream, [&] { CUDA_TRY(launch_gemm(EPI_RESID, tA, tB, g)); });
         ++launches;
         if (inter && inter->Cprod) {  // rows of this block of the m x n planes
-            GemmParams g2 = gp;
+            GemmParams g2 = g;
             g2.C32 = (int32_t*)ws.x_cprod.get(4 * (size_t)N * (size_t)(m * n)) + r0 * n;
             g2.ldc32 = n;
             g2.cplane = m * n;
-            CUDA_TRY(launch_gemm(EPI_I32, tA, tBres, g2)); ++launches;
+            CUDA_TRY(launch_gemm(EPI_I32, tA, tB, g2)); ++launches;
         }
         cudaStream_t crt_stream = stream;
         if (overlap) {  // this block's CRT beside the next block's GEMM
-            const cudaEvent_t eg = ws.pool_event(2 * bi);
+            const cudaEvent_t eg = ws.pool_event(evn++);
             CUDA_TRY(cudaEventRecord(eg, stream));
             CUDA_TRY(cudaStreamWaitEvent(ws.s_aux, eg, 0));
             crt_stream = ws.s_aux;
@@ -731,23 +705,160 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             if (exb.bnd.tight) exb.bnd.tight += eo;
         }
         tm.span(6, crt_stream, [&] {
-            CUDA_TRY(launch_crt(prec, Wb, ldw, wrows * ldw, rc, n, cc, mu + r0, nu,
-                                (char*)dC + esz * (size_t)(r0 * ldc_d), ldc_d, exb, st, crt_stream));
+            CUDA_TRY(launch_crt(prec, Wb, ldw, wrows * ldw, rc, nc, cc, mu + r0, nu + c0,
+                                (char*)dC + esz * (size_t)(r0 * ldc_d + c0), ldc_d, exb, sb, crt_stream));
         });
         ++launches;
         if (pipe) {  // download this C block while the next one computes
-            const cudaEvent_t ec = ws.pool_event(2 * bi + 1);
+            const cudaEvent_t ec = ws.pool_event(evn++);
             CUDA_TRY(cudaEventRecord(ec, crt_stream));
             CUDA_TRY(cudaStreamWaitEvent(ws.s_d2h, ec, 0));
             tm.span(7, ws.s_d2h, [&] {
-                CUDA_TRY(cudaMemcpy2DAsync((char*)C + esz * (size_t)(r0 * ldc), esz * ldc,
-                                           (const char*)dC + esz * (size_t)(r0 * n), esz * n, esz * n, rc,
+                CUDA_TRY(cudaMemcpy2DAsync((char*)C + esz * (size_t)(r0 * ldc + c0), esz * ldc,
+                                           (const char*)dC + esz * (size_t)(r0 * n + c0), esz * n, esz * nc, rc,
                                            cudaMemcpyDeviceToHost, ws.s_d2h));
             });
         }
+    };
+
+    // ---- K1 (A) + K2 per row chunk: row pre-exponents, Abar, clearance product with fused maxima ----
+    // Pipelined: B is complete before the first chunk, so a chunk's row maxima
+    // are final after its clearance GEMM and its mu and A residues follow at
+    // once, overlapping the upload of the next chunks.
+    size_t next_block = 0;
+    for (int c = 0; c < (scan ? nchunks : 0); ++c) {
+        const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
+        if (pipe) CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_a[c], 0));
+        tm.span(1, stream, [&] {
+            CUDA_TRY(launch_row_scan_A(prec, (const char*)dA + esz * (size_t)(r0 * lda_d), lda_d, rc, k, kp,
+                                       mup + r0, abar + r0 * kp, st, stream, r0));
+        });
+        launches += rc > 0;
+        if (rc > 0 && n > 0) tm.span(2, stream, [&] {
+            const CUtensorMap tA = make_plane_map(abar + r0 * kp, kp, rc, 1, boxA);
+            const CUtensorMap tB = make_plane_map_mn(bbar, n, ldn, kp, 1, kp * ldn);
+            GemmParams g = gp;
+            set_rows(g, rc);
+            g.planes = 1;
+            g.rowmax = cmax_row + r0;
+            g.colmax = cmax_col;
+            CUDA_TRY(launch_gemm(EPI_MAX, tA, tB, g)); ++launches;
+            if (inter && inter->Cbar) {
+                GemmParams g2 = g;
+                g2.C32 = (int32_t*)ws.x_cbar.get(4 * (size_t)(m * n));
+                g2.ldc32 = n;
+                g2.cplane = m * n;
+                CUDA_TRY(launch_gemm(EPI_I32, tA, tB, g2)); ++launches;
+            }
+        });
+        if (pipe && rc > 0) {
+            tm.span(3, stream, [&] {
+                CUDA_TRY(launch_exponents(cmax_row + r0, rc, cmax_col, 0, mup + r0, nup, tab.shift0, tab.nthr,
+                                          tab.thr, mu + r0, nu, ev + r0, fv, st, stream));
+                if (spec) {  // column exponents from the maxima so far (final after the last chunk)
+                    if (c > 0) std::memset(changed_h, 0, 4 * (size_t)(1 + ntiles));  // idle: last check was read
+                    CUDA_TRY(launch_exponents(cmax_row, 0, cmax_col, n, mup, nup, tab.shift0, tab.nthr, tab.thr, mu,
+                                              nu, ev, fv, c == nchunks - 1 ? st : sx, stream,
+                                              c > 0 ? changed : nullptr));
+                    ++launches;
+                }
+            });
+            tm.span(4, stream, [&] {
+                CUDA_TRY(launch_resid_A(prec, (const char*)dA + esz * (size_t)(r0 * lda_d), lda_d, rc, k, kp,
+                                        mu + r0, rc_dev, N, ares + r0 * kp, m * kp, st, stream));
+            });
+            launches += 2;
+        }
+        if (spec) {
+            bool moved = c == 0;
+            if (c > 0) {
+                CUDA_TRY(cudaEventRecord(ws.ev_check, stream));
+                CUDA_TRY(cudaEventSynchronize(ws.ev_check));
+                moved = ((volatile int32_t*)changed_h)[0] != 0;
+            }
+            if (moved) {
+                tm.span(4, stream, [&] {
+                    CUDA_TRY(cudaMemsetAsync(sx + 1, 0, sizeof(DevStatus), stream));
+                    CUDA_TRY(launch_resid_B_rows(prec, dB, ldb_d, k, n, kp, ldn, nu, rc_dev, N, bres, sx + 1, stream));
+                });
+                ++launches;
+            }
+            if (c > 0 && moved) {  // redo the moved column tiles of every block computed so far
+                spec_state = 2;
+                for (size_t bi = 0; bi < next_block; ++bi) {
+                    repaired[bi] = 1;
+                    for (int64_t t = 0; t < ntiles;) {
+                        if (!((volatile int32_t*)changed_h)[1 + t]) { ++t; continue; }
+                        int64_t t1 = t + 1;
+                        while (t1 < ntiles && ((volatile int32_t*)changed_h)[1 + t1]) ++t1;
+                        run_block(bi, 256 * t, std::min<int64_t>(n, 256 * t1) - 256 * t, sx + 2 + nb + bi);
+                        t = t1;
+                    }
+                }
+            }
+            for (; next_block < nb && blocks[next_block].chunk <= c; ++next_block)
+                run_block(next_block, 0, n, sx + 2 + next_block);
+        }
+    }
+    if (reduce_fn) {
+        if (reduce_fn(cmax_row, m, cmax_col, n, (void*)stream, reduce_user) != 0)
+        {
+            Fail f{OZ2G_CUDA_ERROR, "oz2g_gemm: reduce_maxima callback failed"};
+            f.order = 201;  // a peer's own failure (multi-device) is the one to report
+            throw f;
+        }
+    }
+
+    if (spec) {
+        if (ws.ev_inputs_free) CUDA_TRY(cudaEventRecord(ws.ev_inputs_free, stream));
+    } else {
+        // ---- K3: scaling exponents; K4: residue planes ----
+        // (pipelined: row exponents and A residues were produced per chunk during the upload)
+        tm.span(3, stream, [&] {
+            CUDA_TRY(launch_exponents(cmax_row, pipe ? 0 : m, cmax_col, n, mup, nup, tab.shift0, tab.nthr, tab.thr,
+                                      mu, nu, ev, fv, st, stream));
+        });
+        ++launches;
+        tm.span(4, stream, [&] {
+            if (!pipe) {
+                CUDA_TRY(launch_resid_A(prec, dA, lda_d, m, k, kp, mu, rc_dev, N, ares, 0, st, stream));
+                launches += m > 0;
+            }
+            CUDA_TRY(launch_resid_B_rows(prec, dB, ldb_d, k, n, kp, ldn, nu, rc_dev, N, bres, st, stream));
+            launches += n > 0;
+        });
+
+        if (bo && m * n) {
+            // bounds.hpp:143-206 evaluated in the CRT pass
+            const BoundScalars bs = bound_scalars(tab, k);
+            double* vec = (double*)ws.x_bvec.get(8 * (size_t)(2 * (m + n)) + 4 * (size_t)(m + n) + 16);
+            BoundVecs v;
+            v.RA = vec; v.PA = vec + m; v.CB = vec + 2 * m; v.PB = vec + 2 * m + n;
+            v.ea = reinterpret_cast<int32_t*>(vec + 2 * (m + n));
+            v.eb = v.ea + m;
+            double* scratch = (double*)ws.x_bscr.get(8 * bound_scratch_doubles(m, n, k));
+            CUDA_TRY(launch_bound_vectors(prec, dA, lda_d, m, dB, ldb_d, k, n, cmax_row, cmax_col, mup, nup, bs.t_up,
+                                          scratch, v, stream));
+            launches += 5;
+            bmax_dev = (unsigned long long*)ws.x_bmax.get(16);
+            CUDA_TRY(cudaMemsetAsync(bmax_dev, 0, 16, stream));
+            ex.bnd.on = 1;
+            ex.bnd.v = v;
+            ex.bnd.t2_up = bs.t2_up;
+            ex.bnd.rconst_up = bs.rconst_up;
+            ex.bnd.ucoef = bs.ucoef;
+            ex.bnd.kpr_cheap_up = bs.kpr_cheap_up;
+            ex.bnd.k_rconst_up = bs.k_rconst_up;
+            ex.bnd.max_bits = bmax_dev;
+            if (bo->cheap) ex.bnd.cheap = bo->device ? bo->cheap : (double*)ws.x_bcheap.get(mn8);
+            if (bo->tight) ex.bnd.tight = bo->device ? bo->tight : (double*)ws.x_btight.get(mn8);
+        }
+        // every read of the device copies of A and B is enqueued by now
+        if (host && ws.ev_inputs_free) CUDA_TRY(cudaEventRecord(ws.ev_inputs_free, stream));
+        for (size_t bi = 0; bi < nb; ++bi) run_block(bi, 0, n, st);
     }
     if (overlap) {  // join the side stream
-        const cudaEvent_t ej = ws.pool_event(2 * blocks.size());
+        const cudaEvent_t ej = ws.pool_event(evn++);
         CUDA_TRY(cudaEventRecord(ej, ws.s_aux));
         CUDA_TRY(cudaStreamWaitEvent(stream, ej, 0));
     }
@@ -829,6 +940,35 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     CUDA_TRY(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, stream));
     CUDA_TRY(cudaStreamSynchronize(stream));
     CUDA_TRY(cudaGetLastError());
+    if (spec) {
+        std::vector<DevStatus> hx(2 + 2 * nb);
+        CUDA_TRY(cudaMemcpy(hx.data(), sx, sizeof(DevStatus) * hx.size(), cudaMemcpyDeviceToHost));
+        bool redo = false;
+        for (size_t bi = 0; bi < nb; ++bi)
+            redo |= repaired[bi] && (hx[2 + bi].err || hx[2 + bi].subnormal);
+        if (redo) {
+            // a block computed with a superseded nu raised a flag that may not
+            // hold for the final nu: redo every stage after the upload from the
+            // device copies of A and B (the unspeculated device path, which also
+            // reports this call's errors) and download C again
+            const int outer = launches;
+            run_gemm(prec, m, n, k, dA, lda_d, dB, ldb_d, dC, ldc_d, nmod, OZ2G_DEVICE_PTRS | (flags & OZ2G_TIMING),
+                     stream, inter, diag, nullptr, nullptr, row_base, col_base, slot, false);
+            if (m * n)
+                CUDA_TRY(cudaMemcpy2DAsync(C, esz * ldc, dC, esz * n, esz * n, m, cudaMemcpyDeviceToHost, stream));
+            CUDA_TRY(cudaStreamSynchronize(stream));
+            if (diag) {
+                diag->kernels_launched += outer;
+                diag->speculation = 3;
+            }
+            return OZ2G_OK;
+        }
+        // flags of the B residues (last run, final nu) and of every CRT
+        for (size_t i = 1; i < hx.size(); ++i) {
+            hs.err |= hx[i].err;
+            hs.subnormal |= hx[i].subnormal;
+        }
+    }
     if (bo) {
         double v0, v1;
         std::memcpy(&v0, &bmax_host[0], 8);
@@ -843,6 +983,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     if (diag) {
         diag->subnormal = hs.subnormal ? 1 : 0;
         diag->kernels_launched = launches;
+        diag->speculation = spec_state;
         if (tm.on) {
             // stage order: 0 H2D, 1 K1 scale, 2 clearance GEMM, 3 exponents, 4 residues,
             //              5 residue GEMMs, 6 CRT, 7 D2H
@@ -874,7 +1015,7 @@ int run_suggest_n(int prec, int64_t m, int64_t n, int64_t k, const void* A, int6
     int dev = 0;
     CUDA_TRY(cudaGetDevice(&dev));
     Workspace& ws = workspace(dev);
-    std::lock_guard<std::mutex> dev_lock(ws.mtx);
+    std::lock_guard<std::recursive_mutex> dev_lock(ws.mtx);
     if (!ws.pending.empty()) {  // complete earlier OZ2G_ASYNC calls (they may still read ws.A / ws.B)
         Fail f{OZ2G_OK, ""};
         if (complete_pending(ws, f)) throw f;
@@ -1074,7 +1215,7 @@ int run_gemm_multi(int prec, int64_t m, int64_t n, int64_t k, const void* A, int
             CUDA_TRY(cudaSetDevice(devices[t]));
             Workspace& ws = workspace(devices[t], t);
             {
-                std::lock_guard<std::mutex> lk(ws.mtx);
+                std::lock_guard<std::recursive_mutex> lk(ws.mtx);
                 ws.ensure_streams();
             }
             run_gemm(prec, r1 - r0, c1 - c0, k, (const char*)A + esz * (size_t)(r0 * lda), lda,
@@ -1244,7 +1385,7 @@ int oz2g_init(const int* devices, int count) {
         for (int t = 0; t < count; ++t) {
             CUDA_TRY(cudaSetDevice(devices[t]));
             Workspace& ws = workspace(devices[t], 0);
-            std::lock_guard<std::mutex> lk(ws.mtx);
+            std::lock_guard<std::recursive_mutex> lk(ws.mtx);
             ws.ensure_streams();
             for (int mode : {OZ2G_FP32, OZ2G_FP64})
                 for (int nm = 2; nm <= 49; ++nm) {
@@ -1268,7 +1409,7 @@ int oz2g_synchronize(void) {
         int dev = 0;
         CUDA_TRY(cudaGetDevice(&dev));
         Workspace& ws = workspace(dev, 0);
-        std::lock_guard<std::mutex> lk(ws.mtx);
+        std::lock_guard<std::recursive_mutex> lk(ws.mtx);
         Fail f{OZ2G_OK, ""};
         if (complete_pending(ws, f)) throw f;
         return OZ2G_OK;
@@ -1353,7 +1494,7 @@ void oz2g_release_workspace(void) {
     std::lock_guard<std::mutex> lk(g_ws_mtx);
     for (auto& kv : g_ws)
         if (kv.first / 256 == dev) {
-            std::lock_guard<std::mutex> wl(kv.second->mtx);
+            std::lock_guard<std::recursive_mutex> wl(kv.second->mtx);
             for (const auto& p : kv.second->pending) cudaStreamSynchronize(p.stream);
             kv.second->pending.clear();
             kv.second->release();

@@ -72,7 +72,7 @@ cudaError_t launch_bbar_rows(int prec, const void* B, int64_t ldb, int64_t k, in
 cudaError_t launch_exponents(const int32_t* cmax_row, int64_t m, const int32_t* cmax_col, int64_t n,
                              const int32_t* mu_prime, const int32_t* nu_prime, int shift0, int nthr,
                              const int32_t* thr, int32_t* mu, int32_t* nu, float* e, float* f, DevStatus* st,
-                             cudaStream_t s);
+                             cudaStream_t s, int32_t* changed = nullptr);
 // plane_stride: bytes between residue planes (0 = m * kp); a row block of the
 // planes is written by passing the block's A / mu / planes offsets.
 cudaError_t launch_resid_A(int prec, const void* A, int64_t lda, int64_t m, int64_t k, int64_t kp,

@@ -206,7 +206,8 @@ __global__ void exponents_kernel(const int32_t* __restrict__ cmax_row, int64_t m
                                  const int32_t* __restrict__ cmax_col, int64_t n,
                                  const int32_t* __restrict__ mu_prime, const int32_t* __restrict__ nu_prime,
                                  const ThrTable tt, int32_t* __restrict__ mu, int32_t* __restrict__ nu,
-                                 float* __restrict__ e, float* __restrict__ f, DevStatus* st) {
+                                 float* __restrict__ e, float* __restrict__ f, DevStatus* st,
+                                 int32_t* __restrict__ changed) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= m + n) return;
     const bool is_row = t < m;
@@ -224,7 +225,16 @@ __global__ void exponents_kernel(const int32_t* __restrict__ cmax_row, int64_t m
     const int v = base + shift;
     if (v < -32768 || v > 32767) flag(st, is_row ? ERR_MU_RANGE : ERR_NU_RANGE);
     if (is_row) { mu[idx] = v; if (e) e[idx] = ev; }
-    else { nu[idx] = v; if (f) f[idx] = ev; }
+    else {
+        // changed != null: nu holds exponents speculated from partial column
+        // maxima; flag every 256-column tile in which one of them moves
+        if (changed && nu[idx] != v) {
+            changed[0] = 1;
+            changed[1 + (idx >> 8)] = 1;
+        }
+        nu[idx] = v;
+        if (f) f[idx] = ev;
+    }
 }
 
 template <class T>
@@ -290,14 +300,14 @@ cudaError_t launch_col_exp_B(const unsigned long long* bmax, int64_t n, int32_t*
 cudaError_t launch_exponents(const int32_t* cmax_row, int64_t m, const int32_t* cmax_col, int64_t n,
                              const int32_t* mu_prime, const int32_t* nu_prime, int shift0, int nthr,
                              const int32_t* thr, int32_t* mu, int32_t* nu, float* e, float* f, DevStatus* st,
-                             cudaStream_t s) {
+                             cudaStream_t s, int32_t* changed) {
     if (m + n == 0) return cudaSuccess;
     ThrTable tt;
     tt.shift0 = shift0;
     tt.nthr = nthr;
     for (int q = 0; q < 64; ++q) tt.thr[q] = q < nthr ? thr[q] : 0;
     exponents_kernel<<<blocks_for(m + n, 256), 256, 0, s>>>(cmax_row, m, cmax_col, n, mu_prime, nu_prime, tt, mu,
-                                                            nu, e, f, st);
+                                                            nu, e, f, st, changed);
     return cudaGetLastError();
 }
 

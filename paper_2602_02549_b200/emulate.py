@@ -131,6 +131,7 @@ class EmulationResult:
     kernels_launched: int = 0
     stage_ms: tuple = ()
     bounds: Optional[dict] = None
+    speculation: int = 0  # 0 none, 1 speculated column exponents confirmed, 2 missed and redone
 
 
 def _is_torch_cuda(x) -> bool:
@@ -293,7 +294,8 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
     if bnd_c is not None:
         bres = dict(cheap_max=bnd_c.cheap_max, tight_max=bnd_c.tight_max, **bnd_arrays)
     return EmulationResult(C=C_out, scaling=sc, crt=cr, table=table_for(n, prec), subnormal=bool(diag.subnormal),
-                           kernels_launched=diag.kernels_launched, stage_ms=tuple(diag.stage_ms), bounds=bres)
+                           kernels_launched=diag.kernels_launched, stage_ms=tuple(diag.stage_ms), bounds=bres,
+                           speculation=diag.speculation)
 
 
 def os_ii_sweep(a, b, ns, stream=None) -> list:
