@@ -125,7 +125,7 @@ struct Workspace {
         return ev_pool[i];
     }
     cudaEvent_t ev_start = nullptr, ev_b = nullptr, ev_done = nullptr;
-    cudaEvent_t ev_a[kPipeChunks] = {}, ev_c[kPipeChunks + kTailSplit] = {};
+    cudaEvent_t ev_a[kPipeChunks] = {}, ev_bc[kPipeChunks + 1] = {}, ev_c[kPipeChunks + kTailSplit] = {};
     void ensure_streams() {
         if (s_h2d) return;
         CUDA_TRY(cudaStreamCreateWithFlags(&s_main, cudaStreamNonBlocking));
@@ -134,7 +134,11 @@ struct Workspace {
         CUDA_TRY(cudaStreamCreateWithFlags(&s_aux, cudaStreamNonBlocking));
         for (cudaEvent_t* e : {&ev_start, &ev_b, &ev_done, &ev_inputs_free})
             CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-        for (int c = 0; c < kPipeChunks; ++c) CUDA_TRY(cudaEventCreateWithFlags(&ev_a[c], cudaEventDisableTiming));
+        for (int c = 0; c < kPipeChunks; ++c) {
+            CUDA_TRY(cudaEventCreateWithFlags(&ev_a[c], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&ev_bc[c], cudaEventDisableTiming));
+        }
+        CUDA_TRY(cudaEventCreateWithFlags(&ev_bc[kPipeChunks], cudaEventDisableTiming));
         for (int c = 0; c < kPipeChunks + kTailSplit; ++c)
             CUDA_TRY(cudaEventCreateWithFlags(&ev_c[c], cudaEventDisableTiming));
     }
@@ -295,11 +299,15 @@ int crt_overlap_blocks() {
     return v;
 }
 
-// Speculative column exponents on the pipelined host path (run_gemm);
-// OZ2G_SPEC=0 turns them off (read per call).
-bool speculation_enabled() {
+// Speculated exponents on the blocking pipelined host path (run_gemm):
+// OZ2G_SPEC=0 off, 1 column exponents only (B uploaded first), otherwise
+// (default) row and column exponents (A row chunks interleaved with B column
+// chunks).  Read per call.
+int speculation_mode() {
     const char* s = std::getenv("OZ2G_SPEC");
-    return !(s && s[0] == '0');
+    if (s && s[0] == '0') return 0;
+    if (s && s[0] == '1') return 1;
+    return 2;
 }
 
 // Raster group height: one wave of persistent CTAs covers group_m tile-rows,
@@ -463,6 +471,28 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     const bool pipe = host && !inter_mats && reduce_fn == nullptr && m >= 2048 && n >= 256;
     const int64_t chunk_rows = pipe ? round_up((m + kPipeChunks - 1) / kPipeChunks, 256) : m;
     const int nchunks = m > 0 ? (int)((m + chunk_rows - 1) / chunk_rows) : 1;
+    // speculated exponents (blocking pipelined calls): 2 = rows and columns
+    // (A row chunks and B column chunks uploaded alternately), 1 = columns
+    const int spec_mode = (pipe && !async && !reuse_scaling && crt_overlap_blocks() <= 1) ? speculation_mode() : 0;
+    const bool spec2 = spec_mode == 2 && n >= 2 * 256;
+    // spec2 column chunks: units of cu columns (a multiple of 128), chunks of two
+    // units except the last two, one unit each (a short last arrival leaves less
+    // work after the upload); cstart[c] = first column of chunk c, cstart[ncc] = n
+    const int64_t col_chunk = round_up((n + kPipeChunks - 1) / kPipeChunks, 256);
+    const int64_t cu = col_chunk / 2;
+    const int64_t nunits = (n + cu - 1) / cu;
+    std::vector<int64_t> cstart;
+    for (int64_t u = 0; spec2 && u < nunits;) {
+        cstart.push_back(u * cu);
+        u += (nunits - u <= 2 && nunits >= 3) ? 1 : 2;
+    }
+    const int ncc = (int)cstart.size();
+    cstart.push_back(n);
+    std::vector<std::pair<bool, int>> arrivals;  // spec2 upload order: (is an A row chunk, index)
+    for (int j = 0; spec2 && j < std::max(nchunks, ncc); ++j) {
+        if (j < nchunks) arrivals.emplace_back(true, j);
+        if (j < ncc) arrivals.emplace_back(false, j);
+    }
     if (host) {
         dA = ws.A.get(esz * (size_t)(m * k));
         dB = ws.B.get(esz * (size_t)(k * n));
@@ -473,6 +503,27 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             // the device copies of A and B are free once the previous call's last
             // reader ran (its residue GEMMs may still be running: uploads overlap them)
             CUDA_TRY(cudaStreamWaitEvent(ws.s_h2d, ws.ev_inputs_free, 0));
+            for (const auto& a : arrivals) {  // spec2: A row chunks and B column chunks alternately
+                if (a.first) {
+                    const int64_t r0 = a.second * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
+                    tm.span(0, ws.s_h2d, [&] {
+                        CUDA_TRY(cudaMemcpy2DAsync((char*)const_cast<void*>(dA) + esz * (size_t)(r0 * k), esz * k,
+                                                   (const char*)A + esz * (size_t)(r0 * lda), esz * lda, esz * k, rc,
+                                                   cudaMemcpyHostToDevice, ws.s_h2d));
+                    });
+                    CUDA_TRY(cudaEventRecord(ws.ev_a[a.second], ws.s_h2d));
+                } else {
+                    const int64_t c0 = cstart[(size_t)a.second], nc = cstart[(size_t)a.second + 1] - c0;
+                    tm.span(0, ws.s_h2d, [&] {
+                        CUDA_TRY(cudaMemcpy2DAsync((char*)const_cast<void*>(dB) + esz * (size_t)c0, esz * n,
+                                                   (const char*)B + esz * (size_t)c0, esz * ldb, esz * nc, k,
+                                                   cudaMemcpyHostToDevice, ws.s_h2d));
+                    });
+                    CUDA_TRY(cudaEventRecord(ws.ev_bc[a.second], ws.s_h2d));
+                }
+            }
+        }
+        if (pipe && !spec2) {
             // B first: the column scan needs all of it
             tm.span(0, ws.s_h2d, [&] {
                 CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dB), esz * n, B, esz * ldb, esz * n, k,
@@ -488,7 +539,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
                 });
                 CUDA_TRY(cudaEventRecord(ws.ev_a[c], ws.s_h2d));
             }
-        } else {
+        } else if (!pipe) {
             tm.span(0, stream, [&] {
                 if (m * k) CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dA), esz * k, A, esz * lda, esz * k, m, cudaMemcpyHostToDevice, stream));
                 if (k * n) CUDA_TRY(cudaMemcpy2DAsync(const_cast<void*>(dB), esz * n, B, esz * ldb, esz * n, k, cudaMemcpyHostToDevice, stream));
@@ -532,8 +583,8 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     if (scan && n) CUDA_TRY(cudaMemsetAsync(cmax_col, 0, 4 * (size_t)n, stream));
 
     // ---- K1 (B): column pre-exponents and Bbar^T ----
-    if (pipe) CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_b, 0));
-    if (scan) tm.span(1, stream, [&] {
+    if (pipe && !spec2) CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_b, 0));
+    if (scan && !spec2) tm.span(1, stream, [&] {
         CUDA_TRY(launch_col_max_B(prec, dB, ldb_d, k, n, bmax, st, stream)); launches += n > 0;
         CUDA_TRY(launch_col_exp_B(bmax, n, nup, st, stream)); launches += n > 0;
         CUDA_TRY(launch_bbar_rows(prec, dB, ldb_d, k, n, kp, ldn, nup, bbar, st, stream)); launches += n > 0;
@@ -617,7 +668,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     for (int c = 0; c < nchunks; ++c) {
         const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
         if (rc <= 0) continue;
-        const int64_t sub = (pipe && c == nchunks - 1 && rc >= 2 * 128)
+        const int64_t sub = (pipe && !spec2 && c == nchunks - 1 && rc >= 2 * 128)
                                 ? std::min<int64_t>(max_block, round_up((rc + kTailSplit - 1) / kTailSplit, 128))
                                 : max_block;
         for (int64_t q = r0; q < r0 + rc; q += sub) blocks.push_back({q, std::min<int64_t>(sub, r0 + rc - q), c});
@@ -638,14 +689,14 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     // nu (B residues, CRT) are kept per stage / block so that flags raised with
     // a superseded nu are dropped; a repaired block whose first CRT raised any
     // flag makes the call redo every stage after the upload unspeculated.
-    const bool spec = pipe && !async && scan && !overlap && n > 0 && speculation_enabled();
+    const bool spec = spec_mode >= 1 && !spec2 && n > 0;
     const size_t nb = blocks.size();
     const int64_t ntiles = (n + 255) / 256;
     DevStatus* sx = nullptr;       // [0] discarded, [1] B residues, [2 + b] CRT of block b, [2 + nb + b] its repairs
     int32_t* changed_h = nullptr;  // [0] any column moved, [1 + t] a column of tile t moved (host view)
     int32_t* changed = nullptr;    // its device alias
     std::vector<char> repaired;
-    int spec_state = spec ? 1 : 0;
+    int spec_state = (spec || spec2) ? 1 : 0;
     if (spec) {
         ws.ensure_streams();
         sx = (DevStatus*)ws.spec_st.get(sizeof(DevStatus) * (2 + 2 * nb));
@@ -654,6 +705,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         CUDA_TRY(cudaHostGetDevicePointer((void**)&changed, changed_h, 0));
         repaired.assign(nb, 0);
     }
+    const ChangeFlags cf1{changed, 0, 256, 0};
     size_t evn = 0;  // per-call event index (downloads wait for their CRT)
 
     // ---- K5 + K6 of one row block of C (columns c0 .. c0 + nc): residue GEMMs
@@ -721,12 +773,193 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         }
     };
 
+    // ---- speculated row and column exponents (spec2) ----
+    // A row chunks and B column chunks arrive alternately.  Each arrival is
+    // scanned and its clearance products with everything already present are
+    // formed; mu / nu of every row / column present are then re-derived from
+    // the maxima so far (final after the last arrival).  The residues of a new
+    // chunk, or of one whose exponents moved, are (re)computed, and every
+    // tile (row chunk x column chunk) of C that is new or lies in a moved
+    // chunk is (re)computed: residue GEMMs, CRT, download.  Status flags of
+    // every stage that reads mu / nu are kept per chunk / tile and a tile's
+    // are reset when it is redone, so only flags of the final exponents count.
+    const int64_t nrs = spec2 ? nchunks : 0;
+    const size_t nst2 = spec2 ? (size_t)(1 + nrs + ncc + nrs * nunits) : 0;
+    std::vector<DevStatus> hx2;
+    auto run_spec2 = [&]() {
+        ws.ensure_streams();
+        // statuses: [0] discarded, [1 + r] A residues of row chunk r, [1 + nrs + c] B residues of
+        // column chunk c, [1 + nrs + ncc + r * nunits + u] CRT of row chunk r x column unit u
+        sx = (DevStatus*)ws.spec_st.get(sizeof(DevStatus) * nst2);
+        CUDA_TRY(cudaMemsetAsync(sx, 0, sizeof(DevStatus) * nst2, stream));
+        DevStatus* const st_tile = sx + 1 + nrs + ncc;
+        changed_h = ws.changed_flags((size_t)(1 + nrs + nunits));
+        CUDA_TRY(cudaHostGetDevicePointer((void**)&changed, changed_h, 0));
+        const ChangeFlags cf{changed, chunk_rows, cu, nrs};
+        volatile int32_t* const flags = changed_h;
+        // W of one region launch, compact: [N][rows][round_up(cols, 16)]
+        const int64_t wcap = (int64_t)N * std::max(chunk_rows * ldw, m * round_up(col_chunk, 16));
+        int8_t* W2 = (int8_t*)ws.W.get((size_t)wcap);
+        auto rows_of = [&](int r) { return std::min<int64_t>(chunk_rows, m - r * chunk_rows); };
+        auto cols_of = [&](int c) { return cstart[(size_t)c + 1] - cstart[(size_t)c]; };
+        auto unit_lo = [&](int c) { return cstart[(size_t)c] / cu; };
+        auto unit_hi = [&](int c) { return (cstart[(size_t)c + 1] + cu - 1) / cu; };  // exclusive
+        // GEMM + CRT + download of rows [r0, r0 + rc) x columns [c0, c0 + nc), whole tiles, in
+        // pieces of at most one row chunk (each piece's download overlaps the next piece)
+        auto run_region = [&](int64_t r0, int64_t rc, int64_t c0, int64_t nc) {
+            const int64_t pitch = round_up(nc, 16);
+            for (int64_t q = r0; q < r0 + rc;) {
+                const int64_t rq = std::min<int64_t>(std::min<int64_t>(r0 + rc - q, chunk_rows), wcap / ((int64_t)N * pitch) / 128 * 128);
+                GemmParams g = gp;
+                g.planes = N;
+                g.ldw = pitch;
+                g.wplane = rq * pitch;
+                g.n = (int)nc;
+                g.tiles_n = (int)((nc + BN - 1) / BN);
+                set_rows(g, rq);
+                g.W = W2;
+                const CUtensorMap tA = make_plane_map(ares + q * kp, kp, rq, N, boxA, m * kp);
+                const CUtensorMap tB = make_plane_map_mn(bres + c0, nc, ldn, kp, N, kp * ldn);
+                tm.span(5, stream, [&] { CUDA_TRY(launch_gemm(EPI_RESID, tA, tB, g)); });
+                CrtExtra exr = ex;
+                exr.sg = StatusGrid{st_tile, q, c0, chunk_rows, cu, nunits};
+                tm.span(6, stream, [&] {
+                    CUDA_TRY(launch_crt(prec, W2, pitch, rq * pitch, rq, nc, cc, mu + q, nu + c0,
+                                        (char*)dC + esz * (size_t)(q * ldc_d + c0), ldc_d, exr, st, stream));
+                });
+                launches += 2;
+                const cudaEvent_t ec = ws.pool_event(evn++);
+                CUDA_TRY(cudaEventRecord(ec, stream));
+                CUDA_TRY(cudaStreamWaitEvent(ws.s_d2h, ec, 0));
+                tm.span(7, ws.s_d2h, [&] {
+                    CUDA_TRY(cudaMemcpy2DAsync((char*)C + esz * (size_t)(q * ldc + c0), esz * ldc,
+                                               (const char*)dC + esz * (size_t)(q * n + c0), esz * n, esz * nc, rq,
+                                               cudaMemcpyDeviceToHost, ws.s_d2h));
+                });
+                q += rq;
+            }
+        };
+        auto clearance = [&](int64_t r0, int64_t rc, int64_t c0, int64_t nc) {
+            tm.span(2, stream, [&] {
+                const CUtensorMap tA = make_plane_map(abar + r0 * kp, kp, rc, 1, boxA);
+                const CUtensorMap tB = make_plane_map_mn(bbar + c0, nc, ldn, kp, 1, kp * ldn);
+                GemmParams g = gp;
+                g.n = (int)nc;
+                g.tiles_n = (int)((nc + BN - 1) / BN);
+                set_rows(g, rc);
+                g.planes = 1;
+                g.rowmax = cmax_row + r0;
+                g.colmax = cmax_col + c0;
+                CUDA_TRY(launch_gemm(EPI_MAX, tA, tB, g));
+            });
+            ++launches;
+        };
+        std::vector<char> haveA((size_t)nrs, 0), haveB((size_t)ncc, 0), done((size_t)(nrs * ncc), 0);
+        int R = 0, Cn = 0;  // row / column chunks present (prefixes)
+        for (const auto& a : arrivals) {
+            if (a.first) {
+                const int r = a.second;
+                const int64_t r0 = r * chunk_rows, rc = rows_of(r);
+                CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_a[r], 0));
+                tm.span(1, stream, [&] {
+                    CUDA_TRY(launch_row_scan_A(prec, (const char*)dA + esz * (size_t)(r0 * lda_d), lda_d, rc, k, kp,
+                                               mup + r0, abar + r0 * kp, st, stream, r0));
+                });
+                ++launches;
+                if (Cn) clearance(r0, rc, 0, cstart[(size_t)Cn]);
+                ++R;
+            } else {
+                const int c = a.second;
+                const int64_t c0 = cstart[(size_t)c], nc = cols_of(c);
+                CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_bc[c], 0));
+                tm.span(1, stream, [&] {
+                    const char* Bc = (const char*)dB + esz * (size_t)c0;
+                    CUDA_TRY(launch_col_max_B(prec, Bc, ldb_d, k, nc, bmax + c0, st, stream));
+                    CUDA_TRY(launch_col_exp_B(bmax + c0, nc, nup + c0, st, stream, c0));
+                    CUDA_TRY(launch_bbar_rows(prec, Bc, ldb_d, k, nc, kp, ldn, nup + c0, bbar + c0, st, stream,
+                                              c == ncc - 1 ? ldn - c0 : nc));
+                });
+                launches += 3;
+                if (R) clearance(0, std::min<int64_t>(m, R * chunk_rows), c0, nc);
+                ++Cn;
+            }
+            if (R == 0 || Cn == 0) continue;
+            const bool last = R == nrs && Cn == ncc;
+            const int64_t mr = std::min<int64_t>(m, R * chunk_rows), nr = cstart[(size_t)Cn];
+            std::memset(changed_h, 0, 4 * (size_t)(1 + nrs + nunits));  // idle: the last check was read
+            tm.span(3, stream, [&] {
+                CUDA_TRY(launch_exponents(cmax_row, mr, cmax_col, nr, mup, nup, tab.shift0, tab.nthr, tab.thr, mu,
+                                          nu, ev, fv, last ? st : sx, stream, &cf));
+            });
+            ++launches;
+            CUDA_TRY(cudaEventRecord(ws.ev_check, stream));
+            CUDA_TRY(cudaEventSynchronize(ws.ev_check));
+            std::vector<char> movR((size_t)R), movC((size_t)Cn);
+            for (int r = 0; r < R; ++r) movR[(size_t)r] = flags[1 + r] != 0 || !haveA[(size_t)r];
+            for (int c = 0; c < Cn; ++c) {
+                bool mv = !haveB[(size_t)c];
+                for (int64_t u = unit_lo(c); u < unit_hi(c); ++u) mv |= flags[1 + nrs + u] != 0;
+                movC[(size_t)c] = mv;
+            }
+            // residues of new chunks and of chunks whose exponents moved
+            tm.span(4, stream, [&] {
+                for (int r = 0; r < R; ++r) {
+                    if (!movR[(size_t)r]) continue;
+                    const int64_t r0 = r * chunk_rows;
+                    CUDA_TRY(cudaMemsetAsync(sx + 1 + r, 0, sizeof(DevStatus), stream));
+                    CUDA_TRY(launch_resid_A(prec, (const char*)dA + esz * (size_t)(r0 * lda_d), lda_d, rows_of(r), k,
+                                            kp, mu + r0, rc_dev, N, ares + r0 * kp, m * kp, sx + 1 + r, stream));
+                    haveA[(size_t)r] = 1;
+                    ++launches;
+                }
+                for (int c = 0; c < Cn; ++c) {
+                    if (!movC[(size_t)c]) continue;
+                    const int64_t c0 = cstart[(size_t)c];
+                    CUDA_TRY(cudaMemsetAsync(sx + 1 + nrs + c, 0, sizeof(DevStatus), stream));
+                    CUDA_TRY(launch_resid_B_rows(prec, (const char*)dB + esz * (size_t)c0, ldb_d, k, cols_of(c), kp,
+                                                 ldn, nu + c0, rc_dev, N, bres + c0, sx + 1 + nrs + c, stream,
+                                                 c == ncc - 1 ? ldn - c0 : cols_of(c)));
+                    haveB[(size_t)c] = 1;
+                    ++launches;
+                }
+            });
+            // tiles: whole moved / new column chunks over every row present, then
+            // the rest of each moved / new row chunk in runs of column chunks
+            auto reset = [&](int r, int c0i, int c1i) {
+                for (int c = c0i; c < c1i; ++c) {
+                    if (done[(size_t)(r * ncc + c)]) spec_state = 2;
+                    done[(size_t)(r * ncc + c)] = 1;
+                }
+                CUDA_TRY(cudaMemsetAsync(st_tile + r * nunits + unit_lo(c0i), 0,
+                                         sizeof(DevStatus) * (size_t)(unit_hi(c1i - 1) - unit_lo(c0i)), stream));
+            };
+            for (int c = 0; c < Cn; ++c) {
+                if (!movC[(size_t)c]) continue;
+                for (int r = 0; r < R; ++r) reset(r, c, c + 1);
+                run_region(0, mr, cstart[(size_t)c], cols_of(c));
+            }
+            for (int r = 0; r < R; ++r) {
+                for (int c = 0; c < Cn;) {
+                    const bool todo = !movC[(size_t)c] && (movR[(size_t)r] || !done[(size_t)(r * ncc + c)]);
+                    if (!todo) { ++c; continue; }
+                    int c1 = c + 1;
+                    while (c1 < Cn && !movC[(size_t)c1] && (movR[(size_t)r] || !done[(size_t)(r * ncc + c1)])) ++c1;
+                    reset(r, c, c1);
+                    run_region(r * chunk_rows, rows_of(r), cstart[(size_t)c], cstart[(size_t)c1] - cstart[(size_t)c]);
+                    c = c1;
+                }
+            }
+        }
+        hx2.resize(nst2);
+    };
+
     // ---- K1 (A) + K2 per row chunk: row pre-exponents, Abar, clearance product with fused maxima ----
     // Pipelined: B is complete before the first chunk, so a chunk's row maxima
     // are final after its clearance GEMM and its mu and A residues follow at
     // once, overlapping the upload of the next chunks.
+    if (spec2) run_spec2();
     size_t next_block = 0;
-    for (int c = 0; c < (scan ? nchunks : 0); ++c) {
+    for (int c = 0; c < (scan && !spec2 ? nchunks : 0); ++c) {
         const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
         if (pipe) CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_a[c], 0));
         tm.span(1, stream, [&] {
@@ -759,7 +992,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
                     if (c > 0) std::memset(changed_h, 0, 4 * (size_t)(1 + ntiles));  // idle: last check was read
                     CUDA_TRY(launch_exponents(cmax_row, 0, cmax_col, n, mup, nup, tab.shift0, tab.nthr, tab.thr, mu,
                                               nu, ev, fv, c == nchunks - 1 ? st : sx, stream,
-                                              c > 0 ? changed : nullptr));
+                                              c > 0 ? &cf1 : nullptr));
                     ++launches;
                 }
             });
@@ -809,7 +1042,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         }
     }
 
-    if (spec) {
+    if (spec || spec2) {
         if (ws.ev_inputs_free) CUDA_TRY(cudaEventRecord(ws.ev_inputs_free, stream));
     } else {
         // ---- K3: scaling exponents; K4: residue planes ----
@@ -940,6 +1173,13 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     CUDA_TRY(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, stream));
     CUDA_TRY(cudaStreamSynchronize(stream));
     CUDA_TRY(cudaGetLastError());
+    if (spec2) {  // flags of every chunk's residues and every tile's CRT (each from its final computation)
+        CUDA_TRY(cudaMemcpy(hx2.data(), sx, sizeof(DevStatus) * nst2, cudaMemcpyDeviceToHost));
+        for (size_t i = 1; i < nst2; ++i) {
+            hs.err |= hx2[i].err;
+            hs.subnormal |= hx2[i].subnormal;
+        }
+    }
     if (spec) {
         std::vector<DevStatus> hx(2 + 2 * nb);
         CUDA_TRY(cudaMemcpy(hx.data(), sx, sizeof(DevStatus) * hx.size(), cudaMemcpyDeviceToHost));

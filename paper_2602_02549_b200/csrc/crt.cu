@@ -179,9 +179,14 @@ __global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, 
                 C[i * ldc + j] = y;
             }
         }
-        if (fr_range) atomicOr(&st->err, (uint32_t)ERR_FR_RANGE);
-        if (inv_range) atomicOr(&st->err, (uint32_t)ERR_INV_RANGE);
-        if (sub) atomicOr(&st->subnormal, 1u);
+        if (fr_range | inv_range | sub) {
+            DevStatus* s = ex.sg.base ? ex.sg.base + ((ex.sg.row0 + i) / ex.sg.row_div) * ex.sg.slots +
+                                            (ex.sg.col0 + j0) / ex.sg.col_div
+                                      : st;
+            if (fr_range) atomicOr(&s->err, (uint32_t)ERR_FR_RANGE);
+            if (inv_range) atomicOr(&s->err, (uint32_t)ERR_INV_RANGE);
+            if (sub) atomicOr(&s->subnormal, 1u);
+        }
     }
     if (BND) {
         bmax_cheap = warp_max_u64(bmax_cheap);

@@ -9,6 +9,15 @@ namespace oz2g {
 
 struct DevStatus;
 
+// Speculated exponents (api.cu run_gemm): the exponents kernel compares each
+// value it writes with the one in place and marks the row / column group that
+// moved: flags[0] = any, flags[1 + i / row_div] for row i (row_div > 0),
+// flags[1 + col_slot0 + j / col_div] for column j (col_div > 0).
+struct ChangeFlags {
+    int32_t* flags;
+    int64_t row_div, col_div, col_slot0;
+};
+
 enum GemmEpilogue { EPI_MAX = 0, EPI_RESID = 1, EPI_I32 = 2 };
 
 struct GemmParams {
@@ -64,15 +73,17 @@ cudaError_t launch_row_scan_A(int prec, const void* A, int64_t lda, int64_t m, i
                               int32_t* mu_prime, int8_t* abar, DevStatus* st, cudaStream_t s, int64_t row0);
 cudaError_t launch_col_max_B(int prec, const void* B, int64_t ldb, int64_t k, int64_t n,
                              unsigned long long* bmax, DevStatus* st, cudaStream_t s);
+// col0: global index of column 0 (zero-column messages of a column chunk)
 cudaError_t launch_col_exp_B(const unsigned long long* bmax, int64_t n, int32_t* nu_prime, DevStatus* st,
-                             cudaStream_t s);
+                             cudaStream_t s, int64_t col0 = 0);
 // Bbar = ceil(|B| 2^nu') in B's layout [kp][ldn] (rows k..kp and columns n..ldn zero)
 cudaError_t launch_bbar_rows(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp, int64_t ldn,
-                             const int32_t* nu_prime, int8_t* bbar, DevStatus* st, cudaStream_t s);
+                             const int32_t* nu_prime, int8_t* bbar, DevStatus* st, cudaStream_t s,
+                             int64_t cols_out = -1);
 cudaError_t launch_exponents(const int32_t* cmax_row, int64_t m, const int32_t* cmax_col, int64_t n,
                              const int32_t* mu_prime, const int32_t* nu_prime, int shift0, int nthr,
                              const int32_t* thr, int32_t* mu, int32_t* nu, float* e, float* f, DevStatus* st,
-                             cudaStream_t s, int32_t* changed = nullptr);
+                             cudaStream_t s, const ChangeFlags* changed = nullptr);
 // plane_stride: bytes between residue planes (0 = m * kp); a row block of the
 // planes is written by passing the block's A / mu / planes offsets.
 cudaError_t launch_resid_A(int prec, const void* A, int64_t lda, int64_t m, int64_t k, int64_t kp,
@@ -81,7 +92,7 @@ cudaError_t launch_resid_A(int prec, const void* A, int64_t lda, int64_t m, int6
 // residue planes of trunc(B 2^nu) in B's layout, [l][kp][ldn]
 cudaError_t launch_resid_B_rows(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp, int64_t ldn,
                                 const int32_t* nu, const ResidConsts* rc_dev, int nmod, int8_t* planes,
-                                DevStatus* st, cudaStream_t s);
+                                DevStatus* st, cudaStream_t s, int64_t cols_out = -1);
 cudaError_t launch_trunc_scaled(int prec, const void* X, int64_t ldx, int64_t rows, int64_t cols,
                                 const int32_t* shift, int by_col, double* out, cudaStream_t s);
 cudaError_t launch_log2f(const float* x, float* out, int64_t count, cudaStream_t s);
@@ -117,10 +128,19 @@ struct BoundCtx {  // evaluated in the CRT pass when `on`
     double *cheap, *tight;             // optional m x n outputs (device)
     unsigned long long* max_bits;      // [0] cheap max, [1] tight max (bits of positive doubles)
 };
+// Status flags per (row group, column group) of C instead of the launch's
+// single status (speculated exponents, api.cu): entry (i, j) of the launch
+// flags base[((row0 + i) / row_div) * slots + (col0 + j) / col_div]; col_div
+// and col0 are multiples of 8 (one CRT thread's columns share an entry).
+struct StatusGrid {
+    DevStatus* base;  // nullptr: the launch's status
+    int64_t row0, col0, row_div, col_div, slots;
+};
 struct CrtExtra {  // optional device outputs (nullptr = skip)
     double *C1, *C2, *Q, *Cpp64;
     float* Cpp32;
     BoundCtx bnd;
+    StatusGrid sg;
 };
 cudaError_t launch_crt(int prec, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
                        const CrtConsts& cc, const int32_t* mu, const int32_t* nu, void* C, int64_t ldc,

@@ -177,8 +177,8 @@ __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, i
 
 template <class T, bool COLSHIFT, int OP>
 __global__ void __launch_bounds__(256) resid_rows_kernel(const T* __restrict__ X, int64_t ldx, int64_t rows_valid,
-                                                         int64_t rows_total, int64_t cols_valid, int64_t ld_out,
-                                                         const int32_t* __restrict__ shift,
+                                                         int64_t rows_total, int64_t cols_valid, int64_t cols_out,
+                                                         int64_t ld_out, const int32_t* __restrict__ shift,
                                                          const ResidHeader* __restrict__ rc_g, int nmod,
                                                          int8_t* __restrict__ planes, int64_t plane, uint32_t err_bit,
                                                          DevStatus* st) {
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(256) resid_rows_kernel(const T* __restrict__ X
     const ResidHeader& hd = *reinterpret_cast<const ResidHeader*>(sh);
     const uint8_t* tab = sh + sizeof(ResidHeader);
     const int64_t h0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * RA_E;
-    if (h0 >= ld_out) return;
+    if (h0 >= cols_out) return;
     bool bad = false;
     int csft[RA_E];  // per-column shifts (B): the same for every row
     if (COLSHIFT) {
@@ -300,38 +300,41 @@ cudaError_t rows_grid(K kernel, size_t smem, int64_t rows, unsigned chunks, dim3
 
 template <class T, bool COLSHIFT, int OP>
 cudaError_t launch_rows(const void* X, int64_t ldx, int64_t rows_valid, int64_t rows_total, int64_t cols_valid,
-                        int64_t ld_out, const int32_t* shift, const ResidConsts* rc, int nmod, int8_t* planes,
-                        int64_t plane, uint32_t err_bit, DevStatus* st, cudaStream_t s) {
-    if (rows_total == 0 || ld_out == 0) return cudaSuccess;
-    const unsigned chunks = blocks_for(ld_out, 256 * RA_E);
+                        int64_t cols_out, int64_t ld_out, const int32_t* shift, const ResidConsts* rc, int nmod,
+                        int8_t* planes, int64_t plane, uint32_t err_bit, DevStatus* st, cudaStream_t s) {
+    if (rows_total == 0 || cols_out == 0) return cudaSuccess;
+    const unsigned chunks = blocks_for(cols_out, 256 * RA_E);
     const size_t sm = OP == 1 ? resid_consts_bytes(nmod) : 0;
     dim3 grid;
     cudaError_t err = rows_grid(resid_rows_kernel<T, COLSHIFT, OP>, sm, rows_total, chunks, grid);
     if (err != cudaSuccess) return err;
     resid_rows_kernel<T, COLSHIFT, OP><<<grid, 256, sm, s>>>((const T*)X, ldx, rows_valid, rows_total, cols_valid,
-                                                            ld_out, shift, rc, nmod, planes, plane, err_bit, st);
+                                                            cols_out, ld_out, shift, rc, nmod, planes, plane,
+                                                            err_bit, st);
     return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_bbar_rows(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp, int64_t ldn,
-                             const int32_t* nu_prime, int8_t* bbar, DevStatus* st, cudaStream_t s) {
+                             const int32_t* nu_prime, int8_t* bbar, DevStatus* st, cudaStream_t s, int64_t cols_out) {
     if (n == 0) return cudaSuccess;
-    return prec ? launch_rows<double, true, 0>(B, ldb, k, kp, n, ldn, nu_prime, nullptr, 1, bbar, 0, ERR_CEIL_LOGIC,
-                                               st, s)
-                : launch_rows<float, true, 0>(B, ldb, k, kp, n, ldn, nu_prime, nullptr, 1, bbar, 0, ERR_CEIL_LOGIC,
-                                              st, s);
+    if (cols_out < 0) cols_out = ldn;
+    return prec ? launch_rows<double, true, 0>(B, ldb, k, kp, n, cols_out, ldn, nu_prime, nullptr, 1, bbar, 0,
+                                               ERR_CEIL_LOGIC, st, s)
+                : launch_rows<float, true, 0>(B, ldb, k, kp, n, cols_out, ldn, nu_prime, nullptr, 1, bbar, 0,
+                                              ERR_CEIL_LOGIC, st, s);
 }
 
 cudaError_t launch_resid_B_rows(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp, int64_t ldn,
                                 const int32_t* nu, const ResidConsts* rc_dev, int nmod, int8_t* planes,
-                                DevStatus* st, cudaStream_t s) {
+                                DevStatus* st, cudaStream_t s, int64_t cols_out) {
     if (n == 0) return cudaSuccess;
+    if (cols_out < 0) cols_out = ldn;
     const int64_t plane = kp * ldn;
-    return prec ? launch_rows<double, true, 1>(B, ldb, k, kp, n, ldn, nu, rc_dev, nmod, planes, plane,
+    return prec ? launch_rows<double, true, 1>(B, ldb, k, kp, n, cols_out, ldn, nu, rc_dev, nmod, planes, plane,
                                                ERR_TRUNC_B_RANGE, st, s)
-                : launch_rows<float, true, 1>(B, ldb, k, kp, n, ldn, nu, rc_dev, nmod, planes, plane,
+                : launch_rows<float, true, 1>(B, ldb, k, kp, n, cols_out, ldn, nu, rc_dev, nmod, planes, plane,
                                               ERR_TRUNC_B_RANGE, st, s);
 }
 

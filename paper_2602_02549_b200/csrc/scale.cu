@@ -181,13 +181,13 @@ __global__ void __launch_bounds__(256) col_max_B_kernel(const T* __restrict__ B,
 }
 
 __global__ void col_exp_B_kernel(const unsigned long long* __restrict__ bmax, int64_t n,
-                                 int32_t* __restrict__ nu_prime, DevStatus* st) {
+                                 int32_t* __restrict__ nu_prime, DevStatus* st, int64_t col0) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     const unsigned long long b = bmax[j];
     if (b == 0) {
         flag(st, ERR_B_ZERO_COL);
-        atomicMin((unsigned long long*)&st->first_col, j);
+        atomicMin((unsigned long long*)&st->first_col, col0 + j);
         nu_prime[j] = 0;
         return;
     }
@@ -207,7 +207,7 @@ __global__ void exponents_kernel(const int32_t* __restrict__ cmax_row, int64_t m
                                  const int32_t* __restrict__ mu_prime, const int32_t* __restrict__ nu_prime,
                                  const ThrTable tt, int32_t* __restrict__ mu, int32_t* __restrict__ nu,
                                  float* __restrict__ e, float* __restrict__ f, DevStatus* st,
-                                 int32_t* __restrict__ changed) {
+                                 const ChangeFlags cf) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= m + n) return;
     const bool is_row = t < m;
@@ -224,13 +224,19 @@ __global__ void exponents_kernel(const int32_t* __restrict__ cmax_row, int64_t m
     const int base = is_row ? mu_prime[idx] : nu_prime[idx];
     const int v = base + shift;
     if (v < -32768 || v > 32767) flag(st, is_row ? ERR_MU_RANGE : ERR_NU_RANGE);
-    if (is_row) { mu[idx] = v; if (e) e[idx] = ev; }
-    else {
-        // changed != null: nu holds exponents speculated from partial column
-        // maxima; flag every 256-column tile in which one of them moves
-        if (changed && nu[idx] != v) {
-            changed[0] = 1;
-            changed[1 + (idx >> 8)] = 1;
+    // cf.flags: mu / nu hold exponents speculated from partial maxima; mark
+    // every row / column group in which one of them moves
+    if (is_row) {
+        if (cf.flags && cf.row_div && mu[idx] != v) {
+            cf.flags[0] = 1;
+            cf.flags[1 + idx / cf.row_div] = 1;
+        }
+        mu[idx] = v;
+        if (e) e[idx] = ev;
+    } else {
+        if (cf.flags && cf.col_div && nu[idx] != v) {
+            cf.flags[0] = 1;
+            cf.flags[1 + cf.col_slot0 + idx / cf.col_div] = 1;
         }
         nu[idx] = v;
         if (f) f[idx] = ev;
@@ -291,23 +297,24 @@ cudaError_t launch_col_max_B(int prec, const void* B, int64_t ldb, int64_t k, in
 }
 
 cudaError_t launch_col_exp_B(const unsigned long long* bmax, int64_t n, int32_t* nu_prime, DevStatus* st,
-                             cudaStream_t s) {
+                             cudaStream_t s, int64_t col0) {
     if (n == 0) return cudaSuccess;
-    col_exp_B_kernel<<<blocks_for(n, 256), 256, 0, s>>>(bmax, n, nu_prime, st);
+    col_exp_B_kernel<<<blocks_for(n, 256), 256, 0, s>>>(bmax, n, nu_prime, st, col0);
     return cudaGetLastError();
 }
 
 cudaError_t launch_exponents(const int32_t* cmax_row, int64_t m, const int32_t* cmax_col, int64_t n,
                              const int32_t* mu_prime, const int32_t* nu_prime, int shift0, int nthr,
                              const int32_t* thr, int32_t* mu, int32_t* nu, float* e, float* f, DevStatus* st,
-                             cudaStream_t s, int32_t* changed) {
+                             cudaStream_t s, const ChangeFlags* changed) {
     if (m + n == 0) return cudaSuccess;
     ThrTable tt;
     tt.shift0 = shift0;
     tt.nthr = nthr;
     for (int q = 0; q < 64; ++q) tt.thr[q] = q < nthr ? thr[q] : 0;
     exponents_kernel<<<blocks_for(m + n, 256), 256, 0, s>>>(cmax_row, m, cmax_col, n, mu_prime, nu_prime, tt, mu,
-                                                            nu, e, f, st, changed);
+                                                            nu, e, f, st,
+                                                            changed ? *changed : ChangeFlags{nullptr, 0, 0, 0});
     return cudaGetLastError();
 }
 

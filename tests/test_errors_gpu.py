@@ -43,13 +43,13 @@ def _expect(oracle, a, b, nmod):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m,k,n", [(64, 48, 40), (2560, 64, 300)])
+@pytest.mark.parametrize("m,k,n", [(64, 48, 40), (2560, 64, 300), (2560, 64, 1100)])
 def test_errors_match_oracle(cuda, oracle, m, k, n):
     import torch
     for name, (a, b) in _cases(oracle, m, k, n).items():
         cls, msg = _expect(oracle, a, b, 14)
         assert cls is not None, name
-        # host pointers (pipelined for the large shape)
+        # host pointers (pipelined for the large shapes; speculated rows and columns at n = 1100)
         with pytest.raises(cls) as ei:
             oz.os_ii(a, b, 14)
         assert str(ei.value) == msg, (name, str(ei.value), msg)
