@@ -855,6 +855,9 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             ++launches;
         };
         std::vector<char> haveA((size_t)nrs, 0), haveB((size_t)ncc, 0), done((size_t)(nrs * ncc), 0);
+        int64_t invalidated = 0;  // tiles computed with exponents that later moved
+        bool seen_move = false;
+        bool give_up = false;     // defer every remaining tile to the final exponents
         int R = 0, Cn = 0;  // row / column chunks present (prefixes)
         for (const auto& a : arrivals) {
             if (a.first) {
@@ -894,17 +897,22 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             ++launches;
             CUDA_TRY(cudaEventRecord(ws.ev_check, stream));
             CUDA_TRY(cudaEventSynchronize(ws.ev_check));
-            std::vector<char> movR((size_t)R), movC((size_t)Cn);
-            for (int r = 0; r < R; ++r) movR[(size_t)r] = flags[1 + r] != 0 || !haveA[(size_t)r];
+            // moved: exponents changed at this check; new: first exponents of the chunk
+            std::vector<char> movR((size_t)R), movC((size_t)Cn), newR((size_t)R), newC((size_t)Cn);
+            for (int r = 0; r < R; ++r) {
+                newR[(size_t)r] = !haveA[(size_t)r];
+                movR[(size_t)r] = flags[1 + r] != 0 && haveA[(size_t)r];
+            }
             for (int c = 0; c < Cn; ++c) {
-                bool mv = !haveB[(size_t)c];
+                bool mv = false;
                 for (int64_t u = unit_lo(c); u < unit_hi(c); ++u) mv |= flags[1 + nrs + u] != 0;
-                movC[(size_t)c] = mv;
+                newC[(size_t)c] = !haveB[(size_t)c];
+                movC[(size_t)c] = mv && haveB[(size_t)c];
             }
             // residues of new chunks and of chunks whose exponents moved
             tm.span(4, stream, [&] {
                 for (int r = 0; r < R; ++r) {
-                    if (!movR[(size_t)r]) continue;
+                    if (!movR[(size_t)r] && !newR[(size_t)r]) continue;
                     const int64_t r0 = r * chunk_rows;
                     CUDA_TRY(cudaMemsetAsync(sx + 1 + r, 0, sizeof(DevStatus), stream));
                     CUDA_TRY(launch_resid_A(prec, (const char*)dA + esz * (size_t)(r0 * lda_d), lda_d, rows_of(r), k,
@@ -913,7 +921,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
                     ++launches;
                 }
                 for (int c = 0; c < Cn; ++c) {
-                    if (!movC[(size_t)c]) continue;
+                    if (!movC[(size_t)c] && !newC[(size_t)c]) continue;
                     const int64_t c0 = cstart[(size_t)c];
                     CUDA_TRY(cudaMemsetAsync(sx + 1 + nrs + c, 0, sizeof(DevStatus), stream));
                     CUDA_TRY(launch_resid_B_rows(prec, (const char*)dB + esz * (size_t)c0, ldb_d, k, cols_of(c), kp,
@@ -923,32 +931,44 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
                     ++launches;
                 }
             });
-            // tiles: whole moved / new column chunks over every row present, then
-            // the rest of each moved / new row chunk in runs of column chunks
-            auto reset = [&](int r, int c0i, int c1i) {
-                for (int c = c0i; c < c1i; ++c) {
-                    if (done[(size_t)(r * ncc + c)]) spec_state = 2;
-                    done[(size_t)(r * ncc + c)] = 1;
+            // tiles.  A tile computed with an exponent that has since moved is
+            // invalid.  Tiles are (re)computed when their row and column chunks
+            // held still at this check (new chunks count as still until anything
+            // has moved) or at the last arrival, so inputs whose maxima keep
+            // moving (wide exponent spreads) are not recomputed at every arrival;
+            // once an eighth of all tiles was invalidated, the rest wait for the
+            // final exponents.
+            for (int r = 0; r < R; ++r)
+                for (int c = 0; c < Cn; ++c) {
+                    const size_t t = (size_t)(r * ncc + c);
+                    if (done[t] && (movR[(size_t)r] || movC[(size_t)c])) {
+                        done[t] = 0;
+                        ++invalidated;
+                        spec_state = 2;
+                    }
                 }
-                CUDA_TRY(cudaMemsetAsync(st_tile + r * nunits + unit_lo(c0i), 0,
-                                         sizeof(DevStatus) * (size_t)(unit_hi(c1i - 1) - unit_lo(c0i)), stream));
+            for (int r = 0; r < R; ++r) seen_move |= movR[(size_t)r] != 0;
+            for (int c = 0; c < Cn; ++c) seen_move |= movC[(size_t)c] != 0;
+            // once anything moved, a new chunk also has to hold still for one check
+            auto still_r = [&](int r) { return !movR[(size_t)r] && !(seen_move && newR[(size_t)r]); };
+            auto still_c = [&](int c) { return !movC[(size_t)c] && !(seen_move && newC[(size_t)c]); };
+            auto ready = [&](int r, int c) {
+                if (done[(size_t)(r * ncc + c)]) return false;
+                return last || (!give_up && still_r(r) && still_c(c));
             };
-            for (int c = 0; c < Cn; ++c) {
-                if (!movC[(size_t)c]) continue;
-                for (int r = 0; r < R; ++r) reset(r, c, c + 1);
-                run_region(0, mr, cstart[(size_t)c], cols_of(c));
-            }
             for (int r = 0; r < R; ++r) {
                 for (int c = 0; c < Cn;) {
-                    const bool todo = !movC[(size_t)c] && (movR[(size_t)r] || !done[(size_t)(r * ncc + c)]);
-                    if (!todo) { ++c; continue; }
+                    if (!ready(r, c)) { ++c; continue; }
                     int c1 = c + 1;
-                    while (c1 < Cn && !movC[(size_t)c1] && (movR[(size_t)r] || !done[(size_t)(r * ncc + c1)])) ++c1;
-                    reset(r, c, c1);
+                    while (c1 < Cn && ready(r, c1)) ++c1;
+                    for (int cc2 = c; cc2 < c1; ++cc2) done[(size_t)(r * ncc + cc2)] = 1;
+                    CUDA_TRY(cudaMemsetAsync(st_tile + r * nunits + unit_lo(c), 0,
+                                             sizeof(DevStatus) * (size_t)(unit_hi(c1 - 1) - unit_lo(c)), stream));
                     run_region(r * chunk_rows, rows_of(r), cstart[(size_t)c], cstart[(size_t)c1] - cstart[(size_t)c]);
                     c = c1;
                 }
             }
+            give_up |= 8 * invalidated >= nrs * ncc;
         }
         hx2.resize(nst2);
     };
