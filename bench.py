@@ -316,6 +316,7 @@ def main():
             # the same calls with column-only speculation (OZ2G_SPEC=1) and none (0), same box
             for mode, key in (("1", "columns_only_value"), ("0", "unspeculated_value")):
                 os.environ["OZ2G_SPEC"] = mode
+                oz.os_ii(a_np, b_np, args.moduli, out=c_np, reduce_maxima=reduce_cb)  # warm (buffer sizes differ)
                 barrier()
                 t0 = time.perf_counter()
                 for _ in range(2):

@@ -473,7 +473,8 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     const int nchunks = m > 0 ? (int)((m + chunk_rows - 1) / chunk_rows) : 1;
     // speculated exponents (blocking pipelined calls): 2 = rows and columns
     // (A row chunks and B column chunks uploaded alternately), 1 = columns
-    const int spec_mode = (pipe && !async && !reuse_scaling && crt_overlap_blocks() <= 1) ? speculation_mode() : 0;
+    // (asynchronous calls: rows + columns only; its statuses are merged on the device)
+    const int spec_mode = (pipe && !reuse_scaling && crt_overlap_blocks() <= 1) ? speculation_mode() : 0;
     const bool spec2 = spec_mode == 2 && n >= 2 * 256;
     // spec2 column chunks: units of cu columns (a multiple of 128), chunks of two
     // units except the last two, one unit each (a short last arrival leaves less
@@ -689,7 +690,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     // nu (B residues, CRT) are kept per stage / block so that flags raised with
     // a superseded nu are dropped; a repaired block whose first CRT raised any
     // flag makes the call redo every stage after the upload unspeculated.
-    const bool spec = spec_mode >= 1 && !spec2 && n > 0;
+    const bool spec = spec_mode >= 1 && !spec2 && n > 0 && !async;
     const size_t nb = blocks.size();
     const int64_t ntiles = (n + 255) / 256;
     DevStatus* sx = nullptr;       // [0] discarded, [1] B residues, [2 + b] CRT of block b, [2 + nb + b] its repairs
@@ -785,7 +786,6 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     // are reset when it is redone, so only flags of the final exponents count.
     const int64_t nrs = spec2 ? nchunks : 0;
     const size_t nst2 = spec2 ? (size_t)(1 + nrs + ncc + nrs * nunits) : 0;
-    std::vector<DevStatus> hx2;
     auto run_spec2 = [&]() {
         ws.ensure_streams();
         // statuses: [0] discarded, [1 + r] A residues of row chunk r, [1 + nrs + c] B residues of
@@ -970,7 +970,9 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             }
             give_up |= 8 * invalidated >= nrs * ncc;
         }
-        hx2.resize(nst2);
+        // flags of every chunk's residues and every tile's CRT (each from its final computation)
+        CUDA_TRY(launch_merge_status(st, sx + 1, (int64_t)nst2 - 1, stream));
+        ++launches;
     };
 
     // ---- K1 (A) + K2 per row chunk: row pre-exponents, Abar, clearance product with fused maxima ----
@@ -1193,13 +1195,6 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     CUDA_TRY(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, stream));
     CUDA_TRY(cudaStreamSynchronize(stream));
     CUDA_TRY(cudaGetLastError());
-    if (spec2) {  // flags of every chunk's residues and every tile's CRT (each from its final computation)
-        CUDA_TRY(cudaMemcpy(hx2.data(), sx, sizeof(DevStatus) * nst2, cudaMemcpyDeviceToHost));
-        for (size_t i = 1; i < nst2; ++i) {
-            hs.err |= hx2[i].err;
-            hs.subnormal |= hx2[i].subnormal;
-        }
-    }
     if (spec) {
         std::vector<DevStatus> hx(2 + 2 * nb);
         CUDA_TRY(cudaMemcpy(hx.data(), sx, sizeof(DevStatus) * hx.size(), cudaMemcpyDeviceToHost));

@@ -259,6 +259,22 @@ __global__ void log2f_kernel(const float* __restrict__ x, float* __restrict__ ou
     if (t < count) out[t] = (float)log2((double)x[t]);
 }
 
+// OR the error bits and subnormal flags of src[0 .. count) into dst (the
+// per-chunk / per-tile statuses of the speculated path, api.cu).
+__global__ void merge_status_kernel(DevStatus* __restrict__ dst, const DevStatus* __restrict__ src, int64_t count) {
+    uint32_t err = 0, sub = 0;
+    for (int64_t i = threadIdx.x; i < count; i += blockDim.x) {
+        err |= src[i].err;
+        sub |= src[i].subnormal;
+    }
+    err = __reduce_or_sync(0xffffffffu, err);
+    sub = __reduce_or_sync(0xffffffffu, sub);
+    if ((threadIdx.x & 31) == 0 && (err | sub)) {
+        if (err) atomicOr(&dst->err, err);
+        if (sub) atomicOr(&dst->subnormal, 1u);
+    }
+}
+
 inline unsigned blocks_for(int64_t work, int per) { return (unsigned)((work + per - 1) / per); }
 
 }  // namespace
@@ -329,6 +345,12 @@ cudaError_t launch_trunc_scaled(int prec, const void* X, int64_t ldx, int64_t ro
 cudaError_t launch_log2f(const float* x, float* out, int64_t count, cudaStream_t s) {
     if (count == 0) return cudaSuccess;
     log2f_kernel<<<blocks_for(count, 256), 256, 0, s>>>(x, out, count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_merge_status(DevStatus* dst, const DevStatus* src, int64_t count, cudaStream_t s) {
+    if (count <= 0) return cudaSuccess;
+    merge_status_kernel<<<1, 256, 0, s>>>(dst, src, count);
     return cudaGetLastError();
 }
 
