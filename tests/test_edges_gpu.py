@@ -51,6 +51,31 @@ def test_strided_host_operands_via_c_abi(cuda, oracle):
     assert (Cp[:, n:] == -1.0).all()
 
 
+@pytest.mark.parametrize("mode", ["0", "1", "2"])
+def test_strided_host_operands_pipelined(cuda, oracle, mode):
+    """The pipelined host path (chunked uploads, per-block / per-tile
+    downloads) with leading dimensions larger than the matrices, for every
+    speculation mode (OZ2G_SPEC): C bit-exact, the padding never written."""
+    import os
+    from paper_2602_02549_b200 import _lib
+    m, k, n = 2304, 96, 1100
+    A = oracle.gen_matrix(m, k, 0.5, 95)
+    B = oracle.gen_matrix(k, n, 0.5, 96)
+    ref = oracle.os_ii(A, B, 12)
+    Ap = np.zeros((m, k + 5)); Ap[:, :k] = A
+    Bp = np.zeros((k, n + 13)); Bp[:, :n] = B
+    Cp = np.full((m, n + 3), -1.0)
+    os.environ["OZ2G_SPEC"] = mode
+    try:
+        rc = _lib.load().oz2g_dgemm(m, n, k, Ap.ctypes.data, k + 5, Bp.ctypes.data, n + 13, Cp.ctypes.data, n + 3,
+                                    12, 0, None, None)
+    finally:
+        del os.environ["OZ2G_SPEC"]
+    assert rc == 0, _lib.load().oz2g_last_error()
+    _same(np.ascontiguousarray(Cp[:, :n]), ref.C)
+    assert (Cp[:, n:] == -1.0).all()
+
+
 @pytest.mark.parametrize("scale,dt", [(1e-160, np.float64), (1e-155, np.float64), (1e-21, np.float32)])
 def test_subnormal_outputs(cuda, oracle, scale, dt):
     A = (oracle.gen_matrix(24, 40, 1.0, 95) * scale).astype(dt)
