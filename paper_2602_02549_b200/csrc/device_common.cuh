@@ -64,6 +64,18 @@ __device__ __forceinline__ int ilogb_exact(double x) {
     return e2 + 52;
 }
 
+// ceil(2^sft |a|) for a shift with 2^sft a normal double (p2 = 2^sft), on the
+// fp64 pipe: |a| p2 is exact unless the product is subnormal, and then the
+// exact value lies in (0, 2^-1022), whose ceiling is 1 (a product rounded to 0
+// is lifted to 1 for a != 0).  Same result as ceil_abs_scaled below; -1 above 64.
+__device__ __forceinline__ bool pow2_normal(int sft) { return sft >= -1022 && sft <= 1023; }
+__device__ __forceinline__ int ceil_scaled_p2(double a, double p2) {
+    double c = ceil(__dmul_rn(fabs(a), p2));
+    c = (c == 0.0 && a != 0.0) ? 1.0 : c;
+    // c is an integer in [0, 2^53) (or inf): its value from the low word of c + 1.5 * 2^52
+    return c > 64.0 ? -1 : (int)(uint32_t)__double_as_longlong(__dadd_rn(c, 6755399441055744.0));
+}
+
 // ceil(2^sft |a|) exactly (scaling.hpp:61-79); -1 on the logic_error paths.
 __device__ __forceinline__ int ceil_abs_scaled(double a, int sft) {
     if (a == 0.0) return 0;

@@ -199,6 +199,16 @@ __global__ void __launch_bounds__(256) resid_rows_kernel(const T* __restrict__ X
     }
     const bool full = h0 + RA_E <= cols_valid;
     const int nplanes = OP == 0 ? 1 : nmod;
+    // Bbar: 2^nu'_j as doubles for the fp64-pipe ceil (ceil_scaled_p2) when all are normal
+    double p2c[RA_E] = {};
+    bool fastc = OP == 0 && COLSHIFT;
+    if (OP == 0 && COLSHIFT) {
+#pragma unroll
+        for (int j = 0; j < RA_E; ++j) {
+            fastc &= pow2_normal(csft[j]);
+            p2c[j] = pow2_normal(csft[j]) ? pow2d(csft[j]) : 0.0;
+        }
+    }
     for (int64_t i = blockIdx.y; i < rows_total; i += gridDim.y) {
         int8_t* out = planes + i * ld_out + h0;
         if (i >= rows_valid) {  // zero padding rows (B: k .. kp)
@@ -230,7 +240,7 @@ __global__ void __launch_bounds__(256) resid_rows_kernel(const T* __restrict__ X
             uint32_t w[2] = {0u, 0u};
 #pragma unroll
             for (int j = 0; j < RA_E; ++j) {
-                const int c = ceil_abs_scaled(x[j], COLSHIFT ? csft[j] : rsft);
+                const int c = fastc ? ceil_scaled_p2(x[j], p2c[j]) : ceil_abs_scaled(x[j], COLSHIFT ? csft[j] : rsft);
                 bad |= c < 0;
                 w[j >> 2] |= (uint32_t)(c & 0xff) << (8 * (j & 3));
             }

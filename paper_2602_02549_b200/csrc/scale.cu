@@ -29,28 +29,54 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
 
 // ---------------------------------------------------------------------------
 // A: one CTA per row (two passes; the second re-reads the row from L2).
-// blockDim is 256 or 1024 (launcher); the reductions below handle both.
+// blockDim is 256 or 1024 (launcher); the reductions below handle both.  Each
+// thread takes 8 consecutive elements per step (16-byte loads, one 8-byte
+// store of Abar); the max runs on the fp64 pipe (fmax of |x|, non-finite
+// detected by |x| <= DBL_MAX) and Abar = ceil(2^mu' |a|) too (ceil_scaled_p2),
+// with the integer routine for the rows whose 2^mu' is not a normal double.
 // ---------------------------------------------------------------------------
+constexpr int kRowE = 8;
+
 template <class T>
-__global__ void __launch_bounds__(1024) row_scan_A_kernel(const T* __restrict__ A, int64_t lda, int64_t k,
-                                                         int64_t kp, int32_t* __restrict__ mu_prime,
-                                                         int8_t* __restrict__ abar, DevStatus* st,
-                                                         int64_t row0) {
-    const int64_t i = blockIdx.x;  // row within this launch; row0 + i in the whole matrix
-    const T* row = A + i * lda;
-    unsigned long long mx = 0;
-    bool bad = false;
-#pragma unroll 8
-    for (int64_t h = threadIdx.x; h < k; h += blockDim.x) {
-        const double v = ld_d(row + h);
-        const unsigned long long b = abs_bits(v);
-        bad |= b >= 0x7ff0000000000000ull;
-        mx = b > mx ? b : mx;
+__device__ __forceinline__ void load8(const T* __restrict__ p, int64_t h0, int64_t k, bool vec, double (&x)[kRowE]) {
+    if (vec && h0 + kRowE <= k) {
+        if constexpr (sizeof(T) == 8) {
+#pragma unroll
+            for (int j = 0; j < kRowE; j += 2) {
+                const double2 t = __ldg(reinterpret_cast<const double2*>(p + h0 + j));
+                x[j] = t.x;
+                x[j + 1] = t.y;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kRowE; j += 4) {
+                const float4 t = __ldg(reinterpret_cast<const float4*>(p + h0 + j));
+                x[j] = t.x; x[j + 1] = t.y; x[j + 2] = t.z; x[j + 3] = t.w;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kRowE; ++j) x[j] = h0 + j < k ? (double)__ldg(p + h0 + j) : 0.0;
     }
-    if (__syncthreads_or(bad)) {
-        if (threadIdx.x == 0) { flag(st, ERR_A_NONFINITE); atomicMin((unsigned long long*)&st->first_row, row0 + i); }
-        return;
+}
+
+// Abar of 8 elements packed in two words; logic |= an entry above 64
+__device__ __forceinline__ uint2 abar8(const double (&x)[kRowE], int sft, bool fast, double p2, bool& logic) {
+    uint32_t w[2] = {0u, 0u};
+#pragma unroll
+    for (int j = 0; j < kRowE; ++j) {
+        const int c = fast ? ceil_scaled_p2(x[j], p2) : ceil_abs_scaled(x[j], sft);
+        logic |= c < 0;
+        w[j >> 2] |= (uint32_t)(c & 0xff) << (8 * (j & 3));
     }
+    return make_uint2(w[0], w[1]);
+}
+
+// block-wide max of the (non-negative) row maxima; thread 0 sets mu' (or the
+// zero-row error) and every thread gets it back
+__device__ __forceinline__ int row_mu_prime(double mxd, int32_t* __restrict__ mu_prime, DevStatus* st, int64_t i,
+                                            int64_t row0) {
+    unsigned long long mx = (unsigned long long)__double_as_longlong(mxd);
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         const unsigned long long t = __shfl_xor_sync(0xffffffffu, mx, o);
@@ -74,24 +100,49 @@ __global__ void __launch_bounds__(1024) row_scan_A_kernel(const T* __restrict__ 
         s_mup = mup;
     }
     __syncthreads();
-    const int sft = s_mup;
+    return s_mup;
+}
+
+template <class T>
+__global__ void __launch_bounds__(1024) row_scan_A_kernel(const T* __restrict__ A, int64_t lda, int64_t k,
+                                                         int64_t kp, int32_t* __restrict__ mu_prime,
+                                                         int8_t* __restrict__ abar, DevStatus* st,
+                                                         int64_t row0) {
+    const int64_t i = blockIdx.x;  // row within this launch; row0 + i in the whole matrix
+    const T* row = A + i * lda;
+    const bool vec = (reinterpret_cast<uintptr_t>(row) & 15) == 0;
+    double mxd = 0.0;
+    bool bad = false;
+    for (int64_t h0 = (int64_t)threadIdx.x * kRowE; h0 < k; h0 += (int64_t)blockDim.x * kRowE) {
+        double x[kRowE];
+        load8(row, h0, k, vec, x);
+#pragma unroll
+        for (int j = 0; j < kRowE; ++j) {
+            bad |= !(fabs(x[j]) <= DBL_MAX);
+            mxd = fmax(mxd, fabs(x[j]));
+        }
+    }
+    if (__syncthreads_or(bad)) {
+        if (threadIdx.x == 0) { flag(st, ERR_A_NONFINITE); atomicMin((unsigned long long*)&st->first_row, row0 + i); }
+        return;
+    }
+    const int sft = row_mu_prime(mxd, mu_prime, st, i, row0);
+    const bool fast = pow2_normal(sft);
+    const double p2 = fast ? pow2d(sft) : 0.0;
     int8_t* out = abar + i * kp;
     bool logic = false;
-    // second pass (row re-read from L2): coalesced loads, each warp store
-    // instruction writes one full 32-byte sector
-#pragma unroll 8
-    for (int64_t h = threadIdx.x; h < kp; h += blockDim.x) {
-        int v = 0;
-        if (h < k) v = ceil_abs_scaled(ld_d(row + h), sft);
-        logic |= v < 0;
-        out[h] = (int8_t)v;
+    // second pass (row re-read from L2); kp is a multiple of 128, columns k.. are zero
+    for (int64_t h0 = (int64_t)threadIdx.x * kRowE; h0 < kp; h0 += (int64_t)blockDim.x * kRowE) {
+        double x[kRowE];
+        load8(row, h0, k, vec, x);
+        *reinterpret_cast<uint2*>(out + h0) = abar8(x, sft, fast, p2, logic);
     }
     if (logic) flag(st, ERR_CEIL_LOGIC);
 }
 
 // Single-pass variant for k <= 16 * blockDim.x (launched up to k = 8192): each
-// thread keeps its (up to 16) elements of the row in registers, so the row is read from HBM once and
-// the ceil pass needs no second load.
+// thread keeps 16 consecutive elements of the row in registers, so the row is
+// read from HBM once and the ceil pass needs no second load.
 constexpr int kRowVPT = 16;
 
 template <class T>
@@ -101,59 +152,30 @@ __global__ void __launch_bounds__(512) row_scan_A_reg_kernel(const T* __restrict
                                                              int64_t row0) {
     const int64_t i = blockIdx.x;
     const T* row = A + i * lda;
-    T v[kRowVPT];
-#pragma unroll
-    for (int q = 0; q < kRowVPT; ++q) {
-        const int64_t h = threadIdx.x + (int64_t)q * blockDim.x;
-        v[q] = h < k ? __ldg(row + h) : T(0);
-    }
-    unsigned long long mx = 0;
+    const bool vec = (reinterpret_cast<uintptr_t>(row) & 15) == 0;
+    const int64_t h0 = (int64_t)threadIdx.x * kRowVPT;
+    double x0[kRowE], x1[kRowE];
+    load8(row, h0, k, vec, x0);
+    load8(row, h0 + kRowE, k, vec, x1);
+    double mxd = 0.0;
     bool bad = false;
 #pragma unroll
-    for (int q = 0; q < kRowVPT; ++q) {
-        const unsigned long long b = abs_bits((double)v[q]);
-        bad |= b >= 0x7ff0000000000000ull;
-        mx = b > mx ? b : mx;
+    for (int j = 0; j < kRowE; ++j) {
+        bad |= !(fabs(x0[j]) <= DBL_MAX) || !(fabs(x1[j]) <= DBL_MAX);
+        mxd = fmax(mxd, fmax(fabs(x0[j]), fabs(x1[j])));
     }
     if (__syncthreads_or(bad)) {
         if (threadIdx.x == 0) { flag(st, ERR_A_NONFINITE); atomicMin((unsigned long long*)&st->first_row, row0 + i); }
         return;
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        const unsigned long long t = __shfl_xor_sync(0xffffffffu, mx, o);
-        mx = t > mx ? t : mx;
-    }
-    __shared__ unsigned long long red[32];
-    __shared__ int s_mup;
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long m2 = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m2 = red[w] > m2 ? red[w] : m2;
-        int mup = 0;
-        if (m2 == 0) {
-            flag(st, ERR_A_ZERO_ROW);
-            atomicMin((unsigned long long*)&st->first_row, row0 + i);
-        } else {
-            mup = 5 - ilogb_exact(__longlong_as_double((long long)m2));
-        }
-        mu_prime[i] = mup;
-        s_mup = mup;
-    }
-    __syncthreads();
-    const int sft = s_mup;
+    const int sft = row_mu_prime(mxd, mu_prime, st, i, row0);
+    const bool fast = pow2_normal(sft);
+    const double p2 = fast ? pow2d(sft) : 0.0;
     int8_t* out = abar + i * kp;
     bool logic = false;
-#pragma unroll
-    for (int q = 0; q < kRowVPT; ++q) {
-        const int64_t h = threadIdx.x + (int64_t)q * blockDim.x;
-        if (h < kp) {
-            const int val = h < k ? ceil_abs_scaled((double)v[q], sft) : 0;
-            logic |= val < 0;
-            out[h] = (int8_t)val;
-        }
-    }
+    // columns k .. kp are zero; a thread past kp (blockDim * 16 > kp) writes nothing
+    if (h0 < kp) *reinterpret_cast<uint2*>(out + h0) = abar8(x0, sft, fast, p2, logic);
+    if (h0 + kRowE < kp) *reinterpret_cast<uint2*>(out + h0 + kRowE) = abar8(x1, sft, fast, p2, logic);
     if (logic) flag(st, ERR_CEIL_LOGIC);
 }
 
