@@ -58,8 +58,11 @@ __device__ __forceinline__ double i8_to_f64_fp(uint32_t wx, int b) {
 
 // NFP of the CV columns convert through i8_to_f64_fp, the rest with I2F (XU):
 // XU converts 16 values/clk/SM, the fp64 pipe 64, so splitting balances them.
+// 8 columns per thread: capped at 64 registers (4 CTAs per SM; the kernel is
+// latency-bound and was at 3 CTAs with 70 registers): 0.238 -> 0.216 ms per
+// 2048-row block at 16384^2 despite a small spill; 5 CTAs spill 112 B, 0.32 ms.
 template <class T, bool DD, bool BND, int NFP, bool INTER, int CV>
-__global__ void __launch_bounds__(256) crt_kernel(const int8_t* __restrict__ W, int64_t ldw, int64_t wplane,
+__global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t* __restrict__ W, int64_t ldw, int64_t wplane,
                                                   int64_t m, int64_t n, const CrtConsts cc,
                                                   const int32_t* __restrict__ mu, const int32_t* __restrict__ nu,
                                                   T* __restrict__ C, int64_t ldc, const CrtExtra ex,
