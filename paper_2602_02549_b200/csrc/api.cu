@@ -299,15 +299,19 @@ int crt_overlap_blocks() {
     return v;
 }
 
-// Speculated exponents on the blocking pipelined host path (run_gemm):
-// OZ2G_SPEC=0 off, 1 column exponents only (B uploaded first), otherwise
-// (default) row and column exponents (A row chunks interleaved with B column
-// chunks).  Read per call.
-int speculation_mode() {
+// Speculated exponents on the pipelined host path (run_gemm): OZ2G_SPEC=0
+// off, 1 column exponents only (B uploaded first), 2 row and column exponents
+// (A row chunks interleaved with B column chunks).  Unset: 2 for inputs of at
+// least 3 GiB, 1 below (measured: row + column speculation wins at 16384^3,
+// 4 GiB, by 4-6%; below that its per-arrival overhead outweighs the earlier
+// start, e.g. 3.8 vs 3.0 ms for SGEMM 4096^3, 41.7 vs 39.9 ms at 2048 x 65536 x
+// 2048).  Read per call.
+int speculation_mode(size_t input_bytes) {
     const char* s = std::getenv("OZ2G_SPEC");
     if (s && s[0] == '0') return 0;
     if (s && s[0] == '1') return 1;
-    return 2;
+    if (s && s[0] == '2') return 2;
+    return input_bytes >= (size_t(3) << 30) ? 2 : 1;
 }
 
 // Raster group height: one wave of persistent CTAs covers group_m tile-rows,
@@ -474,7 +478,8 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     // speculated exponents (blocking pipelined calls): 2 = rows and columns
     // (A row chunks and B column chunks uploaded alternately), 1 = columns
     // (asynchronous calls: rows + columns only; its statuses are merged on the device)
-    const int spec_mode = (pipe && !reuse_scaling && crt_overlap_blocks() <= 1) ? speculation_mode() : 0;
+    const int spec_mode = (pipe && !reuse_scaling && crt_overlap_blocks() <= 1)
+                              ? speculation_mode(esz * (size_t)(m * k + k * n)) : 0;
     const bool spec2 = spec_mode == 2 && n >= 2 * 256;
     // spec2 column chunks: units of cu columns (a multiple of 128), chunks of two
     // units except the last two, one unit each (a short last arrival leaves less
