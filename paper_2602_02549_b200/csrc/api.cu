@@ -712,6 +712,9 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         repaired.assign(nb, 0);
     }
     const ChangeFlags cf1{changed, 0, 256, 0};
+    bool defer1 = false;                    // columns-only speculation: blocks wait for the final exponents
+    int64_t repair_work = 0;                // block tiles recomputed so far
+    std::vector<char> dirty1((size_t)ntiles, 0);  // 256-column tiles whose exponents moved (to repair)
     size_t evn = 0;  // per-call event index (downloads wait for their CRT)
 
     // ---- K5 + K6 of one row block of C (columns c0 .. c0 + nc): residue GEMMs
@@ -776,6 +779,23 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
                                            (const char*)dC + esz * (size_t)(r0 * n + c0), esz * n, esz * nc, rc,
                                            cudaMemcpyDeviceToHost, ws.s_d2h));
             });
+        }
+    };
+
+    // mode 1: redo the dirty 256-column tiles of blocks [0, upto) (their CRT flags
+    // go to the repair statuses; see the fallback after the final status read)
+    auto repair_blocks = [&](size_t upto) {
+        for (size_t bi = 0; bi < upto; ++bi) {
+            bool any = false;
+            for (int64_t t = 0; t < ntiles;) {
+                if (!dirty1[(size_t)t]) { ++t; continue; }
+                int64_t t1 = t + 1;
+                while (t1 < ntiles && dirty1[(size_t)t1]) ++t1;
+                run_block(bi, 256 * t, std::min<int64_t>(n, 256 * t1) - 256 * t, sx + 2 + nb + bi);
+                any = true;
+                t = t1;
+            }
+            if (any) ++repaired[bi];
         }
     };
 
@@ -1036,29 +1056,42 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
                 CUDA_TRY(cudaEventSynchronize(ws.ev_check));
                 moved = ((volatile int32_t*)changed_h)[0] != 0;
             }
-            if (moved) {
+            volatile int32_t* const fl = changed_h;
+            if (c > 0 && moved) {
+                spec_state = 2;
+                int64_t nmoved = 0;
+                for (int64_t t = 0; t < ntiles; ++t) nmoved += fl[1 + t] != 0;
+                // repairs cost (blocks done) x (moved tiles); past an eighth of all
+                // block tiles, stop computing blocks before the final exponents
+                const bool was_deferred = defer1;
+                if (!defer1 && 8 * (repair_work + (int64_t)next_block * nmoved) > (int64_t)nb * ntiles) defer1 = true;
+                for (int64_t t = 0; t < ntiles; ++t)  // tiles to repair (accumulated while deferred)
+                    dirty1[(size_t)t] = (was_deferred && dirty1[(size_t)t]) || fl[1 + t] != 0;
+                if (!defer1) repair_work += (int64_t)next_block * nmoved;
+            }
+            if (moved && !defer1) {  // B residues with the exponents so far, then the repairs
                 tm.span(4, stream, [&] {
                     CUDA_TRY(cudaMemsetAsync(sx + 1, 0, sizeof(DevStatus), stream));
                     CUDA_TRY(launch_resid_B_rows(prec, dB, ldb_d, k, n, kp, ldn, nu, rc_dev, N, bres, sx + 1, stream));
                 });
                 ++launches;
+                if (c > 0) repair_blocks(next_block);
             }
-            if (c > 0 && moved) {  // redo the moved column tiles of every block computed so far
-                spec_state = 2;
-                for (size_t bi = 0; bi < next_block; ++bi) {
-                    repaired[bi] = 1;
-                    for (int64_t t = 0; t < ntiles;) {
-                        if (!((volatile int32_t*)changed_h)[1 + t]) { ++t; continue; }
-                        int64_t t1 = t + 1;
-                        while (t1 < ntiles && ((volatile int32_t*)changed_h)[1 + t1]) ++t1;
-                        run_block(bi, 256 * t, std::min<int64_t>(n, 256 * t1) - 256 * t, sx + 2 + nb + bi);
-                        t = t1;
-                    }
-                }
-            }
-            for (; next_block < nb && blocks[next_block].chunk <= c; ++next_block)
-                run_block(next_block, 0, n, sx + 2 + next_block);
+            if (!defer1)
+                for (; next_block < nb && blocks[next_block].chunk <= c; ++next_block)
+                    run_block(next_block, 0, n, sx + 2 + next_block);
         }
+    }
+    if (spec && defer1) {
+        // the exponents are final: B residues, then the moved tiles of the blocks
+        // computed before deferring, then every remaining block
+        tm.span(4, stream, [&] {
+            CUDA_TRY(cudaMemsetAsync(sx + 1, 0, sizeof(DevStatus), stream));
+            CUDA_TRY(launch_resid_B_rows(prec, dB, ldb_d, k, n, kp, ldn, nu, rc_dev, N, bres, sx + 1, stream));
+        });
+        ++launches;
+        repair_blocks(next_block);
+        for (; next_block < nb; ++next_block) run_block(next_block, 0, n, sx + 2 + next_block);
     }
     if (reduce_fn) {
         if (reduce_fn(cmax_row, m, cmax_col, n, (void*)stream, reduce_user) != 0)
@@ -1204,8 +1237,12 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         std::vector<DevStatus> hx(2 + 2 * nb);
         CUDA_TRY(cudaMemcpy(hx.data(), sx, sizeof(DevStatus) * hx.size(), cudaMemcpyDeviceToHost));
         bool redo = false;
-        for (size_t bi = 0; bi < nb; ++bi)
+        for (size_t bi = 0; bi < nb; ++bi) {
+            // a block whose first CRT, or (repaired more than once) an earlier repair,
+            // raised a flag under exponents that later moved
             redo |= repaired[bi] && (hx[2 + bi].err || hx[2 + bi].subnormal);
+            redo |= repaired[bi] > 1 && (hx[2 + nb + bi].err || hx[2 + nb + bi].subnormal);
+        }
         if (redo) {
             // a block computed with a superseded nu raised a flag that may not
             // hold for the final nu: redo every stage after the upload from the
