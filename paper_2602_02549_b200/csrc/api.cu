@@ -690,7 +690,9 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     // uploading.  After every later chunk's clearance product the exponents
     // are re-derived from the maxima so far; where one moved, the B residues
     // are recomputed and the 256-column tiles holding moved columns are redone
-    // for every block already computed.  After the last chunk nu is final, so C
+    // for every block already computed (once that would exceed an eighth of
+    // all block tiles, the remaining blocks wait for the final exponents and
+    // the moved tiles are repaired once at the end).  After the last chunk nu is final, so C
     // is the unspeculated C bit for bit.  Status flags of the stages that read
     // nu (B residues, CRT) are kept per stage / block so that flags raised with
     // a superseded nu are dropped; a repaired block whose first CRT raised any
