@@ -289,6 +289,7 @@ def main():
         oz.os_ii(a_np, b_np, args.moduli, out=c_np, reduce_maxima=reduce_cb)  # warm
         barrier()
         e_steps = max(1, min(args.steps, 5))
+        p_steps = max(1, min(args.steps, 10))  # a stream of calls: enough of them to amortise fill and drain
         t0 = time.perf_counter()
         for _ in range(e_steps):
             oz.os_ii(a_np, b_np, args.moduli, out=c_np, reduce_maxima=reduce_cb)
@@ -332,11 +333,11 @@ def main():
             oz.os_ii(a_np, b_np, args.moduli, out=c_np, blocking=False)
             oz.synchronize()
             t0 = time.perf_counter()
-            for _ in range(e_steps):
+            for _ in range(p_steps):
                 oz.os_ii(a_np, b_np, args.moduli, out=c_np, blocking=False)
             oz.synchronize()
-            tp = (time.perf_counter() - t0) / e_steps
-            e2e["pipelined"] = {"value": flops / tp / 1e12, "unit": UNIT, "steps": e_steps,
+            tp = (time.perf_counter() - t0) / p_steps
+            e2e["pipelined"] = {"value": flops / tp / 1e12, "unit": UNIT, "steps": p_steps,
                                 "timing": "wall clock around back-to-back os_ii(..., blocking=False) calls and one "
                                           "synchronize(); same host->device / device->host bytes per step"}
             if not torch.equal(torch.from_numpy(c_np).to(dev), Cout):
