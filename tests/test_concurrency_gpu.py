@@ -46,6 +46,47 @@ def test_concurrent_calls_one_device(cuda, oracle):
         assert np.array_equal(np.asarray(got).view(np.uint64), ref.view(np.uint64))
 
 
+def test_concurrent_pipelined_calls(cuda, oracle):
+    """Host-pointer calls large enough for the pipelined, speculated path
+    (chunked uploads, exponent checks through mapped memory) from several
+    threads at once, beside device-pointer calls."""
+    import torch
+    shapes = [(2304, 96, 1100), (2560, 64, 700), (2048, 128, 512)]
+    cases = [(oracle.gen_matrix(m, k, 0.5, 700 + i), oracle.gen_matrix(k, n, 0.5, 800 + i))
+             for i, (m, k, n) in enumerate(shapes)]
+    refs = [oracle.os_ii(a, b, 12).C for a, b in cases]
+    results = [[] for _ in range(4)]
+    errors = []
+
+    def work(t):
+        try:
+            for rep in range(2):
+                i = (t + rep) % len(cases)
+                a, b = cases[i]
+                if t == 3:  # device pointers on a private stream
+                    s = torch.cuda.Stream()
+                    with torch.cuda.stream(s):
+                        c = oz.os_ii(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), 12,
+                                     stream=s.cuda_stream).C
+                        s.synchronize()
+                    results[t].append((i, c.cpu().numpy()))
+                else:
+                    results[t].append((i, oz.os_ii(a, b, 12).C))
+        except Exception as e:  # noqa: BLE001 - reported below
+            errors.append((t, e))
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join(timeout=600)
+    assert not errors, errors
+    for per_thread in results:
+        assert len(per_thread) == 2
+        for i, got in per_thread:
+            assert np.array_equal(np.asarray(got).view(np.uint64), refs[i].view(np.uint64))
+
+
 def test_caller_stream_ordering(cuda, oracle):
     """Inputs produced on the caller's stream are consumed in order on it, and
     the result is ready on that stream when the call returns."""
