@@ -5,6 +5,8 @@ host and device pointers, and strided device operands.  Each C is written into
 a larger sentinel-filled buffer; a write outside the declared m x n window
 fails the test, as does any difference from the oracle (bit-exact C, the same
 exception and message on the error paths)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -79,3 +81,37 @@ def test_fuzz_against_oracle(cuda, oracle, seed):
     Ch = Cd.cpu().numpy()
     assert np.array_equal(np.ascontiguousarray(Ch[:m, :n]).view(np.uint8), ref.C.view(np.uint8))
     assert np.all(Ch[:m, n:] == SENTINEL) and np.all(Ch[m:, :] == SENTINEL)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("OZ2G_FUZZ_SEEDS", "8"))))
+def test_fuzz_pipelined_host_path(cuda, oracle, seed):
+    """Random shapes large enough for the pipelined host path (m >= 2048,
+    n >= 256), random N, precision and exponent spread, under each
+    speculation mode (OZ2G_SPEC 0 / 1 / 2): C bit-exact, the same exception
+    and message on the error paths."""
+    import os
+    rng = np.random.default_rng(7100 + seed)
+    m, n, k = int(rng.integers(2048, 3200)), int(rng.integers(256, 1600)), int(rng.integers(1, 130))
+    dt = np.float64 if rng.random() < 0.7 else np.float32
+    N = int(rng.integers(2, 21 if dt == np.float64 else 17))
+    phi = float(rng.choice([0.0, 0.5, 2.0, 8.0]))
+    A = oracle.gen_matrix(m, k, phi, 7200 + seed).astype(dt)
+    B = oracle.gen_matrix(k, n, phi, 7300 + seed).astype(dt)
+    try:
+        ref, ref_err = oracle.os_ii(A, B, N), None
+    except Exception as e:  # noqa: BLE001 - the device must raise the same
+        ref, ref_err = None, e
+    for mode in ("0", "1", "2"):
+        os.environ["OZ2G_SPEC"] = mode
+        try:
+            got, got_err = oz.os_ii(A, B, N), None
+        except Exception as e:  # noqa: BLE001
+            got, got_err = None, e
+        finally:
+            del os.environ["OZ2G_SPEC"]
+        if ref_err is not None:
+            assert isinstance(got_err, ORACLE_TO_OURS[type(ref_err).__name__]), (mode, got_err, ref_err)
+            assert str(got_err) == str(ref_err), mode
+            continue
+        assert got_err is None, (mode, got_err)
+        assert np.array_equal(got.C.view(np.uint8), ref.C.view(np.uint8)), (mode, m, k, n, N, phi, dt)
