@@ -59,8 +59,10 @@ __device__ __forceinline__ double i8_to_f64_fp(uint32_t wx, int b) {
 // NFP of the CV columns convert through i8_to_f64_fp, the rest with I2F (XU):
 // XU converts 16 values/clk/SM, the fp64 pipe 64, so splitting balances them.
 // 8 columns per thread: capped at 64 registers (4 CTAs per SM; the kernel is
-// latency-bound and was at 3 CTAs with 70 registers): 0.238 -> 0.216 ms per
-// 2048-row block at 16384^2 despite a small spill; 5 CTAs spill 112 B, 0.32 ms.
+// latency-bound and was at 3 CTAs with 70 registers): 0.238 -> 0.206 ms per
+// 2048-row block at 16384^2 with one group of 8 plane loads in flight per
+// thread (double-buffering the groups spilled at 64 registers: 0.216 ms);
+// 5 CTAs spill and lose (0.32 ms).
 template <class T, bool DD, bool BND, int NFP, bool INTER, int CV>
 __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t* __restrict__ W, int64_t ldw, int64_t wplane,
                                                   int64_t m, int64_t n, const CrtConsts cc,
@@ -96,26 +98,15 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
                 if (DD) c2[b] = __fma_rn(s2, wv, c2[b]);
             }
         };
-        // planes in groups of 8, the next group's loads issued before this
-        // group is folded (8-16 loads in flight per thread)
+        // planes in groups of 8 loads in flight per thread
         int l = 0;
         const int nfull = cc.n & ~7;
-        if (nfull) {
+        for (; l < nfull; l += 8) {  // 8 loads in flight per thread; occupancy hides the rest
             Wt cur[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) cur[u] = __ldcs(reinterpret_cast<const Wt*>(wp + (int64_t)u * wplane));
-            for (; l < nfull; l += 8) {
-                Wt nxt[8];
-                if (l + 8 < nfull) {
+            for (int u = 0; u < 8; ++u) cur[u] = __ldcs(reinterpret_cast<const Wt*>(wp + (int64_t)(l + u) * wplane));
 #pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        nxt[u] = __ldcs(reinterpret_cast<const Wt*>(wp + (int64_t)(l + 8 + u) * wplane));
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) fold(cur[u], l + u);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
-            }
+            for (int u = 0; u < 8; ++u) fold(cur[u], l + u);
         }
         for (; l + 4 <= cc.n; l += 4) {
             Wt wv[4];
