@@ -28,6 +28,20 @@ oz.os_ii(Ab[:, :64], Bb[:, :33], 14)
 A = O.gen_matrix(2304, 64, 0.5, 31); B = O.gen_matrix(64, 300, 0.5, 32)
 oz.os_ii(A, B, 16)
 oz.os_ii(A, B, 16, vectors=True)
+# every speculation mode of the pipelined path, bit-identical to the device path
+Ad = oz.os_ii(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), 16).C
+Ad = Ad.cpu().numpy() if hasattr(Ad, "cpu") else np.asarray(Ad)
+for mode in ("0", "1", "2"):
+    os.environ["OZ2G_SPEC"] = mode
+    assert np.array_equal(oz.os_ii(A, B, 16).C.view(np.uint64), Ad.view(np.uint64)), mode
+os.environ.pop("OZ2G_SPEC")
+# asynchronous calls back to back
+outs = [np.empty((A.shape[0], B.shape[1])) for _ in range(3)]
+for c in outs:
+    oz.os_ii(A, B, 16, out=c, blocking=False)
+oz.synchronize()
+for c in outs:
+    assert np.array_equal(c.view(np.uint64), Ad.view(np.uint64))
 # multi-device tiling (device listed twice)
 oz.os_ii(A[:300], B, 12, devices=[0, 0])
 # error paths
