@@ -103,7 +103,9 @@ __device__ __forceinline__ int row_mu_prime(double mxd, int32_t* __restrict__ mu
     return s_mup;
 }
 
-template <class T>
+// U: first-pass steps unrolled (loads in flight per thread); 1 at two rows per
+// SM (32 registers), 4 for the long rows held to one row per SM (launcher)
+template <class T, int U>
 __global__ void __launch_bounds__(1024) row_scan_A_kernel(const T* __restrict__ A, int64_t lda, int64_t k,
                                                          int64_t kp, int32_t* __restrict__ mu_prime,
                                                          int8_t* __restrict__ abar, DevStatus* st,
@@ -113,6 +115,7 @@ __global__ void __launch_bounds__(1024) row_scan_A_kernel(const T* __restrict__ 
     const bool vec = (reinterpret_cast<uintptr_t>(row) & 15) == 0;
     double mxd = 0.0;
     bool bad = false;
+#pragma unroll U
     for (int64_t h0 = (int64_t)threadIdx.x * kRowE; h0 < k; h0 += (int64_t)blockDim.x * kRowE) {
         double x[kRowE];
         load8(row, h0, k, vec, x);
@@ -132,6 +135,7 @@ __global__ void __launch_bounds__(1024) row_scan_A_kernel(const T* __restrict__ 
     int8_t* out = abar + i * kp;
     bool logic = false;
     // second pass (row re-read from L2); kp is a multiple of 128, columns k.. are zero
+#pragma unroll (U > 1 ? 2 : 1)
     for (int64_t h0 = (int64_t)threadIdx.x * kRowE; h0 < kp; h0 += (int64_t)blockDim.x * kRowE) {
         double x[kRowE];
         load8(row, h0, k, vec, x);
@@ -315,8 +319,36 @@ cudaError_t launch_row_scan_A(int prec, const void* A, int64_t lda, int64_t m, i
         if (prec) row_scan_A_reg_kernel<double><<<(unsigned)m, threads, 0, s>>>((const double*)A, lda, k, kp, mu_prime, abar, st, row0);
         else row_scan_A_reg_kernel<float><<<(unsigned)m, threads, 0, s>>>((const float*)A, lda, k, kp, mu_prime, abar, st, row0);
     } else {
-        if (prec) row_scan_A_kernel<double><<<(unsigned)m, 1024, 0, s>>>((const double*)A, lda, k, kp, mu_prime, abar, st, row0);
-        else row_scan_A_kernel<float><<<(unsigned)m, 1024, 0, s>>>((const float*)A, lda, k, kp, mu_prime, abar, st, row0);
+        // rows over 256 KB (k = 65536 fp64): two rows per SM in flight would
+        // outgrow L2 and the second pass would re-read HBM, so an unused
+        // dynamic shared-memory request holds it to one row per SM (cfg5:
+        // DRAM read 2.11 -> 1.11 GB per launch, 0.337 -> 0.324-0.331 ms; the
+        // kernel is bound by the max -> second-pass turnaround, not by HBM)
+        const size_t row_bytes = (size_t)k * (prec ? 8 : 4);
+        const bool long_row = row_bytes > (256u << 10);
+        cudaError_t err;
+        if (long_row) {
+            const size_t pin = 120u << 10;
+            if (prec) {
+                if ((err = cudaFuncSetAttribute(row_scan_A_kernel<double, 4>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pin)) != cudaSuccess)
+                    return err;
+                row_scan_A_kernel<double, 4><<<(unsigned)m, 1024, pin, s>>>((const double*)A, lda, k, kp, mu_prime,
+                                                                           abar, st, row0);
+            } else {
+                if ((err = cudaFuncSetAttribute(row_scan_A_kernel<float, 4>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pin)) != cudaSuccess)
+                    return err;
+                row_scan_A_kernel<float, 4><<<(unsigned)m, 1024, pin, s>>>((const float*)A, lda, k, kp, mu_prime,
+                                                                          abar, st, row0);
+            }
+        } else if (prec) {
+            row_scan_A_kernel<double, 1><<<(unsigned)m, 1024, 0, s>>>((const double*)A, lda, k, kp, mu_prime, abar, st,
+                                                                     row0);
+        } else {
+            row_scan_A_kernel<float, 1><<<(unsigned)m, 1024, 0, s>>>((const float*)A, lda, k, kp, mu_prime, abar, st,
+                                                                    row0);
+        }
     }
     return cudaGetLastError();
 }

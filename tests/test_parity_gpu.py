@@ -52,6 +52,9 @@ CASES = [
     (7, 20, 6, 0.0, 9, np.float32),
     (33, 100, 65, 0.5, 8, np.float32),
     (130, 300, 260, 2.0, 16, np.float32),
+    # rows over 256 KB: the row scan held to one row per SM (scale.cu)
+    (5, 40000, 3, 0.5, 12, np.float64),
+    (4, 70000, 3, 2.0, 8, np.float32),
 ]
 
 
