@@ -10,6 +10,7 @@
 //                maxima with the host-built step table (tables.cpp)
 //   (the residue planes and Bbar^T are written by resid.cu)
 #include <cfloat>
+#include <cstdlib>
 
 #include "device_common.cuh"
 #include "kernels.h"
@@ -29,7 +30,7 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
 
 // ---------------------------------------------------------------------------
 // A: one CTA per row (two passes; the second re-reads the row from L2).
-// blockDim is 256 or 1024 (launcher); the reductions below handle both.  Each
+// blockDim is 256, 512 or 1024 (launcher); the reductions handle each.  Each
 // thread takes 8 consecutive elements per step (16-byte loads, one 8-byte
 // store of Abar); the max runs on the fp64 pipe (fmax of |x|, non-finite
 // detected by |x| <= DBL_MAX) and Abar = ceil(2^mu' |a|) too (ceil_scaled_p2),
@@ -310,9 +311,8 @@ cudaError_t launch_row_scan_A(int prec, const void* A, int64_t lda, int64_t m, i
     if (m == 0) return cudaSuccess;
     // ~16 elements per thread, 32..512 threads per row: up to k = 8192 the row
     // stays in registers (one HBM pass, several rows per SM); longer rows use
-    // two passes with 1024 threads (~2 rows per SM in flight, the second pass
-    // hits L2) — measured faster at k = 16384 than one 1024-thread
-    // register-resident row per SM (0.86 vs 0.90-0.98 ms at 16384^2)
+    // two passes (the second hits L2) — measured faster at k = 16384 than one
+    // 1024-thread register-resident row per SM (0.86 vs 0.90-0.98 ms at 16384^2)
     const int64_t want = (k + kRowVPT - 1) / kRowVPT;
     if (want <= 512) {
         const unsigned threads = (unsigned)(want <= 32 ? 32 : (want + 31) / 32 * 32);
@@ -342,12 +342,23 @@ cudaError_t launch_row_scan_A(int prec, const void* A, int64_t lda, int64_t m, i
                 row_scan_A_kernel<float, 4><<<(unsigned)m, 1024, pin, s>>>((const float*)A, lda, k, kp, mu_prime,
                                                                           abar, st, row0);
             }
-        } else if (prec) {
-            row_scan_A_kernel<double, 1><<<(unsigned)m, 1024, 0, s>>>((const double*)A, lda, k, kp, mu_prime, abar, st,
-                                                                     row0);
         } else {
-            row_scan_A_kernel<float, 1><<<(unsigned)m, 1024, 0, s>>>((const float*)A, lda, k, kp, mu_prime, abar, st,
-                                                                    row0);
+            // 512 threads (4 rows per SM in flight) up to 128 KB rows, 1024 (2
+            // per SM) above, so the rows in flight stay within L2: at 16384^2
+            // 0.51 vs 0.62 ms per launch (256 threads: 0.65, 4.2 GB read);
+            // OZ2G_ROWSCAN_THREADS=256/512/1024 overrides (experiments)
+            static const int thr_env = [] {
+                const char* e = std::getenv("OZ2G_ROWSCAN_THREADS");
+                const int v = e ? std::atoi(e) : 0;
+                return v == 256 || v == 512 || v == 1024 ? v : 0;
+            }();
+            const unsigned thr = thr_env ? (unsigned)thr_env : row_bytes <= (128u << 10) ? 512u : 1024u;
+            if (prec)
+                row_scan_A_kernel<double, 1><<<(unsigned)m, thr, 0, s>>>((const double*)A, lda, k, kp, mu_prime, abar,
+                                                                        st, row0);
+            else
+                row_scan_A_kernel<float, 1><<<(unsigned)m, thr, 0, s>>>((const float*)A, lda, k, kp, mu_prime, abar,
+                                                                       st, row0);
         }
     }
     return cudaGetLastError();
