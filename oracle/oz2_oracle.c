@@ -381,7 +381,7 @@ static void ceil_row(int64_t i, void *v) {
     }
 }
 
-/* scaling.hpp:286-315 truncate_scaled_rows/cols */
+/* scaling.hpp:199-225 truncate_scaled_rows/cols */
 static void trunc_row(int64_t i, void *v) {
     map_ctx *c = (map_ctx *)v;
     for (int64_t h = 0; h < c->cols; ++h) {
@@ -715,43 +715,51 @@ int ora_ceil_scale(const double *X, int64_t rows, int64_t cols, const int16_t *s
     return c.err ? ORA_LOGIC : ORA_OK;
 }
 
-/* Row maxima of Cbar = Abar * Bbar for selected rows (scaling.hpp:175-183). */
+/* Row maxima of Cbar = Abar * Bbar for selected rows (scaling.hpp:175-183);
+ * one selected row per parallel_for index. */
+typedef struct { const int8_t *abar, *bbar; int64_t m, k, n; const int64_t *idx; int32_t *out; } cm_ctx;
+static void cm_row(int64_t q, void *v) {
+    const cm_ctx *c = (const cm_ctx *)v;
+    int32_t *acc = (int32_t *)xmalloc(sizeof(int32_t) * (size_t)c->n);
+    memset(acc, 0, sizeof(int32_t) * (size_t)c->n);
+    const int8_t *a = c->abar + c->idx[q] * c->k;
+    for (int64_t h = 0; h < c->k; ++h) {
+        const int32_t av = a[h];
+        if (!av) continue;
+        const int8_t *b = c->bbar + h * c->n;
+        for (int64_t j = 0; j < c->n; ++j) acc[j] += av * (int32_t)b[j];
+    }
+    int32_t mx = 0;
+    for (int64_t j = 0; j < c->n; ++j) mx = acc[j] > mx ? acc[j] : mx;
+    c->out[q] = mx;
+    free(acc);
+}
 int ora_cbar_row_max(const int8_t *abar, const int8_t *bbar, int64_t k, int64_t n, const int64_t *rows,
                      int64_t count, int32_t *out) {
-    int32_t *acc = (int32_t *)xmalloc(sizeof(int32_t) * (size_t)n);
-    for (int64_t q = 0; q < count; ++q) {
-        memset(acc, 0, sizeof(int32_t) * (size_t)n);
-        const int8_t *a = abar + rows[q] * k;
-        for (int64_t h = 0; h < k; ++h) {
-            const int32_t av = a[h];
-            if (!av) continue;
-            const int8_t *b = bbar + h * n;
-            for (int64_t j = 0; j < n; ++j) acc[j] += av * (int32_t)b[j];
-        }
-        int32_t mx = 0;
-        for (int64_t j = 0; j < n; ++j) mx = acc[j] > mx ? acc[j] : mx;
-        out[q] = mx;
-    }
-    free(acc);
+    cm_ctx c = {abar, bbar, 0, k, n, rows, out};
+    parallel_for(count, cm_row, &c);
     return ORA_OK;
 }
 
 /* Column maxima of Cbar for selected columns (scaling.hpp:184-192). */
+static void cm_col(int64_t q, void *v) {
+    const cm_ctx *c = (const cm_ctx *)v;
+    int8_t *bc = (int8_t *)xmalloc((size_t)c->k);
+    for (int64_t h = 0; h < c->k; ++h) bc[h] = c->bbar[h * c->n + c->idx[q]];
+    int32_t mx = 0;
+    for (int64_t i = 0; i < c->m; ++i) {
+        const int8_t *a = c->abar + i * c->k;
+        int32_t s = 0;
+        for (int64_t h = 0; h < c->k; ++h) s += (int32_t)a[h] * (int32_t)bc[h];
+        mx = s > mx ? s : mx;
+    }
+    c->out[q] = mx;
+    free(bc);
+}
 int ora_cbar_col_max(const int8_t *abar, const int8_t *bbar, int64_t m, int64_t k, int64_t n, const int64_t *cols,
                      int64_t count, int32_t *out) {
-    int8_t *bc = (int8_t *)xmalloc((size_t)k);
-    for (int64_t q = 0; q < count; ++q) {
-        for (int64_t h = 0; h < k; ++h) bc[h] = bbar[h * n + cols[q]];
-        int32_t mx = 0;
-        for (int64_t i = 0; i < m; ++i) {
-            const int8_t *a = abar + i * k;
-            int32_t s = 0;
-            for (int64_t h = 0; h < k; ++h) s += (int32_t)a[h] * (int32_t)bc[h];
-            mx = s > mx ? s : mx;
-        }
-        out[q] = mx;
-    }
-    free(bc);
+    cm_ctx c = {abar, bbar, m, k, n, cols, out};
+    parallel_for(count, cm_col, &c);
     return ORA_OK;
 }
 
@@ -760,43 +768,51 @@ int ora_cbar_col_max(const int8_t *abar, const int8_t *bbar, int64_t m, int64_t 
  * wrapped dot products and signed mod (crt.hpp:69-79), accumulate / Q /
  * final_reduce (crt.hpp:91-150), inverse_scale (emulate.hpp:30-46).
  * prec: 0 fp32 (C out as float), 1 fp64. */
+typedef struct {
+    int prec; const double *A, *B; int64_t k, n; const int16_t *mu, *nu; const int64_t *ri, *cj;
+    const ora_table *t; void *out; volatile int err;
+} en_ctx;
+static void en_one(int64_t q, void *v) {
+    en_ctx *c = (en_ctx *)v;
+    const ora_table *t = c->t;
+    const int N = t->n;
+    const int64_t k = c->k, n = c->n, i = c->ri[q], j = c->cj[q];
+    int8_t *ar = (int8_t *)xmalloc((size_t)k), *bc = (int8_t *)xmalloc((size_t)k);
+    double c1 = 0.0, c2 = 0.0;
+    for (int l = 0; l < N; ++l) {
+        const int p = t->p[l];
+        for (int64_t h = 0; h < k; ++h) {
+            const double a = trunc(ldexp(c->A[i * k + h], c->mu[i]));
+            const double b = trunc(ldexp(c->B[h * n + j], c->nu[j]));
+            if (!isfinite(a) || !isfinite(b)) { c->err = ORA_RANGE; free(ar); free(bc); return; }
+            ora_residue_of(a, p, &ar[h]);
+            ora_residue_of(b, p, &bc[h]);
+        }
+        uint32_t acc = 0;
+        for (int64_t h = 0; h < k; ++h) acc += (uint32_t)((int32_t)ar[h] * (int32_t)bc[h]);
+        long long w = signed_mod_ll((long long)(int32_t)acc, p);
+        if (2 * w == p) w = -w;
+        const double wv = (double)(int8_t)w;
+        c1 = fma(t->s1[l], wv, c1);
+        if (t->mode == 1) c2 = fma(t->s2[l], wv, c2);
+    }
+    const double qv = round_nearest_even(t->P_inv * c1);
+    const double t1 = fma(-qv, t->P1, c1);
+    const double t2 = t1 + c2;
+    const double cpp = fma(-qv, t->P2, t2);
+    if (c->prec == 0) {
+        const float x = ldexpf((float)cpp, -c->mu[i]);
+        ((float *)c->out)[q] = ldexpf(x, -c->nu[j]);
+    } else {
+        const double x = ldexp(cpp, -c->mu[i]);
+        ((double *)c->out)[q] = ldexp(x, -c->nu[j]);
+    }
+    free(ar); free(bc);
+}
 int ora_entries(int prec, const double *A, const double *B, int64_t k, int64_t n, const int16_t *mu,
                 const int16_t *nu, const int64_t *ri, const int64_t *cj, int64_t count, const ora_table *t,
                 void *out) {
-    const int N = t->n;
-    int8_t *ar = (int8_t *)xmalloc((size_t)k), *bc = (int8_t *)xmalloc((size_t)k);
-    for (int64_t q = 0; q < count; ++q) {
-        const int64_t i = ri[q], j = cj[q];
-        double c1 = 0.0, c2 = 0.0;
-        for (int l = 0; l < N; ++l) {
-            const int p = t->p[l];
-            for (int64_t h = 0; h < k; ++h) {
-                const double a = trunc(ldexp(A[i * k + h], mu[i]));
-                const double b = trunc(ldexp(B[h * n + j], nu[j]));
-                if (!isfinite(a) || !isfinite(b)) { free(ar); free(bc); return ORA_RANGE; }
-                ora_residue_of(a, p, &ar[h]);
-                ora_residue_of(b, p, &bc[h]);
-            }
-            uint32_t acc = 0;
-            for (int64_t h = 0; h < k; ++h) acc += (uint32_t)((int32_t)ar[h] * (int32_t)bc[h]);
-            long long v = signed_mod_ll((long long)(int32_t)acc, p);
-            if (2 * v == p) v = -v;
-            const double wv = (double)(int8_t)v;
-            c1 = fma(t->s1[l], wv, c1);
-            if (t->mode == 1) c2 = fma(t->s2[l], wv, c2);
-        }
-        const double qv = round_nearest_even(t->P_inv * c1);
-        const double t1 = fma(-qv, t->P1, c1);
-        const double t2 = t1 + c2;
-        const double cpp = fma(-qv, t->P2, t2);
-        if (prec == 0) {
-            const float x = ldexpf((float)cpp, -mu[i]);
-            ((float *)out)[q] = ldexpf(x, -nu[j]);
-        } else {
-            const double x = ldexp(cpp, -mu[i]);
-            ((double *)out)[q] = ldexp(x, -nu[j]);
-        }
-    }
-    free(ar); free(bc);
-    return ORA_OK;
+    en_ctx c = {prec, A, B, k, n, mu, nu, ri, cj, t, out, 0};
+    parallel_for(count, en_one, &c);
+    return c.err ? c.err : ORA_OK;
 }

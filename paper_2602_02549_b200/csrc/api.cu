@@ -115,6 +115,10 @@ struct Workspace {
     int ring_next = 0;
     std::vector<Pending> pending;
     cudaEvent_t ev_inputs_free = nullptr;  // the last read of the device copies of A and B
+    // end of the last OZ2G_ASYNC call and its stream: an asynchronous call on
+    // another stream waits for it (every call shares this workspace's buffers)
+    cudaEvent_t ev_last_async = nullptr;
+    cudaStream_t last_async_stream = nullptr;
     std::vector<cudaEvent_t> ev_pool;  // per-block events of the overlapped CRT
     cudaEvent_t pool_event(size_t i) {
         while (ev_pool.size() <= i) {
@@ -344,15 +348,17 @@ bool status_failure(const DevStatus& hs, int64_t row_base, int64_t col_base, Fai
         out.index = index;
         return true;
     };
-    if (e & (ERR_A_NONFINITE | ERR_A_ZERO_ROW)) {
-        if (e & ERR_A_NONFINITE) return fail(OZ2G_DOMAIN_ERROR, "matrix entry is not finite", 0, -1);
-        snprintf(buf, sizeof buf, "row_pre_exponents: zero row %lld", (long long)(hs.first_row + row_base));
-        return fail(OZ2G_DOMAIN_ERROR, buf, 0, hs.first_row + row_base);
+    if (e & (ERR_A_NONFINITE | ERR_A_ZERO_ROW)) {  // the first failing row decides (status_key)
+        const int64_t row = (hs.first_row >> 1) + row_base;
+        if (hs.first_row & 1) return fail(OZ2G_DOMAIN_ERROR, "matrix entry is not finite", 0, row);
+        snprintf(buf, sizeof buf, "row_pre_exponents: zero row %lld", (long long)row);
+        return fail(OZ2G_DOMAIN_ERROR, buf, 0, row);
     }
-    if (e & ERR_B_NONFINITE) return fail(OZ2G_DOMAIN_ERROR, "matrix entry is not finite", 1, -1);
-    if (e & ERR_B_ZERO_COL) {
-        snprintf(buf, sizeof buf, "col_pre_exponents: zero column %lld", (long long)(hs.first_col + col_base));
-        return fail(OZ2G_DOMAIN_ERROR, buf, 1, hs.first_col + col_base);
+    if (e & (ERR_B_NONFINITE | ERR_B_ZERO_COL)) {
+        const int64_t col = (hs.first_col >> 1) + col_base;
+        if (hs.first_col & 1) return fail(OZ2G_DOMAIN_ERROR, "matrix entry is not finite", 1, col);
+        snprintf(buf, sizeof buf, "col_pre_exponents: zero column %lld", (long long)col);
+        return fail(OZ2G_DOMAIN_ERROR, buf, 1, col);
     }
     if (e & ERR_CEIL_LOGIC) return fail(OZ2G_LOGIC_ERROR, "ceil_abs_scaled: entry above row/column max", 2);
     if (e & ERR_E_LOGIC) return fail(OZ2G_LOGIC_ERROR, "scaling_exponents: e_i >= 31", 3);
@@ -455,6 +461,8 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         Fail f{OZ2G_OK, ""};
         if (complete_pending(ws, f)) throw f;
     }
+    if (async && !ws.pending.empty() && ws.last_async_stream != stream)
+        CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_last_async, 0));
 
     Timer tm;
     tm.on = diag && (flags & OZ2G_TIMING);
@@ -1219,6 +1227,9 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     }
 
     if (async) {
+        if (!ws.ev_last_async) CUDA_TRY(cudaEventCreateWithFlags(&ws.ev_last_async, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(ws.ev_last_async, stream));
+        ws.last_async_stream = stream;
         CUDA_TRY(cudaGetLastError());
         ws.pending.push_back({ring_slot, row_base, col_base, stream});
         if (diag) diag->kernels_launched = launches;
@@ -1492,6 +1503,12 @@ int run_gemm_multi(int prec, int64_t m, int64_t n, int64_t k, const void* A, int
     for (int t = 0; t < count; ++t)
         if (devices[t] < 0 || devices[t] >= ndev) throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_gemm_multi: no such device"};
     if (diag) std::memset(diag, 0, sizeof *diag);
+    // every tile thread holds its workspace lock while it waits at the
+    // cross-tile barrier of the maxima exchange: two multi calls interleaving
+    // their tiles over the same (device, slot) workspaces could each hold a
+    // lock the other's barrier waits on, so multi calls run one at a time
+    static std::mutex multi_mtx;
+    std::lock_guard<std::mutex> multi_lock(multi_mtx);
     const size_t esz = prec ? 8 : 4;
     int R = 1, Cg = 1;
     grid_shape(count, R, Cg);
@@ -1587,6 +1604,12 @@ int run_gemm_sweep(int prec, int64_t m, int64_t n, int64_t k, const void* A, int
         DevBuf *a, *b, *c;
         ~Release() { a->release(); b->release(); c->release(); }
     } rel{&bufA, &bufB, &bufC};
+    // later iterations reuse mu', nu' and the clearance maxima left in the
+    // device workspace by the first: hold its lock for the whole sweep so no
+    // concurrent call on this device can overwrite them in between
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::recursive_mutex> sweep_lock(workspace(dev, 0).mtx);
     for (int i = 0; i < count; ++i) {
         void* Ci = host ? dC : C[i];
         oz2g_diag d;

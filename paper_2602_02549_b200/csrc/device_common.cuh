@@ -33,9 +33,16 @@ enum ErrBits : uint32_t {
 struct DevStatus {
     uint32_t err;
     uint32_t subnormal;
-    int64_t first_row;  // atomicMin target for zero-row / zero-col messages
-    int64_t first_col;
+    int64_t first_row;  // atomicMin targets: status_key of the first failing row of A /
+    int64_t first_col;  // column of B (zero or non-finite), as the reference scans in order
 };
+
+// 2 * index + kind: the smallest key is the first failing row / column, and
+// its low bit says whether it failed as non-finite (1) or all-zero (0)
+// (scaling.hpp:33-52 throws at the first bad row, whichever the kind).
+__host__ __device__ inline long long status_key(int64_t index, bool nonfinite) {
+    return 2 * (long long)index + (nonfinite ? 1 : 0);
+}
 
 // ----------------------------------------------------------------------------
 // Exact fp helpers

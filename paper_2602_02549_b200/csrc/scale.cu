@@ -93,7 +93,7 @@ __device__ __forceinline__ int row_mu_prime(double mxd, int32_t* __restrict__ mu
         int mup = 0;
         if (m2 == 0) {
             flag(st, ERR_A_ZERO_ROW);
-            atomicMin((unsigned long long*)&st->first_row, row0 + i);
+            atomicMin((unsigned long long*)&st->first_row, status_key(row0 + i, false));
         } else {
             mup = 5 - ilogb_exact(__longlong_as_double((long long)m2));
         }
@@ -127,7 +127,10 @@ __global__ void __launch_bounds__(1024) row_scan_A_kernel(const T* __restrict__ 
         }
     }
     if (__syncthreads_or(bad)) {
-        if (threadIdx.x == 0) { flag(st, ERR_A_NONFINITE); atomicMin((unsigned long long*)&st->first_row, row0 + i); }
+        if (threadIdx.x == 0) {
+            flag(st, ERR_A_NONFINITE);
+            atomicMin((unsigned long long*)&st->first_row, status_key(row0 + i, true));
+        }
         return;
     }
     const int sft = row_mu_prime(mxd, mu_prime, st, i, row0);
@@ -170,7 +173,10 @@ __global__ void __launch_bounds__(512) row_scan_A_reg_kernel(const T* __restrict
         mxd = fmax(mxd, fmax(fabs(x0[j]), fabs(x1[j])));
     }
     if (__syncthreads_or(bad)) {
-        if (threadIdx.x == 0) { flag(st, ERR_A_NONFINITE); atomicMin((unsigned long long*)&st->first_row, row0 + i); }
+        if (threadIdx.x == 0) {
+            flag(st, ERR_A_NONFINITE);
+            atomicMin((unsigned long long*)&st->first_row, status_key(row0 + i, true));
+        }
         return;
     }
     const int sft = row_mu_prime(mxd, mu_prime, st, i, row0);
@@ -203,7 +209,9 @@ __global__ void __launch_bounds__(256) col_max_B_kernel(const T* __restrict__ B,
         bad |= b >= 0x7ff0000000000000ull;
         mx = b > mx ? b : mx;
     }
-    if (bad) { flag(st, ERR_B_NONFINITE); return; }
+    // a non-finite entry leaves bits >= 0x7ff0... in bmax[j]: col_exp_B reports
+    // it with the column index, so the first failing column decides the message
+    (void)bad;
     if (mx) atomicMax(&bmax[j], mx);
 }
 
@@ -212,9 +220,15 @@ __global__ void col_exp_B_kernel(const unsigned long long* __restrict__ bmax, in
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     const unsigned long long b = bmax[j];
+    if (b >= 0x7ff0000000000000ull) {  // col_abs_max: non-finite entry (scaling.hpp:43-51)
+        flag(st, ERR_B_NONFINITE);
+        atomicMin((unsigned long long*)&st->first_col, status_key(col0 + j, true));
+        nu_prime[j] = 0;
+        return;
+    }
     if (b == 0) {
         flag(st, ERR_B_ZERO_COL);
-        atomicMin((unsigned long long*)&st->first_col, col0 + j);
+        atomicMin((unsigned long long*)&st->first_col, status_key(col0 + j, false));
         nu_prime[j] = 0;
         return;
     }

@@ -178,6 +178,13 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
         k2, nn = b.shape
         if k != k2:
             raise InvalidArgument("dimension mismatch: os_ii inner dimension")
+        if out is not None:
+            if not _is_torch_cuda(out) or out.device != a.device:
+                raise InvalidArgument("os_ii: out must be a CUDA tensor on the device of A and B")
+            if out.dtype != a.dtype or tuple(out.shape) != (m, nn):
+                raise InvalidArgument(f"os_ii: out must be {m}x{nn} {a.dtype}")
+            if nn > 1 and out.stride(1) != 1 or m > 1 and out.stride(0) < nn:
+                raise InvalidArgument("os_ii: out must be row-major with unit column stride")
         C_out = out if out is not None else torch.empty((m, nn), dtype=a.dtype, device=a.device)
         pa, pb, pc = a.data_ptr(), b.data_ptr(), C_out.data_ptr()
         lda, ldb, ldc = max(a.stride(0), k), max(b.stride(0), nn), max(C_out.stride(0), nn)
@@ -198,9 +205,22 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
         prec = F64 if a.dtype == np.float64 else F32
         m, k = a.shape
         nn = b.shape[1]
+        ldc = nn
+        if out is not None:
+            if not isinstance(out, np.ndarray):
+                raise InvalidArgument("os_ii: out must be a numpy array for host inputs")
+            if out.dtype != a.dtype or out.shape != (m, nn):
+                raise InvalidArgument(f"os_ii: out must be {m}x{nn} {a.dtype}")
+            isz = out.itemsize
+            if (nn > 1 and out.strides[1] != isz) or (m > 1 and (out.strides[0] % isz or out.strides[0] < nn * isz)):
+                raise InvalidArgument("os_ii: out must be row-major with unit column stride")
+            if not out.flags.writeable:
+                raise InvalidArgument("os_ii: out is read-only")
+            if m > 1:
+                ldc = out.strides[0] // isz
         C_out = np.empty((m, nn), dtype=a.dtype) if out is None else out
         pa, pb, pc = a.ctypes.data, b.ctypes.data, C_out.ctypes.data
-        lda, ldb, ldc = k, nn, nn
+        lda, ldb = k, nn
         flags = _lib.OZ2G_HOST_PTRS
     if timing:
         flags |= _lib.OZ2G_TIMING

@@ -33,6 +33,16 @@ def _cases(oracle, m, k, n):
     a = A.copy(); a[m - 7, :] = 0.0
     b = B.copy(); b[:, 1] = 0.0
     out["zero row and column: the row is reported"] = (a, b)
+    # the first failing row / column decides the message, whatever its kind
+    # (scaling.hpp:33-52 and :86-107 scan in order)
+    a = A.copy(); a[3, :] = 0.0; a[m - 7, 5] = np.nan
+    out["zero row before a nan row"] = (a, B)
+    a = A.copy(); a[2, 1] = np.nan; a[m - 7, :] = 0.0
+    out["nan row before a zero row"] = (a, B)
+    b = B.copy(); b[:, 1] = 0.0; b[2, n - 2] = np.inf
+    out["zero column before an inf column"] = (A, b)
+    b = B.copy(); b[0, 1] = np.inf; b[:, n - 2] = 0.0
+    out["inf column before a zero column"] = (A, b)
     return out
 
 

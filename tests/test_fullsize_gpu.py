@@ -2,14 +2,20 @@
 
 The CPU oracle cannot run a 16384^3, N = 16 emulation (~1.5e14 int8 ops), so
 the device result is verified piecewise with the oracle's exact pieces
-(oracle/oz2_oracle.c, "sampled full-size checks"):
+(oracle/oz2_oracle.c, "sampled full-size checks"), none of which reads a
+device intermediate:
   * mu' and nu' for EVERY row / column (scaling.hpp:86-107);
-  * the clearance-product maxima on sampled rows and columns (O(nk) each,
-    scaling.hpp:140-192) — the device computes them with fused atomics;
-  * mu and nu for EVERY row / column from the maxima (scaling.hpp:159-194);
-  * C at sampled entries, recomputed by the reference pipeline (residues, N
-    wrapped dot products, CRT, inverse scaling) from the device's mu / nu:
-    bit-exact.
+  * the clearance-product maxima of >= 64 rows (every 2048-row block edge of
+    the residue GEMM + CRT, api.cu kWBlockRows, and both ends) and >= 64
+    columns (every 256-column tile edge sampled), computed by the oracle from
+    its own Abar / Bbar (scaling.hpp:111-192);
+  * mu and nu of those rows / columns from the ORACLE's maxima
+    (scaling.hpp:159-194), against the device's;
+  * C at >= 128 entries on those rows x columns, recomputed by the reference
+    pipeline (residues, N wrapped dot products, CRT, inverse scaling) with
+    the oracle's mu / nu: bit-exact;
+  * and, for every row / column, that the device's mu / nu are the step
+    function of its own maxima (the exponents kernel).
 """
 import numpy as np
 import pytest
@@ -18,8 +24,10 @@ import paper_2602_02549_b200 as oz
 
 pytestmark = pytest.mark.gpu
 
+BLOCK_ROWS = 2048  # row block of the residue GEMMs + CRT (api.cu kWBlockRows)
 
-def _gen(shape, phi, seed):
+
+def _gen(shape, phi, seed, dtype=None):
     import torch
     g = torch.Generator(device="cuda")
     g.manual_seed(seed)
@@ -27,8 +35,70 @@ def _gen(shape, phi, seed):
     v = u - 0.5
     if phi:
         v = v * torch.exp(torch.randn(shape, dtype=torch.float64, device="cuda", generator=g) * phi)
+    if dtype is not None:
+        v = v.to(dtype)
     v[v == 0] = 0.25
-    return v
+    return v.contiguous()
+
+
+def sample_rows(m, rng, count=64):
+    edges = {0, m - 1}
+    for r in range(BLOCK_ROWS, m, BLOCK_ROWS):
+        edges.update((r - 1, r))
+    rest = [int(x) for x in rng.permutation(m) if int(x) not in edges]
+    return np.array(sorted(edges | set(rest[:max(0, count - len(edges))])), dtype=np.int64)
+
+
+def sample_cols(n, rng, count=64):
+    edges = {0, n - 1}
+    for c in range(256, n, 256 * max(1, n // 256 // 16)):
+        edges.update((c - 1, c))
+    rest = [int(x) for x in rng.permutation(n) if int(x) not in edges]
+    return np.array(sorted(edges | set(rest[:max(0, count - len(edges))])), dtype=np.int64)
+
+
+def check_sampled(oracle, A, B, res, N, prec, rng, n_entries=128):
+    """The oracle-only checks above on host copies A, B (float64 values) of the inputs."""
+    m, k = A.shape
+    n = B.shape[1]
+    s = res.scaling
+    C = res.C.cpu().numpy() if hasattr(res.C, "cpu") else res.C
+    oracle.set_threads(16)
+    mup = oracle.pre_exponents(A, False)
+    nup = oracle.pre_exponents(B, True)
+    assert np.array_equal(mup, s.mu_prime) and np.array_equal(nup, s.nu_prime)
+    abar = oracle.ceil_scale(A, mup, False)
+    bbar = oracle.ceil_scale(B, nup, True)
+    rows, cols = sample_rows(m, rng), sample_cols(n, rng)
+    assert len(rows) >= min(64, m) and len(cols) >= min(64, n)
+    cmr = oracle.cbar_row_max(abar, bbar, rows)
+    cmc = oracle.cbar_col_max(abar, bbar, cols)
+    del abar, bbar
+    assert np.array_equal(cmr, s.cmax_row[rows]), "clearance row maxima"
+    assert np.array_equal(cmc, s.cmax_col[cols]), "clearance column maxima"
+    mu_o = np.array([mup[i] + oracle.shift_of_cmax(int(c), N)[0] for i, c in zip(rows, cmr)], dtype=np.int16)
+    nu_o = np.array([nup[j] + oracle.shift_of_cmax(int(c), N)[0] for j, c in zip(cols, cmc)], dtype=np.int16)
+    assert np.array_equal(mu_o, s.mu[rows]) and np.array_equal(nu_o, s.nu[cols])
+    # every row / column: the device exponents are the step function of the device maxima
+    sh_r = np.array([oracle.shift_of_cmax(int(c), N)[0] for c in s.cmax_row])
+    sh_c = np.array([oracle.shift_of_cmax(int(c), N)[0] for c in s.cmax_col])
+    assert np.array_equal(s.mu, (s.mu_prime + sh_r).astype(np.int16))
+    assert np.array_equal(s.nu, (s.nu_prime + sh_c).astype(np.int16))
+    # C on rows x cols with the oracle's mu / nu (every sampled row and column at least once)
+    nr, nc = len(rows), len(cols)
+    extra = max(0, n_entries - nr - nc)
+    qi = np.concatenate([np.arange(nr), rng.integers(0, nr, nc), rng.integers(0, nr, extra)])
+    qj = np.concatenate([rng.integers(0, nc, nr), np.arange(nc), rng.integers(0, nc, extra)])
+    mu_full = np.zeros(m, dtype=np.int16)
+    nu_full = np.zeros(n, dtype=np.int16)
+    mu_full[rows] = mu_o
+    nu_full[cols] = nu_o
+    ri, cj = rows[qi], cols[qj]
+    ref = oracle.entries(A, B, N, mu_full, nu_full, ri, cj, prec=prec)
+    got = C[ri, cj]
+    bits = np.uint64 if prec else np.uint32
+    bad = np.flatnonzero(got.view(bits) != ref.view(bits))
+    assert bad.size == 0, f"{bad.size} of {len(ri)} sampled C entries differ, first ({ri[bad[0]]}, {cj[bad[0]]})"
 
 
 @pytest.mark.parametrize("m,k,n,N,phi", [
@@ -42,28 +112,5 @@ def test_sampled_parity_full_size(cuda, oracle, m, k, n, N, phi):
     res = oz.os_ii(dA, dB, N, vectors=True)
     torch.cuda.synchronize()
     A, B = dA.cpu().numpy(), dB.cpu().numpy()
-    C = res.C.cpu().numpy()
-    s = res.scaling
-    oracle.set_threads(8)
-    mup = oracle.pre_exponents(A, False)
-    nup = oracle.pre_exponents(B, True)
-    assert np.array_equal(mup, s.mu_prime) and np.array_equal(nup, s.nu_prime)
-    rng = np.random.default_rng(m + n + N)
-    abar = oracle.ceil_scale(A, mup, False)
-    bbar = oracle.ceil_scale(B, nup, True)
-    rows = np.unique(np.concatenate([[0, m - 1], rng.integers(0, m, 3)]))
-    cols = np.unique(np.concatenate([[0, n - 1], rng.integers(0, n, 3)]))
-    assert np.array_equal(oracle.cbar_row_max(abar, bbar, rows), s.cmax_row[rows])
-    assert np.array_equal(oracle.cbar_col_max(abar, bbar, cols), s.cmax_col[cols])
-    del abar, bbar
-    # mu / nu for every row / column from the (device) maxima
-    sh_r = np.array([oracle.shift_of_cmax(int(c), N)[0] for c in s.cmax_row])
-    sh_c = np.array([oracle.shift_of_cmax(int(c), N)[0] for c in s.cmax_col])
-    assert np.array_equal(s.mu, (s.mu_prime + sh_r).astype(np.int16))
-    assert np.array_equal(s.nu, (s.nu_prime + sh_c).astype(np.int16))
-    # C at sampled entries, bit-exact
-    ri = np.concatenate([rng.integers(0, m, 96), [0, m - 1, 0, m - 1]])
-    cj = np.concatenate([rng.integers(0, n, 96), [0, n - 1, n - 1, 0]])
-    ref = oracle.entries(A, B, N, s.mu, s.nu, ri, cj)
-    got = C[ri, cj]
-    assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
+    del dA, dB
+    check_sampled(oracle, A, B, res, N, 1, np.random.default_rng(m + n + N))
