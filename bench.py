@@ -174,7 +174,10 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator gen.hpp, xoshiro256** stream)",
         "config": {"workload": f"Ozaki-II emulated DGEMM m=n=k={args.m}, N={args.moduli} moduli, phi={args.phi}",
-                   "m": args.m, "n": args.m, "k": args.k, "moduli": args.moduli, "phi": args.phi},
+                   "m": args.m, "n": args.m, "k": args.k, "moduli": args.moduli, "phi": args.phi,
+                   "timed_sample": {"m": m_s, "n": m_s, "k": args.k,
+                                    "note": "each step times os_ii on this bounded sample of the workload "
+                                            "(full k); value = its emulated TFLOP/s"}},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -188,7 +191,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--m", type=int, default=16384)
     ap.add_argument("--k", type=int, default=None)
-    ap.add_argument("--moduli", type=int, default=16)
+    ap.add_argument("--moduli", type=int, default=None,
+                    help="N; default: chosen by suggest_n(bound='tight', relative=True) for --target")
+    ap.add_argument("--target", type=float, default=1e-15, help="relative accuracy target of the automatic N")
     ap.add_argument("--phi", type=float, default=0.0)
     ap.add_argument("--cpu-sample", type=int, default=512, help="rows/cols of the bounded CPU sample (~10 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -199,6 +204,8 @@ def main():
     if args.k is None:
         args.k = args.m
     if args.impl == "reference":
+        if args.moduli is None:
+            args.moduli = 16  # what the automatic rule picks for this workload (tests/test_fullsize_gpu.py)
         run_reference(args)
         return
 
@@ -229,6 +236,24 @@ def main():
     B = B_full[:, cols].contiguous()
     del A_full, B_full
     Cout = torch.empty((A.shape[0], B.shape[1]), dtype=torch.float64, device=dev)
+
+    # N from the paper's bound (north star): the smallest N whose
+    # tight bound certifies args.target relative to (|A||B|)_ij, every smaller N
+    # shown to fail; ranks take the maximum over their tiles
+    auto_n = None
+    if args.moduli is None:
+        t0 = time.perf_counter()
+        sug = oz.suggest_n(A, B, args.target, bound="tight", relative=True)
+        if not sug.achievable:
+            raise SystemExit(f"bench: no N in range certifies {args.target} relative on this workload")
+        n_t = torch.tensor([sug.n], dtype=torch.int64, device=dev)
+        if world > 1:
+            dist.all_reduce(n_t, op=dist.ReduceOp.MAX)
+        args.moduli = int(n_t.item())
+        auto_n = {"rule": f"smallest N with max_ij tight_bound_ij / (|A||B|)_ij <= {args.target} "
+                          "(suggest_n(bound='tight', relative=True), bounds.hpp:182-195)",
+                  "n": args.moduli, "tight_rel_max": sug.tight_rel_max, "excluded_below": sug.excluded_below,
+                  "emulations": sug.emulations, "seconds": round(time.perf_counter() - t0, 3)}
 
     reduce_cb = None
     if world > 1:
@@ -449,7 +474,8 @@ def main():
         "data": "synthetic (reference generator distribution, phi=0 uniform exponent; drawn on device)",
         "config": {"workload": f"Ozaki-II emulated DGEMM m=n=k={m}" + (f" (k={k})" if k != m else "")
                    + f", N={args.moduli} moduli, phi={args.phi}", "m": m, "n": n, "k": k,
-                   "moduli": args.moduli, "phi": args.phi, "parallelism": f"2d-tile {R}x{Cc}",
+                   "moduli": args.moduli, "moduli_choice": auto_n or "fixed (--moduli)",
+                   "phi": args.phi, "parallelism": f"2d-tile {R}x{Cc}",
                    "l2": "inputs 2 GiB each > L2, no flush"},
         "clocks": sampler.summary(),
         "e2e": e2e,

@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define OZ2G_API_VERSION 2
+#define OZ2G_API_VERSION 3
 
 /* Status codes (return value of every entry point). */
 #define OZ2G_OK 0
@@ -76,12 +76,17 @@ extern "C" {
  *   tight: bound_tight (bounds.hpp:182-195) with the exact |A'B'| replaced by
  *          the sound device bound (|C''| + r_const) / (1 - u_coef).
  * `cheap` / `tight` are optional m*n outputs (host buffers, or device buffers
- * when `device` != 0); the maxima are always returned.
+ * when `device` != 0); the maxima are always returned.  With `relative` != 0
+ * also max_ij tight_ij / (|A||B|)_ij, against a lower bound of (|A||B|)_ij
+ * (floor(|A| 2^(mu'+1)) floor(|B| 2^(nu'+1)), one extra int8 GEMM), so it
+ * is >= the exact ratio.
  */
 typedef struct oz2g_bounds {
     double *cheap, *tight;
     int device;
     double cheap_max, tight_max;
+    int relative;           /* in: also evaluate tight_rel_max */
+    double tight_rel_max;   /* out */
 } oz2g_bounds;
 
 typedef struct oz2g_intermediates {
@@ -215,6 +220,23 @@ int oz2g_device_log2f(const float *x_dev, float *out_dev, int64_t count, void *s
  * the returned N (or at the cap).  One clearance pass; A, B as in oz2g_gemm. */
 int oz2g_suggest_n(int prec, int64_t m, int64_t n, int64_t k, const void *A, int64_t lda, const void *B, int64_t ldb,
                    double target, unsigned flags, void *stream, int *n_out, double *bound_max);
+
+/* suggest_n with the tight bound (bounds.hpp:182-195; the paper's choice of N
+ * for a target accuracy): the smallest N in [2, 49] (fp32: [2, 16])
+ * whose device tight-bound maximum is <= `target` — absolute, or with
+ * `relative` != 0 relative to (|A||B|)_ij (oz2g_bounds.tight_rel_max).  Every
+ * smaller N is shown to fail: by a lower estimate of the tight bound
+ * (N < excluded_below) or by its own emulation.  n = 0: not achievable. */
+typedef struct oz2g_suggest {
+    int n;                  /* chosen N (0: none in range meets the target) */
+    int cheap_n;            /* oz2g_suggest_n's answer for the same target (absolute, cheap bound) */
+    int excluded_below;     /* every N < this was excluded by the lower estimate */
+    int emulations;         /* full emulations run (N = excluded_below .. n) */
+    double bound_max;       /* the criterion's maximum at n (or at the last N tried) */
+    double tight_max, tight_rel_max;
+} oz2g_suggest;
+int oz2g_suggest_n_tight(int prec, int64_t m, int64_t n, int64_t k, const void *A, int64_t lda, const void *B,
+                         int64_t ldb, double target, int relative, unsigned flags, void *stream, oz2g_suggest *out);
 
 /* Double-double reference product C = A B (hi + lo) for DEVICE fp64
  * matrices: every product exact (TwoProd), the k-term sum in double-double

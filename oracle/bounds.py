@@ -100,3 +100,31 @@ def suggest_n(A: np.ndarray, B: np.ndarray, target: float, cmax_row, cmax_col):
         if mx <= target:
             return True, n, mx
     return False, 0, last
+
+
+def abs_product(A: np.ndarray, B: np.ndarray):
+    """(|A||B|)_ij exactly, as Fractions (small sizes)."""
+    return exact_product(np.abs(A.astype(np.float64)), np.abs(B.astype(np.float64)))
+
+
+def tight_max(A: np.ndarray, B: np.ndarray, n: int, relative: bool, ora):
+    """max_ij of the reference's tight bound (bounds.hpp:182-195, exact |A'B'|
+    from the oracle's A', B' at this N), absolute or over (|A||B|)_ij."""
+    r = ora.os_ii(A, B, n, keep_intermediates=True)
+    _, tight = bounds(A, B, n, r.inter["cmax_row"], r.inter["cmax_col"], r.inter["Aprime"], r.inter["Bprime"])
+    if not relative:
+        return max(max(row) for row in tight)
+    ab = abs_product(A, B)
+    return max(tight[i][j] / (mpmath.mpf(ab[i][j].numerator) / ab[i][j].denominator)
+               for i in range(len(tight)) for j in range(len(tight[0])))
+
+
+def suggest_n_tight(A: np.ndarray, B: np.ndarray, target: float, relative: bool, ora, n_hi: int = None):
+    """Smallest N whose reference tight-bound maximum meets `target` (the
+    criterion oz2g_suggest_n_tight certifies from above)."""
+    mode = M.F64 if A.dtype == np.float64 else M.F32
+    n_max = M.fp32_safe_moduli_max() if mode == M.F32 else M.K_MAX_MODULI
+    for n in range(2, min(n_max, n_hi or n_max) + 1):
+        if tight_max(A, B, n, relative, ora) <= target:
+            return n
+    return 0

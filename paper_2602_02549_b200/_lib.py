@@ -24,7 +24,13 @@ class Intermediates(C.Structure):
 
 class Bounds(C.Structure):
     _fields_ = [("cheap", C.c_void_p), ("tight", C.c_void_p), ("device", C.c_int),
-                ("cheap_max", C.c_double), ("tight_max", C.c_double)]
+                ("cheap_max", C.c_double), ("tight_max", C.c_double), ("relative", C.c_int),
+                ("tight_rel_max", C.c_double)]
+
+
+class Suggest(C.Structure):
+    _fields_ = [("n", C.c_int), ("cheap_n", C.c_int), ("excluded_below", C.c_int), ("emulations", C.c_int),
+                ("bound_max", C.c_double), ("tight_max", C.c_double), ("tight_rel_max", C.c_double)]
 
 
 class Diag(C.Structure):
@@ -45,7 +51,7 @@ EXPORTED = ("oz2g_gemm", "oz2g_dgemm", "oz2g_sgemm", "oz2g_last_error", "oz2g_ta
             "oz2g_fp32_safe_moduli_max", "oz2g_shift_of_cmax", "oz2g_device_log2f", "oz2g_version",
             "oz2g_release_workspace", "oz2g_dd_gemm", "oz2g_suggest_n", "oz2g_gen_matrix", "oz2g_derive_seed",
             "oz2g_native_gemm", "oz2g_gemm_multi", "oz2g_grid_shape", "oz2g_init", "oz2g_synchronize",
-            "oz2g_gemm_sweep")
+            "oz2g_gemm_sweep", "oz2g_suggest_n_tight")
 
 _LIB = None
 
@@ -74,6 +80,8 @@ def load() -> C.CDLL:
     L.oz2g_suggest_n.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
                                  C.c_int64, C.c_double, C.c_uint, C.c_void_p, C.POINTER(C.c_int),
                                  C.POINTER(C.c_double)]
+    L.oz2g_suggest_n_tight.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                                       C.c_int64, C.c_double, C.c_int, C.c_uint, C.c_void_p, C.POINTER(Suggest)]
     L.oz2g_gen_matrix.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_uint64, C.c_void_p]
     L.oz2g_derive_seed.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
     L.oz2g_derive_seed.restype = C.c_uint64

@@ -86,6 +86,11 @@ struct Workspace {
     DevBuf A, B, C, abar, bbar, ares, bres, W, mup, nup, mu, nu, bmax, cmax_row, cmax_col, e, f, status;
     DevBuf x_cbar, x_cprod, x_c1, x_c2, x_q, x_cpp64, x_cpp32, x_ap, x_bp, x_bvec, x_bscr, x_bmax, x_bcheap, x_btight;
     DevBuf spec_st;  // speculated column exponents: per-stage statuses
+    // relative error criterion (suggest_n tight / relative): floor operands, their
+    // row / column sums and product (launch_floor_operands); valid for the
+    // inputs of the last scan that computed them
+    DevBuf lo_a, lo_b, lo_sum, lo_ab;
+    bool lo_ready = false;
     // changed-tile flags of the speculation checks: mapped pinned host memory
     // written by the check kernel, read by the host after an event
     int32_t* spec_changed = nullptr;
@@ -149,13 +154,15 @@ struct Workspace {
     void release() {
         for (DevBuf* b : {&A, &B, &C, &abar, &bbar, &ares, &bres, &W, &mup, &nup, &mu, &nu, &bmax, &cmax_row,
                           &cmax_col, &e, &f, &status, &x_cbar, &x_cprod, &x_c1, &x_c2, &x_q, &x_cpp64, &x_cpp32,
-                          &x_ap, &x_bp, &x_bvec, &x_bscr, &x_bmax, &x_bcheap, &x_btight, &status_ring, &spec_st})
+                          &x_ap, &x_bp, &x_bvec, &x_bscr, &x_bmax, &x_bcheap, &x_btight, &status_ring, &spec_st,
+                          &lo_a, &lo_b, &lo_sum, &lo_ab})
             b->release();
         if (spec_changed) cudaFreeHost(spec_changed);
         spec_changed = nullptr;
         spec_changed_cap = 0;
         for (auto& kv : rc) cudaFree(kv.second);
         rc.clear();
+        lo_ready = false;
     }
 };
 
@@ -425,6 +432,40 @@ struct Timer {
     }
 };
 
+// Operands of the relative criterion (bounds "relative", suggest_n tight):
+// with Acheck = floor(|A| 2^(mu' + 1)), Bcheck = floor(|B| 2^(nu' + 1))
+// (launch_floor_operands), lo = Acheck Bcheck (one tcgen05 EPI_I32 launch)
+// bounds (|A||B|)_ij from below by lo_ij 2^-(mu'_i + nu'_j + 2) and, with
+// the row / column sums, from above.  Needs mu', nu' of these inputs.
+void compute_relative_operands(Workspace& ws, int prec, const void* dA, int64_t lda, const void* dB, int64_t ldb,
+                               int64_t m, int64_t n, int64_t k, const int32_t* mup, const int32_t* nup,
+                               cudaStream_t stream, int& launches) {
+    const int64_t kp = round_up(k, 128), ldn = round_up(n > 0 ? n : 1, 16);
+    int8_t* la = (int8_t*)ws.lo_a.get((size_t)(m * kp));
+    int8_t* lb = (int8_t*)ws.lo_b.get((size_t)(kp * ldn));
+    int32_t* sums = (int32_t*)ws.lo_sum.get(4 * (size_t)(m + n));
+    int32_t* lab = (int32_t*)ws.lo_ab.get(4 * (size_t)(m * n));
+    CUDA_TRY(launch_floor_operands(prec, dA, lda, m, dB, ldb, k, n, kp, ldn, mup, nup, la, lb, sums, sums + m, stream));
+    launches += 2;
+    GemmParams g;
+    std::memset(&g, 0, sizeof g);
+    g.m = (int)m;
+    g.n = (int)n;
+    g.kblocks = (int)(kp / 128);
+    g.tiles_m = (int)((m + gemm_tile_m() - 1) / gemm_tile_m());
+    g.tiles_n = (int)((n + gemm_tile_n() - 1) / gemm_tile_n());
+    g.group_m = group_m_for(g.tiles_m, g.tiles_n);
+    set_l2_hints(g);
+    g.planes = 1;
+    g.C32 = lab;
+    g.ldc32 = n;
+    g.cplane = m * n;
+    CUDA_TRY(launch_gemm_i8(EPI_I32, make_plane_map(la, kp, m, 1, gemm_tile_m()),
+                            make_plane_map_mn(lb, n, ldn, kp, 1, kp * ldn), g, ws.num_sms, stream));
+    ++launches;
+    ws.lo_ready = true;
+}
+
 // Row block of the residue GEMMs + CRT: one raster group (16 x 128 rows), so
 // W (N int8 planes) is held for one block only.
 constexpr int64_t kWBlockRows = 2048;
@@ -592,6 +633,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     // clearance maxima of the previous call on these same inputs are still in
     // the workspace — they do not depend on N — so K1 / K2 are skipped
     const bool scan = !reuse_scaling;
+    if (scan) ws.lo_ready = false;  // new inputs: the relative-criterion operands are stale
     if (scan && n) CUDA_TRY(cudaMemsetAsync(bmax, 0, 8 * (size_t)n, stream));
     if (scan && m) CUDA_TRY(cudaMemsetAsync(cmax_row, 0, 4 * (size_t)m, stream));
     if (scan && n) CUDA_TRY(cudaMemsetAsync(cmax_col, 0, 4 * (size_t)n, stream));
@@ -774,6 +816,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             exb.bnd.v.ea += r0;
             if (exb.bnd.cheap) exb.bnd.cheap += eo;
             if (exb.bnd.tight) exb.bnd.tight += eo;
+            if (exb.bnd.lo) exb.bnd.lo += eo;
         }
         tm.span(6, crt_stream, [&] {
             CUDA_TRY(launch_crt(prec, Wb, ldw, wrows * ldw, rc, nc, cc, mu + r0, nu + c0,
@@ -1143,8 +1186,11 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             CUDA_TRY(launch_bound_vectors(prec, dA, lda_d, m, dB, ldb_d, k, n, cmax_row, cmax_col, mup, nup, bs.t_up,
                                           scratch, v, stream));
             launches += 5;
-            bmax_dev = (unsigned long long*)ws.x_bmax.get(16);
-            CUDA_TRY(cudaMemsetAsync(bmax_dev, 0, 16, stream));
+            if (bo->relative && !ws.lo_ready)
+                compute_relative_operands(ws, prec, dA, lda_d, dB, ldb_d, m, n, k, mup, nup, stream, launches);
+            bmax_dev = (unsigned long long*)ws.x_bmax.get(24);
+            CUDA_TRY(cudaMemsetAsync(bmax_dev, 0, 24, stream));
+            ex.bnd.lo = bo->relative ? (const int32_t*)ws.lo_ab.p : nullptr;
             ex.bnd.on = 1;
             ex.bnd.v = v;
             ex.bnd.t2_up = bs.t2_up;
@@ -1236,9 +1282,9 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         return OZ2G_OK;
     }
 
-    unsigned long long bmax_host[2] = {0, 0};
+    unsigned long long bmax_host[3] = {0, 0, 0};
     if (bo && bmax_dev) {
-        CUDA_TRY(cudaMemcpyAsync(bmax_host, bmax_dev, 16, cudaMemcpyDeviceToHost, stream));
+        CUDA_TRY(cudaMemcpyAsync(bmax_host, bmax_dev, 24, cudaMemcpyDeviceToHost, stream));
         if (!bo->device && bo->cheap) CUDA_TRY(cudaMemcpyAsync(bo->cheap, ex.bnd.cheap, mn8, cudaMemcpyDeviceToHost, stream));
         if (!bo->device && bo->tight) CUDA_TRY(cudaMemcpyAsync(bo->tight, ex.bnd.tight, mn8, cudaMemcpyDeviceToHost, stream));
     }
@@ -1285,6 +1331,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         std::memcpy(&v1, &bmax_host[1], 8);
         bo->cheap_max = v0;
         bo->tight_max = v1;
+        if (bo->relative) std::memcpy(&bo->tight_rel_max, &bmax_host[2], 8);
     }
 
     if (inter && inter->Dbar && inter->Cbar)
@@ -1406,6 +1453,94 @@ int run_suggest_n(int prec, int64_t m, int64_t n, int64_t k, const void* A, int6
         }
     }
     return OZ2G_OK;  // not achievable: n_out = 0, bound_out = bound max at the cap
+}
+
+// suggest_n with the TIGHT bound (bounds.hpp:182-195), absolute or relative
+// to (|A||B|)_ij: the smallest N whose device tight-bound maximum (the sound
+// |A'B'| <= (|C''| + r_const) / (1 - u_coef) form, bounds.cu) meets `target`.
+// The tight bound needs C'' at that N, i.e. a full emulation, so:
+//  1. one scaling + clearance pass and the N-independent bound factors;
+//  2. N = 2, 3, ...: a lower estimate of the tight bound (tight without its
+//     |A'B'| term, over an upper bound of |A||B|) proves N too small while it
+//     exceeds the target; the first N it does not exclude is N0;
+//  3. N = N0, N0 + 1, ...: the emulation with the bounds evaluated in its CRT
+//     pass (the N sweep: scaling reused) until the maximum meets the target.
+// So every N below the answer is shown to fail — by the lower estimate or by
+// its own emulation.
+int run_suggest_tight(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
+                      int64_t ldb, double target, int relative, unsigned flags, cudaStream_t stream,
+                      oz2g_suggest* out) {
+    if (!out) throw Fail{OZ2G_INVALID_ARGUMENT, "suggest_n: null result"};
+    std::memset(out, 0, sizeof *out);
+    int n_cheap = 0;
+    double cheap_max = 0.0;
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    Workspace& ws = workspace(dev, 0);
+    std::lock_guard<std::recursive_mutex> dev_lock(ws.mtx);
+    // steps 1 (the cheap search's scaling pass leaves mu', nu', the clearance
+    // maxima and the bound factors with t = 1 in the workspace)
+    run_suggest_n(prec, m, n, k, A, lda, B, ldb, target, flags, stream, &n_cheap, &cheap_max);
+    out->cheap_n = n_cheap;
+    if (m == 0 || n == 0) return OZ2G_OK;
+    const bool host = (flags & OZ2G_DEVICE_PTRS) == 0;
+    const size_t esz = prec ? 8 : 4;
+    const void* dA = host ? ws.A.p : A;
+    const void* dB = host ? ws.B.p : B;
+    const int64_t lda_d = host ? k : lda, ldb_d = host ? n : ldb;
+    int launches = 0;
+    int32_t* mup = (int32_t*)ws.mup.p;
+    int32_t* nup = (int32_t*)ws.nup.p;
+    if (relative) compute_relative_operands(ws, prec, dA, lda_d, dB, ldb_d, m, n, k, mup, nup, stream, launches);
+    const double* vec = (const double*)ws.x_bvec.p;
+    BoundVecs v;
+    v.RA = const_cast<double*>(vec); v.PA = v.RA + m; v.CB = v.RA + 2 * m; v.PB = v.RA + 2 * m + n;
+    v.ea = reinterpret_cast<int32_t*>(v.RA + 2 * (m + n));
+    v.eb = v.ea + m;
+    const int32_t* sums = (const int32_t*)ws.lo_sum.p;
+    unsigned long long* bits = (unsigned long long*)ws.x_bmax.get(24);
+    const int n_max = prec == OZ2G_FP32 ? fp32_safe_moduli_max() : kMaxModuli;
+    int n0 = 0;
+    for (int nm = 2; nm <= n_max && !n0; ++nm) {
+        const BoundScalars bs = bound_scalars(table_for(nm, prec), k);
+        CUDA_TRY(cudaMemsetAsync(bits, 0, 8, stream));
+        CUDA_TRY(launch_tight_lower_max(v, m, n, k, bs.t_up, __builtin_nextafter(bs.k_rconst_up * bs.t2_up, 1e308),
+                                        relative ? (const int32_t*)ws.lo_ab.p : nullptr, relative ? sums : nullptr,
+                                        relative ? sums + m : nullptr, bits, ws.num_sms, stream));
+        unsigned long long hb = 0;
+        CUDA_TRY(cudaMemcpyAsync(&hb, bits, 8, cudaMemcpyDeviceToHost, stream));
+        CUDA_TRY(cudaStreamSynchronize(stream));
+        double lower;
+        std::memcpy(&lower, &hb, 8);
+        if (!(lower > target)) n0 = nm;
+        else out->excluded_below = nm + 1;
+    }
+    if (!n0) return OZ2G_OK;  // every N excluded: not achievable
+    // step 3: emulations on the kept scaling (lo_ready survives reuse_scaling calls)
+    DevBuf cbuf;
+    struct Rel { DevBuf* b; ~Rel() { b->release(); } } rel{&cbuf};
+    void* dC = cbuf.get(esz * (size_t)(m * n));
+    for (int nm = n0; nm <= n_max; ++nm) {
+        oz2g_bounds bo;
+        std::memset(&bo, 0, sizeof bo);
+        bo.relative = relative;
+        oz2g_intermediates in;
+        std::memset(&in, 0, sizeof in);
+        in.bounds = &bo;
+        oz2g_diag d;
+        run_gemm(prec, m, n, k, dA, lda_d, dB, ldb_d, dC, n, nm, OZ2G_DEVICE_PTRS, stream, &in, &d, nullptr, nullptr,
+                 0, 0, 0, /*reuse_scaling=*/true);
+        ++out->emulations;
+        const double val = relative ? bo.tight_rel_max : bo.tight_max;
+        out->bound_max = val;
+        out->tight_max = bo.tight_max;
+        out->tight_rel_max = bo.tight_rel_max;
+        if (val <= target) {
+            out->n = nm;
+            return OZ2G_OK;
+        }
+    }
+    return OZ2G_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -1785,6 +1920,13 @@ int oz2g_suggest_n(int prec, int64_t m, int64_t n, int64_t k, const void* A, int
                    double target, unsigned flags, void* stream, int* n_out, double* bound_max) {
     return guarded([&] {
         return run_suggest_n(prec, m, n, k, A, lda, B, ldb, target, flags, (cudaStream_t)stream, n_out, bound_max);
+    });
+}
+
+int oz2g_suggest_n_tight(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
+                         int64_t ldb, double target, int relative, unsigned flags, void* stream, oz2g_suggest* out) {
+    return guarded([&] {
+        return run_suggest_tight(prec, m, n, k, A, lda, B, ldb, target, relative, flags, (cudaStream_t)stream, out);
     });
 }
 

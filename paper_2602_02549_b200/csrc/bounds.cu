@@ -178,6 +178,42 @@ __global__ void __launch_bounds__(256) cheap_bound_max_kernel(BoundVecs v, int64
     if ((threadIdx.x & 31) == 0) atomicMax(out_bits, best);
 }
 
+
+// Pruning for the tight-bound search of suggest_n (api.cu run_suggest_tight):
+// max_ij of a LOWER estimate of the tight bound for one N — the tight formula
+// (bounds.hpp:182-195) without its u_coef |A'B'| term (>= 0), evaluated with
+// upward roundings and then scaled by (1 - 2^-30), which is below the exact
+// formula because the upward roundings overshoot by < 2^-34 relative — divided
+// (rounded down) by an UPPER bound of (|A||B|)_ij when `lo` is set (relative
+// criterion), see launch_floor_operands.  A maximum above the target proves
+// that N cannot meet it.
+__global__ void __launch_bounds__(256) tight_lower_max_kernel(BoundVecs v, int64_t m, int64_t n, int64_t k,
+                                                              double t_up, double kt2_up, const int32_t* lo,
+                                                              const int32_t* rsum, const int32_t* csum,
+                                                              unsigned long long* out_bits) {
+    unsigned long long best = 0;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m * n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / n, j = e - i * n;
+        const double b1 = ldexp_ru(__dmul_ru(__dmul_ru(t_up, v.RA[i]), v.PB[j]), v.eb[j]);
+        const double b2 = ldexp_ru(__dmul_ru(__dmul_ru(t_up, v.CB[j]), v.PA[i]), v.ea[i]);
+        const double b3 = ldexp_ru(__dmul_ru(kt2_up, __dmul_ru(v.PA[i], v.PB[j])), v.ea[i] + v.eb[j]);
+        double r = __dmul_rd(__dadd_ru(__dadd_ru(b1, b2), b3), 1.0 - 0x1p-30);
+        if (lo) {
+            const long long hi = (long long)lo[e] + rsum[i] + csum[j] + k;  // exact, < 2^33
+            const double up = ldexp_ru(__ll2double_ru(hi), v.ea[i] + v.eb[j] - 12);
+            r = up > 0.0 ? __ddiv_rd(r, up) : 0.0;
+        }
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(r);
+        best = bits > best ? bits : best;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+        best = t > best ? t : best;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(out_bits, best);
+}
+
 // The experiment harness's "native" GEMM (experiment.hpp:55-68): per entry a
 // sequential loop h = 0..k-1 with a separate RN multiply and RN add in the
 // working precision T (no FMA), exactly the reference's err_native reference.
@@ -251,6 +287,17 @@ cudaError_t launch_dd_gemm(const double* A, int64_t lda, const double* B, int64_
     if (m * n == 0) return cudaSuccess;
     dim3 grid(blocks_for(n, 64), blocks_for(m, 64));
     dd_gemm_kernel<<<grid, 256, 0, s>>>(A, lda, B, ldb, m, n, k, Chi, Clo, ldc);
+    return cudaGetLastError();
+}
+
+
+cudaError_t launch_tight_lower_max(const BoundVecs& v, int64_t m, int64_t n, int64_t k, double t_up, double kt2_up,
+                                   const int32_t* lo, const int32_t* rsum, const int32_t* csum,
+                                   unsigned long long* out_bits, int num_sms, cudaStream_t s) {
+    if (m * n == 0) return cudaSuccess;
+    const int64_t want = (m * n + 255) / 256;
+    const unsigned grid = (unsigned)(want < (int64_t)num_sms * 8 ? want : (int64_t)num_sms * 8);
+    tight_lower_max_kernel<<<grid, 256, 0, s>>>(v, m, n, k, t_up, kt2_up, lo, rsum, csum, out_bits);
     return cudaGetLastError();
 }
 

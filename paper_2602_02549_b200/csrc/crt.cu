@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
     const int64_t qn = (n + CV - 1) / CV;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = t < m * qn;
-    unsigned long long bmax_cheap = 0, bmax_tight = 0;
+    unsigned long long bmax_cheap = 0, bmax_tight = 0, bmax_rel = 0;
     if (active) {
         const int64_t i = t / qn;
         const int64_t j0 = (t - i * qn) * CV;
@@ -126,7 +126,12 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
         for (int b = 0; b < CV; ++b) {
             if (b >= jn) break;
             const int64_t j = j0 + b;
-            const double q = rint(__dmul_rn(cc.P_inv, c1[b]));   // crt.hpp:113-119
+            // crt.hpp:113-119, round_nearest_even (softfp.hpp:94-102): rint,
+            // except that the reference's floor(x) + 1 returns +0.0 for x in
+            // [-0.5, -0.0) where rint gives -0.0 (C'' and C are the same either way)
+            const double qx = __dmul_rn(cc.P_inv, c1[b]);
+            double q = rint(qx);
+            if (q == 0.0 && qx != 0.0) q = 0.0;
             const double t1 = __fma_rn(-q, cc.P1, c1[b]);         // crt.hpp:136-138
             const double t2 = __dadd_rn(t1, c2[b]);
             const double cpp = __fma_rn(-q, cc.P2, t2);
@@ -155,6 +160,12 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
                 const unsigned long long tb = (unsigned long long)__double_as_longlong(tight);
                 bmax_cheap = cb > bmax_cheap ? cb : bmax_cheap;
                 bmax_tight = tb > bmax_tight ? tb : bmax_tight;
+                if (bc.lo) {  // tight / (|A||B|)_ij, rounded up against a lower bound of |A||B|
+                    const int32_t lv = bc.lo[o];
+                    const double rel = lv > 0 ? ldexp_ru(__ddiv_ru(tight, (double)lv), 12 - eai - ebj) : __longlong_as_double(0x7ff0000000000000ll);
+                    const unsigned long long rb = (unsigned long long)__double_as_longlong(rel);
+                    bmax_rel = rb > bmax_rel ? rb : bmax_rel;
+                }
             }
             if constexpr (sizeof(T) == 4) {
                 if (fabs(cpp) >= 0x1.ffffffp+127) { fr_range = true; continue; }  // crt.hpp:144-145
@@ -185,9 +196,11 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
     if (BND) {
         bmax_cheap = warp_max_u64(bmax_cheap);
         bmax_tight = warp_max_u64(bmax_tight);
+        bmax_rel = warp_max_u64(bmax_rel);
         if ((threadIdx.x & 31) == 0) {
             atomicMax(&ex.bnd.max_bits[0], bmax_cheap);
             atomicMax(&ex.bnd.max_bits[1], bmax_tight);
+            if (ex.bnd.lo) atomicMax(&ex.bnd.max_bits[2], bmax_rel);
         }
     }
 }

@@ -111,6 +111,13 @@ cudaError_t launch_bound_vectors(int prec, const void* A, int64_t lda, int64_t m
 size_t bound_scratch_doubles(int64_t m, int64_t n, int64_t k);
 cudaError_t launch_cheap_bound_max(const BoundVecs& v, int64_t m, int64_t n, double t_up, double kt2_up,
                                    unsigned long long* out_bits, int num_sms, cudaStream_t s);
+cudaError_t launch_tight_lower_max(const BoundVecs& v, int64_t m, int64_t n, int64_t k, double t_up, double kt2_up,
+                                   const int32_t* lo, const int32_t* rsum, const int32_t* csum,
+                                   unsigned long long* out_bits, int num_sms, cudaStream_t s);
+cudaError_t launch_floor_operands(int prec, const void* A, int64_t lda, int64_t m, const void* B, int64_t ldb,
+                                  int64_t k, int64_t n, int64_t kp, int64_t ldn, const int32_t* mu_prime,
+                                  const int32_t* nu_prime, int8_t* a_out, int8_t* b_out, int32_t* rsum,
+                                  int32_t* csum, cudaStream_t s);
 cudaError_t launch_dd_gemm(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t m, int64_t n,
                            int64_t k, double* Chi, double* Clo, int64_t ldc, cudaStream_t s);
 cudaError_t launch_native_gemm(int prec, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m,
@@ -127,7 +134,10 @@ struct BoundCtx {  // evaluated in the CRT pass when `on`
     BoundVecs v;
     double t2_up, rconst_up, ucoef, kpr_cheap_up, k_rconst_up;
     double *cheap, *tight;             // optional m x n outputs (device)
-    unsigned long long* max_bits;      // [0] cheap max, [1] tight max (bits of positive doubles)
+    unsigned long long* max_bits;      // [0] cheap max, [1] tight max, [2] tight / |A||B| max (bits)
+    // relative criterion: (|A||B|)_ij >= lo[i * n + j] 2^-(mu'_i + nu'_j + 2) (launch_floor_operands);
+    // nullptr: no relative maximum
+    const int32_t* lo;
 };
 // Status flags per (row group, column group) of C instead of the launch's
 // single status (speculated exponents, api.cu): entry (i, j) of the launch

@@ -316,6 +316,52 @@ __global__ void merge_status_kernel(DevStatus* __restrict__ dst, const DevStatus
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Lower-bound operands for the relative error criterion of suggest_n (f1):
+// Acheck_ih = floor(|a_ih| 2^(mu'_i + 1)), Bcheck_hj = floor(|b_hj| 2^(nu'_j + 1)),
+// both in [0, 127] because |a| 2^mu' < 64 (scaling.hpp:86-107).  Then
+//   2^-(mu'_i + nu'_j + 2) (Acheck Bcheck)_ij <= (|A||B|)_ij
+//     < 2^-(mu'_i + nu'_j + 2) ((Acheck Bcheck)_ij + SA_i + SB_j + k),
+// with SA / SB the row / column sums of Acheck / Bcheck.  Layouts as Abar /
+// Bbar: [m][kp] and [kp][ldn], zero padded.
+// ---------------------------------------------------------------------------
+template <class T>
+__global__ void __launch_bounds__(256) floor_rows_A_kernel(const T* __restrict__ A, int64_t lda, int64_t k,
+                                                           int64_t kp, const int32_t* __restrict__ mu_prime,
+                                                           int8_t* __restrict__ out, int32_t* __restrict__ rsum) {
+    const int64_t i = blockIdx.x;
+    const int s = mu_prime[i] + 1;
+    int acc = 0;
+    for (int64_t h = threadIdx.x; h < kp; h += blockDim.x) {
+        int v = 0;
+        if (h < k) v = (int)floor(ldexp_rn(fabs((double)A[i * lda + h]), s));
+        out[i * kp + h] = (int8_t)v;
+        acc += v;
+    }
+    acc = __reduce_add_sync(0xffffffffu, acc);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&rsum[i], acc);
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) floor_rows_B_kernel(const T* __restrict__ B, int64_t ldb, int64_t k,
+                                                           int64_t n, int64_t kp, int64_t ldn,
+                                                           const int32_t* __restrict__ nu_prime,
+                                                           int8_t* __restrict__ out, int32_t* __restrict__ csum) {
+    const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (j >= ldn) return;
+    const int64_t h0 = (int64_t)blockIdx.y * 64;
+    const int s = j < n ? nu_prime[j] + 1 : 0;
+    int acc = 0;
+    for (int64_t h = h0; h < h0 + 64 && h < kp; ++h) {
+        int v = 0;
+        if (h < k && j < n) v = (int)floor(ldexp_rn(fabs((double)B[h * ldb + j]), s));
+        out[h * ldn + j] = (int8_t)v;
+        acc += v;
+    }
+    if (j < n && acc) atomicAdd(&csum[j], acc);
+}
+
 inline unsigned blocks_for(int64_t work, int per) { return (unsigned)((work + per - 1) / per); }
 
 }  // namespace
@@ -430,6 +476,26 @@ cudaError_t launch_log2f(const float* x, float* out, int64_t count, cudaStream_t
 cudaError_t launch_merge_status(DevStatus* dst, const DevStatus* src, int64_t count, cudaStream_t s) {
     if (count <= 0) return cudaSuccess;
     merge_status_kernel<<<1, 256, 0, s>>>(dst, src, count);
+    return cudaGetLastError();
+}
+
+
+cudaError_t launch_floor_operands(int prec, const void* A, int64_t lda, int64_t m, const void* B, int64_t ldb,
+                                  int64_t k, int64_t n, int64_t kp, int64_t ldn, const int32_t* mu_prime,
+                                  const int32_t* nu_prime, int8_t* a_out, int8_t* b_out, int32_t* rsum,
+                                  int32_t* csum, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(rsum, 0, 4 * (size_t)(m > 0 ? m : 1), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(csum, 0, 4 * (size_t)(n > 0 ? n : 1), s);
+    if (e != cudaSuccess) return e;
+    if (m && kp) {
+        if (prec) floor_rows_A_kernel<double><<<(unsigned)m, 256, 0, s>>>((const double*)A, lda, k, kp, mu_prime, a_out, rsum);
+        else floor_rows_A_kernel<float><<<(unsigned)m, 256, 0, s>>>((const float*)A, lda, k, kp, mu_prime, a_out, rsum);
+    }
+    if (ldn && kp) {
+        dim3 grid(blocks_for(ldn, 256), blocks_for(kp, 64));
+        if (prec) floor_rows_B_kernel<double><<<grid, 256, 0, s>>>((const double*)B, ldb, k, n, kp, ldn, nu_prime, b_out, csum);
+        else floor_rows_B_kernel<float><<<grid, 256, 0, s>>>((const float*)B, ldb, k, n, kp, ldn, nu_prime, b_out, csum);
+    }
     return cudaGetLastError();
 }
 

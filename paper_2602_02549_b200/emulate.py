@@ -140,7 +140,8 @@ def _is_torch_cuda(x) -> bool:
 
 def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = False, out=None,
           stream=None, timing: bool = False, bounds=False, vectors: bool = False,
-          reduce_maxima: Optional[Callable] = None, devices=None, blocking: bool = True) -> EmulationResult:
+          reduce_maxima: Optional[Callable] = None, devices=None, blocking: bool = True,
+          relative: bool = False) -> EmulationResult:
     """C ~ A*B by Ozaki-II accurate mode with `n` moduli (emulate.hpp:54-88).
 
     `a`, `b`: 2-D float32/float64 numpy arrays (host) or CUDA torch tensors
@@ -152,7 +153,9 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
     `bounds=True` evaluates the
     paper's error bounds (bounds.hpp) and returns their maxima;
     `bounds="full"` also returns the m x n cheap / tight bound matrices (same
-    memory space as the inputs).  `reduce_maxima(row_ptr, m, col_ptr, n,
+    memory space as the inputs); with `relative=True` also
+    bounds["tight_rel_max"] = max_ij tight_ij / (|A||B|)_ij (a certificate:
+    against a lower bound of |A||B|).  `reduce_maxima(row_ptr, m, col_ptr, n,
     stream)` is the multi-GPU hook of oz2g.h.  `devices=[d0, d1, ...]` tiles
     one call over those devices of this process (oz2g_gemm_multi; host arrays,
     C only) with a result identical to the single-device call.
@@ -278,6 +281,7 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
         if inter_c is None:
             inter_c = _lib.Intermediates()
         bnd_c = _lib.Bounds()
+        bnd_c.relative = 1 if relative else 0
         if bounds == "full":
             for name in ("cheap", "tight"):
                 if dev:
@@ -313,6 +317,8 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
     bres = None
     if bnd_c is not None:
         bres = dict(cheap_max=bnd_c.cheap_max, tight_max=bnd_c.tight_max, **bnd_arrays)
+        if relative:
+            bres["tight_rel_max"] = bnd_c.tight_rel_max
     return EmulationResult(C=C_out, scaling=sc, crt=cr, table=table_for(n, prec), subnormal=bool(diag.subnormal),
                            kernels_launched=diag.kernels_launched, stage_ms=tuple(diag.stage_ms), bounds=bres,
                            speculation=diag.speculation)
@@ -397,22 +403,43 @@ def device_log2f(x_dev, out_dev, stream=None) -> None:
 
 @dataclass
 class SuggestResult:
-    """bounds.hpp:208-212."""
+    """bounds.hpp:208-212 (+ the tight search's bookkeeping)."""
     achievable: bool
     n: int
     bound_max: float
+    bound: str = "cheap"
+    relative: bool = False
+    excluded_below: int = 0      # tight: every N below this excluded by the lower estimate
+    emulations: int = 0          # tight: full emulations run to settle N
+    tight_max: float = 0.0
+    tight_rel_max: float = 0.0
 
 
-def suggest_n(a, b, target: float) -> SuggestResult:
-    """Smallest N whose cheap error bound (bounds.hpp:198-206) is <= `target`
-    everywhere (bounds.hpp:217-243); host numpy arrays or CUDA tensors."""
+def suggest_n(a, b, target: float, bound: str = "cheap", relative: bool = False) -> SuggestResult:
+    """Smallest N whose error bound is <= `target` everywhere.
+
+    bound="cheap" (default, the reference's suggest_n, bounds.hpp:217-243):
+    the cheap bound (bounds.hpp:198-206), absolute target.
+    bound="tight": the tight bound (bounds.hpp:182-195) with the sound device
+    |A'B'| <= (|C''| + r_const)/(1 - u_coef); `relative=True` measures it
+    against (|A||B|)_ij (the north star's "N from the paper's bound for 1e-15
+    relative accuracy").  Every smaller N is shown to fail.  Host numpy arrays
+    or CUDA tensors."""
+    if bound not in ("cheap", "tight"):
+        raise InvalidArgument("suggest_n: bound must be 'cheap' or 'tight'")
+    if relative and bound != "tight":
+        raise InvalidArgument("suggest_n: relative=True needs bound='tight'")
     L = _lib.load()
     if _is_torch_cuda(a):
         import torch
+        if a.dtype != b.dtype or a.dtype not in (torch.float32, torch.float64):
+            raise TypeError("suggest_n: A and B must both be float32 or float64")
+        if a.stride(1) != 1 or b.stride(1) != 1:
+            raise InvalidArgument("suggest_n: unit column stride required (row-major)")
         prec = F64 if a.dtype == torch.float64 else F32
         m, k = a.shape
         nn = b.shape[1]
-        pa, pb, lda, ldb = a.data_ptr(), b.data_ptr(), a.stride(0), b.stride(0)
+        pa, pb, lda, ldb = a.data_ptr(), b.data_ptr(), max(a.stride(0), k), max(b.stride(0), nn)
         flags = _lib.OZ2G_DEVICE_PTRS
         stream = torch.cuda.current_stream(a.device).cuda_stream
     else:
@@ -428,6 +455,13 @@ def suggest_n(a, b, target: float) -> SuggestResult:
         stream = 0
     if a.shape[1] != b.shape[0]:
         raise InvalidArgument("dimension mismatch: suggest_n inner dimension")
+    if bound == "tight":
+        res = _lib.Suggest()
+        _check(L.oz2g_suggest_n_tight(prec, m, nn, k, pa, lda, pb, ldb, float(target), 1 if relative else 0, flags,
+                                      C.c_void_p(int(stream)), C.byref(res)))
+        return SuggestResult(achievable=res.n > 0, n=res.n, bound_max=res.bound_max, bound="tight",
+                             relative=bool(relative), excluded_below=res.excluded_below, emulations=res.emulations,
+                             tight_max=res.tight_max, tight_rel_max=res.tight_rel_max)
     n_out = C.c_int()
     bmax = C.c_double()
     _check(L.oz2g_suggest_n(prec, m, nn, k, pa, lda, pb, ldb, float(target), flags, C.c_void_p(int(stream)),

@@ -93,3 +93,42 @@ def test_suggest_n_matches_oracle(cuda, oracle, phi, target, dt):
     assert got.n == n_or
     if ok:
         assert got.bound_max <= target and mpmath.mpf(got.bound_max) >= mx_or
+
+
+@pytest.mark.parametrize("phi,target,relative,dt", [(0.0, 1e-15, True, np.float64), (0.5, 3e-15, True, np.float64),
+                                                    (2.0, 1e-13, True, np.float64), (0.0, 1e-13, False, np.float64),
+                                                    (0.0, 1e-6, True, np.float32)])
+def test_suggest_n_tight(cuda, oracle, phi, target, relative, dt):
+    """suggest_n(bound="tight", relative=...): the device criterion is a
+    certificate of the reference's tight bound (bounds.hpp:182-195 with the
+    exact |A'B'|, exact |A||B|), so its N is >= the reference-exact one and
+    at most one more (only when the exact maximum sits within a few percent
+    of the target); every smaller N fails — below `excluded_below` by the
+    lower estimate (checked here against the exact maximum), above it by its
+    own emulation."""
+    from oracle import bounds as OB
+    A = oracle.gen_matrix(10, 48, phi, 81, dt)
+    B = oracle.gen_matrix(48, 9, phi, 82, dt)
+    got = oz.suggest_n(A, B, target, bound="tight", relative=relative)
+    n_ref = OB.suggest_n_tight(A, B, target, relative, oracle)
+    assert got.achievable == (n_ref > 0) or (n_ref > 0 and got.n == 0)
+    if n_ref == 0:
+        return
+    assert n_ref <= got.n <= n_ref + 1, (got, n_ref)
+    if got.n > n_ref:
+        assert OB.tight_max(A, B, n_ref, relative, oracle) > 0.9 * target
+    # certificate and tightness at the chosen N
+    exact = OB.tight_max(A, B, got.n, relative, oracle)
+    crit = got.tight_rel_max if relative else got.tight_max
+    assert crit <= target and mpmath.mpf(crit) >= exact and crit <= 1.1 * float(exact)
+    # minimality: the lower estimate only excludes N whose exact maximum exceeds the target
+    for nn in range(2, got.excluded_below):
+        assert OB.tight_max(A, B, nn, relative, oracle) > target, nn
+    for nn in range(got.excluded_below, got.n):
+        r = oz.os_ii(A, B, nn, bounds=True, relative=relative)
+        assert (r.bounds["tight_rel_max"] if relative else r.bounds["tight_max"]) > target, nn
+    # the same N through device tensors
+    import torch
+    got_d = oz.suggest_n(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), target, bound="tight",
+                         relative=relative)
+    assert got_d.n == got.n and got_d.bound_max == got.bound_max

@@ -114,3 +114,15 @@ def test_sampled_parity_full_size(cuda, oracle, m, k, n, N, phi):
     A, B = dA.cpu().numpy(), dB.cpu().numpy()
     del dA, dB
     check_sampled(oracle, A, B, res, N, 1, np.random.default_rng(m + n + N))
+
+
+def test_auto_n_cfg4(cuda):
+    """The metric config's N from the paper's bound: at
+    16384^3, phi = 0, the smallest N whose tight bound certifies 1e-15
+    relative to (|A||B|)_ij is 16 (N = 15 is shown to fail)."""
+    import torch
+    dA, dB = _gen((16384, 16384), 0.0, 1234), _gen((16384, 16384), 0.0, 5678)
+    r = oz.suggest_n(dA, dB, 1e-15, bound="tight", relative=True)
+    torch.cuda.synchronize()
+    assert r.achievable and r.n == 16, r
+    assert r.tight_rel_max <= 1e-15

@@ -32,7 +32,7 @@ def test_library_exports_header_symbols():
 
 
 def test_version():
-    assert oz.load_library().oz2g_version() == 2
+    assert oz.load_library().oz2g_version() == 3
 
 
 @pytest.mark.parametrize("mode", [oz.F32, oz.F64])

@@ -17,7 +17,7 @@ def _eq(a, b):
     b = np.asarray(b)
     assert a.shape == b.shape
     if a.dtype.kind == "f":
-        ok = np.array_equal(a.view(np.uint8), b.view(np.uint8)) or np.array_equal(a, b)
+        ok = np.array_equal(a.view(np.uint8), b.view(np.uint8))  # bitwise: -0.0 != +0.0
     else:
         ok = np.array_equal(a, b)
     if not ok:
