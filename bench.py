@@ -139,6 +139,27 @@ def gen_device(rows, cols, phi, seed, dtype, device):
     return v.contiguous()
 
 
+def measure_int8_peak(oz):
+    """Dense INT8 tensor peak of this GPU (oz2g_i8_peak): burst = one ~30 ms
+    launch, sustained = ~2 s of back-to-back launches (the power-capped state
+    the residue GEMM runs in)."""
+    import ctypes as C
+    L = oz.load_library()
+    out = {}
+    try:
+        iters = 40000
+        for key, launches in (("warm", 1), ("burst", 1), ("sustained", 60)):
+            ms, ops = C.c_double(), C.c_double()
+            if L.oz2g_i8_peak(iters, launches, C.byref(ms), C.byref(ops)) != 0:
+                return None
+            if key != "warm":
+                out[key + "_tops"] = ops.value / (ms.value * 1e-3) / 1e12
+                out[key + "_ms"] = ms.value
+    except Exception:
+        return None
+    return out
+
+
 def cpu_baseline(sample_m: int, sample_n: int, k: int, nmod: int, phi: float, threads: int):
     """The oracle port (oracle/oz2_oracle.c, restating os_ii) on host cores."""
     from oracle import oracle as O
@@ -199,6 +220,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-native", action="store_true")
+    ap.add_argument("--no-int8-peak", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.k is None:
@@ -229,11 +251,17 @@ def main():
     R, Cc = tile.R, tile.C
     rows, cols = tile.rows, tile.cols
 
-    # global inputs from one seed, then this rank's blocks (inputs pre-distributed)
+    # global inputs from one seed; this rank's blocks (for the automatic N) and,
+    # with several ranks, its 1-D shards — what each rank holds before a step:
+    # the library all-gathers the row / column blocks over NVLink (comm.cpp)
     A_full = gen_device(m, k, args.phi, 1234, torch.float64, dev)
     B_full = gen_device(k, n, args.phi, 5678, torch.float64, dev)
     A = A_full[rows].contiguous()
     B = B_full[:, cols].contiguous()
+    if world > 1:
+        lay = pdist.layout(world, rank, m, n)
+        A_sh = A_full[lay["a_shard"]].contiguous()
+        B_sh = B_full[:, lay["b_shard"]].contiguous()
     del A_full, B_full
     Cout = torch.empty((A.shape[0], B.shape[1]), dtype=torch.float64, device=dev)
 
@@ -256,13 +284,22 @@ def main():
                   "emulations": sug.emulations, "seconds": round(time.perf_counter() - t0, 3)}
 
     reduce_cb = None
+    comm = None
     if world > 1:
-        row_groups, col_groups = pdist.make_groups(dist, world)
-        reduce_cb = pdist.max_reduce_hook(dist, tile, row_groups, col_groups, dev)
+        # the library's own NCCL communicator (world + ncclCommSplit row / column comms)
+        comm = pdist.NativeComm(dist, world, rank)
+        del A, B
 
     stream = torch.cuda.current_stream(dev)
 
+    class _Step:
+        def __init__(self, d):
+            self.stage_ms = tuple(d.stage_ms)
+            self.kernels_launched = d.kernels_launched
+
     def step(timing=False):
+        if comm is not None:  # shards in, tile out: all-gathers + pipeline + MAX all-reduce (oz2g_gemm_dist)
+            return _Step(comm.gemm(A_sh, B_sh, args.moduli, m, n, Cout, timing=timing))
         return oz.os_ii(A, B, args.moduli, out=Cout, timing=timing, reduce_maxima=reduce_cb)
 
     for _ in range(args.warmup):
@@ -304,7 +341,37 @@ def main():
 
     # ---- end-to-end through the public API with pinned host buffers ----
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and comm is not None:
+        # each rank: its shards from pinned host memory, the library call, its C tile back
+        A_h = torch.empty(A_sh.shape, dtype=torch.float64, pin_memory=True)
+        B_h = torch.empty(B_sh.shape, dtype=torch.float64, pin_memory=True)
+        C_h = torch.empty(Cout.shape, dtype=torch.float64, pin_memory=True)
+        A_h.copy_(A_sh)
+        B_h.copy_(B_sh)
+        Ad, Bd = torch.empty_like(A_sh), torch.empty_like(B_sh)
+
+        def e2e_step():
+            Ad.copy_(A_h, non_blocking=True)
+            Bd.copy_(B_h, non_blocking=True)
+            comm.gemm(Ad, Bd, args.moduli, m, n, Cout)
+            C_h.copy_(Cout, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+
+        e2e_step()
+        barrier()
+        e_steps = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            e2e_step()
+        barrier()
+        te = torch.tensor([(time.perf_counter() - t0) / e_steps], dtype=torch.float64, device=dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": flops / float(te.item()) / 1e12, "unit": UNIT,
+               "h2d_bytes_per_step": int(8 * (A_sh.numel() + B_sh.numel()) * world),
+               "d2h_bytes_per_step": int(8 * m * n),
+               "timing": "wall clock, max over ranks: pinned host shards -> device, oz2g_gemm_dist "
+                         "(NCCL all-gathers + pipeline + MAX all-reduce), C tile -> pinned host"}
+    elif not args.no_e2e:
         A_h = torch.empty(A.shape, dtype=torch.float64, pin_memory=True)
         B_h = torch.empty(B.shape, dtype=torch.float64, pin_memory=True)
         C_h = torch.empty(Cout.shape, dtype=torch.float64, pin_memory=True)
@@ -441,21 +508,31 @@ def main():
 
     peaks, peak_kind = _peaks()
     # dominant kernel: the N residue GEMMs (one launch); algorithmic int8 ops = 2*N*m_loc*n_loc*k
-    ops = 2.0 * args.moduli * A.shape[0] * B.shape[1] * k
+    ops = 2.0 * args.moduli * Cout.shape[0] * Cout.shape[1] * k
     gemm_avg = float(np.mean(gemm_ms))   # all residue-GEMM launches of one step
     achieved = ops / (gemm_avg * 1e-3) / 1e12
     # the residue GEMMs run per 2048-row block of C (W is held per block): equal launches
-    n_gemm_launches = -(-A.shape[0] // 2048)
-    # the residue GEMM is timed inside back-to-back steps: the sustained (power-capped) figure applies
-    int8_peak = 2.0 * peaks["bf16_tflops_sustained"]
-    int8_burst = 2.0 * peaks["bf16_tflops"]
+    n_gemm_launches = -(-Cout.shape[0] // 2048)
+    # the residue GEMM is timed inside back-to-back steps: the sustained (power-capped) figure applies.
+    # Denominator: the dense INT8 peak measured live on this GPU by a tcgen05 kind::i8 microbenchmark
+    # (oz2g_i8_peak: MMAs from shared memory on every SM, no loads / epilogue), burst and sustained.
+    i8 = measure_int8_peak(oz) if not args.no_int8_peak else None
+    if i8:
+        int8_peak, int8_burst = i8["sustained_tops"], i8["burst_tops"]
+        peak_note = (f"dense INT8 measured live (scripts/int8_peak.py microbenchmark): sustained "
+                     f"{int8_peak:.0f} TOP/s over {i8['sustained_ms']:.0f} ms back to back, burst {int8_burst:.0f}; "
+                     f"2 x bf16 of {peak_kind} peaks = {2 * peaks['bf16_tflops_sustained']:.0f} sustained")
+    else:
+        int8_peak = 2.0 * peaks["bf16_tflops_sustained"]
+        int8_burst = 2.0 * peaks["bf16_tflops"]
+        peak_note = (f"of {peak_kind}: dense INT8 = 2 x bf16 sustained ({peaks['bf16_tflops_sustained']} TF/s, "
+                     f"burst {peaks['bf16_tflops']}); int8 ops counted as FLOPs")
     traffic = _ncu_traffic(m, args.moduli) if world == 1 else None
     roof = {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s", "frac": achieved / int8_peak,
             "frac_of_burst": achieved / int8_burst,
             "traffic": traffic, "traffic_unit": "bytes per launch (ncu --set full, profiles/)",
             "kernel": "gemm_i8_tc_kernel<EPI_RESID> (N residue GEMMs of one 2048-row block of C per launch)",
-            "peak_note": f"of {peak_kind}: dense INT8 = 2 x bf16 sustained ({peaks['bf16_tflops_sustained']} TF/s, "
-                         f"burst {peaks['bf16_tflops']}); int8 ops counted as FLOPs",
+            "peak_note": peak_note, "int8_peak": i8,
             "algorithmic_ops_per_launch": ops / n_gemm_launches, "launch_ms": gemm_avg / n_gemm_launches,
             "launches_per_step": n_gemm_launches}
 

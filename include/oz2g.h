@@ -257,6 +257,55 @@ uint64_t oz2g_derive_seed(uint64_t seed, uint64_t trial, uint64_t role);
 int oz2g_native_gemm(int prec, int64_t m, int64_t n, int64_t k, const void *A, int64_t lda, const void *B,
                      int64_t ldb, void *C, int64_t ldc, void *stream);
 
+/* Dense INT8 tensor-core peak (the roofline denominator of the residue GEMM):
+ * `launches` back-to-back launches of a kernel in which every SM issues
+ * `iters` x 4 tcgen05.mma.kind::i8 128x256x32 from shared memory (no loads,
+ * no epilogue).  *ms_out = device time of all launches (CUDA events),
+ * *ops_out = int8 operations (2 per multiply-add) they performed. */
+int oz2g_i8_peak(long long iters, int launches, double *ms_out, double *ops_out);
+
+/*
+ * One emulated GEMM across P processes (one GPU each) with NCCL driven by the
+ * library.  C is tiled R x C (oz2g_grid_shape), rank q = r*C + c
+ * owns tile (r, c): rows [r*ceil(m/R), ...) and columns [c*ceil(n/C), ...).
+ *
+ *   oz2g_comm_unique_id   rank 0 creates the id (128 bytes) and shares it
+ *                         (e.g. torch.distributed broadcast);
+ *   oz2g_comm_init        every rank, with its CUDA device current: the world
+ *                         comm plus the row / column comms (ncclCommSplit);
+ *   oz2g_gemm_dist        the rank's C tile.  Device pointers.  Inputs:
+ *     default (OZ2G_DIST_SHARDS): 1-D shards — A rows [q m/P, (q+1) m/P)
+ *       (lda >= k) and the B columns of shard s = c*R + r, width n/P
+ *       (ldb >= n/P); m, n multiples of P.  The row / column blocks are
+ *       all-gathered over NVLink inside the call.
+ *     OZ2G_DIST_TILES: A is the row block r (all of k), B the column block c.
+ *   The clearance maxima are max-reduced (ncclAllReduce, int32, MAX) over the
+ *   row / column comms between the clearance product and the scaling
+ *   exponents, so every tile equals the corresponding part of the
+ *   single-device C bit for bit.  Errors are the tile's own.
+ * Failures of the comm functions: oz2g_comm_last_error().
+ */
+#define OZ2G_DIST_SHARDS 0u
+#define OZ2G_DIST_TILES 8u
+typedef struct oz2g_comm oz2g_comm;
+typedef struct oz2g_dist_tile {
+    int R, C, r, c;
+    int64_t row0, rows, col0, cols;                 /* this rank's C tile */
+    int64_t a_shard_row0, a_shard_rows;             /* its A shard (OZ2G_DIST_SHARDS) */
+    int64_t b_shard_col0, b_shard_cols;             /* its B shard */
+} oz2g_dist_tile;
+int oz2g_comm_available(void);
+int oz2g_comm_unique_id(unsigned char *id_out);
+int oz2g_comm_init(const unsigned char *id, int nranks, int rank, oz2g_comm **out);
+int oz2g_comm_grid(const oz2g_comm *comm, int *R, int *C, int *r, int *c);
+int oz2g_comm_destroy(oz2g_comm *comm);
+const char *oz2g_comm_last_error(void);
+/* Tile and shard ranges of `rank` (host-only; callable without a GPU). */
+int oz2g_dist_layout(int nranks, int rank, int64_t m, int64_t n, oz2g_dist_tile *out);
+int oz2g_gemm_dist(int prec, int64_t m, int64_t n, int64_t k, const void *A, int64_t lda, const void *B,
+                   int64_t ldb, void *C, int64_t ldc, int nmod, unsigned flags, void *stream, oz2g_comm *comm,
+                   oz2g_diag *diag);
+
 /* Library information (compiled arch, number of SMs used, version). */
 int oz2g_version(void);
 

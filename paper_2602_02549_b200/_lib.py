@@ -28,6 +28,15 @@ class Bounds(C.Structure):
                 ("tight_rel_max", C.c_double)]
 
 
+class DistTile(C.Structure):
+    _fields_ = [("R", C.c_int), ("C", C.c_int), ("r", C.c_int), ("c", C.c_int), ("row0", C.c_int64),
+                ("rows", C.c_int64), ("col0", C.c_int64), ("cols", C.c_int64), ("a_shard_row0", C.c_int64),
+                ("a_shard_rows", C.c_int64), ("b_shard_col0", C.c_int64), ("b_shard_cols", C.c_int64)]
+
+
+OZ2G_DIST_SHARDS, OZ2G_DIST_TILES = 0, 8
+
+
 class Suggest(C.Structure):
     _fields_ = [("n", C.c_int), ("cheap_n", C.c_int), ("excluded_below", C.c_int), ("emulations", C.c_int),
                 ("bound_max", C.c_double), ("tight_max", C.c_double), ("tight_rel_max", C.c_double)]
@@ -51,7 +60,9 @@ EXPORTED = ("oz2g_gemm", "oz2g_dgemm", "oz2g_sgemm", "oz2g_last_error", "oz2g_ta
             "oz2g_fp32_safe_moduli_max", "oz2g_shift_of_cmax", "oz2g_device_log2f", "oz2g_version",
             "oz2g_release_workspace", "oz2g_dd_gemm", "oz2g_suggest_n", "oz2g_gen_matrix", "oz2g_derive_seed",
             "oz2g_native_gemm", "oz2g_gemm_multi", "oz2g_grid_shape", "oz2g_init", "oz2g_synchronize",
-            "oz2g_gemm_sweep", "oz2g_suggest_n_tight")
+            "oz2g_gemm_sweep", "oz2g_suggest_n_tight", "oz2g_i8_peak", "oz2g_comm_available", "oz2g_comm_unique_id",
+            "oz2g_comm_init", "oz2g_comm_grid", "oz2g_comm_destroy", "oz2g_comm_last_error", "oz2g_dist_layout",
+            "oz2g_gemm_dist")
 
 _LIB = None
 
@@ -82,6 +93,16 @@ def load() -> C.CDLL:
                                  C.POINTER(C.c_double)]
     L.oz2g_suggest_n_tight.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
                                        C.c_int64, C.c_double, C.c_int, C.c_uint, C.c_void_p, C.POINTER(Suggest)]
+    L.oz2g_i8_peak.argtypes = [C.c_longlong, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.oz2g_comm_unique_id.argtypes = [C.c_void_p]
+    L.oz2g_comm_init.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+    L.oz2g_comm_grid.argtypes = [C.c_void_p] + [C.POINTER(C.c_int)] * 4
+    L.oz2g_comm_destroy.argtypes = [C.c_void_p]
+    L.oz2g_comm_last_error.restype = C.c_char_p
+    L.oz2g_dist_layout.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.POINTER(DistTile)]
+    L.oz2g_gemm_dist.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                                 C.c_int64, C.c_void_p, C.c_int64, C.c_int, C.c_uint, C.c_void_p, C.c_void_p,
+                                 C.POINTER(Diag)]
     L.oz2g_gen_matrix.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_uint64, C.c_void_p]
     L.oz2g_derive_seed.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
     L.oz2g_derive_seed.restype = C.c_uint64

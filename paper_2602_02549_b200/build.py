@@ -15,7 +15,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "liboz2g.so")
-SOURCES = ["api.cu", "gemm_tc.cu", "scale.cu", "resid.cu", "crt.cu", "bounds.cu", "tables.cpp", "harness.cpp"]
+SOURCES = ["api.cu", "gemm_tc.cu", "scale.cu", "resid.cu", "crt.cu", "bounds.cu", "tables.cpp", "harness.cpp",
+           "comm.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
@@ -48,7 +49,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as pool:
         objs = list(pool.map(compile_one, SOURCES))
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", OUT, *objs,
-           "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-L/usr/local/cuda/lib64", "-lcudart"]
+           "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-L/usr/local/cuda/lib64", "-lcudart", "-ldl"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

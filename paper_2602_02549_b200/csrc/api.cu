@@ -89,7 +89,7 @@ struct Workspace {
     // relative error criterion (suggest_n tight / relative): floor operands, their
     // row / column sums and product (launch_floor_operands); valid for the
     // inputs of the last scan that computed them
-    DevBuf lo_a, lo_b, lo_sum, lo_ab;
+    DevBuf lo_a, lo_b, lo_sum, lo_ab, ab_lo;
     bool lo_ready = false;
     // changed-tile flags of the speculation checks: mapped pinned host memory
     // written by the check kernel, read by the host after an event
@@ -155,7 +155,7 @@ struct Workspace {
         for (DevBuf* b : {&A, &B, &C, &abar, &bbar, &ares, &bres, &W, &mup, &nup, &mu, &nu, &bmax, &cmax_row,
                           &cmax_col, &e, &f, &status, &x_cbar, &x_cprod, &x_c1, &x_c2, &x_q, &x_cpp64, &x_cpp32,
                           &x_ap, &x_bp, &x_bvec, &x_bscr, &x_bmax, &x_bcheap, &x_btight, &status_ring, &spec_st,
-                          &lo_a, &lo_b, &lo_sum, &lo_ab})
+                          &lo_a, &lo_b, &lo_sum, &lo_ab, &ab_lo})
             b->release();
         if (spec_changed) cudaFreeHost(spec_changed);
         spec_changed = nullptr;
@@ -462,7 +462,13 @@ void compute_relative_operands(Workspace& ws, int prec, const void* dA, int64_t 
     g.cplane = m * n;
     CUDA_TRY(launch_gemm_i8(EPI_I32, make_plane_map(la, kp, m, 1, gemm_tile_m()),
                             make_plane_map_mn(lb, n, ldn, kp, 1, kp * ldn), g, ws.num_sms, stream));
-    ++launches;
+    // the fp64 lower bound per entry, refined by rounded-down dot products
+    // where the floor product is loose (at most 2^32 multiply-adds)
+    double* abl = (double*)ws.ab_lo.get(8 * (size_t)(m * n));
+    unsigned long long* budget = (unsigned long long*)ws.x_bmax.get(32) + 3;
+    CUDA_TRY(launch_ab_lower(prec, dA, lda, dB, ldb, m, n, k, lab, mup, nup, sums, sums + m, abl, budget,
+                             1ull << 32, stream));
+    launches += 2;
     ws.lo_ready = true;
 }
 
@@ -816,7 +822,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             exb.bnd.v.ea += r0;
             if (exb.bnd.cheap) exb.bnd.cheap += eo;
             if (exb.bnd.tight) exb.bnd.tight += eo;
-            if (exb.bnd.lo) exb.bnd.lo += eo;
+            if (exb.bnd.ab_lo) exb.bnd.ab_lo += eo;
         }
         tm.span(6, crt_stream, [&] {
             CUDA_TRY(launch_crt(prec, Wb, ldw, wrows * ldw, rc, nc, cc, mu + r0, nu + c0,
@@ -1188,9 +1194,9 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             launches += 5;
             if (bo->relative && !ws.lo_ready)
                 compute_relative_operands(ws, prec, dA, lda_d, dB, ldb_d, m, n, k, mup, nup, stream, launches);
-            bmax_dev = (unsigned long long*)ws.x_bmax.get(24);
+            bmax_dev = (unsigned long long*)ws.x_bmax.get(32);
             CUDA_TRY(cudaMemsetAsync(bmax_dev, 0, 24, stream));
-            ex.bnd.lo = bo->relative ? (const int32_t*)ws.lo_ab.p : nullptr;
+            ex.bnd.ab_lo = bo->relative ? (const double*)ws.ab_lo.p : nullptr;
             ex.bnd.on = 1;
             ex.bnd.v = v;
             ex.bnd.t2_up = bs.t2_up;
@@ -1498,7 +1504,7 @@ int run_suggest_tight(int prec, int64_t m, int64_t n, int64_t k, const void* A, 
     v.ea = reinterpret_cast<int32_t*>(v.RA + 2 * (m + n));
     v.eb = v.ea + m;
     const int32_t* sums = (const int32_t*)ws.lo_sum.p;
-    unsigned long long* bits = (unsigned long long*)ws.x_bmax.get(24);
+    unsigned long long* bits = (unsigned long long*)ws.x_bmax.get(32);
     const int n_max = prec == OZ2G_FP32 ? fp32_safe_moduli_max() : kMaxModuli;
     int n0 = 0;
     for (int nm = 2; nm <= n_max && !n0; ++nm) {
@@ -1946,6 +1952,37 @@ int oz2g_native_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, i
         if (m < 0 || n < 0 || k < 0 || lda < k || ldb < n || ldc < n)
             throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_native_gemm: bad dimensions"};
         CUDA_TRY(launch_native_gemm(prec, A, lda, B, ldb, m, n, k, C, ldc, (cudaStream_t)stream));
+        return OZ2G_OK;
+    });
+}
+
+int oz2g_i8_peak(long long iters, int launches, double* ms_out, double* ops_out) {
+    return guarded([&] {
+        if (iters < 1 || launches < 1) throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_i8_peak: iters, launches >= 1"};
+        int dev = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        Workspace& ws = workspace(dev, 0);
+        std::lock_guard<std::recursive_mutex> lk(ws.mtx);
+        int* sink = (int*)ws.x_bmax.get(32);
+        cudaStream_t s = nullptr;
+        cudaEvent_t e0, e1;
+        CUDA_TRY(cudaEventCreate(&e0));
+        CUDA_TRY(cudaEventCreate(&e1));
+        double ops = 0, one = 0;
+        CUDA_TRY(launch_i8_peak(iters, ws.num_sms, sink, s, &one));  // warm-up
+        CUDA_TRY(cudaEventRecord(e0, s));
+        for (int i = 0; i < launches; ++i) {
+            CUDA_TRY(launch_i8_peak(iters, ws.num_sms, sink, s, &one));
+            ops += one;
+        }
+        CUDA_TRY(cudaEventRecord(e1, s));
+        CUDA_TRY(cudaEventSynchronize(e1));
+        float ms = 0;
+        CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (ms_out) *ms_out = ms;
+        if (ops_out) *ops_out = ops;
         return OZ2G_OK;
     });
 }

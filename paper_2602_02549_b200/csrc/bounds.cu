@@ -214,6 +214,38 @@ __global__ void __launch_bounds__(256) tight_lower_max_kernel(BoundVecs v, int64
     if ((threadIdx.x & 31) == 0) atomicMax(out_bits, best);
 }
 
+
+// Lower bound of (|A||B|)_ij for the relative criterion, m x n fp64:
+// lo_ij 2^-(mu'_i + nu'_j + 2) from the floor-operand product, or — where
+// that is loose (its upper counterpart exceeds it by more than 1/16, e.g.
+// entries whose large terms do not meet: wide exponent spreads) — the dot
+// product sum_h |a_ih||b_hj| with every operation rounded down (each term is
+// exact for fp32 inputs, and rounding down keeps a lower bound), within a
+// global budget of refined multiply-adds (the rest keep the floor bound).
+template <class T>
+__global__ void __launch_bounds__(256) ab_lower_kernel(const T* __restrict__ A, int64_t lda, const T* __restrict__ B,
+                                                       int64_t ldb, int64_t m, int64_t n, int64_t k,
+                                                       const int32_t* __restrict__ lo, const int32_t* __restrict__ mup,
+                                                       const int32_t* __restrict__ nup,
+                                                       const int32_t* __restrict__ rsum,
+                                                       const int32_t* __restrict__ csum, double* __restrict__ out,
+                                                       unsigned long long* budget, unsigned long long cap) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m * n) return;
+    const int64_t i = e / n, j = e - i * n;
+    const long long l = lo[e];
+    const long long slack = (long long)rsum[i] + csum[j] + k;
+    const int sc = -(mup[i] + nup[j] + 2);
+    double v = l > 0 ? ldexp_rd(__ll2double_rd(l), sc) : 0.0;
+    if (16 * slack > l && atomicAdd(budget, (unsigned long long)k) + (unsigned long long)k <= cap) {
+        double acc = 0.0;
+        for (int64_t h = 0; h < k; ++h)
+            acc = __fma_rd(fabs((double)A[i * lda + h]), fabs((double)B[h * ldb + j]), acc);
+        v = acc > v ? acc : v;
+    }
+    out[e] = v;
+}
+
 // The experiment harness's "native" GEMM (experiment.hpp:55-68): per entry a
 // sequential loop h = 0..k-1 with a separate RN multiply and RN add in the
 // working precision T (no FMA), exactly the reference's err_native reference.
@@ -298,6 +330,23 @@ cudaError_t launch_tight_lower_max(const BoundVecs& v, int64_t m, int64_t n, int
     const int64_t want = (m * n + 255) / 256;
     const unsigned grid = (unsigned)(want < (int64_t)num_sms * 8 ? want : (int64_t)num_sms * 8);
     tight_lower_max_kernel<<<grid, 256, 0, s>>>(v, m, n, k, t_up, kt2_up, lo, rsum, csum, out_bits);
+    return cudaGetLastError();
+}
+
+
+cudaError_t launch_ab_lower(int prec, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n,
+                            int64_t k, const int32_t* lo, const int32_t* mup, const int32_t* nup, const int32_t* rsum,
+                            const int32_t* csum, double* out, unsigned long long* budget, unsigned long long cap,
+                            cudaStream_t s) {
+    if (m * n == 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(budget, 0, 8, s);
+    if (e != cudaSuccess) return e;
+    if (prec)
+        ab_lower_kernel<double><<<blocks_for(m * n, 256), 256, 0, s>>>((const double*)A, lda, (const double*)B, ldb, m,
+                                                                      n, k, lo, mup, nup, rsum, csum, out, budget, cap);
+    else
+        ab_lower_kernel<float><<<blocks_for(m * n, 256), 256, 0, s>>>((const float*)A, lda, (const float*)B, ldb, m, n,
+                                                                     k, lo, mup, nup, rsum, csum, out, budget, cap);
     return cudaGetLastError();
 }
 

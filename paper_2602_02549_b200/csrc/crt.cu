@@ -160,9 +160,9 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
                 const unsigned long long tb = (unsigned long long)__double_as_longlong(tight);
                 bmax_cheap = cb > bmax_cheap ? cb : bmax_cheap;
                 bmax_tight = tb > bmax_tight ? tb : bmax_tight;
-                if (bc.lo) {  // tight / (|A||B|)_ij, rounded up against a lower bound of |A||B|
-                    const int32_t lv = bc.lo[o];
-                    const double rel = lv > 0 ? ldexp_ru(__ddiv_ru(tight, (double)lv), 12 - eai - ebj) : __longlong_as_double(0x7ff0000000000000ll);
+                if (bc.ab_lo) {  // tight / (|A||B|)_ij, rounded up against a lower bound of |A||B|
+                    const double lv = bc.ab_lo[o];
+                    const double rel = lv > 0.0 ? __ddiv_ru(tight, lv) : __longlong_as_double(0x7ff0000000000000ll);
                     const unsigned long long rb = (unsigned long long)__double_as_longlong(rel);
                     bmax_rel = rb > bmax_rel ? rb : bmax_rel;
                 }
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
         if ((threadIdx.x & 31) == 0) {
             atomicMax(&ex.bnd.max_bits[0], bmax_cheap);
             atomicMax(&ex.bnd.max_bits[1], bmax_tight);
-            if (ex.bnd.lo) atomicMax(&ex.bnd.max_bits[2], bmax_rel);
+            if (ex.bnd.ab_lo) atomicMax(&ex.bnd.max_bits[2], bmax_rel);
         }
     }
 }

@@ -134,6 +134,12 @@ __device__ __forceinline__ double ldexp_rn(double x, int s) {
 }
 
 // x * 2^s rounded upward, x >= 0 (each step rounds up: the result is >= exact).
+__device__ __forceinline__ double ldexp_rd(double x, int s) {
+    while (s > 1000) { x = __dmul_rd(x, pow2d(1000)); s -= 1000; }
+    while (s < -1000) { x = __dmul_rd(x, pow2d(-1000)); s += 1000; }
+    return __dmul_rd(x, pow2d(s));
+}
+
 __device__ __forceinline__ double ldexp_ru(double x, int s) {
     while (s > 1000) { x = __dmul_ru(x, pow2d(1000)); s -= 1000; }
     while (s < -1000) { x = __dmul_ru(x, pow2d(-1000)); s += 1000; }

@@ -550,6 +550,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Dense INT8 tensor-core peak (the roofline denominator of the residue GEMM,
+// SURVEY §6): one CTA per SM issues `iters` x 4 tcgen05.mma kind::i8
+// 128x256x32 from one shared-memory stage (the residue GEMM's own operand
+// layouts and instruction descriptor) into one TMEM accumulator — no TMA, no
+// epilogue — so the launch time is the tensor pipe's alone.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128, 1) i8_peak_kernel(long long iters, int* sink) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + A_BYTES;
+    uint64_t* done = reinterpret_cast<uint64_t*>(sB + B_BYTES);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < (A_BYTES + B_BYTES) / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t*>(smem)[i] = 0x01010101u * (uint32_t)(i & 3);
+    if (threadIdx.x == 0) { mbar_init(done, 1); fence_mbar_init(); }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (warp == 1) { tmem_alloc(tmem_slot, 256); tmem_relinquish(); }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (warp == 0 && lane == 0) {
+        const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+        for (long long it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int k = 0; k < BK / 32; ++k)
+                mma_i8(tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128_mn(b0 + k * 32 * 128, B_CHUNK), IDESC,
+                       (it | k) != 0 ? 1u : 0u);
+        }
+        mma_commit(done);
+    }
+    __syncwarp();
+    mbar_wait(done, 0);
+    tc_fence_after();
+    if (warp == 0) {  // keep the result live
+        uint32_t v[32];
+        tmem_ld32(tmem, v);
+        tmem_ld_wait();
+        if (v[0] == 0x7fffffffu && lane == 0) *sink = 1;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) { tc_fence_after(); tmem_dealloc(tmem, 256); }
+}
+
 }  // namespace
 
 int gemm_smem_bytes() { return SMEM_BYTES; }
@@ -655,6 +705,18 @@ cudaError_t launch_gemm_i8_pair(int mode, const CUtensorMap& tmA, const CUtensor
     if (stages == 6) return launch_pair_s<6>(mode, grid, tmA, tmB, P, stream);
     if (stages == 5) return launch_pair_s<5>(mode, grid, tmA, tmB, P, stream);
     return launch_pair_s<4>(mode, grid, tmA, tmB, P, stream);
+}
+
+
+// Dense INT8 peak microbenchmark: one launch of i8_peak_kernel on every SM,
+// `iters` x 4 MMAs (2 x 128 x 256 x 32 int8 ops each) per SM.
+cudaError_t launch_i8_peak(long long iters, int num_sms, int* sink, cudaStream_t stream, double* ops) {
+    const int smem = A_BYTES + B_BYTES + 1024 + 64;
+    cudaError_t err = cudaFuncSetAttribute(i8_peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return err;
+    i8_peak_kernel<<<num_sms, 128, smem, stream>>>(iters, sink);
+    if (ops) *ops = (double)num_sms * (double)iters * 4.0 * 2.0 * BM * BN * 32.0;
+    return cudaGetLastError();
 }
 
 }  // namespace oz2g

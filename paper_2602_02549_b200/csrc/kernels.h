@@ -40,6 +40,7 @@ struct GemmParams {
 };
 
 int gemm_smem_bytes();
+cudaError_t launch_i8_peak(long long iters, int num_sms, int* sink, cudaStream_t stream, double* ops);
 int gemm_tile_m();
 int gemm_tile_n();
 int gemm_tile_k();
@@ -114,6 +115,10 @@ cudaError_t launch_cheap_bound_max(const BoundVecs& v, int64_t m, int64_t n, dou
 cudaError_t launch_tight_lower_max(const BoundVecs& v, int64_t m, int64_t n, int64_t k, double t_up, double kt2_up,
                                    const int32_t* lo, const int32_t* rsum, const int32_t* csum,
                                    unsigned long long* out_bits, int num_sms, cudaStream_t s);
+cudaError_t launch_ab_lower(int prec, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n,
+                            int64_t k, const int32_t* lo, const int32_t* mup, const int32_t* nup, const int32_t* rsum,
+                            const int32_t* csum, double* out, unsigned long long* budget, unsigned long long cap,
+                            cudaStream_t s);
 cudaError_t launch_floor_operands(int prec, const void* A, int64_t lda, int64_t m, const void* B, int64_t ldb,
                                   int64_t k, int64_t n, int64_t kp, int64_t ldn, const int32_t* mu_prime,
                                   const int32_t* nu_prime, int8_t* a_out, int8_t* b_out, int32_t* rsum,
@@ -135,9 +140,8 @@ struct BoundCtx {  // evaluated in the CRT pass when `on`
     double t2_up, rconst_up, ucoef, kpr_cheap_up, k_rconst_up;
     double *cheap, *tight;             // optional m x n outputs (device)
     unsigned long long* max_bits;      // [0] cheap max, [1] tight max, [2] tight / |A||B| max (bits)
-    // relative criterion: (|A||B|)_ij >= lo[i * n + j] 2^-(mu'_i + nu'_j + 2) (launch_floor_operands);
-    // nullptr: no relative maximum
-    const int32_t* lo;
+    // relative criterion: (|A||B|)_ij >= ab_lo[i * n + j] (launch_ab_lower); nullptr: no relative maximum
+    const double* ab_lo;
 };
 // Status flags per (row group, column group) of C instead of the launch's
 // single status (speculated exponents, api.cu): entry (i, j) of the launch
