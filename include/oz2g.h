@@ -260,9 +260,11 @@ int oz2g_native_gemm(int prec, int64_t m, int64_t n, int64_t k, const void *A, i
 /* Dense INT8 tensor-core peak (the roofline denominator of the residue GEMM):
  * `launches` back-to-back launches of a kernel in which every SM issues
  * `iters` x 4 tcgen05.mma.kind::i8 128x256x32 from shared memory (no loads,
- * no epilogue).  *ms_out = device time of all launches (CUDA events),
- * *ops_out = int8 operations (2 per multiply-add) they performed. */
-int oz2g_i8_peak(long long iters, int launches, double *ms_out, double *ops_out);
+ * no epilogue), on a low-toggle operand pattern (random = 0: the clock-limited
+ * peak) or pseudo-random bytes (random = 1: the power draw of real residue
+ * planes).  *ms_out = device time of all launches (CUDA events), *ops_out =
+ * int8 operations (2 per multiply-add) they performed. */
+int oz2g_i8_peak(long long iters, int launches, int random, double *ms_out, double *ops_out);
 
 /*
  * One emulated GEMM across P processes (one GPU each) with NCCL driven by the

@@ -93,7 +93,7 @@ def load() -> C.CDLL:
                                  C.POINTER(C.c_double)]
     L.oz2g_suggest_n_tight.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
                                        C.c_int64, C.c_double, C.c_int, C.c_uint, C.c_void_p, C.POINTER(Suggest)]
-    L.oz2g_i8_peak.argtypes = [C.c_longlong, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.oz2g_i8_peak.argtypes = [C.c_longlong, C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.oz2g_comm_unique_id.argtypes = [C.c_void_p]
     L.oz2g_comm_init.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
     L.oz2g_comm_grid.argtypes = [C.c_void_p] + [C.POINTER(C.c_int)] * 4

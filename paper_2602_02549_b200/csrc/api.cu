@@ -1956,7 +1956,7 @@ int oz2g_native_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, i
     });
 }
 
-int oz2g_i8_peak(long long iters, int launches, double* ms_out, double* ops_out) {
+int oz2g_i8_peak(long long iters, int launches, int random, double* ms_out, double* ops_out) {
     return guarded([&] {
         if (iters < 1 || launches < 1) throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_i8_peak: iters, launches >= 1"};
         int dev = 0;
@@ -1969,10 +1969,10 @@ int oz2g_i8_peak(long long iters, int launches, double* ms_out, double* ops_out)
         CUDA_TRY(cudaEventCreate(&e0));
         CUDA_TRY(cudaEventCreate(&e1));
         double ops = 0, one = 0;
-        CUDA_TRY(launch_i8_peak(iters, ws.num_sms, sink, s, &one));  // warm-up
+        CUDA_TRY(launch_i8_peak(iters, random, ws.num_sms, sink, s, &one));  // warm-up
         CUDA_TRY(cudaEventRecord(e0, s));
         for (int i = 0; i < launches; ++i) {
-            CUDA_TRY(launch_i8_peak(iters, ws.num_sms, sink, s, &one));
+            CUDA_TRY(launch_i8_peak(iters, random, ws.num_sms, sink, s, &one));
             ops += one;
         }
         CUDA_TRY(cudaEventRecord(e1, s));

@@ -558,7 +558,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 // layouts and instruction descriptor) into one TMEM accumulator — no TMA, no
 // epilogue — so the launch time is the tensor pipe's alone.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128, 1) i8_peak_kernel(long long iters, int* sink) {
+__global__ void __launch_bounds__(128, 1) i8_peak_kernel(long long iters, int random, int* sink) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -567,8 +567,13 @@ __global__ void __launch_bounds__(128, 1) i8_peak_kernel(long long iters, int* s
     uint64_t* done = reinterpret_cast<uint64_t*>(sB + B_BYTES);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < (A_BYTES + B_BYTES) / 4; i += blockDim.x)
-        reinterpret_cast<uint32_t*>(smem)[i] = 0x01010101u * (uint32_t)(i & 3);
+    // operand bytes: a low-toggle pattern (the tensor pipe's clock-limited peak) or
+    // pseudo-random bytes (its power draw on data like the residue planes)
+    for (int i = threadIdx.x; i < (A_BYTES + B_BYTES) / 4; i += blockDim.x) {
+        uint32_t x = (uint32_t)i * 0x9E3779B1u + blockIdx.x * 0x85EBCA77u;
+        x ^= x >> 15; x *= 0x2C1B3C6Du; x ^= x >> 12; x *= 0x297A2D39u; x ^= x >> 15;
+        reinterpret_cast<uint32_t*>(smem)[i] = random ? x : 0x01010101u * (uint32_t)(i & 3);
+    }
     if (threadIdx.x == 0) { mbar_init(done, 1); fence_mbar_init(); }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (warp == 1) { tmem_alloc(tmem_slot, 256); tmem_relinquish(); }
@@ -710,11 +715,11 @@ cudaError_t launch_gemm_i8_pair(int mode, const CUtensorMap& tmA, const CUtensor
 
 // Dense INT8 peak microbenchmark: one launch of i8_peak_kernel on every SM,
 // `iters` x 4 MMAs (2 x 128 x 256 x 32 int8 ops each) per SM.
-cudaError_t launch_i8_peak(long long iters, int num_sms, int* sink, cudaStream_t stream, double* ops) {
+cudaError_t launch_i8_peak(long long iters, int random, int num_sms, int* sink, cudaStream_t stream, double* ops) {
     const int smem = A_BYTES + B_BYTES + 1024 + 64;
     cudaError_t err = cudaFuncSetAttribute(i8_peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
-    i8_peak_kernel<<<num_sms, 128, smem, stream>>>(iters, sink);
+    i8_peak_kernel<<<num_sms, 128, smem, stream>>>(iters, random, sink);
     if (ops) *ops = (double)num_sms * (double)iters * 4.0 * 2.0 * BM * BN * 32.0;
     return cudaGetLastError();
 }

@@ -40,7 +40,7 @@ struct GemmParams {
 };
 
 int gemm_smem_bytes();
-cudaError_t launch_i8_peak(long long iters, int num_sms, int* sink, cudaStream_t stream, double* ops);
+cudaError_t launch_i8_peak(long long iters, int random, int num_sms, int* sink, cudaStream_t stream, double* ops);
 int gemm_tile_m();
 int gemm_tile_n();
 int gemm_tile_k();

@@ -17,9 +17,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def measure(L, iters, launches):
+def measure(L, iters, launches, random):
     ms, ops = C.c_double(), C.c_double()
-    rc = L.oz2g_i8_peak(iters, launches, C.byref(ms), C.byref(ops))
+    rc = L.oz2g_i8_peak(iters, launches, random, C.byref(ms), C.byref(ops))
     if rc:
         raise RuntimeError(L.oz2g_last_error().decode())
     return ops.value / (ms.value * 1e-3) / 1e12, ms.value
@@ -37,17 +37,20 @@ def main():
     L = oz.load_library()
     # iterations per launch for ~30 ms at ~3 POP/s: 148 SMs x 4 MMAs x 2^21 ops
     iters = 40000
-    measure(L, iters, 1)
-    with ClockSampler(0) as cs_b:
-        burst, ms_b = measure(L, iters, 1)
-        time.sleep(0.2)
-    with ClockSampler(0) as cs_s:
-        sustained, ms_s = measure(L, iters, 130)
     res = {"what": "dense INT8 tensor peak: tcgen05.mma.cta_group::1.kind::i8 128x256x32, operands in shared memory, "
-                   "one CTA per SM, int8 ops = 2 x multiply-adds",
-           "burst_tops": burst, "burst_ms": ms_b, "burst_clocks": cs_b.summary(),
-           "sustained_tops": sustained, "sustained_ms": ms_s, "sustained_clocks": cs_s.summary(),
+                   "one CTA per SM, int8 ops = 2 x multiply-adds; 'ideal' = low-toggle operand bytes, 'random' = "
+                   "pseudo-random operand bytes (power draw of real data)",
            "gpu": torch.cuda.get_device_name(0), "sms": torch.cuda.get_device_properties(0).multi_processor_count}
+    for rnd, key in ((0, "ideal"), (1, "random")):
+        measure(L, iters, 3, rnd)
+        with ClockSampler(0) as cs_b:
+            burst, ms_b = measure(L, iters, 1, rnd)
+            time.sleep(0.2)
+        with ClockSampler(0) as cs_s:
+            sustained, ms_s = measure(L, iters, 130, rnd)
+        res[key] = {"burst_tops": burst, "burst_ms": ms_b, "burst_clocks": cs_b.summary(),
+                    "sustained_tops": sustained, "sustained_ms": ms_s, "sustained_clocks": cs_s.summary()}
+        time.sleep(2.0)
     print(json.dumps(res))
     if a.out:
         json.dump(res, open(a.out, "w"), indent=1)
