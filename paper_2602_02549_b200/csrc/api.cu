@@ -310,6 +310,13 @@ int crt_overlap_blocks() {
     return v;
 }
 
+// Residue GEMMs + CRT fused in one kernel (fused.cu) instead of the int8-W
+// GEMM epilogue followed by the CRT pass: OZ2G_FUSED=1 on, 0 off.  Read per call.
+int fused_mode() {
+    const char* s = std::getenv("OZ2G_FUSED");
+    return s ? std::atoi(s) : 0;
+}
+
 // Speculated exponents on the pipelined host path (run_gemm): OZ2G_SPEC=0
 // off, 1 column exponents only (B uploaded first), 2 row and column exponents
 // (A row chunks interleaved with B column chunks).  Unset: 2 for inputs of at
@@ -1210,7 +1217,33 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         }
         // every read of the device copies of A and B is enqueued by now
         if (host && ws.ev_inputs_free) CUDA_TRY(cudaEventRecord(ws.ev_inputs_free, stream));
-        for (size_t bi = 0; bi < nb; ++bi) run_block(bi, 0, n, st);
+        const bool fused = fused_mode() == 1 && !inter && !bo && !overlap && m * n > 0;
+        if (fused) {
+            // the N residue GEMMs with the CRT and the inverse scaling in their epilogue:
+            // one launch over every 128 x 128 tile of C, no W
+            FusedParams fp;
+            std::memset(&fp, 0, sizeof fp);
+            fp.g = gp;
+            fp.g.planes = N;
+            fp.g.m = (int)m;
+            fp.g.n = (int)n;
+            fp.g.tiles_m = (int)((m + fused_tile_m() - 1) / fused_tile_m());
+            fp.g.tiles_n = (int)((n + fused_tile_n() - 1) / fused_tile_n());
+            fp.g.group_m = group_m_for(fp.g.tiles_m, fp.g.tiles_n);
+            for (int l = 0; l < N; ++l) { fp.s1[l] = tab.s1[l]; fp.s2[l] = tab.s2[l]; }
+            fp.P1 = tab.P1; fp.P2 = tab.P2; fp.P_inv = tab.P_inv;
+            fp.mode = tab.mode;
+            fp.mu = mu;
+            fp.nu = nu;
+            fp.C = dC;
+            fp.ldc = ldc_d;
+            fp.st = st;
+            const CUtensorMap tA = make_plane_map(ares, kp, m, N, fused_tile_m(), m * kp);
+            tm.span(5, stream, [&] { CUDA_TRY(launch_gemm_crt_fused(prec, tA, tBres, fp, ws.num_sms, stream)); });
+            ++launches;
+        } else {
+            for (size_t bi = 0; bi < nb; ++bi) run_block(bi, 0, n, st);
+        }
     }
     if (overlap) {  // join the side stream
         const cudaEvent_t ej = ws.pool_event(evn++);

@@ -128,6 +128,24 @@ cudaError_t launch_dd_gemm(const double* A, int64_t lda, const double* B, int64_
 cudaError_t launch_native_gemm(int prec, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m,
                                int64_t n, int64_t k, void* C, int64_t ldc, cudaStream_t s);
 
+// Residue GEMMs with the CRT + inverse scaling in the epilogue (fused.cu):
+// one launch over every 128 x 128 tile of C, all N planes per tile.
+struct FusedParams {
+    GemmParams g;                // m, n, kblocks, planes = N, tiles, group_m, hints, p / magic / off
+    double s1[49], s2[49];
+    double P1, P2, P_inv;
+    int mode;                    // 1: fp64 table (C2 chain), 0: fp32 table
+    const int32_t* mu;           // [m]
+    const int32_t* nu;           // [n]
+    void* C;                     // T [m][ldc]
+    int64_t ldc;
+    DevStatus* st;
+};
+int fused_tile_m();
+int fused_tile_n();
+cudaError_t launch_gemm_crt_fused(int prec, const CUtensorMap& tmA, const CUtensorMap& tmB, const FusedParams& P,
+                                  int num_sms, cudaStream_t stream);
+
 // CRT + inverse scaling (crt.cu).
 struct CrtConsts {
     int n, mode;
