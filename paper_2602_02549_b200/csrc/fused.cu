@@ -90,7 +90,7 @@ __device__ __forceinline__ int residue_w(uint32_t v, uint32_t p, uint32_t magic,
 }
 
 template <class T, bool DD>
-__global__ void __maxnreg__(200)
+__global__ void __maxnreg__(192)
     gemm_crt_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ FusedParams P) {
     extern __shared__ uint8_t smem_raw[];
