@@ -19,8 +19,9 @@
 //   warps 2..9    epilogue, 8 warps: warp w reads TMEM lanes 32 (w % 4) ..
 //                 (the tcgen05.ld lane restriction) and columns 64 ((w-2) / 4)
 //                 .. +63, so each thread owns 64 entries of one row.
-// Per entry the state across planes is C1 (fp64, in the thread's registers)
-// and C2 (fp64, in TMEM columns 256..511 — 2 columns per entry), both updated
+// Per entry the state across planes is C1 (fp64, in the thread's registers
+// for 32 of its entries, in shared memory for the other 32) and C2 (fp64, in
+// TMEM columns 256..511 — 2 columns per entry), both updated
 // by the reference's fma in plane order l = 0, 1, ..., so C1 and C2 are the
 // reference's ordered chains bit for bit (in fp64 mode C1 is even exact,
 // Lemma 2; in fp32 mode it is not, and the order is what makes it match).
@@ -37,14 +38,20 @@ namespace oz2g {
 
 namespace {
 
-constexpr int FBM = 128, FBN = 128, FBK = 128, FSTAGES = 6;
+constexpr int FBM = 128, FBN = 128, FBK = 128, FSTAGES = 5;
 constexpr int FA_BYTES = FBM * FBK;  // 16 KB
 constexpr int FB_BYTES = FBN * FBK;  // 16 KB (one MN-major box: 128 columns x 128 K-rows)
 constexpr int F_EPI_WARPS = 8;
 constexpr int F_COLS = FBN / (F_EPI_WARPS / 4);  // columns of the tile per epilogue thread
 constexpr int F_THREADS = 64 + 32 * F_EPI_WARPS;
 constexpr uint32_t FIDESC = idesc_i8(FBM, FBN, true);
-constexpr int F_SMEM = FSTAGES * (FA_BYTES + FB_BYTES) + 1024 + 256;
+// C1 of the upper half of each thread's columns lives in shared memory
+// ([column][row] doubles: a warp's lanes hit consecutive words), the lower half
+// in registers: 10 warps are 3 per SM sub-partition, whose 16K registers
+// allow 168 per thread, too few for 64 fp64 accumulators plus the work.
+constexpr int F_COLS_REG = 32;
+constexpr int F_C1S_BYTES = (FBN / 2) * FBM * 8;  // 64 KB: 2 column groups x 32 columns x 128 rows
+constexpr int F_SMEM = FSTAGES * (FA_BYTES + FB_BYTES) + F_C1S_BYTES + 1024 + 256;
 constexpr uint32_t F_C2_COL = 256;  // first TMEM column of the C2 state
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
@@ -90,7 +97,7 @@ __device__ __forceinline__ int residue_w(uint32_t v, uint32_t p, uint32_t magic,
 }
 
 template <class T, bool DD>
-__global__ void __maxnreg__(192)
+__global__ void __launch_bounds__(F_THREADS, 1)
     gemm_crt_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ FusedParams P) {
     extern __shared__ uint8_t smem_raw[];
@@ -98,7 +105,8 @@ __global__ void __maxnreg__(192)
     uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
     uint8_t* sA = smem;
     uint8_t* sB = smem + FSTAGES * FA_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + FSTAGES * FB_BYTES);
+    double* c1s = reinterpret_cast<double*>(sB + FSTAGES * FB_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + FSTAGES * FB_BYTES + F_C1S_BYTES);
     uint64_t* empty = full + FSTAGES;
     uint64_t* tfull = empty + FSTAGES;
     uint64_t* tempty = tfull + 2;
@@ -185,9 +193,11 @@ __global__ void __maxnreg__(192)
             decode_tile(u, G.tiles_m, G.tiles_n, G.group_m, tm, tn);
             const int64_t row = (int64_t)tm * FBM + quad * 32 + lane;
             const int64_t col0 = (int64_t)tn * FBN + cgrp * F_COLS;
-            double c1[F_COLS];
+            double c1[F_COLS_REG];                           // columns 0 .. 31 of the thread's 64
 #pragma unroll
-            for (int j = 0; j < F_COLS; ++j) c1[j] = 0.0;   // crt.hpp:99: both chains start at +0.0
+            for (int j = 0; j < F_COLS_REG; ++j) c1[j] = 0.0;   // crt.hpp:99: both chains start at +0.0
+            // columns 32 .. 63: c1s[(cgrp * 32 + j) * 128 + row in tile]
+            double* c1x = c1s + (size_t)cgrp * 32 * FBM + quad * 32 + lane;
             for (int l = 0; l < N; ++l, ++it) {
                 const int acc = it & 1;
                 mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
@@ -208,7 +218,13 @@ __global__ void __maxnreg__(192)
 #pragma unroll
                     for (int b = 0; b < 8; ++b) {
                         const double wv = (double)residue_w(v[b], p, magic, off);
-                        c1[ch * 8 + b] = __fma_rn(s1, wv, c1[ch * 8 + b]);          // crt.hpp:99-104
+                        const int jj = ch * 8 + b;
+                        if (jj < F_COLS_REG) {
+                            c1[jj] = __fma_rn(s1, wv, c1[jj]);                          // crt.hpp:99-104
+                        } else {
+                            double* cp = c1x + (size_t)(jj - F_COLS_REG) * FBM;
+                            *cp = __fma_rn(s1, wv, l > 0 ? *cp : 0.0);
+                        }
                         if (DD) {
                             const double prev = l > 0 ? __hiloint2double((int)c2w[2 * b + 1], (int)c2w[2 * b]) : 0.0;
                             const double c2 = __fma_rn(s2, wv, prev);
@@ -224,7 +240,8 @@ __global__ void __maxnreg__(192)
                     for (int b = 0; b < 8; ++b) {
                         const int64_t j = col0 + ch * 8 + b;
                         if (j >= G.n) break;
-                        const double c1v = c1[ch * 8 + b];
+                        const int jj = ch * 8 + b;
+                        const double c1v = jj < F_COLS_REG ? c1[jj] : c1x[(size_t)(jj - F_COLS_REG) * FBM];
                         const double c2v = DD ? __hiloint2double((int)c2w[2 * b + 1], (int)c2w[2 * b]) : 0.0;
                         const double qx = __dmul_rn(P.P_inv, c1v);
                         double q = rint(qx);
