@@ -219,7 +219,6 @@ std::vector<uint8_t> build_resid_consts(const Table& t) {
     std::vector<uint8_t> buf(resid_consts_bytes(t.n), 0);
     ResidHeader* h = reinterpret_cast<ResidHeader*>(buf.data());
     h->n = t.n;
-    h->row_bytes = (uint32_t)(16 * resid_pairs(t.n));
     uint32_t* tab = reinterpret_cast<uint32_t*>(buf.data() + sizeof(ResidHeader));
     for (int l = 0; l < t.n; ++l) {
         const uint32_t p = (uint32_t)t.p[l];
@@ -235,8 +234,7 @@ std::vector<uint8_t> build_resid_consts(const Table& t) {
                     if (sg) rep = -rep;                                  // -128 == 128 (mod 256)
                     w[b] = (uint32_t)rep & 0xffu;
                 }
-                // [G][sign][l]: row (G, sign) of h->row_bytes, modulus l at byte 8 l
-                uint32_t* cell = tab + ((size_t)(G * 2 + sg) * h->row_bytes + 8 * (size_t)l) / 4;
+                uint32_t* cell = tab + 2 * (((size_t)l * kResidE8 + G) * 2 + sg);  // [l][G][sign]
                 cell[0] = w[0] | (w[1] << 8) | (w[2] << 16) | (w[3] << 24);
                 cell[1] = w[4] | (w[5] << 8) | (w[6] << 16) | (w[7] << 24);
             }

@@ -122,8 +122,10 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
         int eai = 0;
         if (BND) { RAi = ex.bnd.v.RA[i]; PAi = ex.bnd.v.PA[i]; eai = ex.bnd.v.ea[i]; }
         bool fr_range = false, inv_range = false, sub = false;
+        T yv[CV];  // this thread's C entries, stored together below
 #pragma unroll
         for (int b = 0; b < CV; ++b) {
+            yv[b] = T(0);
             if (b >= jn) break;
             const int64_t j = j0 + b;
             // crt.hpp:113-119, round_nearest_even (softfp.hpp:94-102): rint,
@@ -175,14 +177,32 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
                 const float y = ldexpf_rn(x, -nuj);
                 inv_range |= !isfinite(x) || !isfinite(y);
                 sub |= (x != 0.0f && fabsf(x) < FLT_MIN) || (y != 0.0f && fabsf(y) < FLT_MIN);
-                C[i * ldc + j] = y;
+                yv[b] = y;
             } else {
                 const double x = ldexp_rn(cpp, -mui);
                 const double y = ldexp_rn(x, -nuj);
                 inv_range |= !isfinite(x) || !isfinite(y);
                 sub |= (x != 0.0 && fabs(x) < DBL_MIN) || (y != 0.0 && fabs(y) < DBL_MIN);
-                C[i * ldc + j] = y;
+                yv[b] = y;
             }
+        }
+        // C: 32-byte stores when the thread's CV entries are whole and aligned
+        // (a warp's stores then cover its 2 KB of C exactly once), else scalar
+        T* crow = C + i * ldc + j0;
+        if (jn == CV && (reinterpret_cast<uintptr_t>(crow) & 31) == 0) {
+            if constexpr (sizeof(T) == 8) {
+#pragma unroll
+                for (int b = 0; b < CV; b += 4)
+                    st_global_v4f64(reinterpret_cast<double*>(crow) + b, yv[b], yv[b + 1], yv[b + 2], yv[b + 3]);
+            } else {
+#pragma unroll
+                for (int b = 0; b < CV; b += 4)
+                    *reinterpret_cast<float4*>(crow + b) = make_float4(yv[b], yv[b + 1], yv[b + 2], yv[b + 3]);
+            }
+        } else {
+#pragma unroll
+            for (int b = 0; b < CV; ++b)
+                if (b < jn) crow[b] = yv[b];
         }
         if (fr_range | inv_range | sub) {
             DevStatus* s = ex.sg.base ? ex.sg.base + ((ex.sg.row0 + i) / ex.sg.row_div) * ex.sg.slots +

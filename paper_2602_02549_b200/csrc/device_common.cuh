@@ -191,6 +191,12 @@ __device__ __forceinline__ uint32_t mod_u32(uint32_t x, ModP mp) {
     return r;
 }
 
+// 32-byte global store (sm_100 STG.256): 4 doubles or 8 floats at a 32-byte
+// aligned address.
+__device__ __forceinline__ void st_global_v4f64(double* p, double a, double b, double c, double d) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
 // ----------------------------------------------------------------------------
 // mbarrier / TMA / tcgen05 PTX wrappers
 // ----------------------------------------------------------------------------

@@ -56,23 +56,17 @@ cudaError_t launch_gemm_i8_pair(int mode, const CUtensorMap& tmA, const CUtensor
                                 int num_sms, cudaStream_t stream);
 
 // Residue constants for the residue kernels (uploaded once per table): a
-// header followed by the weight table w[G][s][l] (G in [0, kResidE8), s =
-// sign, l = modulus) of two packed words whose signed bytes are the symmetric
-// representatives of (-1)^s 2^(8 (t + G)) mod p_l, t = 0..7 (resid.cu explains
-// the arithmetic).  The moduli of one (G, s) are adjacent, so one 16-byte
-// shared load gives the weights of two moduli; a (G, s) row holds
-// resid_pairs(n) such 16-byte cells (row_bytes).
-struct alignas(16) ResidHeader {  // size a multiple of 16: the table that follows is read as uint4
-    int n;
-    uint32_t row_bytes;
+// header followed by the weight table w[l][G][s] (G in [0, kResidE8), s = sign)
+// of two packed words whose signed bytes are the symmetric representatives of
+// (-1)^s 2^(8 (t + G)) mod p_l, t = 0..7 (resid.cu explains the arithmetic).
+struct alignas(16) ResidHeader {  // size a multiple of 16: the table that follows is read as int2/uint4
+    int n, pad;
     uint32_t p[49];
     float inv_p[49];  // RN32(1 / p)
 };
 constexpr int kResidE8 = 16;  // E' / 8 <= 15: |A'| < 2^(6 + P') and P' < 171 for N <= 49
-__host__ __device__ inline int resid_pairs(int n) { return (n + 1) / 2; }
-__host__ __device__ inline size_t resid_consts_bytes(int n) {
-    return sizeof(ResidHeader) + (size_t)kResidE8 * 2 * 16 * resid_pairs(n);
-}
+constexpr int kResidRow = kResidE8 * 2 * 8;  // bytes per modulus: [G][sign][8 bytes]
+__host__ __device__ inline size_t resid_consts_bytes(int n) { return sizeof(ResidHeader) + (size_t)kResidRow * n; }
 typedef ResidHeader ResidConsts;
 
 // Stage launchers (scale.cu).  T = float or double inputs; prec selects.

@@ -43,13 +43,13 @@ __device__ __forceinline__ double ld_d(const T* p) { return (double)__ldg(p); }
 
 struct ElemDec {
     uint32_t lo, hi;  // bytes 0-3 / 4-7 of m' << (E' mod 8)  (< 2^60)
-    uint32_t off;     // byte offset of the weight row (G, sign) = (2 (E' / 8) + (x < 0)) * row_bytes
+    uint32_t off;     // byte offset of the weights: 16 * (E' / 8) (+ 8 for x < 0)
 };
 
 // Branch-free: x = mant * 2^(max(ef, 1) - 1075) holds for normals, subnormals
 // (ef = 0, no hidden bit) and zero (mant = 0, which gives S = 0 for any table
 // row), so no case needs separate code.
-__device__ __forceinline__ ElemDec elem_dec(double x, int shift, bool& overflow, uint32_t row_bytes) {
+__device__ __forceinline__ ElemDec elem_dec(double x, int shift, bool& overflow) {
     const uint64_t bits = (uint64_t)__double_as_longlong(x);
     const int ef = (int)((bits >> 52) & 0x7ff);
     const uint64_t mant = (bits & 0x000fffffffffffffull) | ((uint64_t)(ef != 0) << 52);
@@ -63,7 +63,7 @@ __device__ __forceinline__ ElemDec elem_dec(double x, int shift, bool& overflow,
     ElemDec d;
     d.lo = (uint32_t)g;
     d.hi = (uint32_t)(g >> 32);
-    d.off = ((uint32_t)(Ec >> 3) * 2u + (uint32_t)(bits >> 63)) * row_bytes;
+    d.off = (uint32_t)(Ec >> 3) * 16u + (uint32_t)(bits >> 63) * 8u;
     return d;
 }
 
@@ -85,8 +85,9 @@ constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23 (bits 0x4B400000): ulp 1 on
 // bits(t) = 0x4B400000 + q with q = round(S / p) (the only inexact fp32 step
 // rounds to that integer), so bits - p * bits(t) = S - p q + 0x4B400000 (1 - p),
 // whose low byte is r = S - p q: 0x4B400000 is a multiple of 256.
-__device__ __forceinline__ uint32_t resid_w(const ElemDec& d, int wlo, int whi, const ModC& c) {
-    const int bits = dp4a_us(d.hi, whi, dp4a_us(d.lo, wlo, 0x4B400000));  // bits of the float M + S
+__device__ __forceinline__ uint32_t resid_w(const ElemDec& d, const uint8_t* __restrict__ row_l, const ModC& c) {
+    const int2 w = *reinterpret_cast<const int2*>(row_l + d.off);
+    const int bits = dp4a_us(d.hi, w.y, dp4a_us(d.lo, w.x, 0x4B400000));  // bits of the float M + S
     const float u = __fsub_rn(__int_as_float(bits), kMagic);              // S
     const float t = __fmaf_rn(u, c.inv_p, kMagic);                         // M + round(S / p)
     return (uint32_t)bits - (uint32_t)__float_as_int(t) * c.p;
@@ -97,22 +98,6 @@ __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2,
     const uint32_t hi = __byte_perm(b2, b3, 0x0040);
     return __byte_perm(lo, hi, 0x5410);
 }
-
-// The 8 residue bytes of 8 elements for the moduli 2q and 2q + 1: one 16-byte
-// shared load per element gives both moduli's weights (the table is [G][s][l]).
-__device__ __forceinline__ void resid_pair(const ElemDec (&d)[8], const uint8_t* __restrict__ tab, int q,
-                                           const ModC& c0, const ModC& c1, uint2& out0, uint2& out1) {
-    uint32_t r0[8], r1[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const int4 w = *reinterpret_cast<const int4*>(tab + d[j].off + 16 * q);
-        r0[j] = resid_w(d[j], w.x, w.y, c0);
-        r1[j] = resid_w(d[j], w.z, w.w, c1);
-    }
-    out0 = make_uint2(pack4(r0[0], r0[1], r0[2], r0[3]), pack4(r0[4], r0[5], r0[6], r0[7]));
-    out1 = make_uint2(pack4(r1[0], r1[1], r1[2], r1[3]), pack4(r1[4], r1[5], r1[6], r1[7]));
-}
-
 
 __device__ __forceinline__ void load_resid_consts(const ResidHeader* __restrict__ g, int n, uint8_t* sh) {
     const uint4* src = reinterpret_cast<const uint4*>(g);
@@ -139,7 +124,7 @@ constexpr int RA_E = 8;
 // A: the row-shift case of the writer below, kept as its own kernel (48
 // registers, 5 CTAs per SM; the general one needs 60).
 template <class T>
-__global__ void __launch_bounds__(256, 4) resid_A_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t k,
+__global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t k,
                                                       int64_t kp, const int32_t* __restrict__ mu,
                                                       const ResidHeader* __restrict__ rc_g, int nmod,
                                                       int8_t* __restrict__ planes, int64_t plane, DevStatus* st) {
@@ -148,7 +133,6 @@ __global__ void __launch_bounds__(256, 4) resid_A_kernel(const T* __restrict__ A
     __syncthreads();
     const ResidHeader& hd = *reinterpret_cast<const ResidHeader*>(sh);
     const uint8_t* tab = sh + sizeof(ResidHeader);
-    const uint32_t rb = hd.row_bytes;
     const int64_t h0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * RA_E;
     bool ovf = false;
     if (h0 >= kp) return;
@@ -160,36 +144,39 @@ __global__ void __launch_bounds__(256, 4) resid_A_kernel(const T* __restrict__ A
 #pragma unroll
             for (int j = 0; j < RA_E; j += 2) {
                 const double2 v = __ldg(reinterpret_cast<const double2*>(row + j));
-                d[j] = elem_dec(v.x, sft, ovf, rb);
-                d[j + 1] = elem_dec(v.y, sft, ovf, rb);
+                d[j] = elem_dec(v.x, sft, ovf);
+                d[j + 1] = elem_dec(v.y, sft, ovf);
             }
         } else if (sizeof(T) == 4 && h0 + RA_E <= k && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
 #pragma unroll
             for (int j = 0; j < RA_E; j += 4) {
                 const float4 v = __ldg(reinterpret_cast<const float4*>(row + j));
-                d[j] = elem_dec((double)v.x, sft, ovf, rb);
-                d[j + 1] = elem_dec((double)v.y, sft, ovf, rb);
-                d[j + 2] = elem_dec((double)v.z, sft, ovf, rb);
-                d[j + 3] = elem_dec((double)v.w, sft, ovf, rb);
+                d[j] = elem_dec((double)v.x, sft, ovf);
+                d[j + 1] = elem_dec((double)v.y, sft, ovf);
+                d[j + 2] = elem_dec((double)v.z, sft, ovf);
+                d[j + 3] = elem_dec((double)v.w, sft, ovf);
             }
         } else {
 #pragma unroll
-            for (int j = 0; j < RA_E; ++j) d[j] = elem_dec(h0 + j < k ? ld_d(row + j) : 0.0, sft, ovf, rb);
+            for (int j = 0; j < RA_E; ++j) d[j] = elem_dec(h0 + j < k ? ld_d(row + j) : 0.0, sft, ovf);
         }
         int8_t* out = planes + i * kp + h0;
-#pragma unroll 1
-        for (int l = 0; l < nmod; l += 2) {  // moduli in pairs: one 16-byte weight load per element
-            uint2 o0, o1;
-            resid_pair(d, tab, l >> 1, modc(hd, l), modc(hd, l + 1 < nmod ? l + 1 : l), o0, o1);
-            *reinterpret_cast<uint2*>(out + (int64_t)l * plane) = o0;
-            if (l + 1 < nmod) *reinterpret_cast<uint2*>(out + (int64_t)(l + 1) * plane) = o1;
+#pragma unroll 2
+        for (int l = 0; l < nmod; ++l) {
+            const ModC c = modc(hd, l);
+            const uint8_t* rl = tab + (size_t)l * kResidRow;
+            const uint32_t w0 = pack4(resid_w(d[0], rl, c), resid_w(d[1], rl, c), resid_w(d[2], rl, c),
+                                      resid_w(d[3], rl, c));
+            const uint32_t w1 = pack4(resid_w(d[4], rl, c), resid_w(d[5], rl, c), resid_w(d[6], rl, c),
+                                      resid_w(d[7], rl, c));
+            *reinterpret_cast<uint2*>(out + (int64_t)l * plane) = make_uint2(w0, w1);
         }
     }
     if (ovf) flag(st, ERR_TRUNC_A_RANGE);
 }
 
 template <class T, bool COLSHIFT, int OP>
-__global__ void __launch_bounds__(256, 4) resid_rows_kernel(const T* __restrict__ X, int64_t ldx, int64_t rows_valid,
+__global__ void __launch_bounds__(256) resid_rows_kernel(const T* __restrict__ X, int64_t ldx, int64_t rows_valid,
                                                          int64_t rows_total, int64_t cols_valid, int64_t cols_out,
                                                          int64_t ld_out, const int32_t* __restrict__ shift,
                                                          const ResidHeader* __restrict__ rc_g, int nmod,
@@ -202,7 +189,6 @@ __global__ void __launch_bounds__(256, 4) resid_rows_kernel(const T* __restrict_
     }
     const ResidHeader& hd = *reinterpret_cast<const ResidHeader*>(sh);
     const uint8_t* tab = sh + sizeof(ResidHeader);
-    const uint32_t rb = hd.row_bytes;
     const int64_t h0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * RA_E;
     if (h0 >= cols_out) return;
     bool bad = false;
@@ -267,29 +253,32 @@ __global__ void __launch_bounds__(256, 4) resid_rows_kernel(const T* __restrict_
 #pragma unroll
             for (int j = 0; j < RA_E; j += 2) {
                 const double2 t = __ldg(reinterpret_cast<const double2*>(row + j));
-                d[j] = elem_dec(t.x, COLSHIFT ? csft[j] : rsft, bad, rb);
-                d[j + 1] = elem_dec(t.y, COLSHIFT ? csft[j + 1] : rsft, bad, rb);
+                d[j] = elem_dec(t.x, COLSHIFT ? csft[j] : rsft, bad);
+                d[j + 1] = elem_dec(t.y, COLSHIFT ? csft[j + 1] : rsft, bad);
             }
         } else if (vec && sizeof(T) == 4) {
 #pragma unroll
             for (int j = 0; j < RA_E; j += 4) {
                 const float4 t = __ldg(reinterpret_cast<const float4*>(row + j));
-                d[j] = elem_dec((double)t.x, COLSHIFT ? csft[j] : rsft, bad, rb);
-                d[j + 1] = elem_dec((double)t.y, COLSHIFT ? csft[j + 1] : rsft, bad, rb);
-                d[j + 2] = elem_dec((double)t.z, COLSHIFT ? csft[j + 2] : rsft, bad, rb);
-                d[j + 3] = elem_dec((double)t.w, COLSHIFT ? csft[j + 3] : rsft, bad, rb);
+                d[j] = elem_dec((double)t.x, COLSHIFT ? csft[j] : rsft, bad);
+                d[j + 1] = elem_dec((double)t.y, COLSHIFT ? csft[j + 1] : rsft, bad);
+                d[j + 2] = elem_dec((double)t.z, COLSHIFT ? csft[j + 2] : rsft, bad);
+                d[j + 3] = elem_dec((double)t.w, COLSHIFT ? csft[j + 3] : rsft, bad);
             }
         } else {
 #pragma unroll
             for (int j = 0; j < RA_E; ++j)
-                d[j] = elem_dec(h0 + j < cols_valid ? (double)__ldg(row + j) : 0.0, COLSHIFT ? csft[j] : rsft, bad, rb);
+                d[j] = elem_dec(h0 + j < cols_valid ? (double)__ldg(row + j) : 0.0, COLSHIFT ? csft[j] : rsft, bad);
         }
-#pragma unroll 1
-        for (int l = 0; l < nmod; l += 2) {  // moduli in pairs: one 16-byte weight load per element
-            uint2 o0, o1;
-            resid_pair(d, tab, l >> 1, modc(hd, l), modc(hd, l + 1 < nmod ? l + 1 : l), o0, o1);
-            *reinterpret_cast<uint2*>(out + (int64_t)l * plane) = o0;
-            if (l + 1 < nmod) *reinterpret_cast<uint2*>(out + (int64_t)(l + 1) * plane) = o1;
+#pragma unroll 2
+        for (int l = 0; l < nmod; ++l) {
+            const ModC c = modc(hd, l);
+            const uint8_t* rl = tab + (size_t)l * kResidRow;
+            const uint32_t w0 = pack4(resid_w(d[0], rl, c), resid_w(d[1], rl, c), resid_w(d[2], rl, c),
+                                      resid_w(d[3], rl, c));
+            const uint32_t w1 = pack4(resid_w(d[4], rl, c), resid_w(d[5], rl, c), resid_w(d[6], rl, c),
+                                      resid_w(d[7], rl, c));
+            *reinterpret_cast<uint2*>(out + (int64_t)l * plane) = make_uint2(w0, w1);
         }
     }
     if (bad) flag(st, err_bit);
