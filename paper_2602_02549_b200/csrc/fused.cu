@@ -88,12 +88,20 @@ __device__ __forceinline__ void decode_tile(int u, int tiles_m, int tiles_n, int
     tn = r / gm;
 }
 
-// W = signed_mod(C', p) (softfp.hpp:117-125 with the p/2 tie to -p/2), as the
-// two-pass epilogue computes it (gemm_tc.cu EPI_RESID).
-__device__ __forceinline__ int residue_w(uint32_t v, uint32_t p, uint32_t magic, uint32_t off) {
-    if (p == 256u) return (int)(int8_t)(v & 0xffu);
-    const uint32_t r = mod_u32(v + off, ModP{p, magic});
-    return (2u * r > p) ? (int)r - (int)p : (int)r;
+// W = signed_mod(C', p) (softfp.hpp:117-125 with the p/2 tie to -p/2),
+// branch-free for every modulus: r = (C' + off) mod p with off a multiple of
+// p >= 2^31; the representative is r - p when 2r >= p (for odd p the same as
+// 2r > p; for p = 256, magic = 2^24 makes q exact and maps 128 to -128 as the
+// two-pass epilogue's byte cast does).  Returned as the exact double
+// W = (2^52 + 128 + W) - (2^52 + 128), built on the fp64 pipe (the I2F
+// conversion would run on the XU pipe, the epilogue's bottleneck).
+__device__ __forceinline__ double residue_wd(uint32_t v, uint32_t p, uint32_t magic, uint32_t off) {
+    const uint32_t x = v + off;
+    const uint32_t q = __umulhi(x, magic);
+    uint32_t r = x - q * p;
+    r = r >= p ? r - p : r;
+    const uint32_t biased = (2u * r >= p ? r - p : r) + 128u;  // W + 128 in [0, 255]
+    return __dsub_rn(__hiloint2double(0x43300000, (int)biased), 4503599627370624.0);
 }
 
 template <class T, bool DD>
@@ -217,7 +225,7 @@ __global__ void __launch_bounds__(F_THREADS, 1)
                     tmem_ld_wait();
 #pragma unroll
                     for (int b = 0; b < 8; ++b) {
-                        const double wv = (double)residue_w(v[b], p, magic, off);
+                        const double wv = residue_wd(v[b], p, magic, off);
                         const int jj = ch * 8 + b;
                         if (jj < F_COLS_REG) {
                             c1[jj] = __fma_rn(s1, wv, c1[jj]);                          // crt.hpp:99-104
