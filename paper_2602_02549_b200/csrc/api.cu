@@ -17,6 +17,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <condition_variable>
 #include <cstring>
 #include <map>
@@ -53,12 +54,21 @@ struct Fail {
             throw Fail{OZ2G_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(e_)};    \
     } while (0)
 
+// Bumped whenever any workspace buffer is (re)allocated: a captured CUDA
+// graph (run_gemm_graph) embeds buffer addresses and is valid only while this
+// is unchanged.
+std::atomic<uint64_t> g_alloc_gen{0};
+
+// run_gemm enqueues only (no final status read-back) while a graph is captured.
+thread_local bool g_capture = false;
+
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
     void* get(size_t bytes) {
         if (bytes == 0) bytes = 16;
         if (bytes > cap) {
+            ++g_alloc_gen;
             if (p) cudaFree(p);
             p = nullptr;
             cap = 0;
@@ -108,6 +118,21 @@ struct Workspace {
         return spec_changed;
     }
     std::map<std::pair<int, int>, ResidConsts*> rc;  // device copies of residue constants
+    // CUDA graphs of device-pointer calls (run_gemm_graph), keyed by the call's
+    // shape, pointers, N, stream and path; valid for one allocation generation
+    struct GraphEntry {
+        cudaGraphExec_t exec = nullptr;
+        uint64_t gen = 0;
+        int launches = 0;
+        int seen = 0;
+    };
+    std::map<std::vector<int64_t>, GraphEntry> graphs;
+    DevStatus* status_host = nullptr;  // pinned copy of the status word read after a replay
+    void drop_graphs() {
+        for (auto& kv : graphs)
+            if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        graphs.clear();
+    }
     int num_sms = 0;
     std::recursive_mutex mtx;           // calls on one workspace are serialised (re-entered by the
                                         // speculation fallback of run_gemm)
@@ -162,6 +187,9 @@ struct Workspace {
         spec_changed_cap = 0;
         for (auto& kv : rc) cudaFree(kv.second);
         rc.clear();
+        drop_graphs();
+        if (status_host) cudaFreeHost(status_host);
+        status_host = nullptr;
         lo_ready = false;
     }
 };
@@ -1321,6 +1349,10 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         return OZ2G_OK;
     }
 
+    if (g_capture) {  // run_gemm_graph reads the status after the replay
+        if (diag) diag->kernels_launched = launches;
+        return OZ2G_OK;
+    }
     unsigned long long bmax_host[3] = {0, 0, 0};
     if (bo && bmax_dev) {
         CUDA_TRY(cudaMemcpyAsync(bmax_host, bmax_dev, 24, cudaMemcpyDeviceToHost, stream));
@@ -1389,6 +1421,78 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
 
     Fail f{OZ2G_OK, ""};
     if (status_failure(hs, row_base, col_base, f)) throw f;
+    return OZ2G_OK;
+}
+
+// Device-pointer calls repeated with the same shape, pointers, N and stream
+// replay a CUDA graph of the whole pipeline (memsets, every kernel) instead of
+// re-enqueuing ~20 launches: the first call runs normally (and allocates), the
+// second captures, later ones replay; a workspace reallocation anywhere
+// (g_alloc_gen) invalidates the graphs.  The status word is read after the
+// replay from pinned memory, so errors are reported exactly as run_gemm does.
+// OZ2G_GRAPH=0 disables.
+bool graph_enabled() {
+    const char* e = std::getenv("OZ2G_GRAPH");
+    return !(e && e[0] == '0');
+}
+
+int run_gemm_graph(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
+                   void* C, int64_t ldc, int nmod, unsigned flags, cudaStream_t stream, oz2g_diag* diag) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    Workspace& ws = workspace(dev, 0);
+    std::lock_guard<std::recursive_mutex> dev_lock(ws.mtx);
+    if (!ws.pending.empty()) {
+        Fail f{OZ2G_OK, ""};
+        if (complete_pending(ws, f)) throw f;
+    }
+    const std::vector<int64_t> key{prec, m, n, k, (int64_t)(uintptr_t)A, lda, (int64_t)(uintptr_t)B, ldb,
+                                   (int64_t)(uintptr_t)C, ldc, nmod, (int64_t)(uintptr_t)stream, fused_mode(),
+                                   (int64_t)flags};
+    Workspace::GraphEntry& e = ws.graphs[key];
+    const uint64_t gen = g_alloc_gen.load();
+    if (!e.exec || e.gen != gen) {
+        if (e.exec) { cudaGraphExecDestroy(e.exec); e.exec = nullptr; }
+        if (e.seen++ == 0 || ws.graphs.size() > 64) {  // first sight: a plain call (allocates, uploads tables)
+            if (ws.graphs.size() > 64) ws.drop_graphs();
+            return run_gemm(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, stream, nullptr, diag, nullptr,
+                            nullptr);
+        }
+        oz2g_diag d;
+        std::memset(&d, 0, sizeof d);
+        cudaGraph_t g = nullptr;
+        CUDA_TRY(cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed));
+        g_capture = true;
+        try {
+            run_gemm(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, stream, nullptr, &d, nullptr, nullptr);
+        } catch (...) {
+            g_capture = false;
+            cudaStreamEndCapture(stream, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        g_capture = false;
+        CUDA_TRY(cudaStreamEndCapture(stream, &g));
+        const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
+        cudaGraphDestroy(g);
+        if (ie != cudaSuccess) {
+            e.exec = nullptr;
+            throw Fail{OZ2G_CUDA_ERROR, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie)};
+        }
+        e.gen = g_alloc_gen.load();
+        e.launches = d.kernels_launched;
+    }
+    if (!ws.status_host) CUDA_TRY(cudaHostAlloc((void**)&ws.status_host, sizeof(DevStatus), cudaHostAllocDefault));
+    if (diag) std::memset(diag, 0, sizeof *diag);
+    CUDA_TRY(cudaGraphLaunch(e.exec, stream));
+    CUDA_TRY(cudaMemcpyAsync(ws.status_host, ws.status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    if (diag) {
+        diag->kernels_launched = e.launches;
+        diag->subnormal = ws.status_host->subnormal != 0;
+    }
+    Fail f{OZ2G_OK, ""};
+    if (status_failure(*ws.status_host, 0, 0, f)) throw f;
     return OZ2G_OK;
 }
 
@@ -1837,6 +1941,8 @@ int oz2g_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t 
               void* C, int64_t ldc, int nmod, unsigned flags, void* stream, oz2g_intermediates* inter,
               oz2g_diag* diag, oz2g_reduce_maxima_fn reduce_fn, void* reduce_user) {
     return guarded([&] {
+        if (flags == OZ2G_DEVICE_PTRS && !inter && !reduce_fn && graph_enabled() && m > 0 && n > 0 && k > 0)
+            return run_gemm_graph(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, (cudaStream_t)stream, diag);
         return run_gemm(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, (cudaStream_t)stream, inter, diag,
                         reduce_fn, reduce_user);
     });

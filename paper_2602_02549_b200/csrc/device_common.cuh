@@ -108,10 +108,14 @@ __device__ __forceinline__ float pow2f(int s) { return __int_as_float((s + 127) 
 
 // RN(x * 2^s) with a single rounding: glibc ldexp/scalbn semantics used by
 // inverse_scale (emulate.hpp:37-38).
+static __device__ __noinline__ double ldexp_rn_slow(double x, int s);
 __device__ __forceinline__ double ldexp_rn(double x, int s) {
     // 2^s normal: one multiplication is one RN rounding of the exact x*2^s
     // (exact unless the result is subnormal, inf on overflow) == scalbn.
     if (s >= -1022 && s <= 1023) return __dmul_rn(x, pow2d(s));
+    return ldexp_rn_slow(x, s);  // out of line: keeps unrolled epilogues small
+}
+static __device__ __noinline__ double ldexp_rn_slow(double x, int s) {
     if (x == 0.0 || !isfinite(x)) return x;
     const int ex = ilogb_exact(x);
     const int et = ex + s;
@@ -155,8 +159,12 @@ __device__ __forceinline__ int ilogbf_exact(float x) {
 }
 
 // RN(x * 2^s) for float (std::ldexp(float, int) == scalbnf).
+static __device__ __noinline__ float ldexpf_rn_slow(float x, int s);
 __device__ __forceinline__ float ldexpf_rn(float x, int s) {
     if (s >= -126 && s <= 127) return __fmul_rn(x, pow2f(s));
+    return ldexpf_rn_slow(x, s);
+}
+static __device__ __noinline__ float ldexpf_rn_slow(float x, int s) {
     if (x == 0.0f || !isfinite(x)) return x;
     const int ex = ilogbf_exact(x);
     const int et = ex + s;
