@@ -128,6 +128,7 @@ struct Workspace {
     };
     std::map<std::vector<int64_t>, GraphEntry> graphs;
     DevStatus* status_host = nullptr;  // pinned copy of the status word read after a replay
+    cudaStream_t s_cap = nullptr;      // graphs are captured on this stream (the legacy stream cannot be)
     void drop_graphs() {
         for (auto& kv : graphs)
             if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -1461,18 +1462,19 @@ int run_gemm_graph(int prec, int64_t m, int64_t n, int64_t k, const void* A, int
         oz2g_diag d;
         std::memset(&d, 0, sizeof d);
         cudaGraph_t g = nullptr;
-        CUDA_TRY(cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed));
+        if (!ws.s_cap) CUDA_TRY(cudaStreamCreateWithFlags(&ws.s_cap, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamBeginCapture(ws.s_cap, cudaStreamCaptureModeRelaxed));
         g_capture = true;
         try {
-            run_gemm(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, stream, nullptr, &d, nullptr, nullptr);
+            run_gemm(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, ws.s_cap, nullptr, &d, nullptr, nullptr);
         } catch (...) {
             g_capture = false;
-            cudaStreamEndCapture(stream, &g);
+            cudaStreamEndCapture(ws.s_cap, &g);
             if (g) cudaGraphDestroy(g);
             throw;
         }
         g_capture = false;
-        CUDA_TRY(cudaStreamEndCapture(stream, &g));
+        CUDA_TRY(cudaStreamEndCapture(ws.s_cap, &g));
         const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
         cudaGraphDestroy(g);
         if (ie != cudaSuccess) {

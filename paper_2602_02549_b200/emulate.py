@@ -77,6 +77,18 @@ class ModuliTable:
 
 
 def table_for(n: int, mode: int = F64) -> ModuliTable:
+    """moduli.hpp:145-153: built once per (n, mode) and cached (immutable)."""
+    key = (int(n), int(mode))
+    t = _TABLES.get(key)
+    if t is None:
+        t = _TABLES[key] = _table_for(*key)
+    return t
+
+
+_TABLES: dict = {}
+
+
+def _table_for(n: int, mode: int) -> ModuliTable:
     t = _lib.TableC()
     _check(_lib.load().oz2g_table_for(int(n), int(mode), C.byref(t)))
     k = t.n
