@@ -1246,7 +1246,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         }
         // every read of the device copies of A and B is enqueued by now
         if (host && ws.ev_inputs_free) CUDA_TRY(cudaEventRecord(ws.ev_inputs_free, stream));
-        const bool fused = fused_mode() == 1 && !inter && !bo && !overlap && m * n > 0;
+        const bool fused = fused_mode() >= 1 && !inter && !bo && !overlap && m * n > 0;
         if (fused) {
             // the N residue GEMMs with the CRT and the inverse scaling in their epilogue:
             // one launch over every 128 x 128 tile of C, no W
@@ -1262,6 +1262,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             for (int l = 0; l < N; ++l) { fp.s1[l] = tab.s1[l]; fp.s2[l] = tab.s2[l]; }
             fp.P1 = tab.P1; fp.P2 = tab.P2; fp.P_inv = tab.P_inv;
             fp.mode = tab.mode;
+            fp.probe = fused_mode() == 2 ? 1 : 0;
             fp.mu = mu;
             fp.nu = nu;
             fp.C = dC;

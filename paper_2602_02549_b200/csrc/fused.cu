@@ -210,6 +210,12 @@ __global__ void __launch_bounds__(F_THREADS, 1)
                 const int acc = it & 1;
                 mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
                 tc_fence_after();
+                if (P.probe == 1) {  // experiment: MMA + operand feed alone (no CRT; C not written)
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
+                    continue;
+                }
                 const uint32_t p = G.p[l], magic = G.magic[l], off = G.off[l];
                 const double s1 = P.s1[l], s2 = P.s2[l];
                 const bool last = l == N - 1;

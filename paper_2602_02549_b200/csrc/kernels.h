@@ -135,6 +135,7 @@ struct FusedParams {
     double s1[49], s2[49];
     double P1, P2, P_inv;
     int mode;                    // 1: fp64 table (C2 chain), 0: fp32 table
+    int probe;                   // experiments (OZ2G_FUSED=2: skip the CRT epilogue); 0 normally
     const int32_t* mu;           // [m]
     const int32_t* nu;           // [n]
     void* C;                     // T [m][ldc]
