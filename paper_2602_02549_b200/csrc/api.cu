@@ -231,11 +231,11 @@ CUtensorMap make_plane_map(const void* base, int64_t kp, int64_t rows, int64_t p
 // columns, 128 rows, 1}, 128-B swizzle; `pitch` = bytes between rows (16-byte
 // multiple), columns past `cols` read as zeros.
 CUtensorMap make_plane_map_mn(const void* base, int64_t cols, int64_t pitch, int64_t rows, int64_t planes,
-                              int64_t plane_stride) {
+                              int64_t plane_stride, int box_rows = 128) {
     CUtensorMap tm;
     cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)planes};
     cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)plane_stride};
-    cuuint32_t box[3] = {128u, 128u, 1u};
+    cuuint32_t box[3] = {128u, (cuuint32_t)box_rows, 1u};
     cuuint32_t estr[3] = {1u, 1u, 1u};
     CUresult r = get_encode()(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box,
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1263,13 +1263,27 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             fp.P1 = tab.P1; fp.P2 = tab.P2; fp.P_inv = tab.P_inv;
             fp.mode = tab.mode;
             fp.probe = fused_mode() == 2 ? 1 : 0;
+            static const bool no_fence = [] {
+                const char* e = std::getenv("OZ2G_FUSED_FENCE");
+                return e && e[0] == '0';
+            }();
+            if (!no_fence) {
+                fp.plane_sync = (unsigned long long*)ws.x_bmax.get(64) + 4;
+                CUDA_TRY(cudaMemsetAsync(fp.plane_sync, 0, 8, stream));
+            }
             fp.mu = mu;
             fp.nu = nu;
             fp.C = dC;
             fp.ldc = ldc_d;
             fp.st = st;
+            // OZ2G_FUSED_MC=0: one CTA per tile without the B multicast
+            static const bool mc = [] {
+                const char* e = std::getenv("OZ2G_FUSED_MC");
+                return !(e && e[0] == '0');
+            }();
             const CUtensorMap tA = make_plane_map(ares, kp, m, N, fused_tile_m(), m * kp);
-            tm.span(5, stream, [&] { CUDA_TRY(launch_gemm_crt_fused(prec, tA, tBres, fp, ws.num_sms, stream)); });
+            const CUtensorMap tB = make_plane_map_mn(bres, n, ldn, kp, N, kp * ldn, fused_b_box_rows(mc));
+            tm.span(5, stream, [&] { CUDA_TRY(launch_gemm_crt_fused(prec, tA, tB, fp, ws.num_sms, mc, stream)); });
             ++launches;
         } else {
             for (size_t bi = 0; bi < nb; ++bi) run_block(bi, 0, n, st);

@@ -75,6 +75,11 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
         "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
         : "memory");
 }
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // Grouped raster over the C tiles (B tiles reused across group_m tile-rows).
@@ -104,7 +109,11 @@ __device__ __forceinline__ double residue_wd(uint32_t v, uint32_t p, uint32_t ma
     return __dsub_rn(__hiloint2double(0x43300000, (int)biased), 4503599627370624.0);
 }
 
-template <class T, bool DD>
+// MC: CTAs run in clusters of 2 on vertically adjacent tiles that share the
+// B tile; each CTA loads half of the B stage's K-rows with .multicast::cluster
+// into both CTAs (B crosses L2 -> SM once per pair), and a stage is refilled
+// only when both CTAs' MMAs have read it (commits multicast to both).
+template <class T, bool DD, bool MC>
 __global__ void __launch_bounds__(F_THREADS, 1)
     gemm_crt_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ FusedParams P) {
@@ -124,47 +133,85 @@ __global__ void __launch_bounds__(F_THREADS, 1)
     const int lane = threadIdx.x & 31;
     const GemmParams& G = P.g;
 
+    const uint32_t rank = MC ? cluster_ctarank() : 0u;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < FSTAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < FSTAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], MC ? 2 : 1); }
         for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], F_EPI_WARPS); }
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
     if (warp == 1) { tmem_alloc(tmem_slot, 512); tmem_relinquish(); }
     tc_fence_before();
-    __syncthreads();
+    if (MC) cluster_sync_all();  // the peer's barriers exist before any multicast reaches them
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int total = G.tiles_m * G.tiles_n;
+    // work units: tiles (or vertically adjacent tile pairs for MC) in raster order
+    const int units_m = MC ? (G.tiles_m + 1) >> 1 : G.tiles_m;
+    const int ugroup = MC ? max(1, G.group_m >> 1) : G.group_m;
+    const int total = units_m * G.tiles_n;
+    const int first = MC ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int stride = MC ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     const int N = G.planes;
 
     if (warp == 0) {
         // ===== TMA producer: for each tile, planes in order, all of K =====
+        // Plane fence: before the loads of its g-th plane step a CTA waits until
+        // every CTA has issued all loads of its first g steps, so the CTAs of a
+        // wave stay within one plane of each other and the wave's operand blocks
+        // (~50 MB per plane at k = 16384) stay in L2 — unsynchronised, the CTAs
+        // drift over several planes and re-read the planes from HBM (381 GB per
+        // 16384^3 call, measured).  Bounded wait: a CTA that is not resident
+        // (another kernel holds its SM) only costs the time-out, not a hang.
         int stage = 0;
         uint32_t phase = 0;
-        for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        uint32_t g = 0;
+        const uint32_t steps_total = (uint32_t)((total + stride - 1) / stride) * (uint32_t)N;
+        for (int u = first; u < total; u += stride) {
             int tm, tn;
-            decode_tile(u, G.tiles_m, G.tiles_n, G.group_m, tm, tn);
-            for (int l = 0; l < N; ++l) {
+            decode_tile(u, units_m, G.tiles_n, ugroup, tm, tn);
+            if (MC) tm = 2 * tm + (int)rank;  // rows past m are TMA zero fill
+            for (int l = 0; l < N; ++l, ++g) {
+                if (P.plane_sync && lane == 0) {
+                    const unsigned long long need = (unsigned long long)g * gridDim.x;
+                    const long long t0 = clock64();
+                    while (ld_acquire_u64(P.plane_sync) < need && clock64() - t0 < (1ll << 26)) __nanosleep(64);
+                }
+                __syncwarp();
                 for (int kb = 0; kb < G.kblocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1u);
                     if (lane == 0) {
                         mbar_arrive_expect_tx(&full[stage], FA_BYTES + FB_BYTES);
                         tma_load_3d(sA + stage * FA_BYTES, &tmA, &full[stage], kb * FBK, tm * FBM, l, G.hintA);
-                        tma_load_3d(sB + stage * FB_BYTES, &tmB, &full[stage], tn * FBN, kb * FBK, l, G.hintB);
+                        if (MC)  // this CTA's half of the K-rows, into both CTAs of the pair
+                            tma_load_3d_mc(sB + stage * FB_BYTES + (int)rank * (FB_BYTES / 2), &tmB, &full[stage],
+                                           tn * FBN, kb * FBK + (int)rank * (FBK / 2), l, (uint16_t)0x3, G.hintB);
+                        else
+                            tma_load_3d(sB + stage * FB_BYTES, &tmB, &full[stage], tn * FBN, kb * FBK, l, G.hintB);
                     }
                     __syncwarp();
                     if (++stage == FSTAGES) { stage = 0; phase ^= 1u; }
                 }
+                if (P.plane_sync && lane == 0) atomicAdd(P.plane_sync, 1ull);
+            }
+        }
+        // CTAs with fewer tiles release the steps they do not have
+        if (P.plane_sync && lane == 0 && g < steps_total) atomicAdd(P.plane_sync, (unsigned long long)(steps_total - g));
+        if (MC) {  // every stage released by both CTAs before the pair may exit (the peer's commits target us)
+            for (int s2 = 0; s2 < FSTAGES; ++s2) {
+                mbar_wait(&empty[stage], phase ^ 1u);
+                if (++stage == FSTAGES) { stage = 0; phase ^= 1u; }
             }
         }
     } else if (warp == 1) {
         // ===== MMA issuer: plane l of a tile into accumulator (running plane count) & 1 =====
+        const uint64_t adesc0 = umma_desc_sw128(smem_u32(sA));
+        const uint64_t bdesc0 = umma_desc_sw128_mn(smem_u32(sB), FB_BYTES);
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
-        for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        for (int u = first; u < total; u += stride) {
             for (int l = 0; l < N; ++l, ++it) {
                 const int acc = it & 1;
                 mbar_wait(&tempty[acc], (uint32_t)((it >> 1) & 1) ^ 1u);
@@ -174,13 +221,16 @@ __global__ void __launch_bounds__(F_THREADS, 1)
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     if (lane == 0) {
-                        const uint32_t a0 = smem_u32(sA + stage * FA_BYTES);
-                        const uint32_t b0 = smem_u32(sB + stage * FB_BYTES);
+                        // descriptors = the stage-0 descriptor + the byte offset / 16 in the
+                        // 14-bit address field (shared addresses < 2^18: no carry out)
+                        const uint64_t ad = adesc0 + (uint64_t)((stage * FA_BYTES) >> 4);
+                        const uint64_t bd = bdesc0 + (uint64_t)((stage * FB_BYTES) >> 4);
 #pragma unroll
                         for (int k = 0; k < FBK / 32; ++k)
-                            mma_i8(dtmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128_mn(b0 + k * 32 * 128, FB_BYTES),
-                                   FIDESC, (kb | k) != 0 ? 1u : 0u);
-                        mma_commit(&empty[stage]);
+                            mma_i8(dtmem, ad + (uint64_t)(k * 32 >> 4), bd + (uint64_t)(k * 32 * 128 >> 4), FIDESC,
+                                   (kb | k) != 0 ? 1u : 0u);
+                        if (MC) mma_commit_mc(&empty[stage], (uint16_t)0x3);
+                        else mma_commit(&empty[stage]);
                     }
                     __syncwarp();
                     if (++stage == FSTAGES) { stage = 0; phase ^= 1u; }
@@ -196,9 +246,10 @@ __global__ void __launch_bounds__(F_THREADS, 1)
         const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16);
         int it = 0;
         uint32_t err_bits = 0, sub = 0;
-        for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        for (int u = first; u < total; u += stride) {
             int tm, tn;
-            decode_tile(u, G.tiles_m, G.tiles_n, G.group_m, tm, tn);
+            decode_tile(u, units_m, G.tiles_n, ugroup, tm, tn);
+            if (MC) tm = 2 * tm + (int)rank;
             const int64_t row = (int64_t)tm * FBM + quad * 32 + lane;
             const int64_t col0 = (int64_t)tn * FBN + cgrp * F_COLS;
             double c1[F_COLS_REG];                           // columns 0 .. 31 of the thread's 64
@@ -292,27 +343,46 @@ __global__ void __launch_bounds__(F_THREADS, 1)
         if (sub) atomicOr(&P.st->subnormal, 1u);
     }
 
-    __syncthreads();
+    tc_fence_before();
+    if (MC) cluster_sync_all();
+    else __syncthreads();
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem_base, 512);
     }
 }
 
-template <class T, bool DD>
+template <class T, bool DD, bool MC>
 cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const FusedParams& P, int grid,
                      cudaStream_t stream) {
     static int configured[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !configured[dev]) {
-        const cudaError_t err = cudaFuncSetAttribute(gemm_crt_fused_kernel<T, DD>,
+        const cudaError_t err = cudaFuncSetAttribute(gemm_crt_fused_kernel<T, DD, MC>,
                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM);
         if (err != cudaSuccess) return err;
         configured[dev] = 1;
     }
-    gemm_crt_fused_kernel<T, DD><<<grid, F_THREADS, F_SMEM, stream>>>(tmA, tmB, P);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(F_THREADS);
+    cfg.dynamicSmemBytes = F_SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = MC ? 2 : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, gemm_crt_fused_kernel<T, DD, MC>, tmA, tmB, P);
+}
+
+template <class T, bool DD>
+cudaError_t launch_mc(bool mc, const CUtensorMap& tmA, const CUtensorMap& tmB, const FusedParams& P, int grid,
+                      cudaStream_t stream) {
+    return mc ? launch_t<T, DD, true>(tmA, tmB, P, grid, stream) : launch_t<T, DD, false>(tmA, tmB, P, grid, stream);
 }
 
 }  // namespace
@@ -320,14 +390,19 @@ cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const Fused
 int fused_tile_m() { return FBM; }
 int fused_tile_n() { return FBN; }
 
+int fused_b_box_rows(bool mc) { return mc ? FBK / 2 : FBK; }
+
 cudaError_t launch_gemm_crt_fused(int prec, const CUtensorMap& tmA, const CUtensorMap& tmB, const FusedParams& P,
-                                  int num_sms, cudaStream_t stream) {
-    const int total = P.g.tiles_m * P.g.tiles_n;
-    if (total == 0) return cudaSuccess;
-    const int grid = total < num_sms ? total : num_sms;
+                                  int num_sms, bool mc, cudaStream_t stream) {
+    const int units = (mc ? (P.g.tiles_m + 1) / 2 : P.g.tiles_m) * P.g.tiles_n;
+    if (units == 0) return cudaSuccess;
+    const int per = mc ? 2 : 1;
+    const int slots = num_sms / per;
+    const int grid = (units < slots ? units : slots) * per;
     const bool dd = P.mode != 0;
-    if (prec) return dd ? launch_t<double, true>(tmA, tmB, P, grid, stream) : launch_t<double, false>(tmA, tmB, P, grid, stream);
-    return dd ? launch_t<float, true>(tmA, tmB, P, grid, stream) : launch_t<float, false>(tmA, tmB, P, grid, stream);
+    if (prec) return dd ? launch_mc<double, true>(mc, tmA, tmB, P, grid, stream)
+                        : launch_mc<double, false>(mc, tmA, tmB, P, grid, stream);
+    return dd ? launch_mc<float, true>(mc, tmA, tmB, P, grid, stream) : launch_mc<float, false>(mc, tmA, tmB, P, grid, stream);
 }
 
 }  // namespace oz2g

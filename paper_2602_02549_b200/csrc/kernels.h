@@ -136,6 +136,7 @@ struct FusedParams {
     double P1, P2, P_inv;
     int mode;                    // 1: fp64 table (C2 chain), 0: fp32 table
     int probe;                   // experiments (OZ2G_FUSED=2: skip the CRT epilogue); 0 normally
+    unsigned long long* plane_sync;  // zeroed counter of the plane fence (fused.cu), or nullptr
     const int32_t* mu;           // [m]
     const int32_t* nu;           // [n]
     void* C;                     // T [m][ldc]
@@ -144,8 +145,9 @@ struct FusedParams {
 };
 int fused_tile_m();
 int fused_tile_n();
+int fused_b_box_rows(bool mc);  // K-rows of the B TMA box (half a stage with multicast)
 cudaError_t launch_gemm_crt_fused(int prec, const CUtensorMap& tmA, const CUtensorMap& tmB, const FusedParams& P,
-                                  int num_sms, cudaStream_t stream);
+                                  int num_sms, bool mc, cudaStream_t stream);
 
 // CRT + inverse scaling (crt.cu).
 struct CrtConsts {
