@@ -1,15 +1,24 @@
-# round artifacts: GPU tests, smoke, bench line, reference arm, launch list, full captures
+# Round artifacts on one B200 (gpurun -- 'bash scripts/gpurun_round.sh'): GPU test suite, smoke(),
+# the default bench line, the reference arm, the launch list, ncu --set full captures of the residue GEMM,
+# the auxiliary kernels and the fused kernel, the INT8 peak, every BASELINE config, the multi-GPU tile
+# projection and kernel timelines.  Outputs in gpurun_out/r2_*; the summaries go to profiles/.
 set -x
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q -rf > gpurun_out/r_tests.log 2>&1; echo tests=$?
-tail -3 gpurun_out/r_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r_smoke.log 2>&1; echo smoke=$?
-timeout 900 python bench.py > gpurun_out/r_bench.json 2> gpurun_out/r_bench.err; echo bench=$?
-timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/r_bench_ref.json 2> gpurun_out/r_bench_ref.err; echo ref=$?
-B="--steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-native"
-timeout 300 python bench.py $B > /dev/null 2>&1 && \
+R=gpurun_out/r2
+timeout 1500 python -m pytest tests -m gpu -q -rf > ${R}_tests.log 2>&1; echo tests=$?
+tail -3 ${R}_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > ${R}_smoke.log 2>&1; echo smoke=$?
+timeout 900 python bench.py > ${R}_bench.json 2> ${R}_bench.err; echo bench=$?
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > ${R}_bench_ref.json 2> ${R}_bench_ref.err; echo ref=$?
+timeout 300 python scripts/int8_peak.py --out ${R}_int8_peak.json > /dev/null 2>&1; echo peak=$?
+B="--steps 2 --warmup 3 --moduli 16 --no-cpu-baseline --no-e2e --no-native --no-int8-peak"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
-    --log-file gpurun_out/r_launches.csv python bench.py $B > /dev/null 2>&1; echo launches=$?
-B1="--steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-native"
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:gemm_i8_tc -s 1 -c 1 -o gpurun_out/r_gemm python bench.py $B1 > /dev/null 2>&1; echo gemm=$?
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"row_scan|col_max|resid_rows|resid_A|crt" -c 6 -o gpurun_out/r_aux python bench.py $B1 > /dev/null 2>&1; echo aux=$?
+    --log-file ${R}_launches.csv python bench.py $B > /dev/null 2>&1; echo launches=$?
+B1="--steps 1 --warmup 3 --moduli 16 --no-cpu-baseline --no-e2e --no-native --no-int8-peak"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"gemm_i8_tc_kernel<1>" -s 2 -c 1 -o ${R}_gemm python bench.py $B1 > /dev/null 2>&1; echo gemm=$?
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"row_scan|col_max|resid_rows|resid_A|crt" -c 6 -o ${R}_aux python bench.py $B1 > /dev/null 2>&1; echo aux=$?
+OZ2G_FUSED=1 timeout 900 ncu --set full --import-source on --clock-control none -k regex:gemm_crt_fused -c 1 -o ${R}_fused python bench.py $B1 --steps 1 --warmup 0 > /dev/null 2>&1; echo fused=$?
+timeout 900 python scripts/configs.py --out ${R}_configs.jsonl > /dev/null 2>&1; echo configs=$?
+timeout 600 python scripts/experiments/tile_projection.py > ${R}_tile_projection.jsonl 2>/dev/null; echo proj=$?
+timeout 300 python scripts/timeline.py --m 16384 --out ${R}_tl_16384.json > /dev/null 2>&1; echo tl=$?
+timeout 300 python scripts/timeline.py --m 1024 --moduli 14 --calls 5 --out ${R}_tl_1024.json > /dev/null 2>&1; echo tl1=$?
