@@ -658,8 +658,6 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     } else {
         st = (DevStatus*)ws.status.get(sizeof(DevStatus));
     }
-    CUDA_TRY(cudaMemsetAsync(st, 0, 8, stream));
-    CUDA_TRY(cudaMemsetAsync(&st->first_row, 0x7f, 16, stream));
     int32_t* mup = (int32_t*)ws.mup.get(4 * (size_t)m);
     int32_t* nup = (int32_t*)ws.nup.get(4 * (size_t)n);
     int32_t* mu = (int32_t*)ws.mu.get(4 * (size_t)m);
@@ -676,17 +674,38 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     // the workspace — they do not depend on N — so K1 / K2 are skipped
     const bool scan = !reuse_scaling;
     if (scan) ws.lo_ready = false;  // new inputs: the relative-criterion operands are stale
-    if (scan && n) CUDA_TRY(cudaMemsetAsync(bmax, 0, 8 * (size_t)n, stream));
-    if (scan && m) CUDA_TRY(cudaMemsetAsync(cmax_row, 0, 4 * (size_t)m, stream));
-    if (scan && n) CUDA_TRY(cudaMemsetAsync(cmax_col, 0, 4 * (size_t)n, stream));
+    // one launch instead of five memsets: the status word (first-failure keys
+    // at their maximum) and, for a scan, the column maxima of B and the
+    // clearance row / column maxima
+    CUDA_TRY(launch_init_call(st, scan ? bmax : nullptr, scan ? n : 0, scan ? cmax_row : nullptr, scan ? m : 0,
+                              scan ? cmax_col : nullptr, scan ? n : 0, stream));
+    ++launches;
 
+    // Unpipelined calls run the independent A-side and B-side passes (the
+    // scans, then the residue splits) on two streams: at small sizes each
+    // kernel alone leaves most of the GPU idle.  Joined before each GEMM.
+    const bool fork = !pipe && !spec_mode && m > 0 && n > 0;
+    size_t evn = 0;  // per-call event index (downloads wait for their CRT; stream forks / joins)
+    cudaStream_t sB = stream;
+    if (fork) {
+        ws.ensure_streams();
+        sB = ws.s_aux;
+        const cudaEvent_t ef = ws.pool_event(evn++);
+        CUDA_TRY(cudaEventRecord(ef, stream));
+        CUDA_TRY(cudaStreamWaitEvent(sB, ef, 0));
+    }
     // ---- K1 (B): column pre-exponents and Bbar^T ----
     if (pipe && !spec2) CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_b, 0));
-    if (scan && !spec2) tm.span(1, stream, [&] {
-        CUDA_TRY(launch_col_max_B(prec, dB, ldb_d, k, n, bmax, st, stream)); launches += n > 0;
-        CUDA_TRY(launch_col_exp_B(bmax, n, nup, st, stream)); launches += n > 0;
-        CUDA_TRY(launch_bbar_rows(prec, dB, ldb_d, k, n, kp, ldn, nup, bbar, st, stream)); launches += n > 0;
+    if (scan && !spec2) tm.span(1, sB, [&] {
+        CUDA_TRY(launch_col_max_B(prec, dB, ldb_d, k, n, bmax, st, sB)); launches += n > 0;
+        CUDA_TRY(launch_col_exp_B(bmax, n, nup, st, sB)); launches += n > 0;
+        CUDA_TRY(launch_bbar_rows(prec, dB, ldb_d, k, n, kp, ldn, nup, bbar, st, sB)); launches += n > 0;
     });
+    cudaEvent_t ev_bdone = nullptr;
+    if (fork) {
+        ev_bdone = ws.pool_event(evn++);
+        CUDA_TRY(cudaEventRecord(ev_bdone, sB));
+    }
 
     // tile shape: single-CTA 128x256 tiles, CTA-pair 256x256 tiles (cta_group::2),
     // or 128x256 tiles in 2-CTA clusters with a multicast B tile
@@ -809,7 +828,6 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     bool defer1 = false;                    // columns-only speculation: blocks wait for the final exponents
     int64_t repair_work = 0;                // block tiles recomputed so far
     std::vector<char> dirty1((size_t)ntiles, 0);  // 256-column tiles whose exponents moved (to repair)
-    size_t evn = 0;  // per-call event index (downloads wait for their CRT)
 
     // ---- K5 + K6 of one row block of C (columns c0 .. c0 + nc): residue GEMMs
     //      (fused signed mod p), CRT + unscale, download ----
@@ -1109,6 +1127,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
                                        mup + r0, abar + r0 * kp, st, stream, r0));
         });
         launches += rc > 0;
+        if (ev_bdone) CUDA_TRY(cudaStreamWaitEvent(stream, ev_bdone, 0));  // join: Bbar and nu' are ready
         if (rc > 0 && n > 0) tm.span(2, stream, [&] {
             const CUtensorMap tA = make_plane_map(abar + r0 * kp, kp, rc, 1, boxA);
             const CUtensorMap tB = make_plane_map_mn(bbar, n, ldn, kp, 1, kp * ldn);
@@ -1207,14 +1226,26 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
                                       mu, nu, ev, fv, st, stream));
         });
         ++launches;
+        if (fork) {  // B residues beside the A residues
+            const cudaEvent_t ef = ws.pool_event(evn++);
+            CUDA_TRY(cudaEventRecord(ef, stream));
+            CUDA_TRY(cudaStreamWaitEvent(sB, ef, 0));
+        }
         tm.span(4, stream, [&] {
             if (!pipe) {
                 CUDA_TRY(launch_resid_A(prec, dA, lda_d, m, k, kp, mu, rc_dev, N, ares, 0, st, stream));
                 launches += m > 0;
             }
-            CUDA_TRY(launch_resid_B_rows(prec, dB, ldb_d, k, n, kp, ldn, nu, rc_dev, N, bres, st, stream));
+        });
+        tm.span(4, sB, [&] {
+            CUDA_TRY(launch_resid_B_rows(prec, dB, ldb_d, k, n, kp, ldn, nu, rc_dev, N, bres, st, sB));
             launches += n > 0;
         });
+        if (fork) {
+            const cudaEvent_t ej = ws.pool_event(evn++);
+            CUDA_TRY(cudaEventRecord(ej, sB));
+            CUDA_TRY(cudaStreamWaitEvent(stream, ej, 0));
+        }
 
         if (bo && m * n) {
             // bounds.hpp:143-206 evaluated in the CRT pass

@@ -97,6 +97,8 @@ cudaError_t launch_resid_B_rows(int prec, const void* B, int64_t ldb, int64_t k,
 cudaError_t launch_trunc_scaled(int prec, const void* X, int64_t ldx, int64_t rows, int64_t cols,
                                 const int32_t* shift, int by_col, double* out, cudaStream_t s);
 cudaError_t launch_log2f(const float* x, float* out, int64_t count, cudaStream_t s);
+cudaError_t launch_init_call(DevStatus* st, unsigned long long* bmax, int64_t nb, int32_t* rmax, int64_t nr,
+                             int32_t* cmax, int64_t nc, cudaStream_t s);
 cudaError_t launch_merge_status(DevStatus* dst, const DevStatus* src, int64_t count, cudaStream_t s);
 
 // Error-bound factors (bounds.cu): RA_i = t (|A|v)_i, PA_i = sqrt(max(1, rowmax_i)),

@@ -362,6 +362,24 @@ __global__ void __launch_bounds__(256) floor_rows_B_kernel(const T* __restrict__
     if (j < n && acc) atomicAdd(&csum[j], acc);
 }
 
+
+// Start of a call: clear the status word (first-failure keys to their maximum)
+// and zero the maxima the scans and the clearance GEMM accumulate into.
+__global__ void init_call_kernel(DevStatus* st, unsigned long long* bmax, int64_t nb, int32_t* rmax, int64_t nr,
+                                 int32_t* cmax, int64_t nc) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t == 0) {
+        st->err = 0;
+        st->subnormal = 0;
+        st->first_row = 0x7f7f7f7f7f7f7f7fll;
+        st->first_col = 0x7f7f7f7f7f7f7f7fll;
+    }
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = t; i < nb; i += stride) bmax[i] = 0;
+    for (int64_t i = t; i < nr; i += stride) rmax[i] = 0;
+    for (int64_t i = t; i < nc; i += stride) cmax[i] = 0;
+}
+
 inline unsigned blocks_for(int64_t work, int per) { return (unsigned)((work + per - 1) / per); }
 
 }  // namespace
@@ -496,6 +514,16 @@ cudaError_t launch_floor_operands(int prec, const void* A, int64_t lda, int64_t 
         if (prec) floor_rows_B_kernel<double><<<grid, 256, 0, s>>>((const double*)B, ldb, k, n, kp, ldn, nu_prime, b_out, csum);
         else floor_rows_B_kernel<float><<<grid, 256, 0, s>>>((const float*)B, ldb, k, n, kp, ldn, nu_prime, b_out, csum);
     }
+    return cudaGetLastError();
+}
+
+
+cudaError_t launch_init_call(DevStatus* st, unsigned long long* bmax, int64_t nb, int32_t* rmax, int64_t nr,
+                             int32_t* cmax, int64_t nc, cudaStream_t s) {
+    const int64_t most = nb > nr ? (nb > nc ? nb : nc) : (nr > nc ? nr : nc);
+    const int64_t blocks = (most + 255) / 256;
+    init_call_kernel<<<(unsigned)(blocks < 1 ? 1 : (blocks > 1184 ? 1184 : blocks)), 256, 0, s>>>(st, bmax, nb, rmax, nr,
+                                                                                                cmax, nc);
     return cudaGetLastError();
 }
 
