@@ -1509,6 +1509,7 @@ int run_gemm_graph(int prec, int64_t m, int64_t n, int64_t k, const void* A, int
         std::memset(&d, 0, sizeof d);
         cudaGraph_t g = nullptr;
         if (!ws.s_cap) CUDA_TRY(cudaStreamCreateWithFlags(&ws.s_cap, cudaStreamNonBlocking));
+        if (!ws.status_host) CUDA_TRY(cudaHostAlloc((void**)&ws.status_host, sizeof(DevStatus), cudaHostAllocDefault));
         CUDA_TRY(cudaStreamBeginCapture(ws.s_cap, cudaStreamCaptureModeRelaxed));
         g_capture = true;
         try {
@@ -1520,7 +1521,14 @@ int run_gemm_graph(int prec, int64_t m, int64_t n, int64_t k, const void* A, int
             throw;
         }
         g_capture = false;
+        // the status read-back is the graph's last node
+        const cudaError_t ce = cudaMemcpyAsync(ws.status_host, ws.status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost,
+                                               ws.s_cap);
         CUDA_TRY(cudaStreamEndCapture(ws.s_cap, &g));
+        if (ce != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            throw Fail{OZ2G_CUDA_ERROR, std::string("cudaMemcpyAsync (status): ") + cudaGetErrorString(ce)};
+        }
         const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
         cudaGraphDestroy(g);
         if (ie != cudaSuccess) {
@@ -1530,10 +1538,8 @@ int run_gemm_graph(int prec, int64_t m, int64_t n, int64_t k, const void* A, int
         e.gen = g_alloc_gen.load();
         e.launches = d.kernels_launched;
     }
-    if (!ws.status_host) CUDA_TRY(cudaHostAlloc((void**)&ws.status_host, sizeof(DevStatus), cudaHostAllocDefault));
     if (diag) std::memset(diag, 0, sizeof *diag);
     CUDA_TRY(cudaGraphLaunch(e.exec, stream));
-    CUDA_TRY(cudaMemcpyAsync(ws.status_host, ws.status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
     CUDA_TRY(cudaStreamSynchronize(stream));
     if (diag) {
         diag->kernels_launched = e.launches;
