@@ -102,8 +102,13 @@ def _ncu_traffic(m: int, nmod: int):
     from the committed `ncu --set full` capture of this configuration (one
     launch), or None when no capture matches."""
     import csv
-    path = os.path.join(ROOT, "profiles", f"r01_ncu_full_residue_gemm_{m}.csv")
-    if nmod != 16 or not os.path.exists(path):
+    path = None
+    for rnd in ("r02", "r01"):  # the newest committed capture
+        p = os.path.join(ROOT, "profiles", f"{rnd}_ncu_full_residue_gemm_{m}.csv")
+        if os.path.exists(p):
+            path = p
+            break
+    if nmod != 16 or path is None:
         return None
     try:
         rows = list(csv.reader(open(path)))
