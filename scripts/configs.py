@@ -25,7 +25,8 @@ from bench import gen_device  # noqa: E402
 
 
 def timed(fn, reps):
-    fn()
+    for _ in range(3):  # plain call, graph capture, first replay (device-pointer calls replay a CUDA graph)
+        fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()

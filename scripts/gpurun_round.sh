@@ -15,7 +15,7 @@ B="--steps 2 --warmup 3 --moduli 16 --no-cpu-baseline --no-e2e --no-native --no-
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
     --log-file ${R}_launches.csv python bench.py $B > /dev/null 2>&1; echo launches=$?
 B1="--steps 1 --warmup 3 --moduli 16 --no-cpu-baseline --no-e2e --no-native --no-int8-peak"
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"gemm_i8_tc_kernel<1>" -s 2 -c 1 -o ${R}_gemm python bench.py $B1 > /dev/null 2>&1; echo gemm=$?
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:gemm_i8_tc -s 1 -c 1 -o ${R}_gemm python bench.py $B1 > /dev/null 2>&1; echo gemm=$?
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"row_scan|col_max|resid_rows|resid_A|crt" -c 6 -o ${R}_aux python bench.py $B1 > /dev/null 2>&1; echo aux=$?
 OZ2G_FUSED=1 timeout 900 ncu --set full --import-source on --clock-control none -k regex:gemm_crt_fused -c 1 -o ${R}_fused python bench.py $B1 --steps 1 --warmup 0 > /dev/null 2>&1; echo fused=$?
 timeout 900 python scripts/configs.py --out ${R}_configs.jsonl > /dev/null 2>&1; echo configs=$?
