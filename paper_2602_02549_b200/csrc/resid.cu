@@ -93,13 +93,6 @@ __device__ __forceinline__ uint32_t resid_w(const ElemDec& d, const uint8_t* __r
     return (uint32_t)bits - (uint32_t)__float_as_int(t) * c.p;
 }
 
-// p = 256: the low byte of bits(M + S) is already S mod 256 (M is a multiple of
-// 256) and the reference's representative (both +-128 are the byte 0x80).
-__device__ __forceinline__ uint32_t resid_w256(const ElemDec& d, const uint8_t* __restrict__ row_l) {
-    const int2 w = *reinterpret_cast<const int2*>(row_l + d.off);
-    return (uint32_t)dp4a_us(d.hi, w.y, dp4a_us(d.lo, w.x, 0x4B400000));
-}
-
 __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
     const uint32_t lo = __byte_perm(b0, b1, 0x0040);
     const uint32_t hi = __byte_perm(b2, b3, 0x0040);
@@ -168,18 +161,8 @@ __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, i
             for (int j = 0; j < RA_E; ++j) d[j] = elem_dec(h0 + j < k ? ld_d(row + j) : 0.0, sft, ovf);
         }
         int8_t* out = planes + i * kp + h0;
-        int l0 = 0;
-        if (hd.p[0] == 256u) {  // the first modulus of every table: no reduction (moduli.hpp:31-36)
-            const uint8_t* rl = tab;
-            const uint32_t w0 = pack4(resid_w256(d[0], rl), resid_w256(d[1], rl), resid_w256(d[2], rl),
-                                      resid_w256(d[3], rl));
-            const uint32_t w1 = pack4(resid_w256(d[4], rl), resid_w256(d[5], rl), resid_w256(d[6], rl),
-                                      resid_w256(d[7], rl));
-            *reinterpret_cast<uint2*>(out) = make_uint2(w0, w1);
-            l0 = 1;
-        }
 #pragma unroll 2
-        for (int l = l0; l < nmod; ++l) {
+        for (int l = 0; l < nmod; ++l) {
             const ModC c = modc(hd, l);
             const uint8_t* rl = tab + (size_t)l * kResidRow;
             const uint32_t w0 = pack4(resid_w(d[0], rl, c), resid_w(d[1], rl, c), resid_w(d[2], rl, c),
@@ -287,18 +270,8 @@ __global__ void __launch_bounds__(256) resid_rows_kernel(const T* __restrict__ X
             for (int j = 0; j < RA_E; ++j)
                 d[j] = elem_dec(h0 + j < cols_valid ? (double)__ldg(row + j) : 0.0, COLSHIFT ? csft[j] : rsft, bad);
         }
-        int l0 = 0;
-        if (hd.p[0] == 256u) {  // the first modulus of every table: no reduction (moduli.hpp:31-36)
-            const uint8_t* rl = tab;
-            const uint32_t w0 = pack4(resid_w256(d[0], rl), resid_w256(d[1], rl), resid_w256(d[2], rl),
-                                      resid_w256(d[3], rl));
-            const uint32_t w1 = pack4(resid_w256(d[4], rl), resid_w256(d[5], rl), resid_w256(d[6], rl),
-                                      resid_w256(d[7], rl));
-            *reinterpret_cast<uint2*>(out) = make_uint2(w0, w1);
-            l0 = 1;
-        }
 #pragma unroll 2
-        for (int l = l0; l < nmod; ++l) {
+        for (int l = 0; l < nmod; ++l) {
             const ModC c = modc(hd, l);
             const uint8_t* rl = tab + (size_t)l * kResidRow;
             const uint32_t w0 = pack4(resid_w(d[0], rl, c), resid_w(d[1], rl, c), resid_w(d[2], rl, c),
