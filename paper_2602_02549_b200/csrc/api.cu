@@ -845,6 +845,14 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         int8_t* Wb = (w_full ? W + r0 * ldw : W) + c0;
         set_rows(g, rc);
         g.W = Wb;
+        static const bool gemm_fence = [] {
+            const char* e = std::getenv("OZ2G_GEMM_FENCE");
+            return e && e[0] == '1';
+        }();
+        if (gemm_fence) {  // experiment: keep the persistent CTAs within one unit of each other
+            g.fence = (unsigned long long*)ws.x_bmax.get(64) + 5;
+            CUDA_TRY(cudaMemsetAsync(g.fence, 0, 8, stream));
+        }
         tm.span(5, stream, [&] { CUDA_TRY(launch_gemm(EPI_RESID, tA, tB, g)); });
         ++launches;
         if (inter && inter->Cprod) {  // rows of this block of the m x n planes

@@ -205,6 +205,19 @@ __device__ __forceinline__ void st_global_v4f64(double* p, double a, double b, d
     asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
 
+// Grid-wide step fence of persistent kernels (one producer lane per CTA):
+// wait until `counter` >= need, bounded (~2^26 cycles) so that CTAs that are
+// not resident cannot hang the launch.
+__device__ __forceinline__ void step_fence_wait(const unsigned long long* counter, unsigned long long need) {
+    const long long t0 = clock64();
+    for (;;) {
+        unsigned long long v;
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(counter) : "memory");
+        if (v >= need || clock64() - t0 > (1ll << 26)) break;
+        __nanosleep(64);
+    }
+}
+
 // ----------------------------------------------------------------------------
 // mbarrier / TMA / tcgen05 PTX wrappers
 // ----------------------------------------------------------------------------

@@ -177,8 +177,11 @@ __global__ void __launch_bounds__(256, 1)
         // ===== TMA producer =====
         int stage = 0;
         uint32_t phase = 0;
-        for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        unsigned long long j = 0;
+        for (int u = blockIdx.x; u < total; u += gridDim.x, ++j) {
             const TileCoord tc = decode_unit(u, P.tiles_m, P.tiles_n, P.group_m);
+            if (P.fence && lane == 0) step_fence_wait(P.fence, j * gridDim.x);
+            __syncwarp();
             for (int kb = 0; kb < P.kblocks; ++kb) {
                 mbar_wait(&empty[stage], phase ^ 1u);
                 if (lane == 0) {
@@ -193,6 +196,11 @@ __global__ void __launch_bounds__(256, 1)
                 __syncwarp();
                 if (++stage == STAGES) { stage = 0; phase ^= 1u; }
             }
+            if (P.fence && lane == 0) atomicAdd(P.fence, 1ull);
+        }
+        if (P.fence && lane == 0) {  // release the units this CTA does not have
+            const unsigned long long steps = (unsigned long long)((total + (int)gridDim.x - 1) / (int)gridDim.x);
+            if (j < steps) atomicAdd(P.fence, steps - j);
         }
     } else if (warp == 1) {
         // ===== MMA issuer =====
@@ -462,10 +470,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         // ===== TMA producer (both CTAs) =====
         int stage = 0;
         uint32_t phase = 0;
-        for (int u = cid; u < total; u += clusters) {
+        unsigned long long j = 0;
+        for (int u = cid; u < total; u += clusters, ++j) {
             const TileCoord tc = decode_unit(u, P.tiles_m, P.tiles_n, P.group_m);
             const int arow = tc.tm * P_BM + (int)rank * P_HALF;
             const int bcol = tc.tn * P_BN + (int)rank * P_HALF;  // this CTA's 128 columns of B
+            if (P.fence && lane == 0) step_fence_wait(P.fence, j * gridDim.x);
+            __syncwarp();
             for (int kb = 0; kb < P.kblocks; ++kb) {
                 mbar_wait(&empty[stage], phase ^ 1u);
                 if (lane == 0) {
@@ -476,6 +487,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                 __syncwarp();
                 if (++stage == P_STAGES) { stage = 0; phase ^= 1u; }
             }
+            if (P.fence && lane == 0) atomicAdd(P.fence, 1ull);
+        }
+        if (P.fence && lane == 0) {
+            const unsigned long long steps = (unsigned long long)((total + clusters - 1) / clusters);
+            if (j < steps) atomicAdd(P.fence, steps - j);
         }
     } else if (warp == 1) {
         // ===== MMA issuer (leader CTA only) =====

@@ -37,6 +37,9 @@ struct GemmParams {
     int32_t* C32;
     int64_t ldc32, cplane;
     uint32_t p[49], magic[49], off[49];
+    // unit fence (experiment, OZ2G_GEMM_FENCE): a zeroed counter; before its
+    // j-th unit a CTA waits until every CTA issued the loads of j units
+    unsigned long long* fence;
 };
 
 int gemm_smem_bytes();
