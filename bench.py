@@ -54,7 +54,8 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
-        self.path = os.path.join("/tmp", f"oz2g_clocks_{os.getpid()}.csv")
+        ClockSampler._n = getattr(ClockSampler, "_n", 0) + 1  # one file per sampler
+        self.path = os.path.join("/tmp", f"oz2g_clocks_{os.getpid()}_{ClockSampler._n}.csv")
 
     def __enter__(self):
         try:
@@ -335,6 +336,7 @@ def main():
         ev1.record(stream)
         barrier()
     t_ms = ev0.elapsed_time(ev1)
+    clocks_timed = sampler.summary()  # the timed region's samples (before any other sampler runs)
     # instrumented steps for the dominant kernel (residue GEMMs), same stream
     gemm_ms = []
     for _ in range(3):
@@ -567,7 +569,7 @@ def main():
                    "moduli": args.moduli, "moduli_choice": auto_n or "fixed (--moduli)",
                    "phi": args.phi, "parallelism": f"2d-tile {R}x{Cc}",
                    "l2": "inputs 2 GiB each > L2, no flush"},
-        "clocks": sampler.summary(),
+        "clocks": clocks_timed,
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
         "roofline": roof,

@@ -146,6 +146,9 @@ class EmulationResult:
     speculation: int = 0  # 0 none, 1 speculated column exponents confirmed, 2 missed and redone
 
 
+_NO_HOOK = _lib.REDUCE_FN()  # the null oz2g_reduce_maxima_fn
+
+
 def _is_torch_cuda(x) -> bool:
     return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
 
@@ -319,7 +322,7 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
                 return 1
         cb = _lib.REDUCE_FN(_cb)
     else:
-        cb = _lib.REDUCE_FN()
+        cb = _NO_HOOK
     rc = L.oz2g_gemm(prec, m, nn, k, pa, lda, pb, ldb, pc, ldc, int(n), flags,
                      C.c_void_p(int(stream) if stream else 0),
                      C.byref(inter_c) if inter_c is not None else None, C.byref(diag), cb, None)
