@@ -160,6 +160,44 @@ EmulationResult<T> os_ii(const Matrix<T>& a, const Matrix<T>& b, int n, bool kee
     return r;
 }
 
+// bounds.hpp:208-243: the smallest N whose cheap error bound (absolute) meets
+// `target`, one clearance pass on the device.
+struct SuggestResult {
+    bool achievable = false;
+    int n = 0;
+    double bound_max = 0;
+};
+
+template <class T>
+SuggestResult suggest_n(const Matrix<T>& a, const Matrix<T>& b, double target) {
+    static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>);
+    require_dims(a.cols() == b.rows(), "suggest_n inner dimension");
+    const int prec = std::is_same_v<T, double> ? OZ2G_FP64 : OZ2G_FP32;
+    SuggestResult r;
+    detail::throw_status(oz2g_suggest_n(prec, a.rows(), b.cols(), a.cols(), a.data(), a.cols(), b.data(), b.cols(),
+                                        target, OZ2G_HOST_PTRS, nullptr, &r.n, &r.bound_max));
+    r.achievable = r.n > 0;
+    return r;
+}
+
+// The same search with the TIGHT bound (bounds.hpp:182-195), absolute or
+// relative to (|A||B|)_ij (oz2g_suggest_n_tight): the N the north star asks
+// for ("N from the paper's bound for 1e-15 relative accuracy").
+template <class T>
+SuggestResult suggest_n_tight(const Matrix<T>& a, const Matrix<T>& b, double target, bool relative = true) {
+    static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>);
+    require_dims(a.cols() == b.rows(), "suggest_n inner dimension");
+    const int prec = std::is_same_v<T, double> ? OZ2G_FP64 : OZ2G_FP32;
+    oz2g_suggest s;
+    detail::throw_status(oz2g_suggest_n_tight(prec, a.rows(), b.cols(), a.cols(), a.data(), a.cols(), b.data(),
+                                              b.cols(), target, relative ? 1 : 0, OZ2G_HOST_PTRS, nullptr, &s));
+    SuggestResult r;
+    r.n = s.n;
+    r.achievable = s.n > 0;
+    r.bound_max = s.bound_max;
+    return r;
+}
+
 // The same emulation tiled over several CUDA devices of this process
 // (oz2g_gemm_multi): C is bit-identical to os_ii<T>; the result carries C,
 // the subnormal flag and the table (no per-stage intermediates).

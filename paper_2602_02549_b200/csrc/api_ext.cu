@@ -38,40 +38,45 @@ int run_gemm_graph(int prec, int64_t m, int64_t n, int64_t k, const void* A, int
     const uint64_t gen = g_alloc_gen.load();
     if (!e.exec || e.gen != gen) {
         if (e.exec) { cudaGraphExecDestroy(e.exec); e.exec = nullptr; }
-        if (e.seen++ == 0 || ws.graphs.size() > 64) {  // first sight: a plain call (allocates, uploads tables)
+        if (e.plain || e.seen++ == 0 || ws.graphs.size() > 64) {  // first sight: a plain call (allocates, uploads)
             if (ws.graphs.size() > 64) ws.drop_graphs();
             return run_gemm(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, stream, nullptr, diag, nullptr,
                             nullptr);
         }
         oz2g_diag d;
         std::memset(&d, 0, sizeof d);
-        cudaGraph_t g = nullptr;
         if (!ws.s_cap) CUDA_TRY(cudaStreamCreateWithFlags(&ws.s_cap, cudaStreamNonBlocking));
         if (!ws.status_host) CUDA_TRY(cudaHostAlloc((void**)&ws.status_host, sizeof(DevStatus), cudaHostAllocDefault));
-        CUDA_TRY(cudaStreamBeginCapture(ws.s_cap, cudaStreamCaptureModeRelaxed));
-        g_capture = true;
-        try {
-            run_gemm(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, ws.s_cap, nullptr, &d, nullptr, nullptr);
-        } catch (...) {
+        // capture; any failure (an operation the capture does not allow, instantiation)
+        // leaves this entry plain and the call runs uncaptured
+        auto capture = [&]() -> bool {
+            cudaGraph_t g = nullptr;
+            if (cudaStreamBeginCapture(ws.s_cap, cudaStreamCaptureModeRelaxed) != cudaSuccess) return false;
+            g_capture = true;
+            bool ok = true;
+            try {
+                run_gemm(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, ws.s_cap, nullptr, &d, nullptr, nullptr);
+            } catch (...) {
+                ok = false;
+            }
             g_capture = false;
-            cudaStreamEndCapture(ws.s_cap, &g);
+            // the status read-back is the graph's last node
+            if (ok && cudaMemcpyAsync(ws.status_host, ws.status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost,
+                                      ws.s_cap) != cudaSuccess)
+                ok = false;
+            if (cudaStreamEndCapture(ws.s_cap, &g) != cudaSuccess) ok = false;
+            if (ok && g && cudaGraphInstantiate(&e.exec, g, 0) != cudaSuccess) {
+                e.exec = nullptr;
+                ok = false;
+            }
             if (g) cudaGraphDestroy(g);
-            throw;
-        }
-        g_capture = false;
-        // the status read-back is the graph's last node
-        const cudaError_t ce = cudaMemcpyAsync(ws.status_host, ws.status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost,
-                                               ws.s_cap);
-        CUDA_TRY(cudaStreamEndCapture(ws.s_cap, &g));
-        if (ce != cudaSuccess) {
-            if (g) cudaGraphDestroy(g);
-            throw Fail{OZ2G_CUDA_ERROR, std::string("cudaMemcpyAsync (status): ") + cudaGetErrorString(ce)};
-        }
-        const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
-        cudaGraphDestroy(g);
-        if (ie != cudaSuccess) {
-            e.exec = nullptr;
-            throw Fail{OZ2G_CUDA_ERROR, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie)};
+            cudaGetLastError();  // clear a capture error
+            return ok && e.exec;
+        };
+        if (!capture()) {
+            e.plain = true;
+            return run_gemm(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, stream, nullptr, diag, nullptr,
+                            nullptr);
         }
         e.gen = g_alloc_gen.load();
         e.launches = d.kernels_launched;

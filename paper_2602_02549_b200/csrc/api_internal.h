@@ -114,6 +114,7 @@ struct Workspace {
         uint64_t gen = 0;
         int launches = 0;
         int seen = 0;
+        bool plain = false;  // capture failed once: always run plainly
     };
     std::map<std::vector<int64_t>, GraphEntry> graphs;
     DevStatus* status_host = nullptr;  // pinned copy of the status word read after a replay

@@ -57,6 +57,14 @@ int main() {
     for (int i = 0; i < 4; ++i)
         for (int j = 0; j < 4; ++j)
             CHECK(std::ldexp(std::ldexp(res.C(i, j), res.scaling.mu[i]), res.scaling.nu[j]) == res.crt.Cpp64(i, j));
+    // bounds.hpp:217-243 suggest_n (cheap, absolute) and the tight / relative search
+    const auto sc = suggest_n(A, B, 1e-6);
+    CHECK(sc.achievable && sc.n >= 2 && sc.bound_max <= 1e-6);
+    CHECK(!suggest_n(A, B, 1e-300).achievable);
+    const auto st = suggest_n_tight(A, B, 1e-13, true);
+    CHECK(st.achievable && st.n >= 2 && st.bound_max <= 1e-13);
+    CHECK(suggest_n_tight(A, B, 1e-13, false).n <= suggest_n(A, B, 1e-13).n || !suggest_n(A, B, 1e-13).achievable);
+    CHECK(throws_as<std::domain_error>([&] { suggest_n(A, B, -1.0); }));
     // multi-device tiling (the device listed twice): C identical to os_ii
     {
         Matrix<double> X(40, 33), Y(33, 27);
