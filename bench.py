@@ -230,6 +230,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-native", action="store_true")
     ap.add_argument("--no-int8-peak", action="store_true")
+    ap.add_argument("--force-comm", action="store_true",
+                    help="run the multi-rank path (library NCCL communicator, shards) even on one GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.k is None:
@@ -252,8 +254,16 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    use_comm = world > 1 or args.force_comm
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    elif use_comm:  # one rank: a local process group only carries the NCCL id
+        import socket
+        so = socket.socket()
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+        so.close()
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
     m = n = args.m
     k = args.k
     tile = pdist.tile_of(rank, world, m, n)
@@ -267,7 +277,7 @@ def main():
     B_full = gen_device(k, n, args.phi, 5678, torch.float64, dev)
     A = A_full[rows].contiguous()
     B = B_full[:, cols].contiguous()
-    if world > 1:
+    if use_comm:
         lay = pdist.layout(world, rank, m, n)
         A_sh = A_full[lay["a_shard"]].contiguous()
         B_sh = B_full[:, lay["b_shard"]].contiguous()
@@ -294,10 +304,11 @@ def main():
 
     reduce_cb = None
     comm = None
-    if world > 1:
+    if use_comm:
         # the library's own NCCL communicator (world + ncclCommSplit row / column comms)
         comm = pdist.NativeComm(dist, world, rank)
-        del A, B
+        if world > 1:
+            del A, B
 
     stream = torch.cuda.current_stream(dev)
 
@@ -375,7 +386,8 @@ def main():
             e2e_step()
         barrier()
         te = torch.tensor([(time.perf_counter() - t0) / e_steps], dtype=torch.float64, device=dev)
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": flops / float(te.item()) / 1e12, "unit": UNIT,
                "h2d_bytes_per_step": int(8 * (A_sh.numel() + B_sh.numel()) * world),
                "d2h_bytes_per_step": int(8 * m * n),
@@ -511,8 +523,11 @@ def main():
             torch.cuda.synchronize()
             by_moduli[str(nm)] = flops / (s0.elapsed_time(s1) / 3 * 1e-3) / 1e12
 
+    if comm is not None:
+        torch.cuda.synchronize()
+        comm.close()
     if rank != 0:
-        if world > 1:
+        if dist.is_initialized():
             dist.destroy_process_group()
         return
 
@@ -580,7 +595,7 @@ def main():
         "tflops_by_moduli": by_moduli,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
