@@ -126,3 +126,22 @@ def test_auto_n_cfg4(cuda):
     torch.cuda.synchronize()
     assert r.achievable and r.n == 16, r
     assert r.tight_rel_max <= 1e-15
+
+
+@pytest.mark.parametrize("m,k,n,N", [(16384, 16384, 16384, 16), (2048, 65536, 2048, 16)])
+def test_host_pipeline_full_size(cuda, m, k, n, N):
+    """The pipelined, speculated host-pointer path (PCIe uploads in row /
+    column chunks, exponents speculated from the chunks present, re-checked at
+    every arrival) returns the device path's C bit for bit at the BASELINE
+    sizes."""
+    import torch
+    dA, dB = _gen((m, k), 0.0, 77 + m), _gen((k, n), 0.0, 78 + n)
+    dev_c = oz.os_ii(dA, dB, N).C
+    Ah = torch.empty((m, k), dtype=torch.float64, pin_memory=True)
+    Bh = torch.empty((k, n), dtype=torch.float64, pin_memory=True)
+    Ch = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
+    Ah.copy_(dA)
+    Bh.copy_(dB)
+    r = oz.os_ii(Ah.numpy(), Bh.numpy(), N, out=Ch.numpy())
+    assert r.speculation in (1, 2, 3)
+    assert torch.equal(Ch.view(torch.int64), dev_c.cpu().view(torch.int64))
