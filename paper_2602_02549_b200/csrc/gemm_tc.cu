@@ -141,8 +141,15 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&v)[32], int row,
     }
 }
 
+// 8 epilogue warps (warps 4..11): warp w reads TMEM lanes 32 (w % 4) .. and
+// the column half (w - 4) / 4 of the 256-column accumulator, so the epilogue
+// of a tile takes half as long — it bounds the GEMM when k is small (each
+// tile's MMAs then take little longer than its epilogue).
+constexpr int EPI_WARPS = 8;
+constexpr int TC_THREADS = 128 + 32 * EPI_WARPS;
+
 template <int MODE>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ GemmParams P) {
     extern __shared__ uint8_t smem_raw[];
@@ -161,7 +168,7 @@ __global__ void __launch_bounds__(256, 1)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], EPI_WARPS); }
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
@@ -233,7 +240,9 @@ __global__ void __launch_bounds__(256, 1)
         }
     } else if (warp >= 4) {
         // ===== Epilogue =====
-        const int wq = warp - 4;
+        const int wq = warp & 3;                                  // TMEM lane quadrant
+        const int c_lo = ((warp - 4) / 4) * (BN / 32 / (EPI_WARPS / 4));  // first 32-column chunk
+        const int c_hi = c_lo + BN / 32 / (EPI_WARPS / 4);
         int it = 0;
         for (int u = blockIdx.x; u < total; u += gridDim.x, ++it) {
             const TileCoord tc = decode_unit(u, P.tiles_m, P.tiles_n, P.group_m);
@@ -244,7 +253,7 @@ __global__ void __launch_bounds__(256, 1)
             const int row = tc.tm * BM + wq * 32 + lane;
             int32_t rowmax = 0;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = c_lo; c < c_hi; ++c) {
                 uint32_t v[32];
                 tmem_ld32(tmem_base + ((uint32_t)(wq * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
                 tmem_ld_wait();
@@ -639,19 +648,19 @@ cudaError_t launch_gemm_i8(int mode, const CUtensorMap& tmA, const CUtensorMap& 
             err = cudaFuncSetAttribute(gemm_i8_tc_kernel<EPI_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        SMEM_BYTES);
             if (err != cudaSuccess) return err;
-            gemm_i8_tc_kernel<EPI_MAX><<<grid, 256, SMEM_BYTES, stream>>>(tmA, tmB, P);
+            gemm_i8_tc_kernel<EPI_MAX><<<grid, TC_THREADS, SMEM_BYTES, stream>>>(tmA, tmB, P);
             break;
         case EPI_RESID:
             err = cudaFuncSetAttribute(gemm_i8_tc_kernel<EPI_RESID>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
             if (err != cudaSuccess) return err;
-            gemm_i8_tc_kernel<EPI_RESID><<<grid, 256, SMEM_BYTES, stream>>>(tmA, tmB, P);
+            gemm_i8_tc_kernel<EPI_RESID><<<grid, TC_THREADS, SMEM_BYTES, stream>>>(tmA, tmB, P);
             break;
         default:
             err = cudaFuncSetAttribute(gemm_i8_tc_kernel<EPI_I32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        SMEM_BYTES);
             if (err != cudaSuccess) return err;
-            gemm_i8_tc_kernel<EPI_I32><<<grid, 256, SMEM_BYTES, stream>>>(tmA, tmB, P);
+            gemm_i8_tc_kernel<EPI_I32><<<grid, TC_THREADS, SMEM_BYTES, stream>>>(tmA, tmB, P);
             break;
     }
     return cudaGetLastError();
