@@ -145,11 +145,10 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&v)[32], int row,
 // the column half (w - 4) / 4 of the 256-column accumulator, so the epilogue
 // of a tile takes half as long — it bounds the GEMM when k is small (each
 // tile's MMAs then take little longer than its epilogue).
-constexpr int EPI_WARPS = 8;
-constexpr int TC_THREADS = 128 + 32 * EPI_WARPS;
+constexpr int tc_threads(int epi_warps) { return 128 + 32 * epi_warps; }
 
-template <int MODE>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+template <int MODE, int EPI_WARPS>
+__global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
     gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ GemmParams P) {
     extern __shared__ uint8_t smem_raw[];
@@ -637,33 +636,35 @@ int gemm_tile_m() { return BM; }
 int gemm_tile_n() { return BN; }
 int gemm_tile_k() { return BK; }
 
+template <int EW>
+cudaError_t launch_tc(int mode, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& P, int grid,
+                      cudaStream_t stream) {
+    static int configured[64][3] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int mi = mode == EPI_MAX ? 0 : mode == EPI_RESID ? 1 : 2;
+    auto kern = mode == EPI_MAX ? gemm_i8_tc_kernel<EPI_MAX, EW>
+              : mode == EPI_RESID ? gemm_i8_tc_kernel<EPI_RESID, EW> : gemm_i8_tc_kernel<EPI_I32, EW>;
+    if (dev < 64 && !configured[dev][mi]) {  // once per device and kernel
+        const cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        if (err != cudaSuccess) return err;
+        configured[dev][mi] = 1;
+    }
+    kern<<<grid, tc_threads(EW), SMEM_BYTES, stream>>>(tmA, tmB, P);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gemm_i8(int mode, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& P,
                            int num_sms, cudaStream_t stream) {
     const int total = P.planes * P.tiles_m * P.tiles_n;
     if (total == 0) return cudaSuccess;
     const int grid = total < num_sms ? total : num_sms;
-    cudaError_t err = cudaSuccess;
-    switch (mode) {
-        case EPI_MAX:
-            err = cudaFuncSetAttribute(gemm_i8_tc_kernel<EPI_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       SMEM_BYTES);
-            if (err != cudaSuccess) return err;
-            gemm_i8_tc_kernel<EPI_MAX><<<grid, TC_THREADS, SMEM_BYTES, stream>>>(tmA, tmB, P);
-            break;
-        case EPI_RESID:
-            err = cudaFuncSetAttribute(gemm_i8_tc_kernel<EPI_RESID>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-            if (err != cudaSuccess) return err;
-            gemm_i8_tc_kernel<EPI_RESID><<<grid, TC_THREADS, SMEM_BYTES, stream>>>(tmA, tmB, P);
-            break;
-        default:
-            err = cudaFuncSetAttribute(gemm_i8_tc_kernel<EPI_I32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       SMEM_BYTES);
-            if (err != cudaSuccess) return err;
-            gemm_i8_tc_kernel<EPI_I32><<<grid, TC_THREADS, SMEM_BYTES, stream>>>(tmA, tmB, P);
-            break;
-    }
-    return cudaGetLastError();
+    // epilogue warps (OZ2G_EPI_WARPS = 4 or 8, default 8)
+    static const int ew = [] {
+        const char* e = getenv("OZ2G_EPI_WARPS");
+        return e && atoi(e) == 4 ? 4 : 8;
+    }();
+    return ew == 4 ? launch_tc<4>(mode, tmA, tmB, P, grid, stream) : launch_tc<8>(mode, tmA, tmB, P, grid, stream);
 }
 
 cudaError_t launch_gemm_i8_mc(int mode, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& P,
