@@ -659,11 +659,14 @@ cudaError_t launch_gemm_i8(int mode, const CUtensorMap& tmA, const CUtensorMap& 
     const int total = P.planes * P.tiles_m * P.tiles_n;
     if (total == 0) return cudaSuccess;
     const int grid = total < num_sms ? total : num_sms;
-    // epilogue warps (OZ2G_EPI_WARPS = 4 or 8, default 8)
-    static const int ew = [] {
+    // epilogue warps: 8 when k is small (k <= 2048: a tile's MMAs take little
+    // longer than its epilogue; cfg1 1024^3 79 vs 88 us per call), 4 above
+    // (equal at 4096^3, 4 within noise ahead at 16384^3); OZ2G_EPI_WARPS=4|8 forces
+    static const int env = [] {
         const char* e = getenv("OZ2G_EPI_WARPS");
-        return e && atoi(e) == 4 ? 4 : 8;
+        return e ? atoi(e) : 0;
     }();
+    const int ew = env == 4 || env == 8 ? env : (P.kblocks <= 16 ? 8 : 4);
     return ew == 4 ? launch_tc<4>(mode, tmA, tmB, P, grid, stream) : launch_tc<8>(mode, tmA, tmB, P, grid, stream);
 }
 
