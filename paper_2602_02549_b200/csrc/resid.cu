@@ -93,28 +93,6 @@ __device__ __forceinline__ uint32_t resid_w(const ElemDec& d, const uint8_t* __r
     return (uint32_t)bits - (uint32_t)__float_as_int(t) * c.p;
 }
 
-// Two elements of one modulus at once: the fp32 reduction of resid_w on
-// packed pairs (FADD2 / FFMA2, sm_100: one instruction for both lanes, the
-// same IEEE RN per lane), saving one instruction per element and modulus.
-__device__ __forceinline__ void resid_w2(const ElemDec& d0, const ElemDec& d1, const uint8_t* __restrict__ row_l,
-                                         const ModC& c, uint32_t& r0, uint32_t& r1) {
-    const int2 w0 = *reinterpret_cast<const int2*>(row_l + d0.off);
-    const int2 w1 = *reinterpret_cast<const int2*>(row_l + d1.off);
-    const int b0 = dp4a_us(d0.hi, w0.y, dp4a_us(d0.lo, w0.x, 0x4B400000));
-    const int b1 = dp4a_us(d1.hi, w1.y, dp4a_us(d1.lo, w1.x, 0x4B400000));
-    unsigned long long bb, u, t;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "r"(b0), "r"(b1));
-    const unsigned long long negm = 0xCB400000CB400000ull;  // (-M, -M)
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(u) : "l"(bb), "l"(negm));  // S (exact)
-    unsigned long long inv2, m2 = 0x4B4000004B400000ull;              // (M, M)
-    asm("mov.b64 %0, {%1, %1};" : "=l"(inv2) : "f"(c.inv_p));
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(t) : "l"(u), "l"(inv2), "l"(m2));  // M + round(S / p)
-    uint32_t t0, t1;
-    asm("mov.b64 {%0, %1}, %2;" : "=r"(t0), "=r"(t1) : "l"(t));
-    r0 = (uint32_t)b0 - t0 * c.p;
-    r1 = (uint32_t)b1 - t1 * c.p;
-}
-
 __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
     const uint32_t lo = __byte_perm(b0, b1, 0x0040);
     const uint32_t hi = __byte_perm(b2, b3, 0x0040);
@@ -187,11 +165,10 @@ __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, i
         for (int l = 0; l < nmod; ++l) {
             const ModC c = modc(hd, l);
             const uint8_t* rl = tab + (size_t)l * kResidRow;
-            uint32_t r[8];
-#pragma unroll
-            for (int j = 0; j < 8; j += 2) resid_w2(d[j], d[j + 1], rl, c, r[j], r[j + 1]);
-            const uint32_t w0 = pack4(r[0], r[1], r[2], r[3]);
-            const uint32_t w1 = pack4(r[4], r[5], r[6], r[7]);
+            const uint32_t w0 = pack4(resid_w(d[0], rl, c), resid_w(d[1], rl, c), resid_w(d[2], rl, c),
+                                      resid_w(d[3], rl, c));
+            const uint32_t w1 = pack4(resid_w(d[4], rl, c), resid_w(d[5], rl, c), resid_w(d[6], rl, c),
+                                      resid_w(d[7], rl, c));
             *reinterpret_cast<uint2*>(out + (int64_t)l * plane) = make_uint2(w0, w1);
         }
     }
@@ -199,7 +176,7 @@ __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, i
 }
 
 template <class T, bool COLSHIFT, int OP>
-__global__ void __launch_bounds__(256, 4) resid_rows_kernel(const T* __restrict__ X, int64_t ldx, int64_t rows_valid,
+__global__ void __launch_bounds__(256) resid_rows_kernel(const T* __restrict__ X, int64_t ldx, int64_t rows_valid,
                                                          int64_t rows_total, int64_t cols_valid, int64_t cols_out,
                                                          int64_t ld_out, const int32_t* __restrict__ shift,
                                                          const ResidHeader* __restrict__ rc_g, int nmod,
@@ -297,11 +274,10 @@ __global__ void __launch_bounds__(256, 4) resid_rows_kernel(const T* __restrict_
         for (int l = 0; l < nmod; ++l) {
             const ModC c = modc(hd, l);
             const uint8_t* rl = tab + (size_t)l * kResidRow;
-            uint32_t r[8];
-#pragma unroll
-            for (int j = 0; j < 8; j += 2) resid_w2(d[j], d[j + 1], rl, c, r[j], r[j + 1]);
-            const uint32_t w0 = pack4(r[0], r[1], r[2], r[3]);
-            const uint32_t w1 = pack4(r[4], r[5], r[6], r[7]);
+            const uint32_t w0 = pack4(resid_w(d[0], rl, c), resid_w(d[1], rl, c), resid_w(d[2], rl, c),
+                                      resid_w(d[3], rl, c));
+            const uint32_t w1 = pack4(resid_w(d[4], rl, c), resid_w(d[5], rl, c), resid_w(d[6], rl, c),
+                                      resid_w(d[7], rl, c));
             *reinterpret_cast<uint2*>(out + (int64_t)l * plane) = make_uint2(w0, w1);
         }
     }
