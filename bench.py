@@ -583,7 +583,8 @@ def main():
                    + f", N={args.moduli} moduli, phi={args.phi}", "m": m, "n": n, "k": k,
                    "moduli": args.moduli, "moduli_choice": auto_n or "fixed (--moduli)",
                    "phi": args.phi, "parallelism": f"2d-tile {R}x{Cc}",
-                   "l2": "inputs 2 GiB each > L2, no flush"},
+                   "l2": "inputs 2 GiB each > L2, no flush",
+                   "library_env": {kk: vv for kk, vv in os.environ.items() if kk.startswith("OZ2G_")} or "defaults"},
         "clocks": clocks_timed,
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
