@@ -354,13 +354,17 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     const bool inter_mats = inter && (inter->Aprime || inter->Bprime || inter->Cbar || inter->Dbar || inter->W ||
                                       inter->C1 || inter->C2 || inter->Q || inter->Cpp64 || inter->Cpp32 ||
                                       inter->Ares || inter->Bres || inter->Cprod || inter->bounds);
-    const bool pipe = host && !inter_mats && reduce_fn == nullptr && m >= 2048 && n >= 256;
+    // With a multi-rank reduce hook the uploads still overlap the scans and the
+    // clearance products, but the exponents (and everything after) wait for
+    // the all-reduced maxima: no per-chunk exponents, no speculation.
+    const bool pipe = host && !inter_mats && m >= 2048 && n >= 256;
+    const bool hooked = reduce_fn != nullptr;
     const int64_t chunk_rows = pipe ? round_up((m + kPipeChunks - 1) / kPipeChunks, 256) : m;
     const int nchunks = m > 0 ? (int)((m + chunk_rows - 1) / chunk_rows) : 1;
     // speculated exponents (blocking pipelined calls): 2 = rows and columns
     // (A row chunks and B column chunks uploaded alternately), 1 = columns
     // (asynchronous calls: rows + columns only; its statuses are merged on the device)
-    const int spec_mode = (pipe && !reuse_scaling && crt_overlap_blocks() <= 1)
+    const int spec_mode = (pipe && !hooked && !reuse_scaling && crt_overlap_blocks() <= 1)
                               ? speculation_mode(esz * (size_t)(m * k + k * n)) : 0;
     const bool spec2 = spec_mode == 2 && n >= 2 * 256;
     // spec2 column chunks: units of cu columns (a multiple of 128), chunks of two
@@ -944,7 +948,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
                 CUDA_TRY(launch_gemm(EPI_I32, tA, tB, g2)); ++launches;
             }
         });
-        if (pipe && rc > 0) {
+        if (pipe && !hooked && rc > 0) {
             tm.span(3, stream, [&] {
                 CUDA_TRY(launch_exponents(cmax_row + r0, rc, cmax_col, 0, mup + r0, nup, tab.shift0, tab.nthr,
                                           tab.thr, mu + r0, nu, ev + r0, fv, st, stream));
@@ -1021,7 +1025,8 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         // ---- K3: scaling exponents; K4: residue planes ----
         // (pipelined: row exponents and A residues were produced per chunk during the upload)
         tm.span(3, stream, [&] {
-            CUDA_TRY(launch_exponents(cmax_row, pipe ? 0 : m, cmax_col, n, mup, nup, tab.shift0, tab.nthr, tab.thr,
+            CUDA_TRY(launch_exponents(cmax_row, (pipe && !hooked) ? 0 : m, cmax_col, n, mup, nup, tab.shift0, tab.nthr,
+                                      tab.thr,
                                       mu, nu, ev, fv, st, stream));
         });
         ++launches;
@@ -1031,7 +1036,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             CUDA_TRY(cudaStreamWaitEvent(sB, ef, 0));
         }
         tm.span(4, stream, [&] {
-            if (!pipe) {
+            if (!pipe || hooked) {
                 CUDA_TRY(launch_resid_A(prec, dA, lda_d, m, k, kp, mu, rc_dev, N, ares, 0, st, stream));
                 launches += m > 0;
             }
