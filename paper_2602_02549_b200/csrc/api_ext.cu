@@ -27,7 +27,10 @@ int run_gemm_graph(int prec, int64_t m, int64_t n, int64_t k, const void* A, int
     CUDA_TRY(cudaGetDevice(&dev));
     Workspace& ws = workspace(dev, 0);
     std::lock_guard<std::recursive_mutex> dev_lock(ws.mtx);
-    if (!ws.pending.empty()) {
+    // OZ2G_ASYNC: the replay is followed by a copy of the call's status into
+    // its ring slot and joins the pending list (complete_pending checks it)
+    const bool async = (flags & OZ2G_ASYNC) != 0;
+    if (!async && !ws.pending.empty()) {
         Fail f{OZ2G_OK, ""};
         if (complete_pending(ws, f)) throw f;
     }
@@ -43,6 +46,10 @@ int run_gemm_graph(int prec, int64_t m, int64_t n, int64_t k, const void* A, int
             return run_gemm(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, stream, nullptr, diag, nullptr,
                             nullptr);
         }
+        if (!ws.pending.empty()) {  // (async key) earlier calls complete before the capture
+            Fail f{OZ2G_OK, ""};
+            if (complete_pending(ws, f)) throw f;
+        }
         oz2g_diag d;
         std::memset(&d, 0, sizeof d);
         if (!ws.s_cap) CUDA_TRY(cudaStreamCreateWithFlags(&ws.s_cap, cudaStreamNonBlocking));
@@ -55,7 +62,8 @@ int run_gemm_graph(int prec, int64_t m, int64_t n, int64_t k, const void* A, int
             g_capture = true;
             bool ok = true;
             try {
-                run_gemm(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, ws.s_cap, nullptr, &d, nullptr, nullptr);
+                run_gemm(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags & ~OZ2G_ASYNC, ws.s_cap, nullptr, &d,
+                         nullptr, nullptr);
             } catch (...) {
                 ok = false;
             }
@@ -82,6 +90,25 @@ int run_gemm_graph(int prec, int64_t m, int64_t n, int64_t k, const void* A, int
         e.launches = d.kernels_launched;
     }
     if (diag) std::memset(diag, 0, sizeof *diag);
+    if (async) {
+        if ((int)ws.pending.size() >= kStatusRing) {  // ring full: complete the oldest calls first
+            Fail f{OZ2G_OK, ""};
+            if (complete_pending(ws, f)) throw f;
+        }
+        if (!ws.pending.empty() && ws.last_async_stream != stream)
+            CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_last_async, 0));
+        const int slot = ws.ring_next;
+        ws.ring_next = (ws.ring_next + 1) % kStatusRing;
+        DevStatus* ring = (DevStatus*)ws.status_ring.get(sizeof(DevStatus) * kStatusRing);
+        CUDA_TRY(cudaGraphLaunch(e.exec, stream));
+        CUDA_TRY(cudaMemcpyAsync(ring + slot, ws.status.p, sizeof(DevStatus), cudaMemcpyDeviceToDevice, stream));
+        if (!ws.ev_last_async) CUDA_TRY(cudaEventCreateWithFlags(&ws.ev_last_async, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(ws.ev_last_async, stream));
+        ws.last_async_stream = stream;
+        ws.pending.push_back({slot, 0, 0, stream});
+        if (diag) diag->kernels_launched = e.launches;
+        return OZ2G_OK;
+    }
     CUDA_TRY(cudaGraphLaunch(e.exec, stream));
     CUDA_TRY(cudaStreamSynchronize(stream));
     if (diag) {
@@ -538,7 +565,8 @@ int oz2g_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t 
               void* C, int64_t ldc, int nmod, unsigned flags, void* stream, oz2g_intermediates* inter,
               oz2g_diag* diag, oz2g_reduce_maxima_fn reduce_fn, void* reduce_user) {
     return guarded([&] {
-        if (flags == OZ2G_DEVICE_PTRS && !inter && !reduce_fn && graph_enabled() && m > 0 && n > 0 && k > 0)
+        if ((flags & ~OZ2G_ASYNC) == OZ2G_DEVICE_PTRS && !inter && !reduce_fn && graph_enabled() && m > 0 && n > 0 &&
+            k > 0)
             return run_gemm_graph(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, (cudaStream_t)stream, diag);
         return run_gemm(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, (cudaStream_t)stream, inter, diag,
                         reduce_fn, reduce_user);

@@ -1,6 +1,8 @@
 """Per-call time of a small emulated DGEMM (default 1024^3, N = 14) through
 the Python API and through the C ABI directly (ctypes, prebuilt arguments):
-the difference is the Python wrapper's cost."""
+the difference is the Python wrapper's cost.  Blocking calls (host sync per
+call, wall clock) and asynchronous ones (device-timed back to back, like the
+native torch.matmul beside them)."""
 import ctypes as C
 import json
 import os
@@ -44,7 +46,28 @@ def main():
     for _ in range(reps):
         L.oz2g_gemm(*args)
     out["c_abi_us"] = (time.perf_counter() - t0) / reps * 1e6
+    # asynchronous calls (OZ2G_ASYNC: graph replays, no per-call host sync),
+    # timed on the device like torch.matmul
+    def dev_us(fn):
+        for _ in range(5):
+            fn()
+        oz.synchronize()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        oz.synchronize()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps * 1e3
+    out["python_async_us"] = dev_us(lambda: oz.os_ii(A, B, N, out=Cout, blocking=False))
+    aargs = args[:11] + (_lib.OZ2G_DEVICE_PTRS | _lib.OZ2G_ASYNC,) + args[12:]
+    out["c_abi_async_us"] = dev_us(lambda: L.oz2g_gemm(*aargs))
+    out["native_us"] = dev_us(lambda: torch.matmul(A, B, out=Cout))
     flops = 2.0 * m * m * m
+    for key in ("python_async", "c_abi_async", "native"):
+        out[key + "_tflops"] = flops / out[key + "_us"] / 1e6
     out["python_tflops"] = flops / out["python_us"] / 1e6
     out["c_abi_tflops"] = flops / out["c_abi_us"] / 1e6
     print(json.dumps(out))

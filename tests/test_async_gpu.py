@@ -70,3 +70,40 @@ def test_async_rejects_intermediates(cuda):
     for kw in ({"keep_intermediates": True}, {"bounds": True}, {"timing": True}, {"devices": [0]}):
         with pytest.raises(oz.InvalidArgument):
             oz.os_ii(A, A, 8, blocking=False, **kw)
+
+
+def test_async_device_graph_replays(cuda, oracle):
+    """Asynchronous device-pointer calls replay the captured graph too (plain,
+    capture, replays); each replay's status lands in its own ring slot, so
+    a failing replay among good ones is reported at synchronize() in order,
+    and contents changed between enqueued calls are read by each call."""
+    import torch
+    m, k, n = 256, 300, 180
+    A1 = oracle.gen_matrix(m, k, 1.0, 981)
+    A2 = oracle.gen_matrix(m, k, 2.0, 982)
+    B = oracle.gen_matrix(k, n, 1.0, 983)
+    bad = A1.copy()
+    bad[9, :] = 0.0
+    r1, r2 = oracle.os_ii(A1, B, 14).C, oracle.os_ii(A2, B, 14).C
+    dA, dB = torch.empty((m, k), dtype=torch.float64, device="cuda"), torch.from_numpy(B).cuda()
+    out = torch.empty((m, n), dtype=torch.float64, device="cuda")
+    seq = [A1, A2, A1, A2, A1, bad, A2, A1]
+    res = []
+    for x in seq:  # same addresses every call: call 1 plain, 2 captures, 3+ replay
+        dA.copy_(torch.from_numpy(x))
+        oz.os_ii(dA, dB, 14, out=out, blocking=False)
+        res.append(out.clone())  # stream-ordered after the call
+    with pytest.raises(oz.DomainError, match="zero row 9"):
+        oz.synchronize()
+    torch.cuda.synchronize()
+    for i, (x, c) in enumerate(zip(seq, res)):
+        if x is bad:
+            continue
+        ref = r1 if x is A1 else r2
+        assert np.array_equal(c.cpu().numpy().view(np.uint64), ref.view(np.uint64)), i
+    # many replays: the status ring wraps (completes the oldest calls itself)
+    dA.copy_(torch.from_numpy(A2))
+    for _ in range(150):
+        oz.os_ii(dA, dB, 14, out=out, blocking=False)
+    oz.synchronize()
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), r2.view(np.uint64))
