@@ -315,6 +315,15 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     if (k > OZ2G_MAX_INNER_DIM) throw Fail{OZ2G_DOMAIN_ERROR, "os_ii: k exceeds 2^17"};
     const Table& tab = table_for(nmod, prec);  // std::domain_error for N outside [2, 49]
     if (diag) std::memset(diag, 0, sizeof *diag);
+    // programmatic dependent launches for small problems only: at 1024^3 they
+    // hide kernel ramps (77.7 -> 76.0 us per call); from 3072^3 up the
+    // early-scheduled CTAs waiting beside the running kernels cost more than
+    // that (8192^3: 8.38 -> 9.6 ms with the GEMM's trigger at its start)
+    struct PdlScope {
+        bool prev;
+        explicit PdlScope(bool on) : prev(g_pdl_call) { g_pdl_call = on; }
+        ~PdlScope() { g_pdl_call = prev; }
+    } pdl_scope((double)m * (double)n * (double)k <= kPdlMaxWork);
     // k == 0: every row of A (and column of B) is zero (scaling.hpp:180/192)
     if (k == 0) {
         if (m > 0) throw Fail{OZ2G_DOMAIN_ERROR, "row_pre_exponents: zero row 0"};

@@ -190,6 +190,7 @@ extern std::mutex g_ws_mtx;
 extern std::map<int, Workspace*> g_ws;  // key device * 256 + slot
 
 constexpr int kStatusRing = 64;
+constexpr double kPdlMaxWork = 2048.0 * 2048.0 * 2048.0;  // m n k up to which run_gemm uses PDL
 // Row block of the residue GEMMs + CRT: one raster group (16 x 128 rows), so
 // W (N int8 planes) is held for one block only.
 constexpr int64_t kWBlockRows = 2048;

@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
                                                   const int32_t* __restrict__ mu, const int32_t* __restrict__ nu,
                                                   T* __restrict__ C, int64_t ldc, const CrtExtra ex,
                                                   DevStatus* st) {
+    pdl_enter();
     const int64_t qn = (n + CV - 1) / CV;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = t < m * qn;
@@ -226,15 +227,16 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
 }
 
 template <class T, bool DD, int NFP, bool INTER, int CV>
-void launch_n(cudaStream_t s, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
-              const CrtConsts& cc, const int32_t* mu, const int32_t* nu, T* C, int64_t ldc, const CrtExtra& ex,
-              DevStatus* st) {
+cudaError_t launch_n(cudaStream_t s, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
+                     const CrtConsts& cc, const int32_t* mu, const int32_t* nu, T* C, int64_t ldc, const CrtExtra& ex,
+                     DevStatus* st) {
     const int64_t work = m * ((n + CV - 1) / CV);
     const unsigned grid = (unsigned)((work + 255) / 256);
     if (ex.bnd.on)
-        crt_kernel<T, DD, true, NFP, INTER, CV><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
-    else
-        crt_kernel<T, DD, false, NFP, INTER, CV><<<grid, 256, 0, s>>>(W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+        return launch_pdl(crt_kernel<T, DD, true, NFP, INTER, CV>, dim3(grid), dim3(256), 0, s, W, ldw, wplane, m, n,
+                          cc, mu, nu, C, ldc, ex, st);
+    return launch_pdl(crt_kernel<T, DD, false, NFP, INTER, CV>, dim3(grid), dim3(256), 0, s, W, ldw, wplane, m, n, cc,
+                      mu, nu, C, ldc, ex, st);
 }
 
 int crt_cv() {
@@ -249,19 +251,18 @@ int crt_cv() {
 // per byte; measured best of {0, 3, 5, 8} at 16384^2, N = 16), 6 of 8 with the
 // single chain of fp32 mode (one DFMA per byte); half of that with 4 columns.
 template <class T, bool DD>
-void launch_t(cudaStream_t s, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
-              const CrtConsts& cc, const int32_t* mu, const int32_t* nu, T* C, int64_t ldc, const CrtExtra& ex,
-              DevStatus* st) {
+cudaError_t launch_t(cudaStream_t s, const int8_t* W, int64_t ldw, int64_t wplane, int64_t m, int64_t n,
+                     const CrtConsts& cc, const int32_t* mu, const int32_t* nu, T* C, int64_t ldc, const CrtExtra& ex,
+                     DevStatus* st) {
     const bool inter = ex.C1 || ex.C2 || ex.Q || ex.Cpp64 || ex.Cpp32;
     if (crt_cv() == 4) {
         constexpr int NFP = DD ? 2 : 3;
-        if (inter) launch_n<T, DD, NFP, true, 4>(s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
-        else launch_n<T, DD, NFP, false, 4>(s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
-    } else {
-        constexpr int NFP = DD ? 3 : 6;
-        if (inter) launch_n<T, DD, NFP, true, 8>(s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
-        else launch_n<T, DD, NFP, false, 8>(s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+        if (inter) return launch_n<T, DD, NFP, true, 4>(s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+        return launch_n<T, DD, NFP, false, 4>(s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
     }
+    constexpr int NFP = DD ? 3 : 6;
+    if (inter) return launch_n<T, DD, NFP, true, 8>(s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
+    return launch_n<T, DD, NFP, false, 8>(s, W, ldw, wplane, m, n, cc, mu, nu, C, ldc, ex, st);
 }
 
 }  // namespace
@@ -271,12 +272,10 @@ cudaError_t launch_crt(int prec, const int8_t* W, int64_t ldw, int64_t wplane, i
                        const CrtExtra& extra, DevStatus* st, cudaStream_t s) {
     if (m * n == 0) return cudaSuccess;
     if (prec) {
-        if (cc.mode == 1) launch_t<double, true>(s, W, ldw, wplane, m, n, cc, mu, nu, (double*)C, ldc, extra, st);
-        else launch_t<double, false>(s, W, ldw, wplane, m, n, cc, mu, nu, (double*)C, ldc, extra, st);
-    } else {
-        launch_t<float, false>(s, W, ldw, wplane, m, n, cc, mu, nu, (float*)C, ldc, extra, st);
+        if (cc.mode == 1) return launch_t<double, true>(s, W, ldw, wplane, m, n, cc, mu, nu, (double*)C, ldc, extra, st);
+        return launch_t<double, false>(s, W, ldw, wplane, m, n, cc, mu, nu, (double*)C, ldc, extra, st);
     }
-    return cudaGetLastError();
+    return launch_t<float, false>(s, W, ldw, wplane, m, n, cc, mu, nu, (float*)C, ldc, extra, st);
 }
 
 }  // namespace oz2g

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -216,6 +217,50 @@ __device__ __forceinline__ void step_fence_wait(const unsigned long long* counte
         if (v >= need || clock64() - t0 > (1ll << 26)) break;
         __nanosleep(64);
     }
+}
+
+// ----------------------------------------------------------------------------
+// Programmatic dependent launch.  A kernel launched by launch_pdl may be
+// scheduled while its predecessor in the stream is still running: it calls
+// pdl_wait() before touching global memory (the predecessor's results become
+// visible there — and every earlier kernel's, since the predecessor waited
+// too) and pdl_trigger() to let its own successor be scheduled into the SMs
+// its tail leaves idle.  Without the launch attribute both are no-ops.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_enter() {
+    pdl_wait();
+    pdl_trigger();
+}
+
+// Set by run_gemm for the calls PDL pays on (small problems, where kernel
+// ramps are a visible share of the call); OZ2G_PDL=0 never, =2 always.
+inline thread_local bool g_pdl_call = false;
+inline bool pdl_enabled() {
+    static const int mode = [] {
+        const char* e = std::getenv("OZ2G_PDL");
+        return e ? std::atoi(e) : 1;
+    }();
+    return mode == 2 || (mode == 1 && g_pdl_call);
+}
+
+// kernel<<<grid, block, smem, s>>>(args...) with programmatic stream
+// serialisation; the kernel must begin with pdl_wait() (pdl_enter()).
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 // ----------------------------------------------------------------------------

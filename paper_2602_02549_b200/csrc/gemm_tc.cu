@@ -176,6 +176,7 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();  // the set-up above overlaps the previous kernel's tail
 
     const int total = P.planes * P.tiles_m * P.tiles_n;
 
@@ -208,6 +209,9 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
             const unsigned long long steps = (unsigned long long)((total + (int)gridDim.x - 1) / (int)gridDim.x);
             if (j < steps) atomicAdd(P.fence, steps - j);
         }
+        // the next kernel may be scheduled once every CTA has issued its last
+        // loads (earlier, its waiting CTAs would sit beside the whole GEMM)
+        if (lane == 0) pdl_trigger();
     } else if (warp == 1) {
         // ===== MMA issuer =====
         int stage = 0;
@@ -650,8 +654,7 @@ cudaError_t launch_tc(int mode, const CUtensorMap& tmA, const CUtensorMap& tmB, 
         if (err != cudaSuccess) return err;
         configured[dev][mi] = 1;
     }
-    kern<<<grid, tc_threads(EW), SMEM_BYTES, stream>>>(tmA, tmB, P);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3(grid), dim3(tc_threads(EW)), SMEM_BYTES, stream, tmA, tmB, P);
 }
 
 cudaError_t launch_gemm_i8(int mode, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& P,

@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, i
                                                       int64_t kp, const int32_t* __restrict__ mu,
                                                       const ResidHeader* __restrict__ rc_g, int nmod,
                                                       int8_t* __restrict__ planes, int64_t plane, DevStatus* st) {
+    pdl_enter();
     extern __shared__ __align__(16) uint8_t sh[];
     load_resid_consts(rc_g, nmod, sh);
     __syncthreads();
@@ -182,6 +183,7 @@ __global__ void __launch_bounds__(256) resid_rows_kernel(const T* __restrict__ X
                                                          const ResidHeader* __restrict__ rc_g, int nmod,
                                                          int8_t* __restrict__ planes, int64_t plane, uint32_t err_bit,
                                                          DevStatus* st) {
+    pdl_enter();
     extern __shared__ __align__(16) uint8_t sh[];
     if (OP == 1) {
         load_resid_consts(rc_g, nmod, sh);
@@ -318,10 +320,8 @@ cudaError_t launch_rows(const void* X, int64_t ldx, int64_t rows_valid, int64_t 
     dim3 grid;
     cudaError_t err = rows_grid(resid_rows_kernel<T, COLSHIFT, OP>, sm, rows_total, chunks, grid);
     if (err != cudaSuccess) return err;
-    resid_rows_kernel<T, COLSHIFT, OP><<<grid, 256, sm, s>>>((const T*)X, ldx, rows_valid, rows_total, cols_valid,
-                                                            cols_out, ld_out, shift, rc, nmod, planes, plane,
-                                                            err_bit, st);
-    return cudaGetLastError();
+    return launch_pdl(resid_rows_kernel<T, COLSHIFT, OP>, grid, dim3(256), sm, s, (const T*)X, ldx, rows_valid,
+                      rows_total, cols_valid, cols_out, ld_out, shift, rc, nmod, planes, plane, err_bit, st);
 }
 
 }  // namespace
@@ -359,12 +359,12 @@ cudaError_t launch_resid_A(int prec, const void* A, int64_t lda, int64_t m, int6
     cudaError_t err;
     if (prec) {
         if ((err = rows_grid(resid_A_kernel<double>, sm, m, chunks, grid)) != cudaSuccess) return err;
-        resid_A_kernel<double><<<grid, 256, sm, s>>>((const double*)A, lda, m, k, kp, mu, rc_dev, nmod, planes, plane, st);
-    } else {
-        if ((err = rows_grid(resid_A_kernel<float>, sm, m, chunks, grid)) != cudaSuccess) return err;
-        resid_A_kernel<float><<<grid, 256, sm, s>>>((const float*)A, lda, m, k, kp, mu, rc_dev, nmod, planes, plane, st);
+        return launch_pdl(resid_A_kernel<double>, grid, dim3(256), sm, s, (const double*)A, lda, m, k, kp, mu, rc_dev,
+                          nmod, planes, plane, st);
     }
-    return cudaGetLastError();
+    if ((err = rows_grid(resid_A_kernel<float>, sm, m, chunks, grid)) != cudaSuccess) return err;
+    return launch_pdl(resid_A_kernel<float>, grid, dim3(256), sm, s, (const float*)A, lda, m, k, kp, mu, rc_dev, nmod,
+                      planes, plane, st);
 }
 
 }  // namespace oz2g

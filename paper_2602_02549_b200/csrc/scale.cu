@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(1024) row_scan_A_kernel(const T* __restrict__ 
                                                          int64_t kp, int32_t* __restrict__ mu_prime,
                                                          int8_t* __restrict__ abar, DevStatus* st,
                                                          int64_t row0) {
+    pdl_enter();
     const int64_t i = blockIdx.x;  // row within this launch; row0 + i in the whole matrix
     const T* row = A + i * lda;
     const bool vec = (reinterpret_cast<uintptr_t>(row) & 15) == 0;
@@ -158,6 +159,7 @@ __global__ void __launch_bounds__(512) row_scan_A_reg_kernel(const T* __restrict
                                                              int64_t kp, int32_t* __restrict__ mu_prime,
                                                              int8_t* __restrict__ abar, DevStatus* st,
                                                              int64_t row0) {
+    pdl_enter();
     const int64_t i = blockIdx.x;
     const T* row = A + i * lda;
     const bool vec = (reinterpret_cast<uintptr_t>(row) & 15) == 0;
@@ -198,6 +200,7 @@ template <class T>
 __global__ void __launch_bounds__(256) col_max_B_kernel(const T* __restrict__ B, int64_t ldb, int64_t k,
                                                         int64_t n, int rows, unsigned long long* __restrict__ bmax,
                                                         DevStatus* st) {
+    pdl_enter();
     const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
     if (j >= n) return;
     const int64_t h0 = (int64_t)blockIdx.y * rows;
@@ -217,6 +220,7 @@ __global__ void __launch_bounds__(256) col_max_B_kernel(const T* __restrict__ B,
 
 __global__ void col_exp_B_kernel(const unsigned long long* __restrict__ bmax, int64_t n,
                                  int32_t* __restrict__ nu_prime, DevStatus* st, int64_t col0) {
+    pdl_enter();
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     const unsigned long long b = bmax[j];
@@ -249,6 +253,7 @@ __global__ void exponents_kernel(const int32_t* __restrict__ cmax_row, int64_t m
                                  const ThrTable tt, int32_t* __restrict__ mu, int32_t* __restrict__ nu,
                                  float* __restrict__ e, float* __restrict__ f, DevStatus* st,
                                  const ChangeFlags cf) {
+    pdl_enter();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= m + n) return;
     const bool is_row = t < m;
@@ -367,6 +372,7 @@ __global__ void __launch_bounds__(256) floor_rows_B_kernel(const T* __restrict__
 // and zero the maxima the scans and the clearance GEMM accumulate into.
 __global__ void init_call_kernel(DevStatus* st, unsigned long long* bmax, int64_t nb, int32_t* rmax, int64_t nr,
                                  int32_t* cmax, int64_t nc) {
+    pdl_enter();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t == 0) {
         st->err = 0;
@@ -394,8 +400,11 @@ cudaError_t launch_row_scan_A(int prec, const void* A, int64_t lda, int64_t m, i
     const int64_t want = (k + kRowVPT - 1) / kRowVPT;
     if (want <= 512) {
         const unsigned threads = (unsigned)(want <= 32 ? 32 : (want + 31) / 32 * 32);
-        if (prec) row_scan_A_reg_kernel<double><<<(unsigned)m, threads, 0, s>>>((const double*)A, lda, k, kp, mu_prime, abar, st, row0);
-        else row_scan_A_reg_kernel<float><<<(unsigned)m, threads, 0, s>>>((const float*)A, lda, k, kp, mu_prime, abar, st, row0);
+        if (prec)
+            return launch_pdl(row_scan_A_reg_kernel<double>, dim3((unsigned)m), dim3(threads), 0, s, (const double*)A, lda,
+                              k, kp, mu_prime, abar, st, row0);
+        return launch_pdl(row_scan_A_reg_kernel<float>, dim3((unsigned)m), dim3(threads), 0, s, (const float*)A, lda, k,
+                          kp, mu_prime, abar, st, row0);
     } else {
         // rows over 256 KB (k = 65536 fp64): two rows per SM in flight would
         // outgrow L2 and the second pass would re-read HBM, so an unused
@@ -411,14 +420,14 @@ cudaError_t launch_row_scan_A(int prec, const void* A, int64_t lda, int64_t m, i
                 if ((err = cudaFuncSetAttribute(row_scan_A_kernel<double, 4>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pin)) != cudaSuccess)
                     return err;
-                row_scan_A_kernel<double, 4><<<(unsigned)m, 1024, pin, s>>>((const double*)A, lda, k, kp, mu_prime,
-                                                                           abar, st, row0);
+                return launch_pdl(row_scan_A_kernel<double, 4>, dim3((unsigned)m), dim3(1024), pin, s, (const double*)A,
+                                  lda, k, kp, mu_prime, abar, st, row0);
             } else {
                 if ((err = cudaFuncSetAttribute(row_scan_A_kernel<float, 4>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pin)) != cudaSuccess)
                     return err;
-                row_scan_A_kernel<float, 4><<<(unsigned)m, 1024, pin, s>>>((const float*)A, lda, k, kp, mu_prime,
-                                                                          abar, st, row0);
+                return launch_pdl(row_scan_A_kernel<float, 4>, dim3((unsigned)m), dim3(1024), pin, s, (const float*)A,
+                                  lda, k, kp, mu_prime, abar, st, row0);
             }
         } else {
             // 512 threads (4 rows per SM in flight) up to 128 KB rows, 1024 (2
@@ -432,11 +441,10 @@ cudaError_t launch_row_scan_A(int prec, const void* A, int64_t lda, int64_t m, i
             }();
             const unsigned thr = thr_env ? (unsigned)thr_env : row_bytes <= (128u << 10) ? 512u : 1024u;
             if (prec)
-                row_scan_A_kernel<double, 1><<<(unsigned)m, thr, 0, s>>>((const double*)A, lda, k, kp, mu_prime, abar,
-                                                                        st, row0);
-            else
-                row_scan_A_kernel<float, 1><<<(unsigned)m, thr, 0, s>>>((const float*)A, lda, k, kp, mu_prime, abar,
-                                                                       st, row0);
+                return launch_pdl(row_scan_A_kernel<double, 1>, dim3((unsigned)m), dim3(thr), 0, s, (const double*)A,
+                                  lda, k, kp, mu_prime, abar, st, row0);
+            return launch_pdl(row_scan_A_kernel<float, 1>, dim3((unsigned)m), dim3(thr), 0, s, (const float*)A, lda,
+                              k, kp, mu_prime, abar, st, row0);
         }
     }
     return cudaGetLastError();
@@ -450,16 +458,14 @@ cudaError_t launch_col_max_B(int prec, const void* B, int64_t ldb, int64_t k, in
     int rows = 64;
     while (rows > 8 && cols * blocks_for(k, rows) < 16 * current_sm_count()) rows /= 2;
     dim3 grid((unsigned)cols, blocks_for(k, rows));
-    if (prec) col_max_B_kernel<double><<<grid, 256, 0, s>>>((const double*)B, ldb, k, n, rows, bmax, st);
-    else col_max_B_kernel<float><<<grid, 256, 0, s>>>((const float*)B, ldb, k, n, rows, bmax, st);
-    return cudaGetLastError();
+    if (prec) return launch_pdl(col_max_B_kernel<double>, grid, dim3(256), 0, s, (const double*)B, ldb, k, n, rows, bmax, st);
+    return launch_pdl(col_max_B_kernel<float>, grid, dim3(256), 0, s, (const float*)B, ldb, k, n, rows, bmax, st);
 }
 
 cudaError_t launch_col_exp_B(const unsigned long long* bmax, int64_t n, int32_t* nu_prime, DevStatus* st,
                              cudaStream_t s, int64_t col0) {
     if (n == 0) return cudaSuccess;
-    col_exp_B_kernel<<<blocks_for(n, 256), 256, 0, s>>>(bmax, n, nu_prime, st, col0);
-    return cudaGetLastError();
+    return launch_pdl(col_exp_B_kernel, dim3(blocks_for(n, 256)), dim3(256), 0, s, bmax, n, nu_prime, st, col0);
 }
 
 cudaError_t launch_exponents(const int32_t* cmax_row, int64_t m, const int32_t* cmax_col, int64_t n,
@@ -471,10 +477,8 @@ cudaError_t launch_exponents(const int32_t* cmax_row, int64_t m, const int32_t* 
     tt.shift0 = shift0;
     tt.nthr = nthr;
     for (int q = 0; q < 64; ++q) tt.thr[q] = q < nthr ? thr[q] : 0;
-    exponents_kernel<<<blocks_for(m + n, 256), 256, 0, s>>>(cmax_row, m, cmax_col, n, mu_prime, nu_prime, tt, mu,
-                                                            nu, e, f, st,
-                                                            changed ? *changed : ChangeFlags{nullptr, 0, 0, 0});
-    return cudaGetLastError();
+    return launch_pdl(exponents_kernel, dim3(blocks_for(m + n, 256)), dim3(256), 0, s, cmax_row, m, cmax_col, n,
+                      mu_prime, nu_prime, tt, mu, nu, e, f, st, changed ? *changed : ChangeFlags{nullptr, 0, 0, 0});
 }
 
 cudaError_t launch_trunc_scaled(int prec, const void* X, int64_t ldx, int64_t rows, int64_t cols,
@@ -522,9 +526,8 @@ cudaError_t launch_init_call(DevStatus* st, unsigned long long* bmax, int64_t nb
                              int32_t* cmax, int64_t nc, cudaStream_t s) {
     const int64_t most = nb > nr ? (nb > nc ? nb : nc) : (nr > nc ? nr : nc);
     const int64_t blocks = (most + 255) / 256;
-    init_call_kernel<<<(unsigned)(blocks < 1 ? 1 : (blocks > 1184 ? 1184 : blocks)), 256, 0, s>>>(st, bmax, nb, rmax, nr,
-                                                                                                cmax, nc);
-    return cudaGetLastError();
+    return launch_pdl(init_call_kernel, dim3((unsigned)(blocks < 1 ? 1 : (blocks > 1184 ? 1184 : blocks))), dim3(256), 0,
+                      s, st, bmax, nb, rmax, nr, cmax, nc);
 }
 
 }  // namespace oz2g
