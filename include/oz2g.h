@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define OZ2G_API_VERSION 3
+#define OZ2G_API_VERSION 4
 
 /* Status codes (return value of every entry point). */
 #define OZ2G_OK 0
@@ -265,6 +265,20 @@ int oz2g_native_gemm(int prec, int64_t m, int64_t n, int64_t k, const void *A, i
  * planes).  *ms_out = device time of all launches (CUDA events), *ops_out =
  * int8 operations (2 per multiply-add) they performed. */
 int oz2g_i8_peak(long long iters, int launches, int random, double *ms_out, double *ops_out);
+
+/* Tuning options for this process (every default is
+ * the measured best).  Names: "gemm" (0 single-CTA tiles, 1 CTA pair, 2
+ * multicast cluster), "fused", "fused_mc", "fused_fence", "spec" (-1 by size,
+ * 0, 1, 2), "graph", "pdl" (0, 1 small calls, 2), "group_m", "group_n",
+ * "l2hint", "crt_overlap", "crt_cv" (4 | 8), "wblock_min_mb", "gemm_fence",
+ * "epi_warps" (0 | 4 | 8), "pair_stages" (4..6), "rowscan_threads" (0 | 256 |
+ * 512 | 1024).  Unset options take OZ2G_<NAME> from the environment at first
+ * use.  A set applies from the next call (captured graphs are re-captured).
+ * Unknown names and out-of-range values: OZ2G_INVALID_ARGUMENT.
+ * oz2g_option_name(i) lists the names (NULL past the last). */
+int oz2g_set_option(const char *name, long long value);
+int oz2g_get_option(const char *name, long long *value);
+const char *oz2g_option_name(int index);
 
 /*
  * One emulated GEMM across P processes (one GPU each) with NCCL driven by the

@@ -62,7 +62,7 @@ EXPORTED = ("oz2g_gemm", "oz2g_dgemm", "oz2g_sgemm", "oz2g_last_error", "oz2g_ta
             "oz2g_native_gemm", "oz2g_gemm_multi", "oz2g_grid_shape", "oz2g_init", "oz2g_synchronize",
             "oz2g_gemm_sweep", "oz2g_suggest_n_tight", "oz2g_i8_peak", "oz2g_comm_available", "oz2g_comm_unique_id",
             "oz2g_comm_init", "oz2g_comm_grid", "oz2g_comm_destroy", "oz2g_comm_last_error", "oz2g_dist_layout",
-            "oz2g_gemm_dist")
+            "oz2g_gemm_dist", "oz2g_set_option", "oz2g_get_option", "oz2g_option_name")
 
 _LIB = None
 
@@ -94,6 +94,10 @@ def load() -> C.CDLL:
     L.oz2g_suggest_n_tight.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
                                        C.c_int64, C.c_double, C.c_int, C.c_uint, C.c_void_p, C.POINTER(Suggest)]
     L.oz2g_i8_peak.argtypes = [C.c_longlong, C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.oz2g_set_option.argtypes = [C.c_char_p, C.c_longlong]
+    L.oz2g_get_option.argtypes = [C.c_char_p, C.POINTER(C.c_longlong)]
+    L.oz2g_option_name.argtypes = [C.c_int]
+    L.oz2g_option_name.restype = C.c_char_p
     L.oz2g_comm_unique_id.argtypes = [C.c_void_p]
     L.oz2g_comm_init.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
     L.oz2g_comm_grid.argtypes = [C.c_void_p] + [C.POINTER(C.c_int)] * 4

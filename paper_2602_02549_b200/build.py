@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "liboz2g.so")
 SOURCES = ["api.cu", "api_ext.cu", "gemm_tc.cu", "scale.cu", "resid.cu", "crt.cu", "bounds.cu", "tables.cpp", "harness.cpp",
-           "comm.cpp", "fused.cu"]
+           "comm.cpp", "fused.cu", "options.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",

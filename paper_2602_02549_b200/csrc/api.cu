@@ -125,82 +125,54 @@ Workspace& workspace(int dev, int slot) {
 }
 
 
-// GEMM variant (OZ2G_GEMM): 0 single-CTA 128x256 tiles (default), 1 "pair"
-// CTA-pair cta_group::2 256x256 tiles, 2 "mcast" 2-CTA clusters sharing a
-// multicast B tile.
-int gemm_variant() {
-    static const int v = [] {
-        const char* s = std::getenv("OZ2G_GEMM");
-        if (s && std::strcmp(s, "pair") == 0) return 1;
-        if (s && std::strcmp(s, "mcast") == 0) return 2;
-        return 0;
-    }();
-    return v;
-}
+// GEMM variant (option "gemm"): 0 single-CTA 128x256 tiles (default), 1
+// "pair" CTA-pair cta_group::2 256x256 tiles, 2 "mcast" 2-CTA clusters sharing
+// a multicast B tile.
+int gemm_variant() { return (int)opt(OPT_GEMM); }
 
 // TMA L2 policies (CUTLASS CacheHintSm90 encodings).  Default EVICT_NORMAL for
 // both operands: measured at 16384^3, EVICT_LAST on A / EVICT_FIRST on B doubled
 // the residue GEMM's DRAM reads (81 -> 156 GB: B tiles are shared by the CTAs of
 // a wave and were evicted before reuse).  OZ2G_L2HINT=1 re-enables for study.
-// TMA L2 eviction hints of the GEMM operand loads (OZ2G_L2HINT):
+// TMA L2 eviction hints of the GEMM operand loads (option "l2hint"):
 //   0 normal/normal (default), 1 A last / B first, 2 A last / B normal,
 //   3 A normal / B first
 void set_l2_hints(GemmParams& g) {
-    static const int mode = [] {
-        const char* s = std::getenv("OZ2G_L2HINT");
-        return s ? std::atoi(s) : 0;
-    }();
+    const int mode = (int)opt(OPT_L2HINT);
     constexpr uint64_t kNormal = 0x1000000000000000ull, kLast = 0x14F0000000000000ull,
                        kFirst = 0x12F0000000000000ull;
     g.hintA = (mode == 1 || mode == 2) ? kLast : kNormal;
     g.hintB = (mode == 1 || mode == 3) ? kFirst : kNormal;
 }
 
-// OZ2G_CRT_OVERLAP = B > 0: the residue GEMMs + CRT of a large call run in B
-// row blocks and each block's CRT runs on a side stream while the next
+// Option "crt_overlap" = B > 1: the residue GEMMs + CRT of a large call run in
+// B row blocks and each block's CRT runs on a side stream while the next
 // block's GEMM computes (the CRT CTAs fit beside the persistent GEMM CTAs).
-int crt_overlap_blocks() {
-    static const int v = [] {
-        const char* s = std::getenv("OZ2G_CRT_OVERLAP");
-        return s ? std::atoi(s) : 0;
-    }();
-    return v;
-}
+int crt_overlap_blocks() { return (int)opt(OPT_CRT_OVERLAP); }
 
 // Residue GEMMs + CRT fused in one kernel (fused.cu) instead of the int8-W
-// GEMM epilogue followed by the CRT pass: OZ2G_FUSED=1 on, 0 off.  Read per call.
-int fused_mode() {
-    const char* s = std::getenv("OZ2G_FUSED");
-    return s ? std::atoi(s) : 0;
-}
+// GEMM epilogue followed by the CRT pass: option "fused" 1 on, 0 off.
+int fused_mode() { return (int)opt(OPT_FUSED); }
 
-// Speculated exponents on the pipelined host path (run_gemm): OZ2G_SPEC=0
-// off, 1 column exponents only (B uploaded first), 2 row and column exponents
-// (A row chunks interleaved with B column chunks).  Unset: 2 for inputs of at
-// least 3 GiB, 1 below (measured: row + column speculation wins at 16384^3,
-// 4 GiB, by 4-6%; below that its per-arrival overhead outweighs the earlier
-// start, e.g. 3.8 vs 3.0 ms for SGEMM 4096^3, 41.7 vs 39.9 ms at 2048 x 65536 x
-// 2048).  Read per call.
+// Speculated exponents on the pipelined host path (run_gemm): option "spec"
+// 0 off, 1 column exponents only (B uploaded first), 2 row and column
+// exponents (A row chunks interleaved with B column chunks).  Default (-1): 2
+// for inputs of at least 3 GiB, 1 below (measured: row + column speculation
+// wins at 16384^3, 4 GiB, by 4-6%; below that its per-arrival overhead
+// outweighs the earlier start, e.g. 3.8 vs 3.0 ms for SGEMM 4096^3, 41.7 vs
+// 39.9 ms at 2048 x 65536 x 2048).
 int speculation_mode(size_t input_bytes) {
-    const char* s = std::getenv("OZ2G_SPEC");
-    if (s && s[0] == '0') return 0;
-    if (s && s[0] == '1') return 1;
-    if (s && s[0] == '2') return 2;
+    const long long v = opt(OPT_SPEC);
+    if (v >= 0) return (int)v;
     return input_bytes >= (size_t(3) << 30) ? 2 : 1;
 }
 
 // Raster group height: one wave of persistent CTAs covers group_m tile-rows,
 // so B tiles are streamed from HBM about tiles_m / group_m times per plane.
-// OZ2G_GROUP_N > 0 groups tile-columns instead (returned negated).
+// Option "group_n" > 0 groups tile-columns instead (returned negated).
 int group_m_for(int tiles_m, int tiles_n) {
-    static const int env = [] {
-        const char* s = std::getenv("OZ2G_GROUP_M");
-        return s ? std::atoi(s) : 0;
-    }();
-    static const int env_n = [] {
-        const char* s = std::getenv("OZ2G_GROUP_N");
-        return s ? std::atoi(s) : 0;
-    }();
+    const int env = (int)opt(OPT_GROUP_M);
+    const int env_n = (int)opt(OPT_GROUP_N);
     if (env_n > 0) return -(env_n < tiles_n ? env_n : (tiles_n > 0 ? tiles_n : 1));
     int g = env > 0 ? env : 16;  // best of {8, 12, 16, 24, 32} at 16384^3 (interleaved A/B)
     return g < tiles_m ? g : (tiles_m > 0 ? tiles_m : 1);
@@ -575,10 +547,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     // matrix is wanted (intermediates) or blocks overlap (side-stream CRT).
     // W per block only when the whole-matrix W would be large (more launches
     // cost more than the memory saves on mid-size problems)
-    static const int64_t w_block_min = [] {
-        const char* e = std::getenv("OZ2G_WBLOCK_MIN_MB");
-        return (int64_t)(e ? std::atoll(e) : 2048) << 20;
-    }();
+    const int64_t w_block_min = (int64_t)opt(OPT_WBLOCK_MIN_MB) << 20;
     const bool w_full = (inter && inter->W) || overlap || (int64_t)N * m * ldw < w_block_min;
     const int64_t wrows = w_full ? m : std::min<int64_t>(m, kWBlockRows);
     int8_t* W = (int8_t*)ws.W.get((size_t)N * (size_t)(wrows * ldw));
@@ -649,11 +618,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         int8_t* Wb = (w_full ? W + r0 * ldw : W) + c0;
         set_rows(g, rc);
         g.W = Wb;
-        static const bool gemm_fence = [] {
-            const char* e = std::getenv("OZ2G_GEMM_FENCE");
-            return e && e[0] == '1';
-        }();
-        if (gemm_fence) {  // experiment: keep the persistent CTAs within one unit of each other
+        if (opt(OPT_GEMM_FENCE) == 1) {  // experiment: keep the persistent CTAs within one unit of each other
             g.fence = (unsigned long long*)ws.x_bmax.get(64) + 5;
             CUDA_TRY(cudaMemsetAsync(g.fence, 0, 8, stream));
         }
@@ -1107,11 +1072,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             fp.P1 = tab.P1; fp.P2 = tab.P2; fp.P_inv = tab.P_inv;
             fp.mode = tab.mode;
             fp.probe = fused_mode() == 2 ? 1 : 0;
-            static const bool no_fence = [] {
-                const char* e = std::getenv("OZ2G_FUSED_FENCE");
-                return e && e[0] == '0';
-            }();
-            if (!no_fence) {
+            if (opt(OPT_FUSED_FENCE) != 0) {
                 fp.plane_sync = (unsigned long long*)ws.x_bmax.get(64) + 4;
                 CUDA_TRY(cudaMemsetAsync(fp.plane_sync, 0, 8, stream));
             }
@@ -1120,11 +1081,8 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             fp.C = dC;
             fp.ldc = ldc_d;
             fp.st = st;
-            // OZ2G_FUSED_MC=0: one CTA per tile without the B multicast
-            static const bool mc = [] {
-                const char* e = std::getenv("OZ2G_FUSED_MC");
-                return !(e && e[0] == '0');
-            }();
+            // option "fused_mc" 0: one CTA per tile without the B multicast
+            const bool mc = opt(OPT_FUSED_MC) != 0;
             const CUtensorMap tA = make_plane_map(ares, kp, m, N, fused_tile_m(), m * kp);
             const CUtensorMap tB = make_plane_map_mn(bres, n, ldn, kp, N, kp * ldn, fused_b_box_rows(mc));
             tm.span(5, stream, [&] { CUDA_TRY(launch_gemm_crt_fused(prec, tA, tB, fp, ws.num_sms, mc, stream)); });

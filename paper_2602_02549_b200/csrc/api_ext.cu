@@ -15,11 +15,8 @@ namespace {
 // second captures, later ones replay; a workspace reallocation anywhere
 // (g_alloc_gen) invalidates the graphs.  The status word is read after the
 // replay from pinned memory, so errors are reported exactly as run_gemm does.
-// OZ2G_GRAPH=0 disables.
-bool graph_enabled() {
-    const char* e = std::getenv("OZ2G_GRAPH");
-    return !(e && e[0] == '0');
-}
+// Option "graph" 0 disables.
+bool graph_enabled() { return opt(OPT_GRAPH) != 0; }
 
 int run_gemm_graph(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
                    void* C, int64_t ldc, int nmod, unsigned flags, cudaStream_t stream, oz2g_diag* diag) {
@@ -719,6 +716,28 @@ int oz2g_native_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, i
         return OZ2G_OK;
     });
 }
+
+int oz2g_set_option(const char* name, long long value) {
+    return guarded([&] {
+        const int i = opt_index(name);
+        if (i < 0) throw Fail{OZ2G_INVALID_ARGUMENT, std::string("oz2g_set_option: unknown option ") + (name ? name : "(null)")};
+        if (!opt_set(i, value))
+            throw Fail{OZ2G_INVALID_ARGUMENT, std::string("oz2g_set_option: value out of range for ") + name};
+        ++g_alloc_gen;  // captured graphs embed the old choice
+        return OZ2G_OK;
+    });
+}
+
+int oz2g_get_option(const char* name, long long* value) {
+    return guarded([&] {
+        const int i = opt_index(name);
+        if (i < 0 || !value) throw Fail{OZ2G_INVALID_ARGUMENT, std::string("oz2g_get_option: unknown option ") + (name ? name : "(null)")};
+        *value = opt((Opt)i);
+        return OZ2G_OK;
+    });
+}
+
+const char* oz2g_option_name(int index) { return opt_name(index); }
 
 int oz2g_i8_peak(long long iters, int launches, int random, double* ms_out, double* ops_out) {
     return guarded([&] {

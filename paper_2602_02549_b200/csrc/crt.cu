@@ -239,13 +239,7 @@ cudaError_t launch_n(cudaStream_t s, const int8_t* W, int64_t ldw, int64_t wplan
                       mu, nu, C, ldc, ex, st);
 }
 
-int crt_cv() {
-    static const int v = [] {
-        const char* e = std::getenv("OZ2G_CRT_CV");
-        return e && std::atoi(e) == 4 ? 4 : 8;
-    }();
-    return v;
-}
+int crt_cv() { return opt(OPT_CRT_CV) == 4 ? 4 : 8; }
 
 // Conversions on the fp64 pipe: 3 of 8 with the double-double chain (two DFMA
 // per byte; measured best of {0, 3, 5, 8} at 16384^2, N = 16), 6 of 8 with the

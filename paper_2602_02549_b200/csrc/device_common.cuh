@@ -9,6 +9,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include "options.h"
+
 namespace oz2g {
 
 // ----------------------------------------------------------------------------
@@ -235,13 +237,10 @@ __device__ __forceinline__ void pdl_enter() {
 }
 
 // Set by run_gemm for the calls PDL pays on (small problems, where kernel
-// ramps are a visible share of the call); OZ2G_PDL=0 never, =2 always.
+// ramps are a visible share of the call); option "pdl" 0 never, 2 always.
 inline thread_local bool g_pdl_call = false;
 inline bool pdl_enabled() {
-    static const int mode = [] {
-        const char* e = std::getenv("OZ2G_PDL");
-        return e ? std::atoi(e) : 1;
-    }();
+    const long long mode = opt(OPT_PDL);
     return mode == 2 || (mode == 1 && g_pdl_call);
 }
 

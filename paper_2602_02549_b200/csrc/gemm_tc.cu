@@ -664,11 +664,8 @@ cudaError_t launch_gemm_i8(int mode, const CUtensorMap& tmA, const CUtensorMap& 
     const int grid = total < num_sms ? total : num_sms;
     // epilogue warps: 8 when k is small (k <= 2048: a tile's MMAs take little
     // longer than its epilogue; cfg1 1024^3 79 vs 88 us per call), 4 above
-    // (equal at 4096^3, 4 within noise ahead at 16384^3); OZ2G_EPI_WARPS=4|8 forces
-    static const int env = [] {
-        const char* e = getenv("OZ2G_EPI_WARPS");
-        return e ? atoi(e) : 0;
-    }();
+    // (equal at 4096^3, 4 within noise ahead at 16384^3); option "epi_warps" 4|8 forces
+    const int env = (int)opt(OPT_EPI_WARPS);
     const int ew = env == 4 || env == 8 ? env : (P.kblocks <= 16 ? 8 : 4);
     return ew == 4 ? launch_tc<4>(mode, tmA, tmB, P, grid, stream) : launch_tc<8>(mode, tmA, tmB, P, grid, stream);
 }
@@ -733,10 +730,7 @@ cudaError_t launch_gemm_i8_pair(int mode, const CUtensorMap& tmA, const CUtensor
     if (total == 0) return cudaSuccess;
     const int pairs = num_sms / 2;
     const int grid = 2 * (total < pairs ? total : pairs);
-    static const int stages = [] {
-        const char* e = getenv("OZ2G_PAIR_STAGES");
-        return e ? atoi(e) : 4;
-    }();
+    const int stages = (int)opt(OPT_PAIR_STAGES);
     // deeper pipelines let the clusters drift apart and lose L2 sharing:
     // DRAM reads 82 GB (4 stages), 245 GB (6), 250 GB (7) at 16384^3, N = 16
     if (stages == 6) return launch_pair_s<6>(mode, grid, tmA, tmB, P, stream);

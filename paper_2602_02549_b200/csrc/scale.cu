@@ -433,12 +433,8 @@ cudaError_t launch_row_scan_A(int prec, const void* A, int64_t lda, int64_t m, i
             // 512 threads (4 rows per SM in flight) up to 128 KB rows, 1024 (2
             // per SM) above, so the rows in flight stay within L2: at 16384^2
             // 0.51 vs 0.62 ms per launch (256 threads: 0.65, 4.2 GB read);
-            // OZ2G_ROWSCAN_THREADS=256/512/1024 overrides (experiments)
-            static const int thr_env = [] {
-                const char* e = std::getenv("OZ2G_ROWSCAN_THREADS");
-                const int v = e ? std::atoi(e) : 0;
-                return v == 256 || v == 512 || v == 1024 ? v : 0;
-            }();
+            // option "rowscan_threads" 256/512/1024 overrides (experiments)
+            const int thr_env = (int)opt(OPT_ROWSCAN_THREADS);
             const unsigned thr = thr_env ? (unsigned)thr_env : row_bytes <= (128u << 10) ? 512u : 1024u;
             if (prec)
                 return launch_pdl(row_scan_A_kernel<double, 1>, dim3((unsigned)m), dim3(thr), 0, s, (const double*)A,

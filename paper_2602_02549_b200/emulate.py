@@ -15,6 +15,7 @@ torch tensors (device pointers, no copies).
 from __future__ import annotations
 
 import ctypes as C
+from contextlib import contextmanager
 from dataclasses import dataclass, field
 from typing import Callable, Optional
 
@@ -54,6 +55,48 @@ def _check(rc: int) -> None:
     if rc != 0:
         msg = _lib.load().oz2g_last_error().decode()
         raise _EXC.get(rc, CudaError)(msg)
+
+
+_GEMM_VARIANTS = {"single": 0, "pair": 1, "mcast": 2}
+
+
+def set_option(name: str, value) -> None:
+    """Set a tuning option for this process (oz2g_set_option: "gemm", "fused",
+    "spec", "graph", "pdl", ...; `option_names()` lists them).  "gemm" also
+    takes "single" / "pair" / "mcast".  Applies from the next call."""
+    if name == "gemm" and isinstance(value, str):
+        if value not in _GEMM_VARIANTS:
+            raise InvalidArgument(f"set_option: gemm must be one of {sorted(_GEMM_VARIANTS)}")
+        value = _GEMM_VARIANTS[value]
+    _check(_lib.load().oz2g_set_option(name.encode(), int(value)))
+
+
+def get_option(name: str) -> int:
+    v = C.c_longlong()
+    _check(_lib.load().oz2g_get_option(name.encode(), C.byref(v)))
+    return v.value
+
+
+def option_names() -> list:
+    L = _lib.load()
+    out, i = [], 0
+    while (nm := L.oz2g_option_name(i)) is not None:
+        out.append(nm.decode())
+        i += 1
+    return out
+
+
+@contextmanager
+def options(**kw):
+    """Temporarily set options: `with options(spec=0, fused=1): ...`."""
+    old = {k: get_option(k) for k in kw}
+    try:
+        for k, v in kw.items():
+            set_option(k, v)
+        yield
+    finally:
+        for k, v in old.items():
+            set_option(k, v)
 
 
 @dataclass

@@ -26,7 +26,7 @@ def main():
         C = torch.empty((m, n), dtype=torch.float64, device=dev)
         ref = None
         for mode in modes:
-            os.environ["OZ2G_FUSED"] = mode
+            oz.set_option("fused", int(mode))
             for _ in range(2):
                 oz.os_ii(A, B, N, out=C)
             torch.cuda.synchronize()
@@ -47,7 +47,7 @@ def main():
                               "stages_ms": [round(x, 3) for x in st]}), flush=True)
         del A, B, C, ref
         torch.cuda.empty_cache()
-    os.environ.pop("OZ2G_FUSED", None)
+    oz.set_option("fused", 0)
 
 
 if __name__ == "__main__":

@@ -31,10 +31,9 @@ oz.os_ii(A, B, 16, vectors=True)
 # every speculation mode of the pipelined path, bit-identical to the device path
 Ad = oz.os_ii(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), 16).C
 Ad = Ad.cpu().numpy() if hasattr(Ad, "cpu") else np.asarray(Ad)
-for mode in ("0", "1", "2"):
-    os.environ["OZ2G_SPEC"] = mode
-    assert np.array_equal(oz.os_ii(A, B, 16).C.view(np.uint64), Ad.view(np.uint64)), mode
-os.environ.pop("OZ2G_SPEC")
+for mode in (0, 1, 2):
+    with oz.options(spec=mode):
+        assert np.array_equal(oz.os_ii(A, B, 16).C.view(np.uint64), Ad.view(np.uint64)), mode
 # asynchronous calls back to back
 outs = [np.empty((A.shape[0], B.shape[1])) for _ in range(3)]
 for c in outs:

@@ -65,12 +65,9 @@ def test_strided_host_operands_pipelined(cuda, oracle, mode):
     Ap = np.zeros((m, k + 5)); Ap[:, :k] = A
     Bp = np.zeros((k, n + 13)); Bp[:, :n] = B
     Cp = np.full((m, n + 3), -1.0)
-    os.environ["OZ2G_SPEC"] = mode
-    try:
+    with oz.options(spec=int(mode)):
         rc = _lib.load().oz2g_dgemm(m, n, k, Ap.ctypes.data, k + 5, Bp.ctypes.data, n + 13, Cp.ctypes.data, n + 3,
                                     12, 0, None, None)
-    finally:
-        del os.environ["OZ2G_SPEC"]
     assert rc == 0, _lib.load().oz2g_last_error()
     _same(np.ascontiguousarray(Cp[:, :n]), ref.C)
     assert (Cp[:, n:] == -1.0).all()

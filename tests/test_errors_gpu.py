@@ -4,7 +4,6 @@ non-finite entries, emulate.hpp:30-46 inverse-scaling overflow).  The device
 raises the reference's exception class with the reference's message, for the
 device-pointer path and for the pipelined host-pointer path (where the row
 exponents and A residues of early chunks run before the last chunk lands)."""
-import os
 
 import numpy as np
 import pytest
@@ -62,14 +61,9 @@ def test_errors_match_oracle(cuda, oracle, m, k, n):
         cls, msg = _expect(oracle, a, b, 14)
         assert cls is not None, name
         # host pointers (pipelined for the large shapes, under every speculation mode)
-        for mode in (("0", "1", "2") if m >= 2048 else ("",)):
-            if mode:
-                os.environ["OZ2G_SPEC"] = mode
-            try:
-                with pytest.raises(cls) as ei:
-                    oz.os_ii(a, b, 14)
-            finally:
-                os.environ.pop("OZ2G_SPEC", None)
+        for mode in ((0, 1, 2) if m >= 2048 else (-1,)):
+            with oz.options(spec=mode), pytest.raises(cls) as ei:
+                oz.os_ii(a, b, 14)
             assert str(ei.value) == msg, (name, mode, str(ei.value), msg)
         # device pointers
         with pytest.raises(cls) as ei:

@@ -3,7 +3,6 @@ residue GEMMs with accumulate / compute_q / final_reduce / inverse_scale
 (crt.hpp:91-150, emulate.hpp:30-46) in their epilogue, no W in HBM.  C must
 equal the oracle and the two-pass path bit for bit: ragged tile edges, fp32
 mode, many N, error flags, subnormal outputs and the BASELINE 16384^3 size."""
-import os
 
 import numpy as np
 import pytest
@@ -15,9 +14,8 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture
 def fused():
-    os.environ["OZ2G_FUSED"] = "1"
-    yield
-    os.environ.pop("OZ2G_FUSED", None)
+    with oz.options(fused=1):
+        yield
 
 
 CASES = [
@@ -69,12 +67,9 @@ def test_fused_equals_two_pass_full_size(cuda):
     import torch
     from test_fullsize_gpu import _gen
     dA, dB = _gen((16384, 16384), 0.0, 1234), _gen((16384, 16384), 0.0, 5678)
-    os.environ.pop("OZ2G_FUSED", None)
-    two = oz.os_ii(dA, dB, 16).C
-    os.environ["OZ2G_FUSED"] = "1"
-    try:
+    with oz.options(fused=0):
+        two = oz.os_ii(dA, dB, 16).C
+    with oz.options(fused=1):
         one = oz.os_ii(dA, dB, 16).C
-    finally:
-        os.environ.pop("OZ2G_FUSED", None)
     torch.cuda.synchronize()
     assert torch.equal(one.view(torch.int64), two.view(torch.int64))

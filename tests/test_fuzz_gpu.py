@@ -101,14 +101,12 @@ def test_fuzz_pipelined_host_path(cuda, oracle, seed):
         ref, ref_err = oracle.os_ii(A, B, N), None
     except Exception as e:  # noqa: BLE001 - the device must raise the same
         ref, ref_err = None, e
-    for mode in ("0", "1", "2"):
-        os.environ["OZ2G_SPEC"] = mode
+    for mode in (0, 1, 2):
         try:
-            got, got_err = oz.os_ii(A, B, N), None
+            with oz.options(spec=mode):
+                got, got_err = oz.os_ii(A, B, N), None
         except Exception as e:  # noqa: BLE001
             got, got_err = None, e
-        finally:
-            del os.environ["OZ2G_SPEC"]
         if ref_err is not None:
             assert isinstance(got_err, ORACLE_TO_OURS[type(ref_err).__name__]), (mode, got_err, ref_err)
             assert str(got_err) == str(ref_err), mode

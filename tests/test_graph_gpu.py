@@ -3,7 +3,6 @@ first call runs plainly, the second captures the pipeline, later calls
 replay it.  Every replay must equal the oracle bit for bit, read the inputs'
 current contents, report errors from the status word like a plain call, and
 be invalidated when a workspace buffer is reallocated."""
-import os
 
 import numpy as np
 import pytest
@@ -70,12 +69,27 @@ def test_graph_disabled_matches(cuda, oracle):
     A = oracle.gen_matrix(130, 70, 1.0, 71)
     B = oracle.gen_matrix(70, 90, 1.0, 72)
     dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
-    os.environ["OZ2G_GRAPH"] = "0"
-    try:
+    with oz.options(graph=0):
         plain = oz.os_ii(dA, dB, 12).C.clone()
-    finally:
-        os.environ.pop("OZ2G_GRAPH", None)
     out = torch.empty_like(plain)
     for _ in range(3):
         oz.os_ii(dA, dB, 12, out=out)
     assert torch.equal(out.view(torch.int64), plain.view(torch.int64))
+
+
+def test_set_option_recaptures(cuda, oracle):
+    """oz2g_set_option invalidates the captured graphs: a replayed call picks
+    up the new choice (the fused kernel launches fewer kernels) with the same C."""
+    import torch
+    A = oracle.gen_matrix(200, 160, 1.0, 81)
+    B = oracle.gen_matrix(160, 140, 1.0, 82)
+    ref = oracle.os_ii(A, B, 14).C
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    out = torch.empty((200, 140), dtype=torch.float64, device="cuda")
+    with oz.options(fused=0):
+        two = [oz.os_ii(dA, dB, 14, out=out).kernels_launched for _ in range(4)]
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), ref.view(np.uint64))
+    with oz.options(fused=1):
+        one = [oz.os_ii(dA, dB, 14, out=out).kernels_launched for _ in range(4)]
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), ref.view(np.uint64))
+    assert len(set(two)) == 1 and len(set(one)) == 1 and one[0] < two[0], (two, one)

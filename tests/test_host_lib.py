@@ -32,7 +32,7 @@ def test_library_exports_header_symbols():
 
 
 def test_version():
-    assert oz.load_library().oz2g_version() == 3
+    assert oz.load_library().oz2g_version() == 4
 
 
 @pytest.mark.parametrize("mode", [oz.F32, oz.F64])

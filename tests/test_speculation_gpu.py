@@ -11,7 +11,6 @@ is redone, so C is the unspeculated C bit for bit:
   * mode 1 only: moved, and a block computed with the superseded exponents
     raised a status flag: speculation 3 (every stage after the upload redone).
     Mode 2 keeps status flags per tile and resets them on recomputation."""
-import os
 
 import numpy as np
 import pytest
@@ -28,11 +27,8 @@ def _same(a, b):
 
 
 def _call(mode, A, B, nmod, **kw):
-    os.environ["OZ2G_SPEC"] = mode
-    try:
+    with oz.options(spec=int(mode)):
         return oz.os_ii(A, B, nmod, **kw)
-    finally:
-        del os.environ["OZ2G_SPEC"]
 
 
 def _unspeculated(A, B, nmod, **kw):
