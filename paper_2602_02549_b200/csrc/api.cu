@@ -552,9 +552,15 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     const int64_t wrows = w_full ? m : std::min<int64_t>(m, kWBlockRows);
     int8_t* W = (int8_t*)ws.W.get((size_t)N * (size_t)(wrows * ldw));
     fill_gemm_moduli(gp, tab);
+    const bool fused = fused_mode() >= 1 && !inter && !bo && !overlap && m * n > 0;
+    // A residues streamed per row block (option "resid_stream"): block b + 1's
+    // split runs on the side stream beside block b's residue GEMMs, so only the
+    // first block's split precedes the GEMMs
+    const bool rstream = opt(OPT_RESID_STREAM) != 0 && fork && !fused && m > kWBlockRows;
     struct Block { int64_t r0, rows; int chunk; };
     std::vector<Block> blocks;  // row blocks of C, one residue-GEMM + CRT launch each
-    const int64_t max_block = w_full ? (overlap ? round_up((m + ovb - 1) / ovb, 128) : m) : kWBlockRows;
+    const int64_t max_block =
+        (w_full && !rstream) ? (overlap ? round_up((m + ovb - 1) / ovb, 128) : m) : kWBlockRows;
     for (int c = 0; c < nchunks; ++c) {
         const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
         if (rc <= 0) continue;
@@ -1010,8 +1016,9 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             CUDA_TRY(cudaStreamWaitEvent(sB, ef, 0));
         }
         tm.span(4, stream, [&] {
-            if (!pipe || hooked) {
-                CUDA_TRY(launch_resid_A(prec, dA, lda_d, m, k, kp, mu, rc_dev, N, ares, 0, st, stream));
+            if (!pipe || hooked) {  // (streamed: the first row block only)
+                const int64_t ra = rstream ? blocks[0].rows : m;
+                CUDA_TRY(launch_resid_A(prec, dA, lda_d, ra, k, kp, mu, rc_dev, N, ares, m * kp, st, stream));
                 launches += m > 0;
             }
         });
@@ -1055,7 +1062,6 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         }
         // every read of the device copies of A and B is enqueued by now
         if (host && ws.ev_inputs_free) CUDA_TRY(cudaEventRecord(ws.ev_inputs_free, stream));
-        const bool fused = fused_mode() >= 1 && !inter && !bo && !overlap && m * n > 0;
         if (fused) {
             // the N residue GEMMs with the CRT and the inverse scaling in their epilogue:
             // one launch over every 128 x 128 tile of C, no W
@@ -1087,6 +1093,22 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             const CUtensorMap tB = make_plane_map_mn(bres, n, ldn, kp, N, kp * ldn, fused_b_box_rows(mc));
             tm.span(5, stream, [&] { CUDA_TRY(launch_gemm_crt_fused(prec, tA, tB, fp, ws.num_sms, mc, stream)); });
             ++launches;
+        } else if (rstream) {
+            size_t ev_res = 0;  // event after the A residues of block bi
+            for (size_t bi = 0; bi < nb; ++bi) {
+                if (bi > 0) CUDA_TRY(cudaStreamWaitEvent(stream, ws.pool_event(ev_res), 0));
+                if (bi + 1 < nb) {
+                    const int64_t r0 = blocks[bi + 1].r0, rb = blocks[bi + 1].rows;
+                    tm.span(4, sB, [&] {
+                        CUDA_TRY(launch_resid_A(prec, (const char*)dA + esz * (size_t)(r0 * lda_d), lda_d, rb, k, kp,
+                                                mu + r0, rc_dev, N, ares + r0 * kp, m * kp, st, sB));
+                    });
+                    ++launches;
+                    ev_res = evn++;
+                    CUDA_TRY(cudaEventRecord(ws.pool_event(ev_res), sB));
+                }
+                run_block(bi, 0, n, st);
+            }
         } else {
             for (size_t bi = 0; bi < nb; ++bi) run_block(bi, 0, n, st);
         }

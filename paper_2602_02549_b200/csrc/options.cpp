@@ -45,6 +45,7 @@ const Spec kSpecs[OPT_COUNT] = {
     {"epi_warps", 0, 0, 0, kEpi},
     {"pair_stages", 4, 0, 0, kStages},
     {"rowscan_threads", 0, 0, 0, kRowscan},
+    {"resid_stream", 0, 0, 1, nullptr},
 };
 
 bool valid(const Spec& s, long long v) {

@@ -25,6 +25,7 @@ enum Opt : int {
     OPT_EPI_WARPS,        // GEMM epilogue warps: 0 by k, 4 or 8
     OPT_PAIR_STAGES,      // CTA-pair GEMM pipeline depth: 4, 5 or 6
     OPT_ROWSCAN_THREADS,  // row-scan CTA size: 0 by row length, 256, 512 or 1024
+    OPT_RESID_STREAM,     // 1: A residues per row block on a side stream beside the previous block's GEMMs
     OPT_COUNT
 };
 

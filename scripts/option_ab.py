@@ -1,0 +1,61 @@
+"""Interleaved A/B of a tuning option (oz2g_set_option) on device-resident
+inputs: per shape, the values take turns (rounds x reps calls each, CUDA
+events around each value's calls), and every value's C must equal the
+first value's bit for bit.  One JSON line per shape.
+
+    python scripts/option_ab.py resid_stream 0,1 16384x16384x16384x16 8192x16384x4096x16 [--rounds 3]
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("option")
+    ap.add_argument("values")
+    ap.add_argument("shapes", nargs="+", help="m x k x n x N")
+    ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    import torch
+
+    import paper_2602_02549_b200 as oz
+    from bench import gen_device
+    dev = torch.device("cuda", 0)
+    values = [int(v) for v in a.values.split(",")]
+    for shape in a.shapes:
+        m, k, n, N = (int(x) for x in shape.split("x"))
+        A = gen_device(m, k, 0.0, 1234, torch.float64, dev)
+        B = gen_device(k, n, 0.0, 5678, torch.float64, dev)
+        C = torch.empty((m, n), dtype=torch.float64, device=dev)
+        ref, ms = None, {v: [] for v in values}
+        for _ in range(a.rounds):
+            for v in values:
+                oz.set_option(a.option, v)
+                for _ in range(2):
+                    oz.os_ii(A, B, N, out=C)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(a.reps):
+                    oz.os_ii(A, B, N, out=C)
+                e1.record()
+                torch.cuda.synchronize()
+                ms[v].append(e0.elapsed_time(e1) / a.reps)
+                if ref is None:
+                    ref = C.clone()
+                elif not torch.equal(C.view(torch.int64), ref.view(torch.int64)):
+                    raise SystemExit(f"{a.option}={v}: C differs at {shape}")
+        flops = 2.0 * m * n * k
+        print(json.dumps({"shape": shape, "option": a.option,
+                          "ms": {v: [round(x, 3) for x in ms[v]] for v in values},
+                          "tflops_best": {v: round(flops / min(ms[v]) / 1e9, 1) for v in values}}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -69,3 +69,26 @@ def test_row_blocked_crt_outputs(cuda, oracle, tmp_path):
     # wrapped INT32 residue products of every block, against the unblocked evidence export
     ev = oz.os_ii(A[:, :], B, 14, evidence=True)
     assert np.array_equal(np.load(tmp_path / "Cprod.npy"), ev.crt.Cprod)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dt,nmod", [(np.float64, 14), (np.float32, 7)])
+def test_streamed_a_residues(cuda, oracle, dt, nmod):
+    """Option "resid_stream": the A residues of row block b + 1 are split on
+    the side stream beside block b's residue GEMMs (device pointers, three
+    2048-row blocks); C and the bounds equal the oracle / the default path."""
+    import torch
+    m, k, n = 4500, 300, 200
+    A = oracle.gen_matrix(m, k, 1.0, 811).astype(dt)
+    B = oracle.gen_matrix(k, n, 1.0, 812).astype(dt)
+    ref = oracle.os_ii(A, B, nmod).C
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    base = oz.os_ii(dA, dB, nmod, bounds="full")
+    with oz.options(resid_stream=1):
+        for _ in range(3):  # plain, captured, replayed
+            r = oz.os_ii(dA, dB, nmod, bounds="full")
+            got = r.C.cpu().numpy()
+            assert np.array_equal(got.view(np.uint64 if dt == np.float64 else np.uint32),
+                                  ref.view(np.uint64 if dt == np.float64 else np.uint32))
+        assert torch.equal(r.bounds["tight"], base.bounds["tight"])
+        assert r.kernels_launched > base.kernels_launched  # three blocks, three A splits
