@@ -41,6 +41,19 @@ for c in outs:
 oz.synchronize()
 for c in outs:
     assert np.array_equal(c.view(np.uint64), Ad.view(np.uint64))
+# device-pointer graph replays (programmatic dependent launches at this size), blocking and asynchronous
+dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+dC = torch.empty((A.shape[0], B.shape[1]), dtype=torch.float64, device="cuda")
+for _ in range(3):
+    oz.os_ii(dA, dB, 16, out=dC)
+for _ in range(3):
+    oz.os_ii(dA, dB, 16, out=dC, blocking=False)
+oz.synchronize()
+assert np.array_equal(dC.cpu().numpy().view(np.uint64), Ad.view(np.uint64))
+# A residues streamed beside the residue GEMMs (three row blocks)
+A3 = O.gen_matrix(4500, 64, 0.5, 41)
+with oz.options(resid_stream=1):
+    oz.os_ii(torch.from_numpy(A3).cuda(), torch.from_numpy(B).cuda(), 12)
 # multi-device tiling (device listed twice)
 oz.os_ii(A[:300], B, 12, devices=[0, 0])
 # error paths
