@@ -213,6 +213,23 @@ def run_reference(args):
     }), flush=True)
 
 
+_OPTION_DEFAULTS = {"gemm": 0, "fused": 0, "fused_mc": 1, "fused_fence": 1, "spec": -1, "graph": 1, "pdl": 1,
+                    "group_m": 0, "group_n": 0, "l2hint": 0, "crt_overlap": 0, "crt_cv": 8, "wblock_min_mb": 2048,
+                    "gemm_fence": 0, "epi_warps": 0, "pair_stages": 4, "rowscan_threads": 0, "resid_stream": 0}
+
+
+def non_default_options() -> dict:
+    """The library's tuning options in effect that differ from the defaults
+    (oz2g_get_option; set through the environment or set_option)."""
+    import paper_2602_02549_b200 as oz
+    out = {}
+    for name in oz.option_names():
+        v = oz.get_option(name)
+        if _OPTION_DEFAULTS.get(name) != v:
+            out[name] = v
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -429,15 +446,14 @@ def main():
         e2e["speculation"] = {0: "none", 1: "confirmed", 2: "missed (call redone)"}[r_e2e.speculation]
         if r_e2e.speculation:
             # the same calls with column-only speculation (OZ2G_SPEC=1) and none (0), same box
-            for mode, key in (("1", "columns_only_value"), ("0", "unspeculated_value")):
-                os.environ["OZ2G_SPEC"] = mode
-                oz.os_ii(a_np, b_np, args.moduli, out=c_np, reduce_maxima=reduce_cb)  # warm (buffer sizes differ)
-                barrier()
-                t0 = time.perf_counter()
-                for _ in range(2):
-                    oz.os_ii(a_np, b_np, args.moduli, out=c_np, reduce_maxima=reduce_cb)
-                barrier()
-                del os.environ["OZ2G_SPEC"]
+            for mode, key in ((1, "columns_only_value"), (0, "unspeculated_value")):
+                with oz.options(spec=mode):
+                    oz.os_ii(a_np, b_np, args.moduli, out=c_np, reduce_maxima=reduce_cb)  # warm (buffer sizes differ)
+                    barrier()
+                    t0 = time.perf_counter()
+                    for _ in range(2):
+                        oz.os_ii(a_np, b_np, args.moduli, out=c_np, reduce_maxima=reduce_cb)
+                    barrier()
                 e2e[key] = flops / ((time.perf_counter() - t0) / 2) / 1e12
         # the same calls enqueued back to back through the asynchronous API
         # (blocking=False, one synchronize at the end): each step still uploads
@@ -584,7 +600,7 @@ def main():
                    "moduli": args.moduli, "moduli_choice": auto_n or "fixed (--moduli)",
                    "phi": args.phi, "parallelism": f"2d-tile {R}x{Cc}",
                    "l2": "inputs 2 GiB each > L2, no flush",
-                   "library_env": {kk: vv for kk, vv in os.environ.items() if kk.startswith("OZ2G_")} or "defaults"},
+                   "library_options": non_default_options() or "defaults"},
         "clocks": clocks_timed,
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,

@@ -15,12 +15,12 @@ for (m, phi, nmod) in [(8192, 0.0, 12), (8192, 0.5, 12), (8192, 2.0, 12), (8192,
     a, b, c = Ah.numpy(), Bh.numpy(), Ch.numpy()
     out = []
     for mode in ("2", "1", "0"):
-        os.environ["OZ2G_SPEC"] = mode
+        oz.set_option("spec", int(mode))
         r = oz.os_ii(a, b, nmod, out=c)
         t0 = time.perf_counter()
         for _ in range(3):
             r = oz.os_ii(a, b, nmod, out=c)
         ms = (time.perf_counter() - t0) / 3 * 1e3
         out.append(f"mode {mode}: {ms:6.1f} ms ({2*m**3/ms/1e9:5.1f} TF/s, spec {r.speculation})")
-    del os.environ["OZ2G_SPEC"]
+    oz.set_option("spec", -1)
     print(f"{m}^3 phi={phi} N={nmod}: " + " | ".join(out), flush=True)

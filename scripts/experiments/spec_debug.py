@@ -13,12 +13,12 @@ B_h = torch.empty(B.shape, dtype=torch.float64, pin_memory=True); B_h.copy_(B)
 C_h = torch.empty(A.shape, dtype=torch.float64, pin_memory=True)
 a, b, c = A_h.numpy(), B_h.numpy(), C_h.numpy()
 for spec in ["2", "1", "0", "2", "1", "0", "2"]:
-    os.environ["OZ2G_SPEC"] = spec
+    oz.set_option("spec", int(spec))
     t0 = time.perf_counter()
     r = oz.os_ii(a, b, 16, out=c)
     print(f"spec={spec} speculation={r.speculation} {1e3*(time.perf_counter()-t0):.1f} ms", flush=True)
 names = ["h2d", "scale", "clearance", "expo", "resid", "gemm", "crt", "d2h"]
 for spec in ["2", "1"]:
-    os.environ["OZ2G_SPEC"] = spec
+    oz.set_option("spec", int(spec))
     r = oz.os_ii(a, b, 16, out=c, timing=True)
     print(f"spec={spec} busy ms:", {nm: round(v, 2) for nm, v in zip(names, r.stage_ms)}, "launches", r.kernels_launched)

@@ -16,12 +16,12 @@ for (m, k, n, dt, nmod) in [(4096, 4096, 4096, torch.float32, 6), (4096, 4096, 4
     a, b, c = Ah.numpy(), Bh.numpy(), Ch.numpy()
     out = []
     for mode in ("2", "1", "0"):
-        os.environ["OZ2G_SPEC"] = mode
+        oz.set_option("spec", int(mode))
         r = oz.os_ii(a, b, nmod, out=c); r = oz.os_ii(a, b, nmod, out=c)
         t0 = time.perf_counter()
         for _ in range(5):
             r = oz.os_ii(a, b, nmod, out=c)
         ms = (time.perf_counter() - t0) / 5 * 1e3
         out.append(f"mode {mode}: {ms:6.2f} ms ({2*m*n*k/ms/1e9:5.1f} TF/s, spec {r.speculation})")
-    del os.environ["OZ2G_SPEC"]
+    oz.set_option("spec", -1)
     print(f"{m}x{k}x{n} {str(dt)[6:]} N={nmod}: " + " | ".join(out), flush=True)
