@@ -116,7 +116,8 @@ def _ncu_traffic(m: int, nmod: int):
         h, units = rows[0], rows[1]
         scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
         for r in rows[2:]:
-            if "gemm_i8_tc_kernel<1>" in r[h.index("Kernel Name")]:
+            name = r[h.index("Kernel Name")]
+            if "gemm_i8_tc_kernel<1>" in name or "gemm_i8_tc_kernel<1," in name:  # <EPI_RESID(, epilogue warps)>
                 tot = 0.0
                 for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                     i = h.index(key)
