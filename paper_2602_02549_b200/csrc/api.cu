@@ -348,18 +348,29 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     const int spec_mode = (pipe && !hooked && !reuse_scaling && crt_overlap_blocks() <= 1)
                               ? speculation_mode(esz * (size_t)(m * k + k * n)) : 0;
     const bool spec2 = spec_mode == 2 && n >= 2 * 256;
-    // spec2 column chunks: units of cu columns (a multiple of 128), chunks of two
-    // units except the last two, one unit each (a short last arrival leaves less
-    // work after the upload); cstart[c] = first column of chunk c, cstart[ncc] = n
-    const int64_t col_chunk = round_up((n + kPipeChunks - 1) / kPipeChunks, 256);
-    const int64_t cu = col_chunk / 2;
+    // spec2 column chunks: units of cu columns (a multiple of 128), chunks of
+    // 2^T units (T = option "spec_tail") and a halving tail — the last 2^T
+    // units arrive as 2^(T-1), ..., 1, 1 units — so the last arrival, and the
+    // work left after the upload, is short; cstart[c] = first column of chunk
+    // c, cstart[ncc] = n
+    const int tail_t = (int)opt(OPT_SPEC_TAIL);
+    const int64_t per_chunk = int64_t(1) << tail_t;
+    const int64_t col_chunk = round_up((n + kPipeChunks - 1) / kPipeChunks, 128 * per_chunk);
+    const int64_t cu = col_chunk / per_chunk;
     const int64_t nunits = (n + cu - 1) / cu;
     std::vector<int64_t> cstart;
     for (int64_t u = 0; spec2 && u < nunits;) {
         cstart.push_back(u * cu);
-        u += (nunits - u <= 2 && nunits >= 3) ? 1 : 2;
+        const int64_t rem = nunits - u;
+        int64_t step = per_chunk;
+        if (rem <= per_chunk) {  // the tail: the largest power of two below rem (1 for rem <= 2)
+            step = 1;
+            while (2 * step < rem) step *= 2;
+        }
+        u += step;
     }
     const int ncc = (int)cstart.size();
+    if (ncc > kMaxColChunks) throw Fail{OZ2G_LOGIC_ERROR, "oz2g_gemm: too many column chunks"};
     cstart.push_back(n);
     std::vector<std::pair<bool, int>> arrivals;  // spec2 upload order: (is an A row chunk, index)
     for (int j = 0; spec2 && j < std::max(nchunks, ncc); ++j) {

@@ -77,6 +77,7 @@ struct DevBuf {
 // (see run_gemm): uploads of A overlap the row scan and the clearance GEMM,
 // and the download of each finished C row block overlaps the next block.
 constexpr int kPipeChunks = 8;
+constexpr int kMaxColChunks = kPipeChunks + 4;  // spec2 column chunks: regular ones + a halving tail
 // The last C row block is split in this many pieces so that only a small
 // download follows the last kernel.
 constexpr int kTailSplit = 4;
@@ -150,7 +151,7 @@ struct Workspace {
         return ev_pool[i];
     }
     cudaEvent_t ev_start = nullptr, ev_b = nullptr, ev_done = nullptr;
-    cudaEvent_t ev_a[kPipeChunks] = {}, ev_bc[kPipeChunks + 1] = {}, ev_c[kPipeChunks + kTailSplit] = {};
+    cudaEvent_t ev_a[kPipeChunks] = {}, ev_bc[kMaxColChunks] = {}, ev_c[kPipeChunks + kTailSplit] = {};
     void ensure_streams() {
         if (s_h2d) return;
         CUDA_TRY(cudaStreamCreateWithFlags(&s_main, cudaStreamNonBlocking));
@@ -159,11 +160,8 @@ struct Workspace {
         CUDA_TRY(cudaStreamCreateWithFlags(&s_aux, cudaStreamNonBlocking));
         for (cudaEvent_t* e : {&ev_start, &ev_b, &ev_done, &ev_inputs_free})
             CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-        for (int c = 0; c < kPipeChunks; ++c) {
-            CUDA_TRY(cudaEventCreateWithFlags(&ev_a[c], cudaEventDisableTiming));
-            CUDA_TRY(cudaEventCreateWithFlags(&ev_bc[c], cudaEventDisableTiming));
-        }
-        CUDA_TRY(cudaEventCreateWithFlags(&ev_bc[kPipeChunks], cudaEventDisableTiming));
+        for (int c = 0; c < kPipeChunks; ++c) CUDA_TRY(cudaEventCreateWithFlags(&ev_a[c], cudaEventDisableTiming));
+        for (int c = 0; c < kMaxColChunks; ++c) CUDA_TRY(cudaEventCreateWithFlags(&ev_bc[c], cudaEventDisableTiming));
         for (int c = 0; c < kPipeChunks + kTailSplit; ++c)
             CUDA_TRY(cudaEventCreateWithFlags(&ev_c[c], cudaEventDisableTiming));
     }

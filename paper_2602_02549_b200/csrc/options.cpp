@@ -46,6 +46,7 @@ const Spec kSpecs[OPT_COUNT] = {
     {"pair_stages", 4, 0, 0, kStages},
     {"rowscan_threads", 0, 0, 0, kRowscan},
     {"resid_stream", 0, 0, 1, nullptr},
+    {"spec_tail", 1, 1, 3, nullptr},
 };
 
 bool valid(const Spec& s, long long v) {

@@ -26,6 +26,7 @@ enum Opt : int {
     OPT_PAIR_STAGES,      // CTA-pair GEMM pipeline depth: 4, 5 or 6
     OPT_ROWSCAN_THREADS,  // row-scan CTA size: 0 by row length, 256, 512 or 1024
     OPT_RESID_STREAM,     // 1: A residues per row block on a side stream beside the previous block's GEMMs
+    OPT_SPEC_TAIL,        // host pipeline, rows + columns: halvings of the last column chunks (1..3)
     OPT_COUNT
 };
 

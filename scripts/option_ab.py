@@ -4,11 +4,14 @@ events around each value's calls), and every value's C must equal the
 first value's bit for bit.  One JSON line per shape.
 
     python scripts/option_ab.py resid_stream 0,1 16384x16384x16384x16 8192x16384x4096x16 [--rounds 3]
+    python scripts/option_ab.py spec_tail 1,2,3 16384x16384x16384x16 --host   # end to end (pinned host
+                                                                               # buffers, wall clock)
 """
 import argparse
 import json
 import os
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -21,6 +24,7 @@ def main():
     ap.add_argument("shapes", nargs="+", help="m x k x n x N")
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--host", action="store_true", help="pinned host buffers (copies inside), wall clock")
     a = ap.parse_args()
     import torch
 
@@ -33,20 +37,35 @@ def main():
         A = gen_device(m, k, 0.0, 1234, torch.float64, dev)
         B = gen_device(k, n, 0.0, 5678, torch.float64, dev)
         C = torch.empty((m, n), dtype=torch.float64, device=dev)
+        if a.host:
+            def pinned(t):
+                h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                h.copy_(t)
+                return h
+            A, B, C = pinned(A), pinned(B), pinned(C)
+            args = (A.numpy(), B.numpy(), C.numpy())
+        else:
+            args = (A, B, C)
         ref, ms = None, {v: [] for v in values}
         for _ in range(a.rounds):
             for v in values:
                 oz.set_option(a.option, v)
                 for _ in range(2):
-                    oz.os_ii(A, B, N, out=C)
+                    oz.os_ii(args[0], args[1], N, out=args[2])
                 torch.cuda.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                for _ in range(a.reps):
-                    oz.os_ii(A, B, N, out=C)
-                e1.record()
-                torch.cuda.synchronize()
-                ms[v].append(e0.elapsed_time(e1) / a.reps)
+                if a.host:
+                    t0 = time.perf_counter()
+                    for _ in range(a.reps):
+                        oz.os_ii(args[0], args[1], N, out=args[2])
+                    ms[v].append((time.perf_counter() - t0) / a.reps * 1e3)
+                else:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    for _ in range(a.reps):
+                        oz.os_ii(A, B, N, out=C)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    ms[v].append(e0.elapsed_time(e1) / a.reps)
                 if ref is None:
                     ref = C.clone()
                 elif not torch.equal(C.view(torch.int64), ref.view(torch.int64)):

@@ -137,3 +137,30 @@ def test_speculation_random(cuda, oracle, mode, phi, seed):
     _same(r.C, oracle.os_ii(A, B, 12).C)
     for nm in ("mu", "nu", "e", "f"):
         assert np.array_equal(getattr(r.scaling, nm), getattr(r0.scaling, nm)), nm
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tail", [2, 3])
+@pytest.mark.parametrize("case", ["moved", "random", "flag"])
+def test_speculation_tail_halvings(cuda, oracle, tail, case):
+    """Option "spec_tail": the last column chunks halve 2 or 3 times (chunks
+    shorter than the default unit, so the per-unit statuses and moved flags
+    use the finer unit); C, exponents and flags equal the unspeculated call."""
+    if case == "random":
+        m, k, n = 2304, 96, 4100
+        A, B = oracle.gen_matrix(m, k, 1.0, 21), oracle.gen_matrix(k, n, 1.0, 22)
+    else:
+        m, k, n = 4096, 128, 4096
+        A, B = _moved_case(oracle, m, k, n, np.float64)
+        if case == "flag":
+            A[:64] *= 1e-300
+            B *= 1e-12
+    with oz.options(spec_tail=tail):
+        r = _call("2", A, B, 14, vectors=True)
+    assert r.speculation in ((2,) if case != "random" else (1, 2))
+    r0 = _unspeculated(A, B, 14, vectors=True)
+    _same(r.C, r0.C)
+    _same(r.C, oracle.os_ii(A, B, 14).C)
+    assert r.subnormal == r0.subnormal == (case == "flag")
+    for nm in ("mu", "nu", "e", "f"):
+        assert np.array_equal(getattr(r.scaling, nm), getattr(r0.scaling, nm)), nm
