@@ -217,4 +217,16 @@ EmulationResult<T> os_ii_multi(const Matrix<T>& a, const Matrix<T>& b, int n, co
     return r;
 }
 
+// Tuning options of the library for this process (oz2g_set_option; names and
+// values in oz2g.h).  std::invalid_argument for an unknown name or a value out
+// of range.
+inline void set_option(const std::string& name, long long value) {
+    detail::throw_status(oz2g_set_option(name.c_str(), value));
+}
+inline long long get_option(const std::string& name) {
+    long long v = 0;
+    detail::throw_status(oz2g_get_option(name.c_str(), &v));
+    return v;
+}
+
 }  // namespace oz2

@@ -65,6 +65,17 @@ int main() {
     CHECK(st.achievable && st.n >= 2 && st.bound_max <= 1e-13);
     CHECK(suggest_n_tight(A, B, 1e-13, false).n <= suggest_n(A, B, 1e-13).n || !suggest_n(A, B, 1e-13).achievable);
     CHECK(throws_as<std::domain_error>([&] { suggest_n(A, B, -1.0); }));
+    // tuning options: a variant gives the same C; bad names / values throw
+    {
+        const auto base = os_ii(A, B, 12);
+        set_option("gemm", 1);  // CTA-pair residue GEMM
+        CHECK(get_option("gemm") == 1);
+        const auto pair = os_ii(A, B, 12);
+        set_option("gemm", 0);
+        CHECK(std::memcmp(base.C.data(), pair.C.data(), sizeof(double) * 4 * 4) == 0);
+        CHECK(throws_as<std::invalid_argument>([&] { set_option("gemm", 7); }));
+        CHECK(throws_as<std::invalid_argument>([&] { get_option("no_such_option"); }));
+    }
     // multi-device tiling (the device listed twice): C identical to os_ii
     {
         Matrix<double> X(40, 33), Y(33, 27);
