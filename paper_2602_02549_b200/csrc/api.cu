@@ -280,7 +280,7 @@ void compute_relative_operands(Workspace& ws, int prec, const void* dA, int64_t 
 int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
              void* C, int64_t ldc, int nmod, unsigned flags, cudaStream_t stream, oz2g_intermediates* inter,
              oz2g_diag* diag, oz2g_reduce_maxima_fn reduce_fn, void* reduce_user, int64_t row_base,
-             int64_t col_base, int slot, bool reuse_scaling) {
+             int64_t col_base, int slot, bool reuse_scaling, const Arrivals* arr) {
     if (prec != OZ2G_FP32 && prec != OZ2G_FP64) throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_gemm: prec must be OZ2G_FP32 or OZ2G_FP64"};
     if (m < 0 || n < 0 || k < 0) throw Fail{OZ2G_INVALID_ARGUMENT, "Matrix: negative dimension"};
     if (lda < k || ldb < n || ldc < n) throw Fail{OZ2G_INVALID_ARGUMENT, "dimension mismatch: leading dimension"};
@@ -338,14 +338,21 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     // With a multi-rank reduce hook the uploads still overlap the scans and the
     // clearance products, but the exponents (and everything after) wait for
     // the all-reduced maxima: no per-chunk exponents, no speculation.
-    const bool pipe = host && !inter_mats && m >= 2048 && n >= 256;
+    // Inputs arriving on other streams (arr, the multi-GPU exchange) take the
+    // same chunked path with device pointers: B first, then A row chunks.
+    if (arr && (host || inter || async)) throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_gemm: arrivals need device pointers, C only"};
+    const bool pipe = (host && !inter_mats && m >= 2048 && n >= 256) || arr;
     const bool hooked = reduce_fn != nullptr;
-    const int64_t chunk_rows = pipe ? round_up((m + kPipeChunks - 1) / kPipeChunks, 256) : m;
+    const int64_t chunk_rows =
+        arr ? std::max<int64_t>(1, arr->chunk_rows) : pipe ? round_up((m + kPipeChunks - 1) / kPipeChunks, 256) : m;
     const int nchunks = m > 0 ? (int)((m + chunk_rows - 1) / chunk_rows) : 1;
+    if (arr && (nchunks > kMaxArrivalChunks || (m > 0 && nchunks != arr->nchunks)))
+        throw Fail{OZ2G_INVALID_ARGUMENT, "oz2g_gemm: arrival chunks do not cover A"};
+    const cudaEvent_t ev_b_in = arr ? arr->b : nullptr;
     // speculated exponents (blocking pipelined calls): 2 = rows and columns
     // (A row chunks and B column chunks uploaded alternately), 1 = columns
     // (asynchronous calls: rows + columns only; its statuses are merged on the device)
-    const int spec_mode = (pipe && !hooked && !reuse_scaling && crt_overlap_blocks() <= 1)
+    const int spec_mode = (pipe && !arr && !hooked && !reuse_scaling && crt_overlap_blocks() <= 1)
                               ? speculation_mode(esz * (size_t)(m * k + k * n)) : 0;
     const bool spec2 = spec_mode == 2 && n >= 2 * 256;
     // spec2 column chunks: units of cu columns (a multiple of 128), chunks of
@@ -482,7 +489,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         CUDA_TRY(cudaStreamWaitEvent(sB, ef, 0));
     }
     // ---- K1 (B): column pre-exponents and Bbar^T ----
-    if (pipe && !spec2) CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_b, 0));
+    if (pipe && !spec2) CUDA_TRY(cudaStreamWaitEvent(stream, arr ? ev_b_in : ws.ev_b, 0));
     if (scan && !spec2) tm.span(1, sB, [&] {
         CUDA_TRY(launch_col_max_B(prec, dB, ldb_d, k, n, bmax, st, sB)); launches += n > 0;
         CUDA_TRY(launch_col_exp_B(bmax, n, nup, st, sB)); launches += n > 0;
@@ -575,7 +582,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     for (int c = 0; c < nchunks; ++c) {
         const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
         if (rc <= 0) continue;
-        const int64_t sub = (pipe && !spec2 && c == nchunks - 1 && rc >= 2 * 128)
+        const int64_t sub = (pipe && host && !spec2 && c == nchunks - 1 && rc >= 2 * 128)
                                 ? std::min<int64_t>(max_block, round_up((rc + kTailSplit - 1) / kTailSplit, 128))
                                 : max_block;
         for (int64_t q = r0; q < r0 + rc; q += sub) blocks.push_back({q, std::min<int64_t>(sub, r0 + rc - q), c});
@@ -677,7 +684,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
                                 (char*)dC + esz * (size_t)(r0 * ldc_d + c0), ldc_d, exb, sb, crt_stream));
         });
         ++launches;
-        if (pipe) {  // download this C block while the next one computes
+        if (pipe && host) {  // download this C block while the next one computes
             const cudaEvent_t ec = ws.pool_event(evn++);
             CUDA_TRY(cudaEventRecord(ec, crt_stream));
             CUDA_TRY(cudaStreamWaitEvent(ws.s_d2h, ec, 0));
@@ -915,7 +922,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     size_t next_block = 0;
     for (int c = 0; c < (scan && !spec2 ? nchunks : 0); ++c) {
         const int64_t r0 = c * chunk_rows, rc = std::min<int64_t>(chunk_rows, m - r0);
-        if (pipe) CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_a[c], 0));
+        if (pipe) CUDA_TRY(cudaStreamWaitEvent(stream, arr ? arr->a[c] : ws.ev_a[c], 0));
         tm.span(1, stream, [&] {
             CUDA_TRY(launch_row_scan_A(prec, (const char*)dA + esz * (size_t)(r0 * lda_d), lda_d, rc, k, kp,
                                        mup + r0, abar + r0 * kp, st, stream, r0));
@@ -1129,7 +1136,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
         CUDA_TRY(cudaEventRecord(ej, ws.s_aux));
         CUDA_TRY(cudaStreamWaitEvent(stream, ej, 0));
     }
-    if (pipe) {
+    if (pipe && host) {
         CUDA_TRY(cudaEventRecord(ws.ev_done, ws.s_d2h));
         CUDA_TRY(cudaStreamWaitEvent(stream, ws.ev_done, 0));
     } else if (host && m * n) {

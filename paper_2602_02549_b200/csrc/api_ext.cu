@@ -717,6 +717,27 @@ int oz2g_native_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, i
     });
 }
 
+}  // extern "C"
+
+namespace oz2g {
+
+int gemm_arrivals(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
+                  int64_t ldb, void* C, int64_t ldc, int nmod, unsigned flags, cudaStream_t stream, oz2g_diag* diag,
+                  oz2g_reduce_maxima_fn reduce_fn, void* reduce_user, const Arrivals& arr, std::string* err) {
+    const int rc = guarded([&] {
+        if ((flags & ~OZ2G_TIMING) != OZ2G_DEVICE_PTRS)
+            throw Fail{OZ2G_INVALID_ARGUMENT, "gemm_arrivals: device pointers, C only"};
+        return run_gemm(prec, m, n, k, A, lda, B, ldb, C, ldc, nmod, flags, stream, nullptr, diag, reduce_fn,
+                        reduce_user, 0, 0, 0, false, &arr);
+    });
+    if (rc != OZ2G_OK && err) *err = g_last_error;
+    return rc;
+}
+
+}  // namespace oz2g
+
+extern "C" {
+
 int oz2g_set_option(const char* name, long long value) {
     return guarded([&] {
         const int i = opt_index(name);

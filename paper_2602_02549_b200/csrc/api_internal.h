@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "../../include/oz2g.h"
+#include "arrivals.h"
 #include "device_common.cuh"
 #include "kernels.h"
 #include "tables.h"
@@ -255,6 +256,6 @@ void compute_relative_operands(Workspace& ws, int prec, const void* dA, int64_t 
 int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
              void* C, int64_t ldc, int nmod, unsigned flags, cudaStream_t stream, oz2g_intermediates* inter,
              oz2g_diag* diag, oz2g_reduce_maxima_fn reduce_fn, void* reduce_user, int64_t row_base = 0,
-             int64_t col_base = 0, int slot = 0, bool reuse_scaling = false);
+             int64_t col_base = 0, int slot = 0, bool reuse_scaling = false, const Arrivals* arr = nullptr);
 
 }  // namespace oz2g

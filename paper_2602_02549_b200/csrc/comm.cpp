@@ -35,6 +35,8 @@
 #include <string>
 
 #include "../../include/oz2g.h"
+#include "arrivals.h"
+#include "options.h"
 
 namespace {
 
@@ -48,6 +50,7 @@ struct NcclApi {
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -75,6 +78,7 @@ NcclApi& nccl() {
         api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
         api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
         api.AllGather = (decltype(api.AllGather))sym("ncclAllGather");
+        api.Broadcast = (decltype(api.Broadcast))sym("ncclBroadcast");
         api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
         api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
         api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
@@ -141,7 +145,27 @@ struct oz2g_comm {
     ncclComm_t world = nullptr, row = nullptr, col = nullptr;
     int P = 1, rank = 0, R = 1, C = 1, r = 0, c = 0, device = 0;
     Buf a_blk, b_stage, b_blk;
+    // the input exchange's own stream and events (overlapped path)
+    cudaStream_t s_in = nullptr;
+    cudaEvent_t ev_start = nullptr;
+    oz2g::Arrivals arr;
     std::mutex mtx;
+    void ensure_stream() {
+        if (s_in) return;
+        CU_TRY(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+        CU_TRY(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+        CU_TRY(cudaEventCreateWithFlags(&arr.b, cudaEventDisableTiming));
+        for (cudaEvent_t& e : arr.a) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    void release_stream() {
+        if (!s_in) return;
+        cudaStreamSynchronize(s_in);
+        cudaStreamDestroy(s_in);
+        cudaEventDestroy(ev_start);
+        cudaEventDestroy(arr.b);
+        for (cudaEvent_t& e : arr.a) cudaEventDestroy(e);
+        s_in = nullptr;
+    }
 };
 
 namespace {
@@ -225,6 +249,7 @@ int oz2g_comm_destroy(oz2g_comm* cm) {
         if (cm->col) nccl().CommDestroy(cm->col);
         if (cm->world) nccl().CommDestroy(cm->world);
     }
+    cm->release_stream();
     cm->a_blk.release();
     cm->b_stage.release();
     cm->b_blk.release();
@@ -271,32 +296,80 @@ int oz2g_gemm_dist(int prec, int64_t m, int64_t n, int64_t k, const void* A, int
         const void* dA = A;
         const void* dB = B;
         int64_t lda_t = lda, ldb_t = ldb;
+        // Overlapped input exchange (option "dist_pipeline", default on): on the
+        // comm's own stream, B's column block first (all-gather in the column
+        // comm + interleave), then A's row block in row chunks — one
+        // ncclBroadcast per chunk from the rank whose shard holds it — each
+        // chunk's row scans and clearance products (run_gemm's chunked path)
+        // overlapping the broadcasts of the next ones.  Off: both blocks are
+        // all-gathered before the pipeline starts.
+        bool overlapped = false;
+        int64_t chunk_rows = 0;
+        int nchunks = 0;
         if (shards) {
             if (m % cm->P || n % cm->P)
                 throw CommFail{OZ2G_INVALID_ARGUMENT, "oz2g_gemm_dist: m and n must be multiples of the rank count"};
             const int64_t ms = m / cm->P, ns = n / cm->P;
             if (lda < k || ldb < ns) throw CommFail{OZ2G_INVALID_ARGUMENT, "dimension mismatch: leading dimension"};
-            // A row block r: all-gather of the C consecutive row shards of grid row r
+            // A row block r: the C consecutive row shards of grid row r
             char* ablk = (char*)cm->a_blk.get(esz * (size_t)(t.rows * k));
             char* bstg = (char*)cm->b_stage.get(esz * (size_t)(cm->R * k * ns));
             char* bblk = (char*)cm->b_blk.get(esz * (size_t)(k * t.cols));
             char* own_a = ablk + esz * (size_t)(cm->c * ms * k);   // in place: this rank's slot
             char* own_b = bstg + esz * (size_t)(cm->r * k * ns);
-            if (ms * k) CU_TRY(cudaMemcpy2DAsync(own_a, esz * k, A, esz * lda, esz * k, ms, cudaMemcpyDeviceToDevice, s));
-            if (k * ns) CU_TRY(cudaMemcpy2DAsync(own_b, esz * ns, B, esz * ldb, esz * ns, k, cudaMemcpyDeviceToDevice, s));
-            NCCL_TRY(nccl().GroupStart());
-            NCCL_TRY(nccl().AllGather(own_a, ablk, esz * (size_t)(ms * k), ncclUint8, cm->row, s));
-            NCCL_TRY(nccl().AllGather(own_b, bstg, esz * (size_t)(k * ns), ncclUint8, cm->col, s));
-            NCCL_TRY(nccl().GroupEnd());
+            // chunks: whole shards, split in two or four when a grid row has
+            // fewer than four shards (one shard: ragged last chunk allowed)
+            int per = cm->C >= 4 ? 1 : 4 / cm->C;
+            if (cm->C > 1 && ms % per) per = 1;
+            chunk_rows = cm->C == 1 ? (ms + per - 1) / per : ms / per;
+            nchunks = chunk_rows > 0 ? (int)((t.rows + chunk_rows - 1) / chunk_rows) : 0;
+            overlapped = oz2g::opt(oz2g::OPT_DIST_PIPELINE) != 0 && nchunks >= 1 &&
+                         nchunks <= oz2g::kMaxArrivalChunks && t.rows > 0 && t.cols > 0 && k > 0;
+            cudaStream_t si = s;
+            if (overlapped) {
+                cm->ensure_stream();
+                si = cm->s_in;
+                CU_TRY(cudaEventRecord(cm->ev_start, s));  // the shards are ready on the caller's stream
+                CU_TRY(cudaStreamWaitEvent(si, cm->ev_start, 0));
+            }
+            if (ms * k) CU_TRY(cudaMemcpy2DAsync(own_a, esz * k, A, esz * lda, esz * k, ms, cudaMemcpyDeviceToDevice, si));
+            if (k * ns) CU_TRY(cudaMemcpy2DAsync(own_b, esz * ns, B, esz * ldb, esz * ns, k, cudaMemcpyDeviceToDevice, si));
+            if (!overlapped) {
+                NCCL_TRY(nccl().GroupStart());
+                NCCL_TRY(nccl().AllGather(own_a, ablk, esz * (size_t)(ms * k), ncclUint8, cm->row, si));
+                NCCL_TRY(nccl().AllGather(own_b, bstg, esz * (size_t)(k * ns), ncclUint8, cm->col, si));
+                NCCL_TRY(nccl().GroupEnd());
+            } else {
+                NCCL_TRY(nccl().AllGather(own_b, bstg, esz * (size_t)(k * ns), ncclUint8, cm->col, si));
+            }
             // B column block c: the R gathered panels [r][k][ns] interleaved into row-major k x (R ns)
             for (int rr = 0; rr < cm->R && k * ns; ++rr)
                 CU_TRY(cudaMemcpy2DAsync(bblk + esz * (size_t)(rr * ns), esz * (size_t)t.cols,
                                          bstg + esz * (size_t)(rr * k * ns), esz * ns, esz * ns, k,
-                                         cudaMemcpyDeviceToDevice, s));
+                                         cudaMemcpyDeviceToDevice, si));
+            if (overlapped) {
+                CU_TRY(cudaEventRecord(cm->arr.b, si));
+                for (int q = 0; q < nchunks; ++q) {
+                    const int64_t r0 = q * chunk_rows, rc = std::min<int64_t>(chunk_rows, t.rows - r0);
+                    char* p = ablk + esz * (size_t)(r0 * k);
+                    NCCL_TRY(nccl().Broadcast(p, p, esz * (size_t)(rc * k), ncclUint8, (int)(r0 / ms), cm->row, si));
+                    CU_TRY(cudaEventRecord(cm->arr.a[q], si));
+                }
+                cm->arr.chunk_rows = chunk_rows;
+                cm->arr.nchunks = nchunks;
+            }
             dA = ablk;
             dB = bblk;
             lda_t = k;
             ldb_t = t.cols;
+        }
+        if (overlapped) {
+            std::string err;
+            const int r = oz2g::gemm_arrivals(prec, t.rows, t.cols, k, dA, lda_t, dB, ldb_t, C, ldc, nmod,
+                                              OZ2G_DEVICE_PTRS | (flags & OZ2G_TIMING), s, diag, nccl_reduce_hook, cm,
+                                              cm->arr, &err);
+            if (r != OZ2G_OK) throw CommFail{r, err};
+            return OZ2G_OK;
         }
         const unsigned f = OZ2G_DEVICE_PTRS | (flags & OZ2G_TIMING);
         int r = oz2g_gemm(prec, t.rows, t.cols, k, dA, lda_t, dB, ldb_t, C, ldc, nmod, f, stream, nullptr, diag,

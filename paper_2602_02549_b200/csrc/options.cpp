@@ -47,6 +47,7 @@ const Spec kSpecs[OPT_COUNT] = {
     {"rowscan_threads", 0, 0, 0, kRowscan},
     {"resid_stream", 0, 0, 1, nullptr},
     {"spec_tail", 1, 1, 3, nullptr},
+    {"dist_pipeline", 1, 0, 1, nullptr},
 };
 
 bool valid(const Spec& s, long long v) {

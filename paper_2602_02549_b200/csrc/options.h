@@ -27,6 +27,7 @@ enum Opt : int {
     OPT_ROWSCAN_THREADS,  // row-scan CTA size: 0 by row length, 256, 512 or 1024
     OPT_RESID_STREAM,     // 1: A residues per row block on a side stream beside the previous block's GEMMs
     OPT_SPEC_TAIL,        // host pipeline, rows + columns: halvings of the last column chunks (1..3)
+    OPT_DIST_PIPELINE,    // oz2g_gemm_dist: 1 A row chunks broadcast under the scans, 0 all-gathers first
     OPT_COUNT
 };
 

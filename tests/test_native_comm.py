@@ -98,17 +98,23 @@ def test_sharded_assembly_equals_single(tmp_path, world):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("dt", [torch.float64, torch.float32])
-def test_nccl_world1(cuda, oracle, dt):
+@pytest.mark.parametrize("dt,overlap,m", [(torch.float64, 1, 640), (torch.float32, 1, 640), (torch.float64, 0, 640),
+                                          (torch.float64, 1, 642), (torch.float64, 1, 4100)])
+def test_nccl_world1(cuda, oracle, dt, overlap, m):
+    """NCCL path at world size 1: with "dist_pipeline" A arrives in four row
+    chunks (ncclBroadcast each, ragged last chunk for m = 642) under the
+    chunked scans; without it the blocks are all-gathered first."""
     import paper_2602_02549_b200 as oz
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ["MASTER_PORT"] = str(_port())
     own = not dist.is_initialized()
     if own:
         dist.init_process_group("gloo", rank=0, world_size=1)
+    prev = oz.get_option("dist_pipeline")
+    oz.set_option("dist_pipeline", overlap)
     try:
         comm = pdist.NativeComm(dist, 1, 0)
-        m, k, n = 640, 300, 520
+        k, n = 300, 520
         npdt = np.float64 if dt == torch.float64 else np.float32
         A = oracle.gen_matrix(m, k, 1.0, 91, npdt)
         B = oracle.gen_matrix(k, n, 1.0, 92, npdt)
@@ -131,5 +137,6 @@ def test_nccl_world1(cuda, oracle, dt):
             comm.gemm(bad, dB, 14, m, n, out)
         comm.close()
     finally:
+        oz.set_option("dist_pipeline", prev)
         if own:
             dist.destroy_process_group()
