@@ -1091,7 +1091,10 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             fp.g.n = (int)n;
             fp.g.tiles_m = (int)((m + fused_tile_m() - 1) / fused_tile_m());
             fp.g.tiles_n = (int)((n + fused_tile_n() - 1) / fused_tile_n());
-            fp.g.group_m = group_m_for(fp.g.tiles_m, fp.g.tiles_n);
+            // the fused kernel rasters by tile-rows only (a "group_n" request
+            // falls back to the default tile-row groups)
+            const int gm = group_m_for(fp.g.tiles_m, fp.g.tiles_n);
+            fp.g.group_m = gm > 0 ? gm : std::max(1, std::min(16, fp.g.tiles_m));
             for (int l = 0; l < N; ++l) { fp.s1[l] = tab.s1[l]; fp.s2[l] = tab.s2[l]; }
             fp.P1 = tab.P1; fp.P2 = tab.P2; fp.P_inv = tab.P_inv;
             fp.mode = tab.mode;

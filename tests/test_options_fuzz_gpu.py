@@ -1,0 +1,67 @@
+"""Every tuning option leaves C unchanged: seeded
+random cases under a random combination of options — GEMM variant, fused CRT,
+graphs, PDL, raster grouping, L2 hints, CRT width, epilogue warps, pair
+stages, fences, row-scan width, streamed residues, W blocking, CRT overlap —
+compared bit for bit with the oracle (host pointers once, device pointers
+three times: plain, captured, replayed), and the same exception and message
+on the error paths.  OZ2G_OPTFUZZ_SEEDS scales the number of cases."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2602_02549_b200 as oz
+from test_fuzz_gpu import ORACLE_TO_OURS, _case
+
+pytestmark = pytest.mark.gpu
+
+CHOICES = {"gemm": [0, 1, 2], "fused": [0, 0, 1], "fused_mc": [0, 1], "fused_fence": [0, 1], "graph": [0, 1],
+           "pdl": [0, 1, 2], "group_m": [0, 1, 4, 16], "group_n": [0, 0, 2], "l2hint": [0, 1, 2, 3], "crt_cv": [4, 8],
+           "epi_warps": [0, 4, 8], "pair_stages": [4, 5, 6], "gemm_fence": [0, 1], "rowscan_threads": [0, 256, 1024],
+           "resid_stream": [0, 1], "wblock_min_mb": [0, 2048], "crt_overlap": [0, 0, 2]}
+
+
+def _options(rng):
+    return {name: int(rng.choice(vals)) for name, vals in CHOICES.items()}
+
+
+def _big_case(rng):
+    """Tall enough for the row-blocked residue GEMMs, streamed residues and
+    the CRT overlap (m > 2048)."""
+    m, k, n = int(rng.integers(2049, 4500)), int(rng.integers(1, 130)), int(rng.integers(1, 300))
+    dt = np.float64 if rng.random() < 0.7 else np.float32
+    N = int(rng.integers(2, 21 if dt == np.float64 else 17))
+    return m, k, n, dt, N, float(rng.choice([0.0, 0.5, 2.0]))
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("OZ2G_OPTFUZZ_SEEDS", "16"))))
+def test_options_fuzz(cuda, oracle, seed):
+    import torch
+    rng = np.random.default_rng(11000 + seed)
+    opts = _options(rng)
+    m, k, n, dt, N, phi = _big_case(rng) if seed % 4 == 3 else _case(rng)
+    A = oracle.gen_matrix(m, k, phi, 12000 + seed).astype(dt)
+    B = oracle.gen_matrix(k, n, phi, 13000 + seed).astype(dt)
+    try:
+        ref, ref_err = oracle.os_ii(A, B, N), None
+    except Exception as e:  # noqa: BLE001 - the device must raise the same
+        ref, ref_err = None, e
+    tdt = torch.float64 if dt == np.float64 else torch.float32
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    out = torch.empty((m, n), dtype=tdt, device="cuda")
+    with oz.options(**opts):
+        # the device output starts as NaN each time, so an output tile a kernel
+        # skipped cannot pass on a previous call's values
+        calls = [lambda: oz.os_ii(A, B, N).C] + [
+            lambda: (out.fill_(float("nan")), oz.os_ii(dA, dB, N, out=out), out.cpu().numpy())[2]] * 3
+        for i, call in enumerate(calls):
+            try:
+                got, got_err = call(), None
+            except Exception as e:  # noqa: BLE001
+                got, got_err = None, e
+            if ref_err is not None:
+                assert isinstance(got_err, ORACLE_TO_OURS[type(ref_err).__name__]), (opts, i, got_err, ref_err)
+                assert str(got_err) == str(ref_err), (opts, i)
+            else:
+                assert got_err is None, (opts, i, got_err)
+                assert np.array_equal(np.ascontiguousarray(got).view(np.uint8), ref.C.view(np.uint8)), (opts, i)
