@@ -1099,6 +1099,7 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             fp.P1 = tab.P1; fp.P2 = tab.P2; fp.P_inv = tab.P_inv;
             fp.mode = tab.mode;
             fp.probe = fused_mode() == 2 ? 1 : 0;
+            fp.dbg = opt(OPT_DEBUG_SYNC) ? 1 : 0;
             if (opt(OPT_FUSED_FENCE) != 0) {
                 fp.plane_sync = (unsigned long long*)ws.x_bmax.get(64) + 4;
                 CUDA_TRY(cudaMemsetAsync(fp.plane_sync, 0, 8, stream));
@@ -1108,12 +1109,20 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
             fp.C = dC;
             fp.ldc = ldc_d;
             fp.st = st;
-            // option "fused_mc" 0: one CTA per tile without the B multicast
+            // option "fused_mc" 1: CTA pairs sharing a multicast B tile (default 0: one CTA per tile)
             const bool mc = opt(OPT_FUSED_MC) != 0;
             const CUtensorMap tA = make_plane_map(ares, kp, m, N, fused_tile_m(), m * kp);
             const CUtensorMap tB = make_plane_map_mn(bres, n, ldn, kp, N, kp * ldn, fused_b_box_rows(mc));
             tm.span(5, stream, [&] { CUDA_TRY(launch_gemm_crt_fused(prec, tA, tB, fp, ws.num_sms, mc, stream)); });
             ++launches;
+            if (pipe && host) {  // the pipelined path downloads on its D2H stream (joined below)
+                const cudaEvent_t ec = ws.pool_event(evn++);
+                CUDA_TRY(cudaEventRecord(ec, stream));
+                CUDA_TRY(cudaStreamWaitEvent(ws.s_d2h, ec, 0));
+                tm.span(7, ws.s_d2h, [&] {
+                    CUDA_TRY(cudaMemcpy2DAsync(C, esz * ldc, dC, esz * n, esz * n, m, cudaMemcpyDeviceToHost, ws.s_d2h));
+                });
+            }
         } else if (rstream) {
             size_t ev_res = 0;  // event after the A residues of block bi
             for (size_t bi = 0; bi < nb; ++bi) {

@@ -8,6 +8,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -214,6 +215,13 @@ struct Timer {
     }
     template <class F>
     void span(int stage, cudaStream_t s, F&& f) {
+        if (opt(OPT_DEBUG_SYNC)) {  // diagnostics: each stage completes before the next is enqueued
+            std::fprintf(stderr, "oz2g: stage %d ...\n", stage);
+            f();
+            const cudaError_t e = cudaStreamSynchronize(s);
+            std::fprintf(stderr, "oz2g: stage %d done (%s)\n", stage, cudaGetErrorString(e));
+            return;
+        }
         if (!on) { f(); return; }
         cudaEvent_t a = rec(s);
         f();

@@ -31,6 +31,8 @@
 #include <cfloat>
 #include <cstdlib>
 
+#include <cstdio>
+
 #include "device_common.cuh"
 #include "kernels.h"
 
@@ -109,6 +111,29 @@ __device__ __forceinline__ double residue_wd(uint32_t v, uint32_t p, uint32_t ma
     return __dsub_rn(__hiloint2double(0x43300000, (int)biased), 4503599627370624.0);
 }
 
+// Diagnostics (FusedParams.dbg): a barrier wait bounded to ~2^32 clocks that
+// reports the stalled barrier and gives up instead of hanging.
+__device__ __noinline__ void mbar_wait_dbg(uint64_t* bar, uint32_t parity, int tag, int a, int b) {
+    const long long t0 = clock64();
+    for (;;) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, P1;\n\t}"
+            : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680) : "memory");
+        if (ok) return;
+        if (clock64() - t0 > (1ll << 32)) {
+            unsigned long long raw;
+            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(raw) : "r"(smem_u32(bar)));
+            if ((threadIdx.x & 31) == 0)
+                printf("oz2g fused stall: block %d warp %d barrier %d (parity %u) at %d / %d raw %016llx\n",
+                       (int)blockIdx.x, (int)(threadIdx.x >> 5), tag, parity, a, b, raw);
+            return;
+        }
+    }
+}
+
 // MC: CTAs run in clusters of 2 on vertically adjacent tiles that share the
 // B tile; each CTA loads half of the B stage's K-rows with .multicast::cluster
 // into both CTAs (B crosses L2 -> SM once per pair), and a stage is refilled
@@ -180,7 +205,8 @@ __global__ void __launch_bounds__(F_THREADS, 1)
                 }
                 __syncwarp();
                 for (int kb = 0; kb < G.kblocks; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1u);
+                    if (P.dbg) mbar_wait_dbg(&empty[stage], phase ^ 1u, 1, u, l);
+                    else mbar_wait(&empty[stage], phase ^ 1u);
                     if (lane == 0) {
                         mbar_arrive_expect_tx(&full[stage], FA_BYTES + FB_BYTES);
                         tma_load_3d(sA + stage * FA_BYTES, &tmA, &full[stage], kb * FBK, tm * FBM, l, G.hintA);
@@ -200,7 +226,8 @@ __global__ void __launch_bounds__(F_THREADS, 1)
         if (P.plane_sync && lane == 0 && g < steps_total) atomicAdd(P.plane_sync, (unsigned long long)(steps_total - g));
         if (MC) {  // every stage released by both CTAs before the pair may exit (the peer's commits target us)
             for (int s2 = 0; s2 < FSTAGES; ++s2) {
-                mbar_wait(&empty[stage], phase ^ 1u);
+                if (P.dbg) mbar_wait_dbg(&empty[stage], phase ^ 1u, 2, s2, stage);
+                else mbar_wait(&empty[stage], phase ^ 1u);
                 if (++stage == FSTAGES) { stage = 0; phase ^= 1u; }
             }
         }
@@ -214,11 +241,13 @@ __global__ void __launch_bounds__(F_THREADS, 1)
         for (int u = first; u < total; u += stride) {
             for (int l = 0; l < N; ++l, ++it) {
                 const int acc = it & 1;
-                mbar_wait(&tempty[acc], (uint32_t)((it >> 1) & 1) ^ 1u);
+                if (P.dbg) mbar_wait_dbg(&tempty[acc], (uint32_t)((it >> 1) & 1) ^ 1u, 3, u, l);
+                else mbar_wait(&tempty[acc], (uint32_t)((it >> 1) & 1) ^ 1u);
                 tc_fence_after();
                 const uint32_t dtmem = tmem_base + (uint32_t)(acc * FBN);
                 for (int kb = 0; kb < G.kblocks; ++kb) {
-                    mbar_wait(&full[stage], phase);
+                    if (P.dbg) mbar_wait_dbg(&full[stage], phase, 4, u, l);
+                    else mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     if (lane == 0) {
                         // descriptors = the stage-0 descriptor + the byte offset / 16 in the
@@ -259,7 +288,8 @@ __global__ void __launch_bounds__(F_THREADS, 1)
             double* c1x = c1s + (size_t)cgrp * 32 * FBM + quad * 32 + lane;
             for (int l = 0; l < N; ++l, ++it) {
                 const int acc = it & 1;
-                mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
+                if (P.dbg) mbar_wait_dbg(&tfull[acc], (uint32_t)((it >> 1) & 1), 5, u, l);
+                else mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
                 tc_fence_after();
                 if (P.probe == 1) {  // experiment: MMA + operand feed alone (no CRT; C not written)
                     tc_fence_before();

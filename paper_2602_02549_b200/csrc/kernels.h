@@ -147,6 +147,7 @@ struct FusedParams {
     void* C;                     // T [m][ldc]
     int64_t ldc;
     DevStatus* st;
+    int dbg;                     // diagnostics (option debug_sync): bounded barrier waits that report a stall
 };
 int fused_tile_m();
 int fused_tile_n();

@@ -30,7 +30,7 @@ const long long kRowscan[] = {0, 256, 512, 1024, kEnd};
 const Spec kSpecs[OPT_COUNT] = {
     {"gemm", 0, 0, 2, nullptr},
     {"fused", 0, 0, 2, nullptr},
-    {"fused_mc", 1, 0, 1, nullptr},
+    {"fused_mc", 0, 0, 1, nullptr},
     {"fused_fence", 1, 0, 1, nullptr},
     {"spec", -1, -1, 2, nullptr},
     {"graph", 1, 0, 1, nullptr},
@@ -48,6 +48,7 @@ const Spec kSpecs[OPT_COUNT] = {
     {"resid_stream", 0, 0, 1, nullptr},
     {"spec_tail", 1, 1, 3, nullptr},
     {"dist_pipeline", 1, 0, 1, nullptr},
+    {"debug_sync", 0, 0, 1, nullptr},
 };
 
 bool valid(const Spec& s, long long v) {

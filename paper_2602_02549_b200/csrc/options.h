@@ -10,7 +10,7 @@ namespace oz2g {
 enum Opt : int {
     OPT_GEMM,             // residue-GEMM kernel: 0 single-CTA 128x256 tiles, 1 CTA pair, 2 multicast cluster
     OPT_FUSED,            // 0 two-pass (GEMM epilogue + CRT pass), 1 CRT fused into the GEMM, 2 fused probe
-    OPT_FUSED_MC,         // fused kernel: 1 B-tile multicast in CTA pairs, 0 one CTA per tile
+    OPT_FUSED_MC,         // fused kernel: 0 one CTA per tile, 1 B-tile multicast in CTA pairs
     OPT_FUSED_FENCE,      // fused kernel: 1 plane fence, 0 off
     OPT_SPEC,             // host-pointer speculation: -1 by size, 0 off, 1 columns, 2 rows + columns
     OPT_GRAPH,            // CUDA-graph replays of repeated device-pointer calls: 1 on, 0 off
@@ -28,6 +28,7 @@ enum Opt : int {
     OPT_RESID_STREAM,     // 1: A residues per row block on a side stream beside the previous block's GEMMs
     OPT_SPEC_TAIL,        // host pipeline, rows + columns: halvings of the last column chunks (1..3)
     OPT_DIST_PIPELINE,    // oz2g_gemm_dist: 1 A row chunks broadcast under the scans, 0 all-gathers first
+    OPT_DEBUG_SYNC,       // diagnostics: 1 synchronises and reports after every stage (stderr)
     OPT_COUNT
 };
 

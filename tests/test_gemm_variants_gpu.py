@@ -49,7 +49,7 @@ VARIANTS = {
     "pair6-fence": {"OZ2G_GEMM": "pair", "OZ2G_PAIR_STAGES": "6", "OZ2G_GEMM_FENCE": "1"},
     "single-fence": {"OZ2G_GEMM_FENCE": "1"},
     # the fused residue-GEMM + CRT kernel without its B multicast / plane fence
-    "fused-no-mc": {"OZ2G_FUSED": "1", "OZ2G_FUSED_MC": "0"},
+    "fused-mc": {"OZ2G_FUSED": "1", "OZ2G_FUSED_MC": "1"},
     "fused-no-fence": {"OZ2G_FUSED": "1", "OZ2G_FUSED_FENCE": "0"},
 }
 
