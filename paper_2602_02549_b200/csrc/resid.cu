@@ -31,6 +31,7 @@
 // two entries, so the weight loads are broadcasts.
 #include "device_common.cuh"
 #include "kernels.h"
+#include "options.h"
 
 namespace oz2g {
 
@@ -99,6 +100,74 @@ __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2,
     return __byte_perm(lo, hi, 0x5410);
 }
 
+// ---------------------------------------------------------------------------
+// Fast path (every element of a thread's chunk with |A'| < 2^62, i.e. E <= 9:
+// the common case — |A'| < 2^(6 + mu_i - mu'_i) and the shift exceeds 56 only
+// for rows whose clearance maximum is tiny).  A' is formed as a 64-bit two's
+// complement integer x and written in balanced base-256 digits
+//   x = sum_t d_t 256^t,  d_t in [-128, 127]:  the bytes of
+//   z = (x + 0x80..80) ^ 0x80..80  (adding 128 per byte, then flipping bit 7)
+// so one set of constant weights per modulus serves every element — the
+// weights of G = 0, s = 0 of the table, read once per modulus and chunk (a
+// broadcast), not once per element.  S = sum_t d_t w_t (two dp4a.s32.s32,
+// |S| <= 2^17) then goes through the same exact fp32 reduction.  The p = 256
+// plane is d_0 itself (x mod 256 in [-128, 127]), no arithmetic.
+// ---------------------------------------------------------------------------
+struct FastDec {
+    uint32_t lo, hi;  // the balanced digits d_0..d_3 / d_4..d_7 as signed bytes
+};
+
+__device__ __forceinline__ FastDec fast_dec(double x, int shift, bool& ok) {
+    const uint64_t bits = (uint64_t)__double_as_longlong(x);
+    const int ef = (int)((bits >> 52) & 0x7ff);
+    const uint64_t mant = (bits & 0x000fffffffffffffull) | ((uint64_t)(ef != 0) << 52);
+    const int E = max(ef, 1) - 1075 + shift;
+    ok &= E <= 9 || mant == 0;
+    const uint64_t mag = E >= 0 ? mant << (E & 15) : mant >> min(-E, 63);
+    const uint64_t s = (uint64_t)((int64_t)bits >> 63);  // 0 or all ones
+    constexpr uint64_t C = 0x8080808080808080ull;
+    const uint64_t z = ((mag ^ s) + (C - s)) ^ C;  // ((sgn * mag) + C) ^ C
+    FastDec d;
+    d.lo = (uint32_t)z;
+    d.hi = (uint32_t)(z >> 32);
+    return d;
+}
+
+__device__ __forceinline__ int dp4a_ss(uint32_t a, int32_t b, int32_t c) {
+    int32_t d;
+    asm("dp4a.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+__device__ __forceinline__ uint32_t resid_fast(const FastDec& d, int2 w, float inv_p, uint32_t p) {
+    const int bits = dp4a_ss(d.hi, w.y, dp4a_ss(d.lo, w.x, 0x4B400000));  // bits of the float M + S
+    const float u = __fsub_rn(__int_as_float(bits), kMagic);
+    const float t = __fmaf_rn(u, inv_p, kMagic);
+    return (uint32_t)bits - (uint32_t)__float_as_int(t) * p;
+}
+
+// All N planes of one 8-element chunk from its balanced digits.
+__device__ __forceinline__ void write_fast(const FastDec (&f)[8], const ResidHeader& hd, const uint8_t* tab, int nmod,
+                                           int8_t* out, int64_t plane) {
+    int l0 = 0;
+    if (hd.p[0] == 256u) {  // the table's first modulus: the plane is d_0
+        *reinterpret_cast<uint2*>(out) =
+            make_uint2(pack4(f[0].lo, f[1].lo, f[2].lo, f[3].lo), pack4(f[4].lo, f[5].lo, f[6].lo, f[7].lo));
+        l0 = 1;
+    }
+#pragma unroll 2
+    for (int l = l0; l < nmod; ++l) {
+        const int2 w = *reinterpret_cast<const int2*>(tab + (size_t)l * kResidRow);  // G = 0, s = 0
+        const float ip = hd.inv_p[l];
+        const uint32_t p = hd.p[l];
+        const uint32_t w0 = pack4(resid_fast(f[0], w, ip, p), resid_fast(f[1], w, ip, p), resid_fast(f[2], w, ip, p),
+                                  resid_fast(f[3], w, ip, p));
+        const uint32_t w1 = pack4(resid_fast(f[4], w, ip, p), resid_fast(f[5], w, ip, p), resid_fast(f[6], w, ip, p),
+                                  resid_fast(f[7], w, ip, p));
+        *reinterpret_cast<uint2*>(out + (int64_t)l * plane) = make_uint2(w0, w1);
+    }
+}
+
 __device__ __forceinline__ void load_resid_consts(const ResidHeader* __restrict__ g, int n, uint8_t* sh) {
     const uint4* src = reinterpret_cast<const uint4*>(g);
     uint4* dst = reinterpret_cast<uint4*>(sh);
@@ -127,7 +196,8 @@ template <class T>
 __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t k,
                                                       int64_t kp, const int32_t* __restrict__ mu,
                                                       const ResidHeader* __restrict__ rc_g, int nmod,
-                                                      int8_t* __restrict__ planes, int64_t plane, DevStatus* st) {
+                                                      int8_t* __restrict__ planes, int64_t plane, DevStatus* st,
+                                                      int fast_on) {
     pdl_enter();
     extern __shared__ __align__(16) uint8_t sh[];
     load_resid_consts(rc_g, nmod, sh);
@@ -140,6 +210,33 @@ __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, i
     for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
         const int sft = mu[i];
         const T* row = A + i * lda + h0;
+        int8_t* out = planes + i * kp + h0;
+        const bool vec = h0 + RA_E <= k && ((reinterpret_cast<uintptr_t>(row) & 15) == 0);
+        if (fast_on && vec) {
+            FastDec f[RA_E];
+            bool ok = true;
+            if (sizeof(T) == 8) {
+#pragma unroll
+                for (int j = 0; j < RA_E; j += 2) {
+                    const double2 v = __ldg(reinterpret_cast<const double2*>(row + j));
+                    f[j] = fast_dec(v.x, sft, ok);
+                    f[j + 1] = fast_dec(v.y, sft, ok);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < RA_E; j += 4) {
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(row + j));
+                    f[j] = fast_dec((double)v.x, sft, ok);
+                    f[j + 1] = fast_dec((double)v.y, sft, ok);
+                    f[j + 2] = fast_dec((double)v.z, sft, ok);
+                    f[j + 3] = fast_dec((double)v.w, sft, ok);
+                }
+            }
+            if (ok) {
+                write_fast(f, hd, tab, nmod, out, plane);
+                continue;
+            }
+        }
         ElemDec d[RA_E];
         if (sizeof(T) == 8 && h0 + RA_E <= k && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
 #pragma unroll
@@ -161,7 +258,6 @@ __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, i
 #pragma unroll
             for (int j = 0; j < RA_E; ++j) d[j] = elem_dec(h0 + j < k ? ld_d(row + j) : 0.0, sft, ovf);
         }
-        int8_t* out = planes + i * kp + h0;
 #pragma unroll 2
         for (int l = 0; l < nmod; ++l) {
             const ModC c = modc(hd, l);
@@ -182,7 +278,7 @@ __global__ void __launch_bounds__(256) resid_rows_kernel(const T* __restrict__ X
                                                          int64_t ld_out, const int32_t* __restrict__ shift,
                                                          const ResidHeader* __restrict__ rc_g, int nmod,
                                                          int8_t* __restrict__ planes, int64_t plane, uint32_t err_bit,
-                                                         DevStatus* st) {
+                                                         DevStatus* st, int fast_on) {
     pdl_enter();
     extern __shared__ __align__(16) uint8_t sh[];
     if (OP == 1) {
@@ -248,6 +344,31 @@ __global__ void __launch_bounds__(256) resid_rows_kernel(const T* __restrict__ X
             }
             *reinterpret_cast<uint2*>(out) = make_uint2(w[0], w[1]);
             continue;
+        }
+        if (fast_on && vec) {
+            FastDec f[RA_E];
+            bool ok = true;
+            if (sizeof(T) == 8) {
+#pragma unroll
+                for (int j = 0; j < RA_E; j += 2) {
+                    const double2 t = __ldg(reinterpret_cast<const double2*>(row + j));
+                    f[j] = fast_dec(t.x, COLSHIFT ? csft[j] : rsft, ok);
+                    f[j + 1] = fast_dec(t.y, COLSHIFT ? csft[j + 1] : rsft, ok);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < RA_E; j += 4) {
+                    const float4 t = __ldg(reinterpret_cast<const float4*>(row + j));
+                    f[j] = fast_dec((double)t.x, COLSHIFT ? csft[j] : rsft, ok);
+                    f[j + 1] = fast_dec((double)t.y, COLSHIFT ? csft[j + 1] : rsft, ok);
+                    f[j + 2] = fast_dec((double)t.z, COLSHIFT ? csft[j + 2] : rsft, ok);
+                    f[j + 3] = fast_dec((double)t.w, COLSHIFT ? csft[j + 3] : rsft, ok);
+                }
+            }
+            if (ok) {
+                write_fast(f, hd, tab, nmod, out, plane);
+                continue;
+            }
         }
         // decode straight from the loads (no staging array: fewer live registers)
         ElemDec d[RA_E];
@@ -321,7 +442,8 @@ cudaError_t launch_rows(const void* X, int64_t ldx, int64_t rows_valid, int64_t 
     cudaError_t err = rows_grid(resid_rows_kernel<T, COLSHIFT, OP>, sm, rows_total, chunks, grid);
     if (err != cudaSuccess) return err;
     return launch_pdl(resid_rows_kernel<T, COLSHIFT, OP>, grid, dim3(256), sm, s, (const T*)X, ldx, rows_valid,
-                      rows_total, cols_valid, cols_out, ld_out, shift, rc, nmod, planes, plane, err_bit, st);
+                      rows_total, cols_valid, cols_out, ld_out, shift, rc, nmod, planes, plane, err_bit, st,
+                      (int)opt(OPT_RESID_FAST));
 }
 
 }  // namespace
@@ -360,11 +482,11 @@ cudaError_t launch_resid_A(int prec, const void* A, int64_t lda, int64_t m, int6
     if (prec) {
         if ((err = rows_grid(resid_A_kernel<double>, sm, m, chunks, grid)) != cudaSuccess) return err;
         return launch_pdl(resid_A_kernel<double>, grid, dim3(256), sm, s, (const double*)A, lda, m, k, kp, mu, rc_dev,
-                          nmod, planes, plane, st);
+                          nmod, planes, plane, st, (int)opt(OPT_RESID_FAST));
     }
     if ((err = rows_grid(resid_A_kernel<float>, sm, m, chunks, grid)) != cudaSuccess) return err;
     return launch_pdl(resid_A_kernel<float>, grid, dim3(256), sm, s, (const float*)A, lda, m, k, kp, mu, rc_dev, nmod,
-                      planes, plane, st);
+                      planes, plane, st, (int)opt(OPT_RESID_FAST));
 }
 
 }  // namespace oz2g

@@ -114,3 +114,45 @@ def test_pipelined_matches_oracle(cuda, oracle):
     ref = oracle.os_ii(A, B, 16)
     got = oz.os_ii(A, B, 16)
     assert np.array_equal(got.C.view(np.uint64), ref.C.view(np.uint64))
+
+
+def _mixed_exponent_pair(oracle, m, k, n, phi, seed, dt):
+    """Reference-generator A and B where every third row of A holds only its
+    column-0 entry, every third column of B only its row-1 entry, and A's
+    column 1 and B's row 0 are scaled by 2^-10: those rows / columns get a tiny
+    clearance maximum, hence a large shift and |A'| >= 2^62 (the
+    exponent-bucket path of the residue split), the others the balanced-digit
+    fast path."""
+    A = oracle.gen_matrix(m, k, phi, oracle.derive_seed(seed, 0, 0), dt).copy()
+    B = oracle.gen_matrix(k, n, phi, oracle.derive_seed(seed, 0, 1), dt).copy()
+    A[:, 1] *= dt(2.0 ** -10)
+    B[0, :] *= dt(2.0 ** -10)
+    A[::3, 1:] = 0
+    B[:1, ::3] = 0
+    B[2:, ::3] = 0
+    return A, B
+
+
+@pytest.mark.parametrize("m,k,n,phi,N,dt", [
+    (96, 520, 72, 0.0, 16, np.float64),
+    (40, 300, 33, 8.0, 20, np.float64),
+    (33, 100, 65, 0.5, 49, np.float64),
+    (64, 260, 48, 1.0, 8, np.float32),
+    (31, 77, 29, 2.0, 16, np.float32),
+])
+@pytest.mark.parametrize("fast", [1, 0])
+def test_residue_split_paths(cuda, oracle, m, k, n, phi, N, dt, fast):
+    """Both residue-split paths (resid.cu: balanced digits for |A'| < 2^62,
+    exponent buckets otherwise; option "resid_fast") give the reference's
+    residue planes, also when both occur in one matrix."""
+    seed = 77 * m + k
+    A, B = _mixed_exponent_pair(oracle, m, k, n, phi, seed, dt)
+    ref = oracle.os_ii(A, B, N, keep_intermediates=True, residues=True)
+    with oz.options(resid_fast=fast):
+        got = oz.os_ii(A, B, N, keep_intermediates=True, evidence=True)
+    _eq(got.scaling.mu, ref.inter["mu"])
+    _eq(got.scaling.nu, ref.inter["nu"])
+    _eq(got.crt.Ares, ref.inter["Ares"])
+    _eq(got.crt.Bres, ref.inter["Bres"])
+    _eq(got.crt.W, ref.inter["W"])
+    _eq(got.C, ref.C)
