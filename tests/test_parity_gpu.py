@@ -55,6 +55,10 @@ CASES = [
     # rows over 256 KB: the row scan held to one row per SM (scale.cu)
     (5, 40000, 3, 0.5, 12, np.float64),
     (4, 70000, 3, 2.0, 8, np.float32),
+    # rows of 8192 < kp <= 65536: the row scan over a cluster of 2 / 4 / 8 CTAs
+    (3, 12000, 5, 1.0, 14, np.float64),
+    (6, 30000, 4, 0.5, 16, np.float64),
+    (5, 50000, 3, 2.0, 8, np.float32),
 ]
 
 
