@@ -104,7 +104,8 @@ __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2,
 // Fast path (every element of a thread's chunk with |A'| < 2^62, i.e. E <= 9:
 // the common case — |A'| < 2^(6 + mu_i - mu'_i) and the shift exceeds 56 only
 // for rows whose clearance maximum is tiny).  A' is formed as a 64-bit two's
-// complement integer x and written in balanced base-256 digits
+// complement integer x (one fp64 multiply by 2^shift and a truncating
+// conversion) and written in balanced base-256 digits
 //   x = sum_t d_t 256^t,  d_t in [-128, 127]:  the bytes of
 //   z = (x + 0x80..80) ^ 0x80..80  (adding 128 per byte, then flipping bit 7)
 // so one set of constant weights per modulus serves every element — the
@@ -118,15 +119,13 @@ struct FastDec {
 };
 
 __device__ __forceinline__ FastDec fast_dec(double x, int shift, bool& ok) {
-    const uint64_t bits = (uint64_t)__double_as_longlong(x);
-    const int ef = (int)((bits >> 52) & 0x7ff);
-    const uint64_t mant = (bits & 0x000fffffffffffffull) | ((uint64_t)(ef != 0) << 52);
-    const int E = max(ef, 1) - 1075 + shift;
-    ok &= E <= 9 || mant == 0;
-    const uint64_t mag = E >= 0 ? mant << (E & 15) : mant >> min(-E, 63);
-    const uint64_t s = (uint64_t)((int64_t)bits >> 63);  // 0 or all ones
+    // A' = trunc(x 2^shift): the product is exact unless it is subnormal, and
+    // then |A'| < 1 truncates to 0 either way (one DMUL, one F2I.S64.TRUNC)
+    ok &= pow2_normal(shift);
+    const double y = __dmul_rn(x, pow2d(shift));
+    ok &= (uint32_t)(__double2hiint(y) & 0x7fffffff) < 0x43D00000u;  // |y| < 2^62 (also rejects inf / nan)
     constexpr uint64_t C = 0x8080808080808080ull;
-    const uint64_t z = ((mag ^ s) + (C - s)) ^ C;  // ((sgn * mag) + C) ^ C
+    const uint64_t z = ((uint64_t)__double2ll_rz(y) + C) ^ C;  // balanced digits
     FastDec d;
     d.lo = (uint32_t)z;
     d.hi = (uint32_t)(z >> 32);
@@ -273,7 +272,7 @@ __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, i
 }
 
 template <class T, bool COLSHIFT, int OP>
-__global__ void __launch_bounds__(256) resid_rows_kernel(const T* __restrict__ X, int64_t ldx, int64_t rows_valid,
+__global__ void __launch_bounds__(256, 4) resid_rows_kernel(const T* __restrict__ X, int64_t ldx, int64_t rows_valid,
                                                          int64_t rows_total, int64_t cols_valid, int64_t cols_out,
                                                          int64_t ld_out, const int32_t* __restrict__ shift,
                                                          const ResidHeader* __restrict__ rc_g, int nmod,
