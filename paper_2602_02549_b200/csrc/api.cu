@@ -97,6 +97,8 @@ std::vector<uint8_t> build_resid_consts(const Table& t) {
                 cell[1] = w[4] | (w[5] << 8) | (w[6] << 16) | (w[7] << 24);
             }
         }
+        const uint32_t* c0 = tab + 2 * ((size_t)l * kResidE8 * 2);  // G = 0, s = 0
+        h->fm[l] = FastMod{(int32_t)c0[0], (int32_t)c0[1], h->inv_p[l], 0u - p};
     }
     return buf;
 }

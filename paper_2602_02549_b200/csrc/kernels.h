@@ -62,10 +62,18 @@ cudaError_t launch_gemm_i8_pair(int mode, const CUtensorMap& tmA, const CUtensor
 // header followed by the weight table w[l][G][s] (G in [0, kResidE8), s = sign)
 // of two packed words whose signed bytes are the symmetric representatives of
 // (-1)^s 2^(8 (t + G)) mod p_l, t = 0..7 (resid.cu explains the arithmetic).
+// Per-modulus constants of the balanced-digit path (resid.cu), one 16-byte
+// load: the weights of G = 0, s = 0, RN32(1 / p) and -p (mod 2^32).
+struct alignas(16) FastMod {
+    int32_t w0, w1;
+    float inv_p;
+    uint32_t negp;
+};
 struct alignas(16) ResidHeader {  // size a multiple of 16: the table that follows is read as int2/uint4
     int n, pad;
     uint32_t p[49];
     float inv_p[49];  // RN32(1 / p)
+    FastMod fm[49];
 };
 constexpr int kResidE8 = 16;  // E' / 8 <= 15: |A'| < 2^(6 + P') and P' < 171 for N <= 49
 constexpr int kResidRow = kResidE8 * 2 * 8;  // bytes per modulus: [G][sign][8 bytes]

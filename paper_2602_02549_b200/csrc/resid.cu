@@ -138,16 +138,24 @@ __device__ __forceinline__ int dp4a_ss(uint32_t a, int32_t b, int32_t c) {
     return d;
 }
 
-__device__ __forceinline__ uint32_t resid_fast(const FastDec& d, int2 w, float inv_p, uint32_t p) {
-    const int bits = dp4a_ss(d.hi, w.y, dp4a_ss(d.lo, w.x, 0x4B400000));  // bits of the float M + S
+// a * b + c (mod 2^32), opaque to the compiler (which would otherwise negate
+// each product instead of using the negated modulus once)
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+__device__ __forceinline__ uint32_t resid_fast(const FastDec& d, const FastMod& f) {
+    const int bits = dp4a_ss(d.hi, f.w1, dp4a_ss(d.lo, f.w0, 0x4B400000));  // bits of the float M + S
     const float u = __fsub_rn(__int_as_float(bits), kMagic);
-    const float t = __fmaf_rn(u, inv_p, kMagic);
-    return (uint32_t)bits - (uint32_t)__float_as_int(t) * p;
+    const float t = __fmaf_rn(u, f.inv_p, kMagic);
+    return mad_u32(__float_as_uint(t), f.negp, (uint32_t)bits);
 }
 
 // All N planes of one 8-element chunk from its balanced digits.
-__device__ __forceinline__ void write_fast(const FastDec (&f)[8], const ResidHeader& hd, const uint8_t* tab, int nmod,
-                                           int8_t* out, int64_t plane) {
+__device__ __forceinline__ void write_fast(const FastDec (&f)[8], const ResidHeader& hd, int nmod, int8_t* out,
+                                           int64_t plane) {
     int l0 = 0;
     if (hd.p[0] == 256u) {  // the table's first modulus: the plane is d_0
         *reinterpret_cast<uint2*>(out) =
@@ -156,13 +164,9 @@ __device__ __forceinline__ void write_fast(const FastDec (&f)[8], const ResidHea
     }
 #pragma unroll 2
     for (int l = l0; l < nmod; ++l) {
-        const int2 w = *reinterpret_cast<const int2*>(tab + (size_t)l * kResidRow);  // G = 0, s = 0
-        const float ip = hd.inv_p[l];
-        const uint32_t p = hd.p[l];
-        const uint32_t w0 = pack4(resid_fast(f[0], w, ip, p), resid_fast(f[1], w, ip, p), resid_fast(f[2], w, ip, p),
-                                  resid_fast(f[3], w, ip, p));
-        const uint32_t w1 = pack4(resid_fast(f[4], w, ip, p), resid_fast(f[5], w, ip, p), resid_fast(f[6], w, ip, p),
-                                  resid_fast(f[7], w, ip, p));
+        const FastMod fm = hd.fm[l];  // one 16-byte broadcast load per modulus
+        const uint32_t w0 = pack4(resid_fast(f[0], fm), resid_fast(f[1], fm), resid_fast(f[2], fm), resid_fast(f[3], fm));
+        const uint32_t w1 = pack4(resid_fast(f[4], fm), resid_fast(f[5], fm), resid_fast(f[6], fm), resid_fast(f[7], fm));
         *reinterpret_cast<uint2*>(out + (int64_t)l * plane) = make_uint2(w0, w1);
     }
 }
@@ -232,7 +236,7 @@ __global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, i
                 }
             }
             if (ok) {
-                write_fast(f, hd, tab, nmod, out, plane);
+                write_fast(f, hd, nmod, out, plane);
                 continue;
             }
         }
@@ -365,7 +369,7 @@ __global__ void __launch_bounds__(256, 4) resid_rows_kernel(const T* __restrict_
                 }
             }
             if (ok) {
-                write_fast(f, hd, tab, nmod, out, plane);
+                write_fast(f, hd, nmod, out, plane);
                 continue;
             }
         }
