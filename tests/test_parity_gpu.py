@@ -160,4 +160,3 @@ def test_residue_split_paths(cuda, oracle, m, k, n, phi, N, dt, fast):
     _eq(got.crt.Bres, ref.inter["Bres"])
     _eq(got.crt.W, ref.inter["W"])
     _eq(got.C, ref.C)
-
