@@ -1,6 +1,6 @@
 # Round artifacts on one B200 (gpurun -- 'bash scripts/gpurun_round.sh'): GPU test suite, smoke(),
 # the default bench line, the reference arm, the launch list, ncu --set full captures of the residue GEMM,
-# the auxiliary kernels and the fused kernel, the INT8 peak, every BASELINE config, the multi-GPU tile
+# the auxiliary kernels at 16384^3 and cfg5, the INT8 peak, every BASELINE config, the multi-GPU tile
 # projection and kernel timelines.  Outputs in gpurun_out/r2_*; the summaries go to profiles/.
 set -x
 mkdir -p gpurun_out
@@ -17,8 +17,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 B1="--steps 1 --warmup 3 --moduli 16 --no-cpu-baseline --no-e2e --no-native --no-int8-peak"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:gemm_i8_tc -s 1 -c 1 -o ${R}_gemm python bench.py $B1 > /dev/null 2>&1; echo gemm=$?
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"row_scan|col_max|resid_rows|resid_A|crt" -c 6 -o ${R}_aux python bench.py $B1 > /dev/null 2>&1; echo aux=$?
-OZ2G_FUSED=1 timeout 900 ncu --set full --import-source on --clock-control none -k regex:gemm_crt_fused -c 1 -o ${R}_fused python bench.py $B1 --steps 1 --warmup 0 > /dev/null 2>&1; echo fused=$?
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"row_scan|col_max|resid_rows|resid_A|crt" -c 6 -o ${R}_aux_cfg5 python bench.py $B1 --m 2048 --k 65536 > /dev/null 2>&1; echo aux5=$?
+B5="--steps 2 --warmup 3 --moduli 16 --m 2048 --k 65536 --no-cpu-baseline --no-e2e --no-native --no-int8-peak"
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv --log-file ${R}_launches_cfg5.csv python bench.py $B5 > /dev/null 2>&1; echo launches5=$?
 timeout 900 python scripts/configs.py --out ${R}_configs.jsonl > /dev/null 2>&1; echo configs=$?
-timeout 600 python scripts/experiments/tile_projection.py > ${R}_tile_projection.jsonl 2>/dev/null; echo proj=$?
+timeout 900 python scripts/experiments/tile_projection.py > ${R}_tile_projection.jsonl 2>/dev/null; echo proj=$?
 timeout 300 python scripts/timeline.py --m 16384 --out ${R}_tl_16384.json > /dev/null 2>&1; echo tl=$?
 timeout 300 python scripts/timeline.py --m 1024 --moduli 14 --calls 5 --out ${R}_tl_1024.json > /dev/null 2>&1; echo tl1=$?
