@@ -123,6 +123,23 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
         int eai = 0;
         if (BND) { RAi = ex.bnd.v.RA[i]; PAi = ex.bnd.v.PA[i]; eai = ex.bnd.v.ea[i]; }
         bool fr_range = false, inv_range = false, sub = false;
+        // the column shifts of this thread (two 16-byte loads when whole and aligned)
+        int nuv[CV];
+        if (jn == CV && (reinterpret_cast<uintptr_t>(nu + j0) & 15) == 0) {
+#pragma unroll
+            for (int b = 0; b < CV; b += 4) {
+                const int4 v = __ldg(reinterpret_cast<const int4*>(nu + j0 + b));
+                nuv[b] = v.x; nuv[b + 1] = v.y; nuv[b + 2] = v.z; nuv[b + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int b = 0; b < CV; ++b) nuv[b] = b < jn ? __ldg(nu + j0 + b) : 0;
+        }
+        // 2^-mu_i and every 2^-nu_j normal: each ldexp is one multiplication (ldexp_rn's own fast path)
+        bool fastsc = pow2_normal(-mui);
+#pragma unroll
+        for (int b = 0; b < CV; ++b) fastsc &= pow2_normal(-nuv[b]);
+        const double pmu = fastsc ? pow2d(-mui) : 0.0;
         T yv[CV];  // this thread's C entries, stored together below
 #pragma unroll
         for (int b = 0; b < CV; ++b) {
@@ -131,10 +148,11 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
             const int64_t j = j0 + b;
             // crt.hpp:113-119, round_nearest_even (softfp.hpp:94-102): rint,
             // except that the reference's floor(x) + 1 returns +0.0 for x in
-            // [-0.5, -0.0) where rint gives -0.0 (C'' and C are the same either way)
+            // [-0.5, -0.0) where rint gives -0.0; adding +0.0 maps exactly that
+            // -0.0 to +0.0 (qx itself is never -0.0: C1 is an fma chain from
+            // +0.0 with s1_l > 0, so an exact zero sum is +0.0)
             const double qx = __dmul_rn(cc.P_inv, c1[b]);
-            double q = rint(qx);
-            if (q == 0.0 && qx != 0.0) q = 0.0;
+            const double q = __dadd_rn(rint(qx), 0.0);
             const double t1 = __fma_rn(-q, cc.P1, c1[b]);         // crt.hpp:136-138
             const double t2 = __dadd_rn(t1, c2[b]);
             const double cpp = __fma_rn(-q, cc.P2, t2);
@@ -145,7 +163,7 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
                 if (ex.Q) ex.Q[o] = q;
                 if (ex.Cpp64) ex.Cpp64[o] = cpp;
             }
-            const int nuj = __ldg(nu + j);
+            const int nuj = nuv[b];
             if (BND) {
                 const BoundCtx& bc = ex.bnd;
                 const double PBj = bc.v.PB[j], CBj = bc.v.CB[j];
@@ -180,10 +198,16 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
                 sub |= (x != 0.0f && fabsf(x) < FLT_MIN) || (y != 0.0f && fabsf(y) < FLT_MIN);
                 yv[b] = y;
             } else {
-                const double x = ldexp_rn(cpp, -mui);
-                const double y = ldexp_rn(x, -nuj);
-                inv_range |= !isfinite(x) || !isfinite(y);
-                sub |= (x != 0.0 && fabs(x) < DBL_MIN) || (y != 0.0 && fabs(y) < DBL_MIN);
+                const double x = fastsc ? __dmul_rn(cpp, pmu) : ldexp_rn(cpp, -mui);
+                const double y = fastsc ? __dmul_rn(x, pow2d(-nuj)) : ldexp_rn(x, -nuj);
+                // exponent field 0 (zero, subnormal) or 0x7ff (inf, nan) in either: check
+                // precisely (integer test on the high words; rarely taken)
+                const uint32_t ux = ((uint32_t)__double2hiint(x) >> 20) & 0x7ffu;
+                const uint32_t uy = ((uint32_t)__double2hiint(y) >> 20) & 0x7ffu;
+                if (((ux + 1u) & 0x7feu) == 0u || ((uy + 1u) & 0x7feu) == 0u) {
+                    inv_range |= !isfinite(x) || !isfinite(y);
+                    sub |= (x != 0.0 && fabs(x) < DBL_MIN) || (y != 0.0 && fabs(y) < DBL_MIN);
+                }
                 yv[b] = y;
             }
         }
