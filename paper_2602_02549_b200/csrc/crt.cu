@@ -56,6 +56,16 @@ __device__ __forceinline__ double i8_to_f64_fp(uint32_t wx, int b) {
     return __dsub_rn(__hiloint2double(0x43300000, (int)lo), 4503599627370624.0);
 }
 
+// Byte t of w as a signed int8 -> fp64 with one I2F.F64.S8 (XU) reading the
+// byte in place (a plain C cast of byte 0 compiled to two PRMTs and an S16
+// conversion here).
+__device__ __forceinline__ double i8_to_f64_xu(uint32_t w, int t) {
+    if (t != 0) return (double)(int8_t)((w >> (8 * t)) & 0xffu);  // folds into I2F.F64.S8 R.Bt
+    double r;
+    asm("{.reg .s8 b; cvt.s8.u32 b, %1; cvt.rn.f64.s8 %0, b;}" : "=d"(r) : "r"(w));
+    return r;
+}
+
 // NFP of the CV columns convert through i8_to_f64_fp, the rest with I2F (XU):
 // XU converts 16 values/clk/SM, the fp64 pipe 64, so splitting balances them.
 // 8 columns per thread: capped at 64 registers (4 CTAs per SM; the kernel is
@@ -93,8 +103,7 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
 #pragma unroll
             for (int b = 0; b < CV; ++b) {
                 const uint32_t w32 = b < 4 ? wlo : whi;
-                const double wv = b >= CV - NFP ? i8_to_f64_fp(b < 4 ? xx : xy, b & 3)
-                                                : (double)(int8_t)((w32 >> (8 * (b & 3))) & 0xffu);
+                const double wv = b >= CV - NFP ? i8_to_f64_fp(b < 4 ? xx : xy, b & 3) : i8_to_f64_xu(w32, b & 3);
                 c1[b] = __fma_rn(s1, wv, c1[b]);
                 if (DD) c2[b] = __fma_rn(s2, wv, c2[b]);
             }
