@@ -154,6 +154,16 @@ __device__ __forceinline__ uint32_t resid_fast(const FastDec& d, const FastMod& 
 }
 
 // All N planes of one 8-element chunk from its balanced digits.
+// Four digits: every element of the chunk has d_4 = .. = d_7 = 0 (|A'| within
+// [-0x80808080, 0x7F7F7F7F]), so one dp4a per element and modulus.
+__device__ __forceinline__ uint32_t resid_fast4(uint32_t lo, const FastMod& f) {
+    const int bits = dp4a_ss(lo, f.w0, 0x4B400000);
+    const float u = __fsub_rn(__int_as_float(bits), kMagic);
+    const float t = __fmaf_rn(u, f.inv_p, kMagic);
+    return mad_u32(__float_as_uint(t), f.negp, (uint32_t)bits);
+}
+
+// All N planes of one 8-element chunk from its balanced digits.
 __device__ __forceinline__ void write_fast(const FastDec (&f)[8], const ResidHeader& hd, int nmod, int8_t* out,
                                            int64_t plane) {
     int l0 = 0;
@@ -161,6 +171,19 @@ __device__ __forceinline__ void write_fast(const FastDec (&f)[8], const ResidHea
         *reinterpret_cast<uint2*>(out) =
             make_uint2(pack4(f[0].lo, f[1].lo, f[2].lo, f[3].lo), pack4(f[4].lo, f[5].lo, f[6].lo, f[7].lo));
         l0 = 1;
+    }
+    const uint32_t hi = f[0].hi | f[1].hi | f[2].hi | f[3].hi | f[4].hi | f[5].hi | f[6].hi | f[7].hi;
+    if (hi == 0u) {  // small |A'| (fp32 inputs, few moduli): four digits
+#pragma unroll 2
+        for (int l = l0; l < nmod; ++l) {
+            const FastMod fm = hd.fm[l];
+            const uint32_t w0 = pack4(resid_fast4(f[0].lo, fm), resid_fast4(f[1].lo, fm), resid_fast4(f[2].lo, fm),
+                                      resid_fast4(f[3].lo, fm));
+            const uint32_t w1 = pack4(resid_fast4(f[4].lo, fm), resid_fast4(f[5].lo, fm), resid_fast4(f[6].lo, fm),
+                                      resid_fast4(f[7].lo, fm));
+            *reinterpret_cast<uint2*>(out + (int64_t)l * plane) = make_uint2(w0, w1);
+        }
+        return;
     }
 #pragma unroll 2
     for (int l = l0; l < nmod; ++l) {
