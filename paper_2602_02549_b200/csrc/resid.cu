@@ -219,7 +219,7 @@ constexpr int RA_E = 8;
 // A: the row-shift case of the writer below, kept as its own kernel (48
 // registers, 5 CTAs per SM; the general one needs 60).
 template <class T>
-__global__ void __launch_bounds__(256) resid_A_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t k,
+__global__ void __launch_bounds__(256, 4) resid_A_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t k,
                                                       int64_t kp, const int32_t* __restrict__ mu,
                                                       const ResidHeader* __restrict__ rc_g, int nmod,
                                                       int8_t* __restrict__ planes, int64_t plane, DevStatus* st,
