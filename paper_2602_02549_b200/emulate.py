@@ -192,6 +192,17 @@ class EmulationResult:
 _NO_HOOK = _lib.REDUCE_FN()  # the null oz2g_reduce_maxima_fn
 
 
+def _current_stream(t) -> int:
+    """The caller's current CUDA stream on the device of tensor `t` (raw
+    handle; torch's internal accessor is ~30x cheaper than
+    torch.cuda.current_stream(...).cuda_stream, which is the fallback)."""
+    import torch
+    get = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if get is not None:
+        return int(get(t.get_device()))
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
 def _is_torch_cuda(x) -> bool:
     return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
 
@@ -251,7 +262,7 @@ def os_ii(a, b, n: int, keep_intermediates: bool = False, *, evidence: bool = Fa
         lda, ldb, ldc = max(a.stride(0), k), max(b.stride(0), nn), max(C_out.stride(0), nn)
         flags = _lib.OZ2G_DEVICE_PTRS
         if stream is None:
-            stream = torch.cuda.current_stream(a.device).cuda_stream
+            stream = _current_stream(a)
     else:
         a = np.asarray(a)
         b = np.asarray(b)
