@@ -144,11 +144,14 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
 #pragma unroll
             for (int b = 0; b < CV; ++b) nuv[b] = b < jn ? __ldg(nu + j0 + b) : 0;
         }
-        // 2^-mu_i and every 2^-nu_j normal: each ldexp is one multiplication (ldexp_rn's own fast path)
-        bool fastsc = pow2_normal(-mui);
+        // 2^-mu_i and every 2^-nu_j normal (in T): each ldexp is one
+        // multiplication (ldexp_rn's / ldexpf_rn's own fast path)
+        auto p2ok = [](int e) { return sizeof(T) == 4 ? (e >= -126 && e <= 127) : pow2_normal(e); };
+        bool fastsc = p2ok(-mui);
 #pragma unroll
-        for (int b = 0; b < CV; ++b) fastsc &= pow2_normal(-nuv[b]);
-        const double pmu = fastsc ? pow2d(-mui) : 0.0;
+        for (int b = 0; b < CV; ++b) fastsc &= p2ok(-nuv[b]);
+        const double pmu = fastsc && sizeof(T) == 8 ? pow2d(-mui) : 0.0;
+        const float pmuf = fastsc && sizeof(T) == 4 ? pow2f(-mui) : 0.0f;
         T yv[CV];  // this thread's C entries, stored together below
 #pragma unroll
         for (int b = 0; b < CV; ++b) {
@@ -201,10 +204,13 @@ __global__ void __launch_bounds__(256, CV == 8 ? 4 : 1) crt_kernel(const int8_t*
                 if (fabs(cpp) >= 0x1.ffffffp+127) { fr_range = true; continue; }  // crt.hpp:144-145
                 const float c32 = __double2float_rn(cpp);
                 if (INTER && ex.Cpp32) ex.Cpp32[o] = c32;
-                const float x = ldexpf_rn(c32, -mui);                             // emulate.hpp:37-38
-                const float y = ldexpf_rn(x, -nuj);
-                inv_range |= !isfinite(x) || !isfinite(y);
-                sub |= (x != 0.0f && fabsf(x) < FLT_MIN) || (y != 0.0f && fabsf(y) < FLT_MIN);
+                const float x = fastsc ? __fmul_rn(c32, pmuf) : ldexpf_rn(c32, -mui);  // emulate.hpp:37-38
+                const float y = fastsc ? __fmul_rn(x, pow2f(-nuj)) : ldexpf_rn(x, -nuj);
+                const uint32_t ux = (__float_as_uint(x) >> 23) & 0xffu, uy = (__float_as_uint(y) >> 23) & 0xffu;
+                if (((ux + 1u) & 0xfeu) == 0u || ((uy + 1u) & 0xfeu) == 0u) {  // zero / subnormal / inf / nan
+                    inv_range |= !isfinite(x) || !isfinite(y);
+                    sub |= (x != 0.0f && fabsf(x) < FLT_MIN) || (y != 0.0f && fabsf(y) < FLT_MIN);
+                }
                 yv[b] = y;
             } else {
                 const double x = fastsc ? __dmul_rn(cpp, pmu) : ldexp_rn(cpp, -mui);
