@@ -87,9 +87,11 @@ def test_concurrent_pipelined_calls(cuda, oracle):
             assert np.array_equal(np.asarray(got).view(np.uint64), refs[i].view(np.uint64))
 
 
-def test_caller_stream_ordering(cuda, oracle):
+@pytest.mark.parametrize("explicit", [True, False])
+def test_caller_stream_ordering(cuda, oracle, explicit):
     """Inputs produced on the caller's stream are consumed in order on it, and
-    the result is ready on that stream when the call returns."""
+    the result is ready on that stream when the call returns (the stream
+    passed, or torch's current stream when none is)."""
     import torch
     A = oracle.gen_matrix(100, 80, 0.5, 701)
     B = oracle.gen_matrix(80, 60, 0.5, 702)
@@ -101,7 +103,7 @@ def test_caller_stream_ordering(cuda, oracle):
         da.copy_(torch.from_numpy(A).pin_memory(), non_blocking=True)
         db.copy_(torch.from_numpy(B).pin_memory(), non_blocking=True)
         out = torch.empty((100, 60), dtype=torch.float64, device="cuda")
-        oz.os_ii(da, db, 14, out=out, stream=s.cuda_stream)
+        oz.os_ii(da, db, 14, out=out, stream=s.cuda_stream if explicit else None)
         host = torch.empty((100, 60), dtype=torch.float64).pin_memory()
         host.copy_(out, non_blocking=True)
     s.synchronize()
