@@ -6,6 +6,7 @@ first value's bit for bit.  One JSON line per shape.
     python scripts/option_ab.py resid_stream 0,1 16384x16384x16384x16 8192x16384x4096x16 [--rounds 3]
     python scripts/option_ab.py spec_tail 1,2,3 16384x16384x16384x16 --host   # end to end (pinned host
                                                                                # buffers, wall clock)
+    python scripts/option_ab.py gemm+pair_stages+gemm_fence 0:4:0,1:6:1 16384x16384x16384x16   # option sets
 """
 import argparse
 import json
@@ -31,7 +32,8 @@ def main():
     import paper_2602_02549_b200 as oz
     from bench import gen_device
     dev = torch.device("cuda", 0)
-    values = [int(v) for v in a.values.split(",")]
+    names = a.option.split("+")
+    values = a.values.split(",")  # one value per name, ':'-separated
     for shape in a.shapes:
         m, k, n, N = (int(x) for x in shape.split("x"))
         A = gen_device(m, k, 0.0, 1234, torch.float64, dev)
@@ -49,7 +51,8 @@ def main():
         ref, ms = None, {v: [] for v in values}
         for _ in range(a.rounds):
             for v in values:
-                oz.set_option(a.option, v)
+                for nm, x in zip(names, v.split(":")):
+                    oz.set_option(nm, int(x))
                 for _ in range(2):
                     oz.os_ii(args[0], args[1], N, out=args[2])
                 torch.cuda.synchronize()
