@@ -9,6 +9,11 @@
 //                in B's own layout, planes [l][kp][ldn] (MN-major for the GEMM).
 //   bbar         ceil_abs_scale_cols (scaling.hpp:122-131) -> Bbar [kp][ldn].
 //
+// Two decompositions of A' feed the same exact reduction: balanced base-256
+// digits with one weight set per modulus (the fast path below, every chunk of
+// 8 elements with |A'| < 2^62 — practically all of them), and the exponent
+// buckets described here (the rest, or option resid_fast = 0).
+//
 // Residue arithmetic.  |A'| = m' * 2^E' with m' < 2^53 (m' = mant >> -E if
 // E < 0, E' = max(E, 0)); write it as g * 2^(8 G) with g = m' << (E' mod 8)
 // < 2^60 and G = E' / 8.  With the signed byte weights
@@ -111,8 +116,9 @@ __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2,
 // so one set of constant weights per modulus serves every element — the
 // weights of G = 0, s = 0 of the table, read once per modulus and chunk (a
 // broadcast), not once per element.  S = sum_t d_t w_t (two dp4a.s32.s32,
-// |S| <= 2^17) then goes through the same exact fp32 reduction.  The p = 256
-// plane is d_0 itself (x mod 256 in [-128, 127]), no arithmetic.
+// |S| <= 2^17; one when d_4..d_7 = 0 for the whole chunk) then goes through the
+// same exact fp32 reduction.  The p = 256 plane is d_0 itself (x mod 256 in
+// [-128, 127]), no arithmetic.
 // ---------------------------------------------------------------------------
 struct FastDec {
     uint32_t lo, hi;  // the balanced digits d_0..d_3 / d_4..d_7 as signed bytes
