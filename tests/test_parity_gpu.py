@@ -143,6 +143,8 @@ def _mixed_exponent_pair(oracle, m, k, n, phi, seed, dt):
     (33, 100, 65, 0.5, 49, np.float64),
     (64, 260, 48, 1.0, 8, np.float32),
     (31, 77, 29, 2.0, 16, np.float32),
+    # wide spread, few moduli: four-digit and eight-digit chunks in one matrix
+    (64, 520, 48, 8.0, 8, np.float64),
 ])
 @pytest.mark.parametrize("fast", [1, 0])
 def test_residue_split_paths(cuda, oracle, m, k, n, phi, N, dt, fast):
