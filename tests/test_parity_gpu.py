@@ -162,3 +162,46 @@ def test_residue_split_paths(cuda, oracle, m, k, n, phi, N, dt, fast):
     _eq(got.crt.Bres, ref.inter["Bres"])
     _eq(got.crt.W, ref.inter["W"])
     _eq(got.C, ref.C)
+
+
+@pytest.mark.parametrize("N", [8, 16])
+def test_residue_digit_boundaries(cuda, oracle, N):
+    """A' placed on the edges of the residue split's paths (resid.cu): four
+    balanced digits (|A'| up to 0x7F7F7F7F / down to -0x80808080) against
+    eight, |A'| just below 2^62 against the exponent buckets (A' = 2^62 at the
+    row maximum), zeros, +-1 and values that truncate to 0.  B has one nonzero
+    row, so every clearance maximum is 32 * 32 and mu = shift(1024) is known
+    from the oracle; the residue planes must equal the oracle's."""
+    k, n = 64, 8
+    B = np.zeros((k, n))
+    B[0, :] = 32.0
+    probe = np.zeros((1, k)); probe[0, 0] = 32.0
+    mu = int(oracle.os_ii(probe, B, N, keep_intermediates=True, residues=True).inter["mu"][0])
+    targets = [0x7F7F7F7F, 0x7F7F7F80, 0x80808080, 0x80808081, (1 << 31) - 1, 1 << 31, 1, 0,
+               (1 << 62) - (1 << 9), (1 << 53) - 1, 0x7F7F7F7F7F7F7F, 255, 256, 0x8080]
+    rows = []
+    for sign in (1, -1):
+        for start in range(0, len(targets), 3):
+            r = np.zeros(k)
+            r[0] = 32.0  # the row maximum: A' = 32 * 2^mu
+            for j, t in enumerate(targets[start:start + 3] + targets[:5]):
+                v = sign * t * 2.0 ** -mu
+                if abs(v) <= 32.0:
+                    r[8 + j] = v  # the second 8-element chunk mixes four- and eight-digit values
+            for j, t in enumerate(targets[start:start + 8]):
+                v = sign * t * 2.0 ** -mu
+                if abs(v) <= 32.0:
+                    r[16 + j] = v
+            for j in range(8):  # a chunk of values that truncate to 0 or +-1
+                r[24 + j] = sign * (0.5 + j) * 2.0 ** -mu
+            rows.append(r)
+    A = np.array(rows)
+    ref = oracle.os_ii(A, B, N, keep_intermediates=True, residues=True)
+    assert int(ref.inter["mu"][0]) == mu
+    for fast in (1, 0):
+        with oz.options(resid_fast=fast):
+            got = oz.os_ii(A, B, N, keep_intermediates=True, evidence=True)
+        _eq(got.scaling.Aprime, ref.inter["Aprime"])
+        _eq(got.crt.Ares, ref.inter["Ares"])
+        _eq(got.crt.W, ref.inter["W"])
+        _eq(got.C, ref.C)
