@@ -222,8 +222,8 @@ __device__ __forceinline__ ModC modc(const ResidHeader& hd, int l) { return ModC
 // ---------------------------------------------------------------------------
 constexpr int RA_E = 8;
 
-// A: the row-shift case of the writer below, kept as its own kernel (48
-// registers, 5 CTAs per SM; the general one needs 60).
+// A: the row-shift case of the writer below, kept as its own kernel (per-row
+// shift; 64 registers, 4 CTAs per SM — 65 would leave 3).
 template <class T>
 __global__ void __launch_bounds__(256, 4) resid_A_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t k,
                                                       int64_t kp, const int32_t* __restrict__ mu,
