@@ -217,7 +217,7 @@ def run_reference(args):
 _OPTION_DEFAULTS = {"gemm": 0, "fused": 0, "fused_mc": 0, "fused_fence": 1, "spec": -1, "graph": 1, "pdl": 1,
                     "group_m": 0, "group_n": 0, "l2hint": 0, "crt_overlap": 0, "crt_cv": 8, "wblock_min_mb": 2048,
                     "gemm_fence": 0, "epi_warps": 0, "pair_stages": 4, "rowscan_threads": 0, "resid_stream": 0,
-                    "spec_tail": 1, "dist_pipeline": 1, "debug_sync": 0, "bbar_fused": 1, "resid_fast": 1}
+                    "spec_tail": 1, "dist_pipeline": 1, "debug_sync": 0, "resid_fast": 1}
 
 
 def non_default_options() -> dict:

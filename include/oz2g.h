@@ -273,8 +273,8 @@ int oz2g_i8_peak(long long iters, int launches, int random, double *ms_out, doub
  * "l2hint", "crt_overlap", "crt_cv" (4 | 8), "wblock_min_mb", "gemm_fence",
  * "epi_warps" (0 | 4 | 8), "pair_stages" (4..6), "rowscan_threads" (0 | 256 |
  * 512 | 1024), "resid_stream", "spec_tail" (1..3), "dist_pipeline",
- * "debug_sync", "bbar_fused" (1 column maxima and Bbar in one read of B),
- * "resid_fast" (1 balanced-digit residue split, 0 exponent buckets only).  Unset options take OZ2G_<NAME> from the environment at first
+ * "debug_sync", "resid_fast" (1 balanced-digit residue split, 0 exponent
+ * buckets only).  Unset options take OZ2G_<NAME> from the environment at first
  * use.  A set applies from the next call (captured graphs are re-captured).
  * Unknown names and out-of-range values: OZ2G_INVALID_ARGUMENT.
  * oz2g_option_name(i) lists the names (NULL past the last). */

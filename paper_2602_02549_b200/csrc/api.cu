@@ -493,17 +493,9 @@ int run_gemm(int prec, int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     // ---- K1 (B): column pre-exponents and Bbar^T ----
     if (pipe && !spec2) CUDA_TRY(cudaStreamWaitEvent(stream, arr ? ev_b_in : ws.ev_b, 0));
     if (scan && !spec2) tm.span(1, sB, [&] {
-        if (opt(OPT_BBAR_FUSED) && k > 0) {  // one read of B for the maxima and (nearly all of) Bbar
-            const int64_t nch = (k + col_chunk_rows(k, n) - 1) / col_chunk_rows(k, n);
-            int16_t* nl = (int16_t*)ws.nuloc.get(sizeof(int16_t) * (size_t)(nch * n));
-            CUDA_TRY(launch_col_max_bbar_B(prec, dB, ldb_d, k, n, ldn, bmax, bbar, nl, st, sB)); launches += n > 0;
-            CUDA_TRY(launch_col_exp_B(bmax, n, nup, st, sB)); launches += n > 0;
-            CUDA_TRY(launch_bbar_fix(prec, dB, ldb_d, k, n, kp, ldn, nup, nl, bbar, st, sB)); launches += n > 0;
-        } else {
-            CUDA_TRY(launch_col_max_B(prec, dB, ldb_d, k, n, bmax, st, sB)); launches += n > 0;
-            CUDA_TRY(launch_col_exp_B(bmax, n, nup, st, sB)); launches += n > 0;
-            CUDA_TRY(launch_bbar_rows(prec, dB, ldb_d, k, n, kp, ldn, nup, bbar, st, sB)); launches += n > 0;
-        }
+        CUDA_TRY(launch_col_max_B(prec, dB, ldb_d, k, n, bmax, st, sB)); launches += n > 0;
+        CUDA_TRY(launch_col_exp_B(bmax, n, nup, st, sB)); launches += n > 0;
+        CUDA_TRY(launch_bbar_rows(prec, dB, ldb_d, k, n, kp, ldn, nup, bbar, st, sB)); launches += n > 0;
     });
     cudaEvent_t ev_bdone = nullptr;
     if (fork) {

@@ -86,7 +86,6 @@ constexpr int kTailSplit = 4;
 
 struct Workspace {
     DevBuf A, B, C, abar, bbar, ares, bres, W, mup, nup, mu, nu, bmax, cmax_row, cmax_col, e, f, status;
-    DevBuf nuloc;  // per-chunk column exponents of the fused column-max + Bbar pass
     DevBuf x_cbar, x_cprod, x_c1, x_c2, x_q, x_cpp64, x_cpp32, x_ap, x_bp, x_bvec, x_bscr, x_bmax, x_bcheap, x_btight;
     DevBuf spec_st;  // speculated column exponents: per-stage statuses
     // relative error criterion (suggest_n tight / relative): floor operands, their
@@ -172,7 +171,7 @@ struct Workspace {
         for (DevBuf* b : {&A, &B, &C, &abar, &bbar, &ares, &bres, &W, &mup, &nup, &mu, &nu, &bmax, &cmax_row,
                           &cmax_col, &e, &f, &status, &x_cbar, &x_cprod, &x_c1, &x_c2, &x_q, &x_cpp64, &x_cpp32,
                           &x_ap, &x_bp, &x_bvec, &x_bscr, &x_bmax, &x_bcheap, &x_btight, &status_ring, &spec_st,
-                          &lo_a, &lo_b, &lo_sum, &lo_ab, &ab_lo, &nuloc})
+                          &lo_a, &lo_b, &lo_sum, &lo_ab, &ab_lo})
             b->release();
         if (spec_changed) cudaFreeHost(spec_changed);
         spec_changed = nullptr;

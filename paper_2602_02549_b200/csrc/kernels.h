@@ -83,17 +83,6 @@ typedef ResidHeader ResidConsts;
 // Stage launchers (scale.cu).  T = float or double inputs; prec selects.
 cudaError_t launch_row_scan_A(int prec, const void* A, int64_t lda, int64_t m, int64_t k, int64_t kp,
                               int32_t* mu_prime, int8_t* abar, DevStatus* st, cudaStream_t s, int64_t row0);
-// Column maxima and Bbar in one read of B (scale.cu): per-chunk Bbar under the
-// chunk's own nu', nu_loc[chunk][j] recorded (chunks of col_chunk_rows rows);
-// bbar_fix recomputes the chunks whose nu' differs from nu'_j and writes the
-// padding (rows k .. kp, columns n .. ldn).
-int col_chunk_rows(int64_t k, int64_t n);
-cudaError_t launch_col_max_bbar_B(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t ldn,
-                                  unsigned long long* bmax, int8_t* bbar, int16_t* nu_loc, DevStatus* st,
-                                  cudaStream_t s);
-cudaError_t launch_bbar_fix(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp, int64_t ldn,
-                            const int32_t* nu_prime, const int16_t* nu_loc, int8_t* bbar, DevStatus* st,
-                            cudaStream_t s);
 cudaError_t launch_col_max_B(int prec, const void* B, int64_t ldb, int64_t k, int64_t n,
                              unsigned long long* bmax, DevStatus* st, cudaStream_t s);
 // col0: global index of column 0 (zero-column messages of a column chunk)

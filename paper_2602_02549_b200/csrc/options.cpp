@@ -49,7 +49,6 @@ const Spec kSpecs[OPT_COUNT] = {
     {"spec_tail", 1, 1, 3, nullptr},
     {"dist_pipeline", 1, 0, 1, nullptr},
     {"debug_sync", 0, 0, 1, nullptr},
-    {"bbar_fused", 1, 0, 1, nullptr},
     {"resid_fast", 1, 0, 1, nullptr},
 };
 

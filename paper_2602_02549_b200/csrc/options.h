@@ -29,7 +29,6 @@ enum Opt : int {
     OPT_SPEC_TAIL,        // host pipeline, rows + columns: halvings of the last column chunks (1..3)
     OPT_DIST_PIPELINE,    // oz2g_gemm_dist: 1 A row chunks broadcast under the scans, 0 all-gathers first
     OPT_DEBUG_SYNC,       // diagnostics: 1 synchronises and reports after every stage (stderr)
-    OPT_BBAR_FUSED,       // 1: column maxima and Bbar in one read of B (chunks re-done where the exponent moved), 0: two passes
     OPT_RESID_FAST,       // residue splits: 1 balanced digits for |A'| < 2^62 (exponent buckets otherwise), 0 buckets only
     OPT_COUNT
 };

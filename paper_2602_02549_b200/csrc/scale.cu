@@ -218,92 +218,6 @@ __global__ void __launch_bounds__(256) col_max_B_kernel(const T* __restrict__ B,
     if (mx) atomicMax(&bmax[j], mx);
 }
 
-// Column maxima and Bbar in one read of B (option bbar_fused).  Each CTA
-// holds 64 (or fewer) rows x 256 columns: it takes the chunk's column maxima
-// (HBM), derives the chunk's own nu'_loc = 5 - ilogb(chunk max) and writes
-// Bbar = ceil(|b| 2^nu'_loc) for the chunk on a second pass that hits L2.
-// Wherever the column's global maximum has the chunk's exponent (nu'_loc ==
-// nu'_j: nearly every chunk of data without a wide exponent spread) that is
-// the reference's Bbar (scaling.hpp:122-131); bbar_fix_kernel recomputes the
-// other chunks after col_exp_B, and writes the zero padding.  An all-zero
-// chunk is final for any nu' (its Bbar is 0).
-constexpr int16_t kNuAnyLoc = -32768;  // all zeros: final whatever nu'_j is
-constexpr int16_t kNuNoLoc = 32767;    // non-finite: always recomputed
-
-template <class T>
-__device__ __forceinline__ int bbar_of(double x, int sft, bool fast, double p2) {
-    return fast ? ceil_scaled_p2(x, p2) : ceil_abs_scaled(x, sft);
-}
-
-template <class T>
-__global__ void __launch_bounds__(256) col_max_bbar_B_kernel(const T* __restrict__ B, int64_t ldb, int64_t k,
-                                                             int64_t n, int rows, unsigned long long* __restrict__ bmax,
-                                                             int8_t* __restrict__ bbar, int64_t ldn,
-                                                             int16_t* __restrict__ nu_loc, DevStatus* st) {
-    pdl_enter();
-    const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
-    if (j >= n) return;
-    const int64_t h0 = (int64_t)blockIdx.y * rows;
-    const int64_t h1 = h0 + rows < k ? h0 + rows : k;
-    unsigned long long mx = 0;
-    for (int64_t h = h0; h < h1; ++h) {
-        const unsigned long long b = abs_bits(ld_d(B + h * ldb + j));
-        mx = b > mx ? b : mx;
-    }
-    if (mx) atomicMax(&bmax[j], mx);  // non-finite: bits >= 0x7ff0.., reported by col_exp_B
-    int16_t nl;
-    if (mx == 0) {
-        nl = kNuAnyLoc;
-        for (int64_t h = h0; h < h1; ++h) bbar[h * ldn + j] = 0;
-    } else if (mx >= 0x7ff0000000000000ull) {
-        nl = kNuNoLoc;
-    } else {
-        const int sft = 5 - ilogb_exact(__longlong_as_double((long long)mx));
-        const bool fast = pow2_normal(sft);
-        const double p2 = fast ? pow2d(sft) : 0.0;
-        bool bad = false;
-        for (int64_t h = h0; h < h1; ++h) {  // the chunk again, from L2
-            const int c = bbar_of<T>(ld_d(B + h * ldb + j), sft, fast, p2);
-            bad |= c < 0;
-            bbar[h * ldn + j] = (int8_t)(c & 0xff);
-        }
-        nl = bad ? kNuNoLoc : (int16_t)sft;  // (cannot overflow under the chunk's own nu')
-    }
-    nu_loc[(int64_t)blockIdx.y * n + j] = nl;
-}
-
-template <class T>
-__global__ void __launch_bounds__(256) bbar_fix_kernel(const T* __restrict__ B, int64_t ldb, int64_t k, int64_t n,
-                                                       int64_t kp, int64_t ldn, int rows,
-                                                       const int32_t* __restrict__ nu_prime,
-                                                       const int16_t* __restrict__ nu_loc,
-                                                       int8_t* __restrict__ bbar, DevStatus* st) {
-    pdl_enter();
-    const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
-    if (j >= ldn) return;
-    const int64_t h0 = (int64_t)blockIdx.y * rows;
-    const int64_t hk = h0 + rows < k ? h0 + rows : k;  // data rows of the chunk
-    const int64_t hp = h0 + rows < kp ? h0 + rows : kp;
-    if (j >= n) {  // padding columns
-        for (int64_t h = h0; h < hp; ++h) bbar[h * ldn + j] = 0;
-        return;
-    }
-    for (int64_t h = (h0 > k ? h0 : k); h < hp; ++h) bbar[h * ldn + j] = 0;  // padding rows k .. kp
-    if (h0 >= k) return;
-    const int nl = nu_loc[(int64_t)blockIdx.y * n + j];
-    const int sft = nu_prime[j];
-    if (nl == kNuAnyLoc || nl == sft) return;  // final
-    const bool fast = pow2_normal(sft);
-    const double p2 = fast ? pow2d(sft) : 0.0;
-    bool bad = false;
-    for (int64_t h = h0; h < hk; ++h) {
-        const int c = bbar_of<T>(ld_d(B + h * ldb + j), sft, fast, p2);
-        bad |= c < 0;
-        bbar[h * ldn + j] = (int8_t)(c & 0xff);
-    }
-    if (bad) flag(st, ERR_CEIL_LOGIC);
-}
-
 __global__ void col_exp_B_kernel(const unsigned long long* __restrict__ bmax, int64_t n,
                                  int32_t* __restrict__ nu_prime, DevStatus* st, int64_t col0) {
     pdl_enter();
@@ -535,44 +449,13 @@ cudaError_t launch_row_scan_A(int prec, const void* A, int64_t lda, int64_t m, i
 cudaError_t launch_col_max_B(int prec, const void* B, int64_t ldb, int64_t k, int64_t n,
                              unsigned long long* bmax, DevStatus* st, cudaStream_t s) {
     if (n == 0 || k == 0) return cudaSuccess;
-    const int rows = col_chunk_rows(k, n);
-    dim3 grid(blocks_for(n, 256), blocks_for(k, rows));
-    if (prec) return launch_pdl(col_max_B_kernel<double>, grid, dim3(256), 0, s, (const double*)B, ldb, k, n, rows, bmax, st);
-    return launch_pdl(col_max_B_kernel<float>, grid, dim3(256), 0, s, (const float*)B, ldb, k, n, rows, bmax, st);
-}
-
-int col_chunk_rows(int64_t k, int64_t n) {
     // 64 rows per CTA, fewer when that leaves under ~16 CTAs per SM
     const int64_t cols = blocks_for(n, 256);
     int rows = 64;
     while (rows > 8 && cols * blocks_for(k, rows) < 16 * current_sm_count()) rows /= 2;
-    return rows;
-}
-
-cudaError_t launch_col_max_bbar_B(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t ldn,
-                                  unsigned long long* bmax, int8_t* bbar, int16_t* nu_loc, DevStatus* st,
-                                  cudaStream_t s) {
-    if (n == 0 || k == 0) return cudaSuccess;
-    const int rows = col_chunk_rows(k, n);
-    dim3 grid(blocks_for(n, 256), blocks_for(k, rows));
-    if (prec)
-        return launch_pdl(col_max_bbar_B_kernel<double>, grid, dim3(256), 0, s, (const double*)B, ldb, k, n, rows,
-                          bmax, bbar, ldn, nu_loc, st);
-    return launch_pdl(col_max_bbar_B_kernel<float>, grid, dim3(256), 0, s, (const float*)B, ldb, k, n, rows, bmax,
-                      bbar, ldn, nu_loc, st);
-}
-
-cudaError_t launch_bbar_fix(int prec, const void* B, int64_t ldb, int64_t k, int64_t n, int64_t kp, int64_t ldn,
-                            const int32_t* nu_prime, const int16_t* nu_loc, int8_t* bbar, DevStatus* st,
-                            cudaStream_t s) {
-    if (n == 0 || kp == 0) return cudaSuccess;
-    const int rows = col_chunk_rows(k > 0 ? k : 1, n);
-    dim3 grid(blocks_for(ldn, 256), blocks_for(kp, rows));
-    if (prec)
-        return launch_pdl(bbar_fix_kernel<double>, grid, dim3(256), 0, s, (const double*)B, ldb, k, n, kp, ldn, rows,
-                          nu_prime, nu_loc, bbar, st);
-    return launch_pdl(bbar_fix_kernel<float>, grid, dim3(256), 0, s, (const float*)B, ldb, k, n, kp, ldn, rows,
-                      nu_prime, nu_loc, bbar, st);
+    dim3 grid((unsigned)cols, blocks_for(k, rows));
+    if (prec) return launch_pdl(col_max_B_kernel<double>, grid, dim3(256), 0, s, (const double*)B, ldb, k, n, rows, bmax, st);
+    return launch_pdl(col_max_B_kernel<float>, grid, dim3(256), 0, s, (const float*)B, ldb, k, n, rows, bmax, st);
 }
 
 cudaError_t launch_col_exp_B(const unsigned long long* bmax, int64_t n, int32_t* nu_prime, DevStatus* st,

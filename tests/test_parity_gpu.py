@@ -205,26 +205,3 @@ def test_residue_digit_boundaries(cuda, oracle, N):
         _eq(got.crt.Ares, ref.inter["Ares"])
         _eq(got.crt.W, ref.inter["W"])
         _eq(got.C, ref.C)
-
-
-@pytest.mark.parametrize("m,k,n,phi,N", [(40, 700, 300, 8.0, 14), (33, 257, 70, 0.0, 16), (20, 1100, 40, 2.0, 20)])
-@pytest.mark.parametrize("fused", [1, 0])
-def test_bbar_fused_pass(cuda, oracle, m, k, n, phi, N, fused):
-    """Column maxima and Bbar in one read of B (option bbar_fused, scale.cu):
-    the chunks whose own exponent differs from the column's are recomputed,
-    all-zero chunks are final, the padding is zero — the clearance product
-    and everything after equal the reference's."""
-    seed = 13 * m + k
-    A = oracle.gen_matrix(m, k, phi, oracle.derive_seed(seed, 0, 0))
-    B = oracle.gen_matrix(k, n, phi, oracle.derive_seed(seed, 0, 1)).copy()
-    B[64:192, :] = 0.0          # whole zero chunks
-    B[:, 3] *= 2.0 ** -30       # a column whose chunks all sit far below ...
-    B[700 % k, 3] = 1.0         # ... its maximum
-    ref = oracle.os_ii(A, B, N, keep_intermediates=True, residues=True)
-    with oz.options(bbar_fused=fused):
-        got = oz.os_ii(A, B, N, keep_intermediates=True, evidence=True)
-    _eq(got.scaling.nu_prime, ref.inter["nu_prime"])
-    _eq(got.scaling.Cbar, ref.inter["Cbar"])
-    _eq(got.scaling.nu, ref.inter["nu"])
-    _eq(got.crt.Bres, ref.inter["Bres"])
-    _eq(got.C, ref.C)
