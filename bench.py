@@ -57,11 +57,21 @@ class ClockSampler:
         ClockSampler._n = getattr(ClockSampler, "_n", 0) + 1  # one file per sampler
         self.path = os.path.join("/tmp", f"oz2g_clocks_{os.getpid()}_{ClockSampler._n}.csv")
 
+    window = None  # (start, end) datetimes of the timed region; None: every sample
+
+    def mark_start(self):
+        import datetime
+        self._t0 = datetime.datetime.now()
+
+    def mark_end(self):
+        import datetime
+        self.window = (self._t0, datetime.datetime.now())
+
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu),
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "--query-gpu=timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                  "--format=csv,noheader,nounits", "-lms", "50"],
@@ -76,14 +86,28 @@ class ClockSampler:
             self.proc.wait()
 
     def summary(self):
-        rows = []
+        """Median SM clock, power and throttle reasons of the samples inside the
+        marked window (nvidia-smi needs ~0.5 s to deliver its first sample, so
+        the sampler starts before the warm-up); all samples when none fall in it."""
+        import datetime
+        rows, stamped = [], []
         try:
             for line in open(self.path):
                 parts = [p.strip() for p in line.split(",")]
-                if len(parts) >= 8 and parts[0].replace(".", "").isdigit():
-                    rows.append(parts)
+                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                    rows.append(parts[1:])
+                    try:
+                        stamped.append((datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f"), parts[1:]))
+                    except ValueError:
+                        pass
         except Exception:
             pass
+        if self.window is not None and stamped:
+            lo = self.window[0] - datetime.timedelta(milliseconds=60)
+            hi = self.window[1] + datetime.timedelta(milliseconds=60)
+            inside = [r for t, r in stamped if lo <= t <= hi]
+            if inside:
+                rows = inside
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = sorted(float(r[0]) for r in rows)
@@ -341,6 +365,8 @@ def main():
             return _Step(comm.gemm(A_sh, B_sh, args.moduli, m, n, Cout, timing=timing))
         return oz.os_ii(A, B, args.moduli, out=Cout, timing=timing, reduce_maxima=reduce_cb)
 
+    sampler = ClockSampler(local)
+    sampler.__enter__()  # running through the warm-up: samples exist when the timed region starts
     for _ in range(args.warmup):
         res = step()
     torch.cuda.synchronize()
@@ -355,16 +381,17 @@ def main():
         torch.cuda.synchronize()
 
     # ---- device-timed region ----
-    sampler = ClockSampler(local)
     barrier()
-    with sampler:
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-        barrier()
+    sampler.mark_start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    barrier()
+    sampler.mark_end()
+    sampler.__exit__(None, None, None)
     t_ms = ev0.elapsed_time(ev1)
     clocks_timed = sampler.summary()  # the timed region's samples (before any other sampler runs)
     # instrumented steps for the dominant kernel (residue GEMMs), same stream

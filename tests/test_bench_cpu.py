@@ -32,3 +32,24 @@ def test_option_defaults_match_library():
     assert set(b._OPTION_DEFAULTS) == set(oz.option_names())
     with oz.options(crt_cv=4):
         assert b.non_default_options().get("crt_cv") == 4
+
+
+def test_clock_sampler_window(tmp_path):
+    """The clock summary keeps only the samples inside the timed window (the
+    sampler runs through the warm-up), and all of them when none fall in it."""
+    import datetime
+    import bench
+    s = bench.ClockSampler(0)
+    s.path = str(tmp_path / "clk.csv")
+    t0 = datetime.datetime(2026, 10, 19, 12, 0, 0)
+    lines = []
+    for i, (mhz, cap) in enumerate([(1965, "Not Active"), (1965, "Not Active"), (1300, "Active"), (1310, "Active"),
+                                    (1320, "Active"), (1900, "Not Active")]):
+        ts = (t0 + datetime.timedelta(milliseconds=200 * i)).strftime("%Y/%m/%d %H:%M:%S.%f")[:-3]
+        lines.append(f"{ts}, {mhz}, 1965, 900.0, 0x4, Not Active, Not Active, Not Active, {cap}")
+    open(s.path, "w").write("\n".join(lines) + "\n")
+    s.window = (t0 + datetime.timedelta(milliseconds=390), t0 + datetime.timedelta(milliseconds=810))
+    out = s.summary()
+    assert out["samples"] == 3 and out["sm_mhz"] == 1310.0 and out["reasons"] == ["sw_power_cap"]
+    s.window = (t0 + datetime.timedelta(seconds=10), t0 + datetime.timedelta(seconds=11))
+    assert s.summary()["samples"] == 6
