@@ -1,7 +1,8 @@
 """Every tuning option leaves C unchanged: seeded
 random cases under a random combination of options — GEMM variant, fused CRT,
 graphs, PDL, raster grouping, L2 hints, CRT width, epilogue warps, pair
-stages, fences, row-scan width, streamed residues, W blocking, CRT overlap —
+stages, fences, row-scan width, streamed residues, W blocking, CRT overlap,
+residue-split path —
 compared bit for bit with the oracle (host pointers once, device pointers
 three times: plain, captured, replayed), and the same exception and message
 on the error paths.  OZ2G_OPTFUZZ_SEEDS scales the number of cases."""
@@ -21,7 +22,7 @@ CHOICES = {"gemm": [0, 1, 2], "fused": [0, 0, 1], "fused_mc": [0], "fused_fence"
            "pdl": [0, 1, 2], "group_m": [0, 1, 4, 16], "group_n": [0, 0, 2], "l2hint": [0, 1, 2, 3], "crt_cv": [4, 8],
            "epi_warps": [0, 4, 8], "pair_stages": [4, 5, 6], "gemm_fence": [0, 1], "rowscan_threads": [0, 256, 1024],
            "resid_stream": [0, 1], "wblock_min_mb": [0, 2048], "crt_overlap": [0, 0, 2], "spec": [-1, 0, 1, 2],
-           "spec_tail": [1, 2, 3]}
+           "spec_tail": [1, 2, 3], "resid_fast": [0, 1, 1]}
 
 
 def _options(rng):
